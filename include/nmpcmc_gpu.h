@@ -1,0 +1,207 @@
+/* nmpcmc_gpu.h -- C ABI of the B200 batched closed-loop Monte Carlo engine.
+ *
+ * Drop-in boundary for the reference's Monte Carlo hot path
+ * (/root/reference/proj/core/include/nmpcmc/montecarlo.hpp). The reference has
+ * no FFI layer; its boundary is the C++ API
+ *     McResult    run_monte_carlo(const Scenario&, int n_sims, int workers)   montecarlo.hpp:121
+ *     SimResult   run_closed_loop(const Scenario&, uint64_t sim_index)        montecarlo.hpp:92
+ *     McAggregate aggregate_stats(const std::vector<SimResult>&)              montecarlo.hpp:108
+ *     Histogram   phi_histogram(const std::vector<double>&, int bins)         montecarlo.hpp:141
+ *     int         validate_scenario(const Scenario&)                          montecarlo.hpp:59
+ * Its Scenario holds type-erased std::function models (model.hpp:28-46) from
+ * which the plant cannot be recovered, so this ABI carries the CSTR parameters
+ * and variants explicitly in a POD. The C++ facade
+ * include/nmpcmc_gpu.hpp keeps the reference's names and result types on top.
+ *
+ * Plain pointers and sizes only; no torch or CUDA types. All functions return
+ * an nmpcmc_status; configuration errors map to the reference's exception
+ * classes (errors.hpp:9-32), per-sample numerical failures never fail a call
+ * (they are recorded in nmpcmc_sim_record.failed, montecarlo.cpp:147-155,228-236).
+ */
+#ifndef NMPCMC_GPU_H
+#define NMPCMC_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NMPCMC_GPU_ABI_VERSION 1
+#define NMPCMC_MAX_SETPOINTS 32
+
+/* Status codes mirror the reference exception taxonomy (errors.hpp:9-32). */
+typedef enum nmpcmc_status {
+    NMPCMC_OK = 0,
+    NMPCMC_DIMENSION_MISMATCH = 1, /* DimensionMismatch errors.hpp:9 */
+    NMPCMC_NOT_POSITIVE_DEFINITE = 2, /* NotPositiveDefinite errors.hpp:15 */
+    NMPCMC_NON_FINITE_STATE = 3,  /* NonFiniteState errors.hpp:20 */
+    NMPCMC_DOMAIN_ERROR = 4,      /* DomainError errors.hpp:25 */
+    NMPCMC_LENGTH_MISMATCH = 5,   /* LengthMismatch errors.hpp:30 */
+    NMPCMC_UNSUPPORTED = 6,       /* valid for the reference, not built on device yet */
+    NMPCMC_INVALID_ARGUMENT = 7,  /* null pointer / bad size at the C boundary */
+    NMPCMC_CUDA_ERROR = 100,
+    NMPCMC_NO_DEVICE = 101
+} nmpcmc_status;
+
+/* ControllerType (montecarlo.hpp:22): nmpc = 0, pi = 1. */
+enum { NMPCMC_CTRL_NMPC = 0, NMPCMC_CTRL_PI = 1 };
+/* CstrVariant (cstr.hpp:19): three_state = 0, one_state = 1. */
+enum { NMPCMC_THREE_STATE = 0, NMPCMC_ONE_STATE = 1 };
+
+/* CstrParams (cstr.hpp:21-34). Flows in mL/min. */
+typedef struct nmpcmc_cstr_params {
+    double V, k0, EaR, beta, cA_in, cB_in, cT_in;
+    double sigmaA, sigmaB, sigmaT;
+    double u_min, u_max;
+} nmpcmc_cstr_params;
+
+/* SqpOptions (sqp.hpp:50-58). */
+typedef struct nmpcmc_sqp_options {
+    double eps;
+    double c1;
+    double backtrack_factor;
+    double qp_tol;
+    int32_t max_iter;
+    int32_t max_backtracks;
+    int32_t qp_max_iter;
+    int32_t _pad;
+} nmpcmc_sqp_options;
+
+/* PiState gains (controllers.hpp:16-25); Ts, u_min, u_max are taken from the
+ * scenario exactly like run_closed_loop does (montecarlo.cpp:97-100). */
+typedef struct nmpcmc_pi_gains {
+    double kP, kI, kaw, u_bar, I_hat;
+} nmpcmc_pi_gains;
+
+/* Scenario (montecarlo.hpp:27-55) for the CSTR case study. */
+typedef struct nmpcmc_scenario {
+    int32_t controller;      /* NMPCMC_CTRL_* */
+    int32_t truth_variant;   /* NMPCMC_THREE_STATE | NMPCMC_ONE_STATE */
+    int32_t ctrl_variant;    /* NMPC controller model; device supports ONE_STATE */
+    int32_t has_noise_R;     /* NoiseSpec::R has rows (model.cpp:41) */
+    nmpcmc_cstr_params truth;
+    nmpcmc_cstr_params ctrl;
+    double noise_R;          /* NoiseSpec::R, 1x1 (n_y = 1) */
+    double R_filter;         /* Scenario::R_filter, 1x1 */
+    double Qz;               /* Scenario::Qz, 1x1 (n_z = 1) */
+    double horizon_Ts;       /* Horizon::Ts */
+    int32_t N;               /* Horizon::N */
+    int32_t Nc;              /* Horizon::Nc */
+    int32_t np;              /* Scenario::np */
+    int32_t Ns;              /* Scenario::Ns */
+    nmpcmc_sqp_options sqp;
+    nmpcmc_pi_gains pi;
+    double u_min, u_max;     /* Scenario::u_min/u_max (n_u = 1) */
+    double t0, tf, Ts;
+    int32_t n_setpoints;     /* SetpointProfile (montecarlo.hpp:15-20), n_z = 1 */
+    int32_t record_stride;   /* Scenario::record_stride */
+    double sp_times[NMPCMC_MAX_SETPOINTS];
+    double sp_values[NMPCMC_MAX_SETPOINTS];
+    double x0[3];            /* truth initial state (n_x of truth_variant) */
+    double x0_hat[3];        /* filter prior mean (n_x of ctrl_variant) */
+    double P0[9];            /* filter prior covariance, column-major */
+    uint64_t base_seed;
+    /* Per-sample parameter uncertainty (BASELINE configs 1, 3, 4). Not a
+     * reference feature: when perturb != 0 each sample's TRUTH parameters
+     * become cA_in*(1+s0*z0), cB_in*(1+s1*z1), EaR*(1+s2*z2) with z the first
+     * three normals of stream (base_seed, sim_index | 2^63). The oracle
+     * applies the same rule through the reference's own CounterRng. */
+    int32_t perturb;
+    int32_t record_trajectories; /* Scenario::record_trajectories */
+    double perturb_rel_std[3];
+} nmpcmc_scenario;
+
+/* SimResult (montecarlo.hpp:72-79) without the trajectory. */
+typedef struct nmpcmc_sim_record {
+    double phi;              /* NaN when failed */
+    int32_t failed;
+    int32_t ocp_solves;
+    int32_t ocp_failures;
+    int32_t status;          /* nmpcmc_status that ended the run (0 if none) */
+} nmpcmc_sim_record;
+
+/* Per-sample work counters (device-measured) for the FP64 roofline
+ * (SURVEY.md §8d). Shooting counts are stage intervals, not sweeps. */
+typedef struct nmpcmc_work_counters {
+    int64_t control_steps;
+    int64_t shoot_full;      /* stage intervals shot with sensitivities */
+    int64_t shoot_fonly;     /* stage intervals shot state-only */
+    int64_t ipm_stage_iters; /* sum over IPM iterations of N */
+    int64_t sqp_stage_iters; /* sum over SQP iterations of N */
+    int64_t qp_solves;
+    int64_t sqp_iterations;
+    int64_t ls_evals;
+} nmpcmc_work_counters;
+
+/* McAggregate (montecarlo.hpp:95-106). */
+typedef struct nmpcmc_aggregate {
+    int32_t n_sims;
+    int32_t n_failed;
+    double mean, variance, min, max;
+    double deciles[11];
+    int64_t ocp_solves;
+    int64_t ocp_failures;
+    double ocp_success_pct;
+} nmpcmc_aggregate;
+
+typedef struct nmpcmc_gpu_ctx nmpcmc_gpu_ctx;
+
+/* ABI self-description so bindings can check their struct layout. */
+int nmpcmc_gpu_abi_version(void);
+int64_t nmpcmc_gpu_struct_size(int which); /* 0 scenario, 1 record, 2 counters, 3 aggregate */
+
+/* validate_scenario (montecarlo.cpp:34-63) plus the device support checks;
+ * writes N_bar. Host only. */
+int nmpcmc_gpu_validate(const nmpcmc_scenario* sc, int32_t* nbar_out);
+
+/* Context = one device + one stream + scratch. Replaces the std::thread pool
+ * of run_monte_carlo (montecarlo.cpp:218-245). */
+int nmpcmc_gpu_ctx_create(int device, nmpcmc_gpu_ctx** out);
+void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx);
+const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx);
+/* CUDA stream the context launches on (as void*; 0 = legacy default). */
+int nmpcmc_gpu_set_stream(nmpcmc_gpu_ctx* ctx, void* stream);
+
+/* run_monte_carlo over the global sample range [first_sim, first_sim+n_sims)
+ * (montecarlo.cpp:213-251; run_closed_loop per sample, montecarlo.cpp:80-157).
+ * HOST buffers: records_out[n_sims] in index order; counters_out and agg_out
+ * may be NULL. Synchronous. */
+int nmpcmc_gpu_run(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
+                   int64_t n_sims, nmpcmc_sim_record* records_out,
+                   nmpcmc_work_counters* counters_out, nmpcmc_aggregate* agg_out);
+
+/* Same, DEVICE-resident outputs (records_dev[n_sims], counters_dev may be
+ * NULL), enqueued on the context stream; returns after the launch. */
+int nmpcmc_gpu_run_device(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
+                          int64_t n_sims, nmpcmc_sim_record* records_dev,
+                          nmpcmc_work_counters* counters_dev);
+
+/* Trajectory recording (montecarlo.cpp:126-146, Trajectory montecarlo.hpp:64-67).
+ * traj_out: HOST, n_sims * rows * 5 doubles, rows = nmpcmc_gpu_traj_rows(sc);
+ * per row (t, z, z_bar, u, y); unused rows of failed runs are NaN. */
+int32_t nmpcmc_gpu_traj_rows(const nmpcmc_scenario* sc);
+int nmpcmc_gpu_run_traj(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
+                        int64_t n_sims, nmpcmc_sim_record* records_out, double* traj_out);
+
+/* aggregate_stats (montecarlo.cpp:172-211), index order, host. */
+int nmpcmc_gpu_aggregate(const nmpcmc_sim_record* records, int64_t n, nmpcmc_aggregate* out);
+
+/* phi_histogram (montecarlo.cpp:268-304), host. edges_out[201], counts_out[200]. */
+int nmpcmc_gpu_histogram(const double* phi, int64_t n, int32_t bins, double* edges_out,
+                         int32_t* counts_out, int32_t* nbins_out);
+
+/* Unit-level device entry points (parity tests of rng.cpp and the libm). */
+/* CounterRng::philox_block (rng.cpp:31-43): in[6*n] = counter[4], key[2]; out[4*n]. */
+int nmpcmc_gpu_philox_blocks(nmpcmc_gpu_ctx* ctx, const uint32_t* in, int64_t n, uint32_t* out);
+/* CounterRng(seed, stream).normal() x n (rng.cpp:78-91). */
+int nmpcmc_gpu_normals(nmpcmc_gpu_ctx* ctx, uint64_t seed, uint64_t stream, int64_t n,
+                       double* out);
+/* fn: 0 exp, 1 log, 2 sin, 3 cos of x[n] with the device libm. */
+int nmpcmc_gpu_libm(nmpcmc_gpu_ctx* ctx, int32_t fn, const double* x, int64_t n, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NMPCMC_GPU_H */

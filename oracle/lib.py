@@ -1,0 +1,99 @@
+"""ctypes loaders for the oracle libraries (TEST INFRASTRUCTURE ONLY).
+
+  ref(libm="xlibm"|"glibc") -> the unmodified reference core + ref_driver.cpp
+                               (oracle/_ref/, built from /root/reference)
+  port()                    -> the C++ restatement (oracle/port/, _build/)
+  xlibm()                   -> host build of the portable libm
+"""
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2212_02197_b200 import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_cache = {}
+
+
+def build(target="all") -> None:
+    subprocess.run(["make", "-s", "-C", HERE, target], check=True)
+
+
+def _load(path):
+    if path not in _cache:
+        _cache[path] = C.CDLL(path)
+    return _cache[path]
+
+
+def ref_available() -> bool:
+    return os.path.exists(os.path.join(HERE, "_ref", "libnmpcmc_ref_xlibm.so"))
+
+
+def ref(libm="xlibm"):
+    path = os.path.join(HERE, "_ref", f"libnmpcmc_ref_{libm}.so")
+    if not os.path.exists(path):
+        if os.path.isdir("/root/reference/proj/core"):
+            build("ref")
+        else:
+            raise FileNotFoundError(f"{path} missing and /root/reference absent (build it in the dev container)")
+    lib = _load(path)
+    _sig(lib, "nmpcmc_ref")
+    return lib
+
+
+def port():
+    path = os.path.join(HERE, "_build", "libnmpcmc_port.so")
+    if not os.path.exists(path):
+        build("port")
+    lib = _load(path)
+    _sig(lib, "nmpcmc_port")
+    return lib
+
+
+def xlibm():
+    path = os.path.join(HERE, "_build", "libxlibm.so")
+    if not os.path.exists(path):
+        build("_build/libxlibm.so")
+    lib = _load(path)
+    for n in ("nmx_exp", "nmx_log", "nmx_sin", "nmx_cos"):
+        getattr(lib, n).restype = C.c_double
+        getattr(lib, n).argtypes = [C.c_double]
+    return lib
+
+
+def _sig(lib, p):
+    S = C.POINTER(abi.Scenario)
+    R = C.POINTER(abi.SimRecord)
+    f = getattr(lib, f"{p}_run_closed_loop")
+    f.argtypes = [S, C.c_uint64, R, C.POINTER(C.c_double), C.c_int]
+    f = getattr(lib, f"{p}_run_batch")
+    f.argtypes = [S, C.c_uint64, C.c_int64, C.c_int, R, C.POINTER(C.c_double)]
+    if hasattr(lib, f"{p}_aggregate"):
+        getattr(lib, f"{p}_aggregate").argtypes = [R, C.c_int64, C.POINTER(abi.Aggregate)]
+    if hasattr(lib, f"{p}_normals"):
+        getattr(lib, f"{p}_normals").argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(C.c_double)]
+    if hasattr(lib, f"{p}_reaction_rate"):
+        getattr(lib, f"{p}_reaction_rate").restype = C.c_double
+        getattr(lib, f"{p}_reaction_rate").argtypes = [C.POINTER(abi.CstrParams), C.POINTER(C.c_double)]
+
+
+def run_batch(lib, sc, first, n, workers=None, prefix="nmpcmc_ref"):
+    """Records (numpy RECORD_DTYPE) and wall seconds for [first, first+n)."""
+    workers = workers or os.cpu_count() or 1
+    out = np.zeros(n, dtype=abi.RECORD_DTYPE)
+    wall = C.c_double(0.0)
+    rc = getattr(lib, f"{prefix}_run_batch")(C.byref(sc), first, n, workers,
+                                             out.ctypes.data_as(C.POINTER(abi.SimRecord)), C.byref(wall))
+    if rc != 0:
+        raise RuntimeError(f"oracle run_batch failed: {rc}")
+    return out, wall.value
+
+
+def run_traj(lib, sc, idx, rows, prefix="nmpcmc_ref"):
+    rec = abi.SimRecord()
+    traj = np.zeros((rows, 5))
+    getattr(lib, f"{prefix}_run_closed_loop")(C.byref(sc), idx, C.byref(rec),
+                                              traj.ctypes.data_as(C.POINTER(C.c_double)), rows)
+    return rec, traj

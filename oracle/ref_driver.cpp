@@ -1,0 +1,279 @@
+// ref_driver.cpp -- C-ABI driver around the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE (oracle): linked against the reference core compiled
+// from /root/reference/proj/core/src/*.cpp by oracle/Makefile into
+// oracle/_ref/. It translates the POD nmpcmc_scenario of include/nmpcmc_gpu.h
+// into the reference's Scenario (montecarlo.hpp:27-55) and calls the
+// reference's own entry points:
+//   run_closed_loop  (montecarlo.cpp:80-157)   -> nmpcmc_ref_run_closed_loop
+//   run_monte_carlo  (montecarlo.cpp:213-251)  -> nmpcmc_ref_run_batch
+//   aggregate_stats  (montecarlo.cpp:172-211)  -> nmpcmc_ref_aggregate
+//   phi_histogram    (montecarlo.cpp:268-304)  -> nmpcmc_ref_histogram
+// and, for unit-level pins, CounterRng / pi_step / nmpc_step.
+// Only tests/, __graft_entry__.smoke() and bench.py's CPU arm load it.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <thread>
+#include <vector>
+
+#include "nmpcmc/controllers.hpp"
+#include "nmpcmc/cstr.hpp"
+#include "nmpcmc/montecarlo.hpp"
+#include "nmpcmc/rng.hpp"
+#include "nmpcmc_gpu.h"
+
+using namespace nmpcmc;
+
+namespace {
+
+CstrParams to_params(const nmpcmc_cstr_params& p) {
+    CstrParams q;
+    q.V = p.V;
+    q.k0 = p.k0;
+    q.EaR = p.EaR;
+    q.beta = p.beta;
+    q.cA_in = p.cA_in;
+    q.cB_in = p.cB_in;
+    q.cT_in = p.cT_in;
+    q.sigmaA = p.sigmaA;
+    q.sigmaB = p.sigmaB;
+    q.sigmaT = p.sigmaT;
+    q.u_min = p.u_min;
+    q.u_max = p.u_max;
+    return q;
+}
+
+CstrVariant to_variant(int v) { return v == NMPCMC_ONE_STATE ? CstrVariant::one_state : CstrVariant::three_state; }
+int nx_of(int v) { return v == NMPCMC_ONE_STATE ? 1 : 3; }
+
+/// Per-sample truth parameters: the BASELINE perturbation rule of
+/// include/nmpcmc_gpu.h, drawn with the reference's own CounterRng.
+CstrParams truth_params(const nmpcmc_scenario& s, std::uint64_t sim_index) {
+    CstrParams p = to_params(s.truth);
+    if (s.perturb) {
+        CounterRng prng(s.base_seed, sim_index | 0x8000000000000000ULL);
+        const double z0 = prng.normal();
+        const double z1 = prng.normal();
+        const double z2 = prng.normal();
+        p.cA_in = p.cA_in * (1.0 + s.perturb_rel_std[0] * z0);
+        p.cB_in = p.cB_in * (1.0 + s.perturb_rel_std[1] * z1);
+        p.EaR = p.EaR * (1.0 + s.perturb_rel_std[2] * z2);
+    }
+    return p;
+}
+
+Scenario make_scenario(const nmpcmc_scenario& s, std::uint64_t sim_index) {
+    Scenario sc;
+    sc.truth = make_cstr_model(truth_params(s, sim_index), to_variant(s.truth_variant));
+    if (s.has_noise_R) sc.noise.R = Matrix::from_rows({{s.noise_R}});
+    sc.noise.n_w = sc.truth.n_w;
+    sc.controller = s.controller == NMPCMC_CTRL_PI ? ControllerType::pi : ControllerType::nmpc;
+    sc.ctrl_model = make_cstr_model(to_params(s.ctrl), to_variant(s.ctrl_variant));
+    sc.horizon = Horizon{s.N, s.horizon_Ts, s.Nc};
+    sc.Qz = Matrix::from_rows({{s.Qz}});
+    sc.R_filter = Matrix::from_rows({{s.R_filter}});
+    const int nxc = nx_of(s.ctrl_variant);
+    sc.x0_hat.assign(s.x0_hat, s.x0_hat + nxc);
+    sc.P0 = Matrix(nxc, nxc);
+    for (int c = 0; c < nxc; ++c)
+        for (int r = 0; r < nxc; ++r) sc.P0(r, c) = s.P0[c * nxc + r];
+    sc.np = s.np;
+    sc.sqp.eps = s.sqp.eps;
+    sc.sqp.max_iter = s.sqp.max_iter;
+    sc.sqp.max_backtracks = s.sqp.max_backtracks;
+    sc.sqp.c1 = s.sqp.c1;
+    sc.sqp.backtrack_factor = s.sqp.backtrack_factor;
+    sc.sqp.qp_tol = s.sqp.qp_tol;
+    sc.sqp.qp_max_iter = s.sqp.qp_max_iter;
+    sc.pi.kP = s.pi.kP;
+    sc.pi.kI = s.pi.kI;
+    sc.pi.kaw = s.pi.kaw;
+    sc.pi.u_bar = s.pi.u_bar;
+    sc.pi.I_hat = s.pi.I_hat;
+    sc.u_min = {s.u_min};
+    sc.u_max = {s.u_max};
+    sc.t0 = s.t0;
+    sc.tf = s.tf;
+    sc.Ts = s.Ts;
+    sc.Ns = s.Ns;
+    for (int i = 0; i < s.n_setpoints; ++i) {
+        sc.setpoints.times.push_back(s.sp_times[i]);
+        sc.setpoints.values.push_back(Vec{s.sp_values[i]});
+    }
+    sc.x0.assign(s.x0, s.x0 + nx_of(s.truth_variant));
+    sc.base_seed = s.base_seed;
+    sc.record_trajectories = s.record_trajectories != 0;
+    sc.record_stride = s.record_stride;
+    return sc;
+}
+
+void to_record(const SimResult& r, nmpcmc_sim_record* out) {
+    out->phi = r.phi;
+    out->failed = r.failed ? 1 : 0;
+    out->ocp_solves = r.ocp_solves;
+    out->ocp_failures = r.ocp_failures;
+    out->status = r.failed ? -1 : 0;  // the reference swallows the cause
+}
+
+/// The worker body of run_monte_carlo (montecarlo.cpp:226-236): anything
+/// run_closed_loop does not absorb still only fails this one simulation.
+void run_one(const nmpcmc_scenario& s, std::uint64_t idx, nmpcmc_sim_record* out, double* traj,
+             int rows) {
+    try {
+        const Scenario sc = make_scenario(s, idx);
+        const SimResult r = run_closed_loop(sc, idx);
+        to_record(r, out);
+        if (traj != nullptr) {
+            const Trajectory& tr = r.trajectory;
+            const double nan = std::numeric_limits<double>::quiet_NaN();
+            for (int i = 0; i < rows; ++i) {
+                const bool have = static_cast<std::size_t>(i) < tr.t.size();
+                traj[i * 5 + 0] = have ? tr.t[i] : nan;
+                traj[i * 5 + 1] = have ? tr.z[i][0] : nan;
+                traj[i * 5 + 2] = have ? tr.z_bar[i][0] : nan;
+                traj[i * 5 + 3] = have ? tr.u[i][0] : nan;
+                traj[i * 5 + 4] = have ? tr.y[i][0] : nan;
+            }
+        }
+    } catch (...) {
+        out->phi = std::numeric_limits<double>::quiet_NaN();
+        out->failed = 1;
+        out->ocp_solves = 0;
+        out->ocp_failures = 0;
+        out->status = -2;
+        if (traj != nullptr)
+            for (int i = 0; i < rows * 5; ++i) traj[i] = std::numeric_limits<double>::quiet_NaN();
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int nmpcmc_ref_validate(const nmpcmc_scenario* s, int* nbar) {
+    try {
+        *nbar = validate_scenario(make_scenario(*s, 0));
+        return 0;
+    } catch (const DomainError&) {
+        return NMPCMC_DOMAIN_ERROR;
+    } catch (...) {
+        return NMPCMC_INVALID_ARGUMENT;
+    }
+}
+
+/// run_closed_loop for one global index; traj (nullable) gets rows*5 doubles.
+int nmpcmc_ref_run_closed_loop(const nmpcmc_scenario* s, std::uint64_t sim_index,
+                               nmpcmc_sim_record* out, double* traj, int rows) {
+    run_one(*s, sim_index, out, traj, rows);
+    return 0;
+}
+
+/// Batch over [first, first+n) on `workers` threads. With no per-sample
+/// parameters and first == 0 this IS the reference's run_monte_carlo;
+/// otherwise the same atomic-counter pool over per-sample Scenarios.
+int nmpcmc_ref_run_batch(const nmpcmc_scenario* s, std::uint64_t first, std::int64_t n,
+                         int workers, nmpcmc_sim_record* out, double* wall_seconds) {
+    if (n < 1 || workers < 1) return NMPCMC_DOMAIN_ERROR;
+    if (!s->perturb && first == 0 && n <= std::numeric_limits<int>::max()) {
+        const Scenario sc = make_scenario(*s, 0);
+        const McResult r = run_monte_carlo(sc, static_cast<int>(n), workers);
+        for (std::int64_t i = 0; i < n; ++i) to_record(r.sims[static_cast<std::size_t>(i)], &out[i]);
+        if (wall_seconds) *wall_seconds = r.wall_seconds;
+        return 0;
+    }
+    std::atomic<std::int64_t> next{0};
+    const auto start = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    const int nt = static_cast<int>(std::min<std::int64_t>(workers, n));
+    for (int w = 0; w < nt; ++w)
+        pool.emplace_back([&]() {
+            for (;;) {
+                const std::int64_t i = next.fetch_add(1, std::memory_order_relaxed);
+                if (i >= n) return;
+                run_one(*s, first + static_cast<std::uint64_t>(i), &out[i], nullptr, 0);
+            }
+        });
+    for (auto& th : pool) th.join();
+    if (wall_seconds)
+        *wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+    return 0;
+}
+
+int nmpcmc_ref_aggregate(const nmpcmc_sim_record* rec, std::int64_t n, nmpcmc_aggregate* out) {
+    std::vector<SimResult> sims(static_cast<std::size_t>(n));
+    for (std::int64_t i = 0; i < n; ++i) {
+        sims[i].phi = rec[i].phi;
+        sims[i].failed = rec[i].failed != 0;
+        sims[i].ocp_solves = rec[i].ocp_solves;
+        sims[i].ocp_failures = rec[i].ocp_failures;
+    }
+    const McAggregate a = aggregate_stats(sims);
+    out->n_sims = a.n_sims;
+    out->n_failed = a.n_failed;
+    out->mean = a.mean;
+    out->variance = a.variance;
+    out->min = a.min;
+    out->max = a.max;
+    for (int d = 0; d < 11; ++d) out->deciles[d] = a.deciles[static_cast<std::size_t>(d)];
+    out->ocp_solves = a.ocp_solves;
+    out->ocp_failures = a.ocp_failures;
+    out->ocp_success_pct = a.ocp_success_pct;
+    return 0;
+}
+
+int nmpcmc_ref_histogram(const double* phi, std::int64_t n, int bins, double* edges,
+                         int* counts, int* nbins) {
+    const Histogram h = phi_histogram(std::vector<double>(phi, phi + n), bins);
+    *nbins = static_cast<int>(h.counts.size());
+    for (std::size_t i = 0; i < h.edges.size(); ++i) edges[i] = h.edges[i];
+    for (std::size_t i = 0; i < h.counts.size(); ++i) counts[i] = h.counts[i];
+    return 0;
+}
+
+void nmpcmc_ref_philox_block(const std::uint32_t* in, std::uint32_t* out) {
+    const auto r = CounterRng::philox_block({in[0], in[1], in[2], in[3]}, {in[4], in[5]});
+    for (int i = 0; i < 4; ++i) out[i] = r[static_cast<std::size_t>(i)];
+}
+
+void nmpcmc_ref_normals(std::uint64_t seed, std::uint64_t stream, std::int64_t n, double* out) {
+    CounterRng rng(seed, stream);
+    for (std::int64_t i = 0; i < n; ++i) out[i] = rng.normal();
+}
+
+/// pi_step (controllers.cpp:12-23): state[8] = kP,kI,kaw,Ts,u_bar,u_min,u_max,I_hat;
+/// out[7] = e, P, I, u_hat, u, I_aw, next.I_hat.
+void nmpcmc_ref_pi_step(const double* st, double y, double ybar, double* out) {
+    PiState s;
+    s.kP = st[0];
+    s.kI = st[1];
+    s.kaw = st[2];
+    s.Ts = st[3];
+    s.u_bar = st[4];
+    s.u_min = st[5];
+    s.u_max = st[6];
+    s.I_hat = st[7];
+    const PiStepResult r = pi_step(s, y, ybar);
+    out[0] = r.e;
+    out[1] = r.P;
+    out[2] = r.I;
+    out[3] = r.u_hat;
+    out[4] = r.u;
+    out[5] = r.I_aw;
+    out[6] = r.next.I_hat;
+}
+
+/// reaction_rate (cstr.cpp:36-40) on the three-state variant; NaN on DomainError.
+double nmpcmc_ref_reaction_rate(const nmpcmc_cstr_params* p, const double* c) {
+    const CstrParams q = to_params(*p);
+    try {
+        return reaction_rate({c[0], c[1], c[2]}, q, stoich_config(CstrVariant::three_state, q));
+    } catch (...) {
+        return std::numeric_limits<double>::quiet_NaN();
+    }
+}
+
+}  // extern "C"

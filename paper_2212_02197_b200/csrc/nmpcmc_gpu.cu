@@ -1,0 +1,269 @@
+// nmpcmc_gpu.cu -- device entry points of the C ABI (include/nmpcmc_gpu.h).
+//
+// One context = one device + one stream. nmpcmc_gpu_run replaces the
+// reference's std::thread pool (run_monte_carlo, montecarlo.cpp:213-251):
+// the sample range becomes the grid (PI: a thread per sample; NMPC: a warp
+// per sample), records land in index order exactly like McResult::sims.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "nmpc_kernel.cuh"
+#include "nmpcmc_gpu.h"
+#include "pi_kernel.cuh"
+
+struct nmpcmc_gpu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    void* d_rec = nullptr;
+    size_t rec_cap = 0;
+    void* d_cnt = nullptr;
+    size_t cnt_cap = 0;
+    void* d_traj = nullptr;
+    size_t traj_cap = 0;
+    void* d_scratch = nullptr;
+    size_t scratch_cap = 0;
+    int sm_count = 0;
+};
+
+namespace {
+
+int fail(nmpcmc_gpu_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int cuda_check(nmpcmc_gpu_ctx* ctx, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return NMPCMC_OK;
+    return fail(ctx, NMPCMC_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int ensure(nmpcmc_gpu_ctx* ctx, void** buf, size_t* cap, size_t need) {
+    if (need <= *cap) return NMPCMC_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMalloc(buf, need);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "cudaMalloc");
+    *cap = need;
+    return NMPCMC_OK;
+}
+
+/// Enqueue the closed-loop kernel for [first, first+n) on ctx->stream.
+int launch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar,
+           nmpcmc_sim_record* d_rec, nmpcmc_work_counters* d_cnt, double* d_traj, int rows) {
+    if (n == 0) return NMPCMC_OK;
+    if (sc.controller == NMPCMC_CTRL_PI) {
+        const int block = 128;
+        const int64_t grid = (n + block - 1) / block;
+        if (sc.truth_variant == NMPCMC_THREE_STATE)
+            nmpcmc_dev::pi_kernel<3><<<(unsigned)grid, block, 0, ctx->stream>>>(
+                sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+        else
+            nmpcmc_dev::pi_kernel<1><<<(unsigned)grid, block, 0, ctx->stream>>>(
+                sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+        return cuda_check(ctx, cudaGetLastError(), "pi_kernel launch");
+    }
+    const int rc = nmpcmc_dev::launch_nmpc(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
+                                           ctx->sm_count, ctx->stream);
+    if (rc != NMPCMC_OK) return fail(ctx, rc, "nmpc launch: unsupported configuration");
+    return cuda_check(ctx, cudaGetLastError(), "nmpc_kernel launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+int nmpcmc_gpu_ctx_create(int device, nmpcmc_gpu_ctx** out) {
+    if (out == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return NMPCMC_NO_DEVICE;
+    if (device < 0 || device >= count) return NMPCMC_NO_DEVICE;
+    auto* ctx = new nmpcmc_gpu_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete ctx;
+        return NMPCMC_CUDA_ERROR;
+    }
+    cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return NMPCMC_CUDA_ERROR;
+    }
+    *out = ctx;
+    return NMPCMC_OK;
+}
+
+void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx) {
+    if (ctx == nullptr) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    for (void* p : {ctx->d_rec, ctx->d_cnt, ctx->d_traj, ctx->d_scratch})
+        if (p) cudaFree(p);
+    delete ctx;
+}
+
+const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : "null context";
+}
+
+int nmpcmc_gpu_set_stream(nmpcmc_gpu_ctx* ctx, void* stream) {
+    if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    return NMPCMC_OK;
+}
+
+int nmpcmc_gpu_run_device(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
+                          int64_t n_sims, nmpcmc_sim_record* records_dev,
+                          nmpcmc_work_counters* counters_dev) {
+    if (ctx == nullptr || sc == nullptr || (records_dev == nullptr && n_sims > 0) || n_sims < 0)
+        return NMPCMC_INVALID_ARGUMENT;
+    int32_t nbar = 0;
+    int rc = nmpcmc_gpu_validate(sc, &nbar);
+    if (rc != NMPCMC_OK) return fail(ctx, rc, "scenario validation failed");
+    cudaSetDevice(ctx->device);
+    return launch(ctx, *sc, first_sim, n_sims, nbar, records_dev, counters_dev, nullptr, 0);
+}
+
+int nmpcmc_gpu_run(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
+                   int64_t n_sims, nmpcmc_sim_record* records_out,
+                   nmpcmc_work_counters* counters_out, nmpcmc_aggregate* agg_out) {
+    if (ctx == nullptr || sc == nullptr || records_out == nullptr || n_sims < 1)
+        return NMPCMC_INVALID_ARGUMENT;
+    int32_t nbar = 0;
+    int rc = nmpcmc_gpu_validate(sc, &nbar);
+    if (rc != NMPCMC_OK) return fail(ctx, rc, "scenario validation failed");
+    cudaSetDevice(ctx->device);
+    const size_t nrec = (size_t)n_sims * sizeof(nmpcmc_sim_record);
+    if ((rc = ensure(ctx, &ctx->d_rec, &ctx->rec_cap, nrec)) != NMPCMC_OK) return rc;
+    nmpcmc_work_counters* d_cnt = nullptr;
+    if (counters_out) {
+        if ((rc = ensure(ctx, &ctx->d_cnt, &ctx->cnt_cap, (size_t)n_sims * sizeof(nmpcmc_work_counters))) != NMPCMC_OK)
+            return rc;
+        d_cnt = static_cast<nmpcmc_work_counters*>(ctx->d_cnt);
+    }
+    auto* d_rec = static_cast<nmpcmc_sim_record*>(ctx->d_rec);
+    if ((rc = launch(ctx, *sc, first_sim, n_sims, nbar, d_rec, d_cnt, nullptr, 0)) != NMPCMC_OK) return rc;
+    if ((rc = cuda_check(ctx, cudaMemcpyAsync(records_out, d_rec, nrec, cudaMemcpyDeviceToHost, ctx->stream), "D2H records")) != NMPCMC_OK)
+        return rc;
+    if (counters_out &&
+        (rc = cuda_check(ctx, cudaMemcpyAsync(counters_out, d_cnt, (size_t)n_sims * sizeof(nmpcmc_work_counters),
+                                              cudaMemcpyDeviceToHost, ctx->stream), "D2H counters")) != NMPCMC_OK)
+        return rc;
+    if ((rc = cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "kernel execution")) != NMPCMC_OK) return rc;
+    if (agg_out) return nmpcmc_gpu_aggregate(records_out, n_sims, agg_out);
+    return NMPCMC_OK;
+}
+
+int nmpcmc_gpu_run_traj(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
+                        int64_t n_sims, nmpcmc_sim_record* records_out, double* traj_out) {
+    if (ctx == nullptr || sc == nullptr || records_out == nullptr || traj_out == nullptr || n_sims < 1)
+        return NMPCMC_INVALID_ARGUMENT;
+    int32_t nbar = 0;
+    int rc = nmpcmc_gpu_validate(sc, &nbar);
+    if (rc != NMPCMC_OK) return fail(ctx, rc, "scenario validation failed");
+    const int rows = nmpcmc_gpu_traj_rows(sc);
+    cudaSetDevice(ctx->device);
+    const size_t nrec = (size_t)n_sims * sizeof(nmpcmc_sim_record);
+    const size_t ntraj = (size_t)n_sims * rows * 5 * sizeof(double);
+    if ((rc = ensure(ctx, &ctx->d_rec, &ctx->rec_cap, nrec)) != NMPCMC_OK) return rc;
+    if ((rc = ensure(ctx, &ctx->d_traj, &ctx->traj_cap, ntraj)) != NMPCMC_OK) return rc;
+    // rows a failed run never reaches stay NaN (0xff.. bytes are a NaN pattern)
+    if ((rc = cuda_check(ctx, cudaMemsetAsync(ctx->d_traj, 0xff, ntraj, ctx->stream), "memset")) != NMPCMC_OK) return rc;
+    auto* d_rec = static_cast<nmpcmc_sim_record*>(ctx->d_rec);
+    auto* d_traj = static_cast<double*>(ctx->d_traj);
+    if ((rc = launch(ctx, *sc, first_sim, n_sims, nbar, d_rec, nullptr, d_traj, rows)) != NMPCMC_OK) return rc;
+    cudaMemcpyAsync(records_out, d_rec, nrec, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(traj_out, d_traj, ntraj, cudaMemcpyDeviceToHost, ctx->stream);
+    return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "kernel execution");
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------- unit entry points
+namespace {
+
+__global__ void philox_kernel(const uint32_t* in, int64_t n, uint32_t* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t* c = in + 6 * i;
+    const uint4 r = nmpcmc_dev::philox4x32_10(make_uint4(c[0], c[1], c[2], c[3]), c[4], c[5]);
+    out[4 * i + 0] = r.x;
+    out[4 * i + 1] = r.y;
+    out[4 * i + 2] = r.z;
+    out[4 * i + 3] = r.w;
+}
+
+__global__ void normals_kernel(uint64_t seed, uint64_t stream, int64_t n, double* out) {
+    // one thread replays the stream serially: exactly the host call pattern
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    nmpcmc_dev::NormalStream rng;
+    rng.init(seed, stream);
+    for (int64_t i = 0; i < n; ++i) out[i] = rng.normal();
+}
+
+__global__ void libm_kernel(int fn, const double* x, int64_t n, double* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = x[i];
+    double r;
+    switch (fn) {
+        case 0: r = xlibm_exp(v); break;
+        case 1: r = xlibm_log(v); break;
+        case 2: r = xlibm_sin(v); break;
+        default: r = xlibm_cos(v); break;
+    }
+    out[i] = r;
+}
+
+template <typename T>
+int scratch_roundtrip(nmpcmc_gpu_ctx* ctx, const void* in, size_t in_bytes, size_t out_bytes,
+                      void* out, T&& kernel_launch) {
+    int rc = ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap, in_bytes + out_bytes + 256);
+    if (rc != NMPCMC_OK) return rc;
+    char* base = static_cast<char*>(ctx->d_scratch);
+    char* d_out = base + ((in_bytes + 255) / 256) * 256;
+    if (in_bytes) cudaMemcpyAsync(base, in, in_bytes, cudaMemcpyHostToDevice, ctx->stream);
+    kernel_launch(base, d_out);
+    if ((rc = cuda_check(ctx, cudaGetLastError(), "unit kernel launch")) != NMPCMC_OK) return rc;
+    cudaMemcpyAsync(out, d_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream);
+    return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "unit kernel");
+}
+
+}  // namespace
+
+extern "C" {
+
+int nmpcmc_gpu_philox_blocks(nmpcmc_gpu_ctx* ctx, const uint32_t* in, int64_t n, uint32_t* out) {
+    if (ctx == nullptr || in == nullptr || out == nullptr || n < 1) return NMPCMC_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    return scratch_roundtrip(ctx, in, n * 6 * sizeof(uint32_t), n * 4 * sizeof(uint32_t), out,
+                             [&](char* din, char* dout) {
+                                 philox_kernel<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(
+                                     reinterpret_cast<uint32_t*>(din), n, reinterpret_cast<uint32_t*>(dout));
+                             });
+}
+
+int nmpcmc_gpu_normals(nmpcmc_gpu_ctx* ctx, uint64_t seed, uint64_t stream, int64_t n, double* out) {
+    if (ctx == nullptr || out == nullptr || n < 1) return NMPCMC_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    return scratch_roundtrip(ctx, nullptr, 0, n * sizeof(double), out, [&](char*, char* dout) {
+        normals_kernel<<<1, 32, 0, ctx->stream>>>(seed, stream, n, reinterpret_cast<double*>(dout));
+    });
+}
+
+int nmpcmc_gpu_libm(nmpcmc_gpu_ctx* ctx, int32_t fn, const double* x, int64_t n, double* out) {
+    if (ctx == nullptr || x == nullptr || out == nullptr || n < 1 || fn < 0 || fn > 3)
+        return NMPCMC_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    return scratch_roundtrip(ctx, x, n * sizeof(double), n * sizeof(double), out, [&](char* din, char* dout) {
+        libm_kernel<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(
+            fn, reinterpret_cast<double*>(din), n, reinterpret_cast<double*>(dout));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,112 @@
+// pi_kernel.cuh -- K2: PI closed loop, one thread per sample.
+//
+// Restates run_closed_loop's PI branch (montecarlo.cpp:80-157) with pi_step
+// (controllers.cpp:12-23), measure / simulate_interval (model.cpp:26-48) and
+// phi_metric (montecarlo.cpp:65-78; accumulated on the fly in the same index
+// order). The whole 720-step loop lives in registers; per-sample I/O is one
+// 24-byte record. Parallelism is across samples only: each sample is a serial
+// recursion in time.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace nmpcmc_dev {
+
+template <int NX>
+__device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar,
+                               nmpcmc_sim_record* rec, nmpcmc_work_counters* cnt, double* traj,
+                               int traj_rows) {
+    const Cstr p = sample_truth(sc, sim_index);
+    NormalStream rng;
+    rng.init(sc.base_seed, sim_index);
+    Plant<NX> pl;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) pl.x[i] = sc.x0[i];
+    const bool has_R = sc.has_noise_R != 0;
+    const double lR = has_R ? chol_semidef_1x1(sc.noise_R) : 0.0;
+    // run_closed_loop copies the gains and takes Ts/bounds from the scenario
+    // (montecarlo.cpp:97-100)
+    const double kP = sc.pi.kP, kI = sc.pi.kI, kaw = sc.pi.kaw, u_bar = sc.pi.u_bar;
+    const double Ts = sc.Ts, u_min = sc.u_min, u_max = sc.u_max;
+    double I_hat = sc.pi.I_hat;
+    const int stride = sc.record_stride < 1 ? 1 : sc.record_stride;
+    const bool record = traj != nullptr;
+
+    double t = sc.t0;
+    double z = pl.x[NX - 1] / p.V;        // output (model.cpp:50-52)
+    double zbar = setpoint_at(sc, t);
+    double acc = 0.0;
+    {
+        const double r = z - zbar;
+        acc += r * r;
+    }
+    int status = ST_OK;
+    int row = 0;
+    for (int i = 0; i < nbar; ++i) {
+        const double y = measure<NX>(p, pl, has_R, lR, rng);
+        // pi_step (controllers.cpp:12-23), evaluated in the documented order
+        const double ybar = setpoint_at(sc, t);
+        const double e = ybar - y;
+        const double P = kP * e;
+        const double I = I_hat + Ts * kI * e;
+        const double u_hat = u_bar + P + I;
+        const double u = smax(u_min, smin(u_max, u_hat));
+        const double I_aw = Ts * kaw * (u_hat - u);
+        I_hat = I + I_aw;
+        if (record && i % stride == 0) {
+            double* rw = traj + (size_t)row * 5;
+            rw[0] = t;
+            rw[1] = z;
+            rw[2] = zbar;
+            rw[3] = u;
+            rw[4] = y;
+            ++row;
+        }
+        status = simulate_interval<NX>(p, pl, t, t + sc.Ts, u, sc.Ns, rng);
+        if (status != ST_OK) break;
+        t = sc.t0 + (i + 1) * sc.Ts;
+        z = pl.x[NX - 1] / p.V;
+        zbar = setpoint_at(sc, t);
+        const double r = z - zbar;
+        acc += r * r;
+    }
+    if (status == ST_OK) {
+        rec->phi = acc / (double)(nbar + 1);
+        rec->failed = 0;
+        if (record) {
+            double* rw = traj + (size_t)row * 5;
+            rw[0] = t;
+            rw[1] = z;
+            rw[2] = zbar;
+            rw[3] = __longlong_as_double(0x7ff8000000000000LL);
+            rw[4] = __longlong_as_double(0x7ff8000000000000LL);
+        }
+    } else {
+        rec->phi = __longlong_as_double(0x7ff8000000000000LL);
+        rec->failed = 1;
+    }
+    rec->ocp_solves = 0;
+    rec->ocp_failures = 0;
+    rec->status = status;
+    if (cnt != nullptr) {
+        nmpcmc_work_counters c = {};
+        c.control_steps = nbar;
+        *cnt = c;
+    }
+    (void)traj_rows;
+}
+
+template <int NX>
+__global__ void __launch_bounds__(128) pi_kernel(const __grid_constant__ nmpcmc_scenario sc,
+                                                 uint64_t first_sim, int64_t n_sims, int nbar,
+                                                 nmpcmc_sim_record* records,
+                                                 nmpcmc_work_counters* counters, double* traj,
+                                                 int traj_rows) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_sims) return;
+    pi_closed_loop<NX>(sc, first_sim + (uint64_t)i, nbar, records + i,
+                       counters ? counters + i : nullptr,
+                       traj ? traj + (size_t)i * traj_rows * 5 : nullptr, traj_rows);
+}
+
+}  // namespace nmpcmc_dev

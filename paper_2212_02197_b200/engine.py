@@ -1,0 +1,287 @@
+"""Python host mirror of the reference's Monte Carlo driver API over the C ABI.
+
+Names and semantics follow /root/reference/proj/core/include/nmpcmc/montecarlo.hpp:
+  validate_scenario(sc)            montecarlo.hpp:59   -> N_bar, raises on bad config
+  run_closed_loop(sc, sim_index)   montecarlo.hpp:92   -> SimResult (+ trajectory)
+  run_monte_carlo(sc, n_sims, ...) montecarlo.hpp:121  -> McResult
+  aggregate_stats(sims)            montecarlo.hpp:108  -> McAggregate (dict)
+  phi_histogram(phi, bins=0)       montecarlo.hpp:141  -> Histogram
+Errors raise the reference's exception classes (errors.hpp:9-32). There is no
+CPU fallback: without the CUDA library or a GPU these calls raise.
+"""
+import ctypes as C
+import os
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import abi
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libnmpcmc_gpu.so")
+_lib = None
+
+
+class NmpcmcError(RuntimeError):
+    pass
+
+
+class DimensionMismatch(NmpcmcError, ValueError):
+    pass
+
+
+class NotPositiveDefinite(NmpcmcError):
+    pass
+
+
+class NonFiniteState(NmpcmcError):
+    pass
+
+
+class DomainError(NmpcmcError, ValueError):
+    pass
+
+
+class LengthMismatch(NmpcmcError, ValueError):
+    pass
+
+
+class Unsupported(NmpcmcError):
+    pass
+
+
+class CudaError(NmpcmcError):
+    pass
+
+
+_EXC = {1: DimensionMismatch, 2: NotPositiveDefinite, 3: NonFiniteState, 4: DomainError,
+        5: LengthMismatch, 6: Unsupported, 7: ValueError, 100: CudaError, 101: CudaError}
+
+
+def _raise(code: int, msg: str = ""):
+    if code != 0:
+        cls = _EXC.get(code, NmpcmcError)
+        raise cls(f"{abi.STATUS_NAMES.get(code, code)}: {msg}")
+
+
+def library():
+    """Load libnmpcmc_gpu.so (built by build.py / __graft_entry__.build()).
+
+    Fails loudly when the extension is missing -- there is no fallback.
+    """
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} not built: run `python -m paper_2212_02197_b200.build`")
+    lib = C.CDLL(_LIB_PATH)
+    abi.check_layout(lib)
+    S = C.POINTER(abi.Scenario)
+    R = C.POINTER(abi.SimRecord)
+    W = C.POINTER(abi.WorkCounters)
+    A = C.POINTER(abi.Aggregate)
+    P = C.c_void_p
+    lib.nmpcmc_gpu_abi_version.restype = C.c_int
+    lib.nmpcmc_gpu_validate.argtypes = [S, C.POINTER(C.c_int32)]
+    lib.nmpcmc_gpu_ctx_create.argtypes = [C.c_int, C.POINTER(P)]
+    lib.nmpcmc_gpu_ctx_destroy.argtypes = [P]
+    lib.nmpcmc_gpu_ctx_destroy.restype = None
+    lib.nmpcmc_gpu_last_error.argtypes = [P]
+    lib.nmpcmc_gpu_last_error.restype = C.c_char_p
+    lib.nmpcmc_gpu_set_stream.argtypes = [P, P]
+    lib.nmpcmc_gpu_run.argtypes = [P, S, C.c_uint64, C.c_int64, R, W, A]
+    lib.nmpcmc_gpu_run_device.argtypes = [P, S, C.c_uint64, C.c_int64, P, P]
+    lib.nmpcmc_gpu_traj_rows.argtypes = [S]
+    lib.nmpcmc_gpu_traj_rows.restype = C.c_int32
+    lib.nmpcmc_gpu_run_traj.argtypes = [P, S, C.c_uint64, C.c_int64, R, C.POINTER(C.c_double)]
+    lib.nmpcmc_gpu_aggregate.argtypes = [R, C.c_int64, A]
+    lib.nmpcmc_gpu_histogram.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int32,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    lib.nmpcmc_gpu_philox_blocks.argtypes = [P, C.POINTER(C.c_uint32), C.c_int64, C.POINTER(C.c_uint32)]
+    lib.nmpcmc_gpu_normals.argtypes = [P, C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(C.c_double)]
+    lib.nmpcmc_gpu_libm.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double)]
+    _lib = lib
+    return lib
+
+
+def validate_scenario(sc: abi.Scenario) -> int:
+    """validate_scenario (montecarlo.cpp:34-63): returns N_bar or raises."""
+    nbar = C.c_int32(0)
+    _raise(library().nmpcmc_gpu_validate(C.byref(sc), C.byref(nbar)), "scenario")
+    return nbar.value
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+class Context:
+    """One device + one CUDA stream (C ABI nmpcmc_gpu_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = library()
+        h = C.c_void_p()
+        _raise(self.lib.nmpcmc_gpu_ctx_create(device, C.byref(h)), f"device {device}")
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            self.lib.nmpcmc_gpu_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            _raise(rc, self.lib.nmpcmc_gpu_last_error(self.handle).decode())
+
+    def set_stream(self, stream_ptr: int):
+        self._check(self.lib.nmpcmc_gpu_set_stream(self.handle, C.c_void_p(stream_ptr)))
+
+    def run(self, sc, first_sim: int, n_sims: int, counters: bool = False):
+        """Records (numpy, index order) and optional work counters; host buffers."""
+        rec = np.zeros(n_sims, dtype=abi.RECORD_DTYPE)
+        cnt = np.zeros(n_sims, dtype=abi.COUNTERS_DTYPE) if counters else None
+        self._check(self.lib.nmpcmc_gpu_run(
+            self.handle, C.byref(sc), first_sim, n_sims, _ptr(rec, abi.SimRecord),
+            _ptr(cnt, abi.WorkCounters) if cnt is not None else None, None))
+        return rec, cnt
+
+    def run_device(self, sc, first_sim: int, n_sims: int, rec_ptr: int, cnt_ptr: int = 0):
+        """Enqueue on the context stream; outputs are device pointers."""
+        self._check(self.lib.nmpcmc_gpu_run_device(
+            self.handle, C.byref(sc), first_sim, n_sims, C.c_void_p(rec_ptr),
+            C.c_void_p(cnt_ptr) if cnt_ptr else None))
+
+    def run_traj(self, sc, first_sim: int, n_sims: int):
+        rows = self.lib.nmpcmc_gpu_traj_rows(C.byref(sc))
+        if rows < 0:
+            validate_scenario(sc)
+        rec = np.zeros(n_sims, dtype=abi.RECORD_DTYPE)
+        traj = np.zeros((n_sims, rows, 5))
+        self._check(self.lib.nmpcmc_gpu_run_traj(self.handle, C.byref(sc), first_sim, n_sims,
+                                                 _ptr(rec, abi.SimRecord), _ptr(traj, C.c_double)))
+        return rec, traj
+
+    # unit-level entry points
+    def philox_blocks(self, ctr_key: np.ndarray) -> np.ndarray:
+        ck = np.ascontiguousarray(ctr_key, dtype=np.uint32).reshape(-1, 6)
+        out = np.zeros((ck.shape[0], 4), dtype=np.uint32)
+        self._check(self.lib.nmpcmc_gpu_philox_blocks(self.handle, _ptr(ck, C.c_uint32), ck.shape[0],
+                                                      _ptr(out, C.c_uint32)))
+        return out
+
+    def normals(self, seed: int, stream: int, n: int) -> np.ndarray:
+        out = np.zeros(n)
+        self._check(self.lib.nmpcmc_gpu_normals(self.handle, seed, stream, n, _ptr(out, C.c_double)))
+        return out
+
+    def libm(self, fn: str, x: np.ndarray) -> np.ndarray:
+        code = {"exp": 0, "log": 1, "sin": 2, "cos": 3}[fn]
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.zeros_like(x)
+        self._check(self.lib.nmpcmc_gpu_libm(self.handle, code, _ptr(x, C.c_double), x.size,
+                                             _ptr(out, C.c_double)))
+        return out
+
+
+@dataclass
+class SimResult:
+    """SimResult (montecarlo.hpp:72-79)."""
+
+    sim_index: int
+    phi: float
+    failed: bool
+    ocp_solves: int
+    ocp_failures: int
+    status: int = 0
+    trajectory: Optional[np.ndarray] = None  # rows x (t, z, z_bar, u, y)
+
+
+@dataclass
+class McResult:
+    """McResult (montecarlo.hpp:112-116); records kept as a numpy array."""
+
+    records: np.ndarray
+    aggregate: dict
+    wall_seconds: float
+    counters: Optional[np.ndarray] = None
+    first_sim: int = 0
+
+    @property
+    def sims(self) -> List[SimResult]:
+        r = self.records
+        return [SimResult(self.first_sim + i, float(r["phi"][i]), bool(r["failed"][i]),
+                          int(r["ocp_solves"][i]), int(r["ocp_failures"][i]), int(r["status"][i]))
+                for i in range(len(r))]
+
+
+_ctx_cache = {}
+
+
+def _context(device: int) -> Context:
+    if device not in _ctx_cache:
+        _ctx_cache[device] = Context(device)
+    return _ctx_cache[device]
+
+
+def run_closed_loop(sc, sim_index: int, device: int = 0) -> SimResult:
+    """run_closed_loop (montecarlo.cpp:80-157); trajectory when sc.record_trajectories."""
+    ctx = _context(device)
+    if sc.record_trajectories:
+        rec, traj = ctx.run_traj(sc, sim_index, 1)
+        t = traj[0]
+        t = t[~np.isnan(t[:, 0])]
+    else:
+        rec, _ = ctx.run(sc, sim_index, 1)
+        t = None
+    r = rec[0]
+    return SimResult(sim_index, float(r["phi"]), bool(r["failed"]), int(r["ocp_solves"]),
+                     int(r["ocp_failures"]), int(r["status"]), t)
+
+
+def run_monte_carlo(sc, n_sims: int, device: int = 0, first_sim: int = 0,
+                    counters: bool = False) -> McResult:
+    """run_monte_carlo (montecarlo.cpp:213-251) on one GPU: samples
+    [first_sim, first_sim + n_sims) in index order, then aggregate_stats."""
+    if n_sims < 1:
+        raise DomainError("run_monte_carlo: n_sims must be at least 1")
+    validate_scenario(sc)
+    ctx = _context(device)
+    t0 = time.perf_counter()
+    rec, cnt = ctx.run(sc, first_sim, n_sims, counters=counters)
+    wall = time.perf_counter() - t0
+    return McResult(rec, aggregate_stats(rec), wall, cnt, first_sim)
+
+
+def aggregate_stats(records: np.ndarray) -> dict:
+    """aggregate_stats (montecarlo.cpp:172-211), index order."""
+    rec = np.ascontiguousarray(records, dtype=abi.RECORD_DTYPE)
+    out = abi.Aggregate()
+    _raise(library().nmpcmc_gpu_aggregate(_ptr(rec, abi.SimRecord), len(rec), C.byref(out)))
+    return abi.aggregate_to_dict(out)
+
+
+@dataclass
+class Histogram:
+    """Histogram (montecarlo.hpp:136-141)."""
+
+    edges: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    counts: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.int32))
+
+
+def phi_histogram(phi, bins: int = 0) -> Histogram:
+    """phi_histogram (montecarlo.cpp:268-304)."""
+    v = np.ascontiguousarray(phi, dtype=np.float64)
+    edges = np.zeros(201)
+    counts = np.zeros(200, dtype=np.int32)
+    nb = C.c_int32(0)
+    _raise(library().nmpcmc_gpu_histogram(_ptr(v, C.c_double), v.size, bins, _ptr(edges, C.c_double),
+                                          _ptr(counts, C.c_int32), C.byref(nb)))
+    return Histogram(edges[: nb.value + 1].copy(), counts[: nb.value].copy())

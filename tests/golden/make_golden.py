@@ -1,0 +1,93 @@
+"""Generate the committed golden fixtures from the UNMODIFIED reference.
+
+Runs only in the dev container (needs /root/reference to build oracle/_ref).
+Every fixture stores the scenario kwargs (configs.make_scenario) and the raw
+scenario bytes, the per-sample records of the reference's run_closed_loop /
+run_monte_carlo in both libm link variants ("xlibm" = exact-libm parity mode,
+"glibc" = reference as shipped), and a few full trajectories.
+
+  python tests/golden/make_golden.py [pi|nmpc|rng|all]
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle import lib as O  # noqa: E402
+from paper_2212_02197_b200 import configs  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def gen_case(name, kwargs, n_sims, n_traj, first=0, workers=None):
+    sc = configs.make_scenario(**kwargs)
+    data = {"kwargs": np.array(json.dumps(kwargs)), "scenario": np.frombuffer(bytes(sc), dtype=np.uint8),
+            "first": np.array(first)}
+    for libm in ("xlibm", "glibc"):
+        L = O.ref(libm)
+        t = time.time()
+        rec, wall = O.run_batch(L, sc, first, n_sims, workers)
+        print(f"{name} {libm}: {n_sims} sims in {wall:.2f}s (failed {rec['failed'].sum()})", flush=True)
+        data[f"rec_{libm}"] = rec
+    if n_traj:
+        sct = configs.make_scenario(**kwargs, record=True)
+        L = O.ref("xlibm")
+        nbar = int(round((sct.tf - sct.t0) / sct.Ts))
+        rows = nbar + 1
+        trajs = []
+        for i in range(n_traj):
+            _, tr = O.run_traj(L, sct, first + i, rows)
+            trajs.append(tr)
+        data["traj_xlibm"] = np.array(trajs)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **data)
+
+
+def gen_rng():
+    L = O.ref("xlibm")
+    G = O.ref("glibc")
+    import ctypes as C
+    streams = [(12345, 7), (42, 0), (0, 0), (2**64 - 1, 2**63 + 5)]
+    out = {}
+    for i, (seed, stream) in enumerate(streams):
+        for name, lib in (("xlibm", L), ("glibc", G)):
+            v = np.zeros(257)
+            lib.nmpcmc_ref_normals(C.c_uint64(seed), C.c_uint64(stream), 257, v.ctypes.data_as(C.POINTER(C.c_double)))
+            out[f"normals_{name}_{i}"] = v
+    out["streams"] = np.array(streams, dtype=np.uint64)
+    rs = np.random.default_rng(7)
+    ck = rs.integers(0, 2**32, size=(512, 6), dtype=np.uint64).astype(np.uint32)
+    blocks = np.zeros((512, 4), dtype=np.uint32)
+    for i in range(512):
+        L.nmpcmc_ref_philox_block(ck[i].ctypes.data_as(C.POINTER(C.c_uint32)),
+                                  blocks[i].ctypes.data_as(C.POINTER(C.c_uint32)))
+    out["philox_in"] = ck
+    out["philox_out"] = blocks
+    np.savez_compressed(os.path.join(OUT, "rng.npz"), **out)
+    print("rng done")
+
+
+def main(which):
+    if which in ("rng", "all"):
+        gen_rng()
+    if which in ("pi", "all"):
+        gen_case("pi_cfg0", dict(controller="pi"), 256, 4)
+        gen_case("pi_cfg1", dict(controller="pi", perturb=True), 256, 2)
+        gen_case("pi_onestate", dict(controller="pi", truth_variant=1), 64, 1)
+        # noise-free, R = 0 edge case (measure is exact, model.cpp:41-45)
+        gen_case("pi_quiet", dict(controller="pi", sigma_t=0.0, noise_R=0.0), 16, 1)
+    if which in ("nmpc", "all"):
+        # full-length BASELINE config 2 shape (N=60, max_iter=20)
+        gen_case("nmpc_cfg2", dict(controller="nmpc", N=60), 16, 2)
+        # shorter runs, more samples and horizons
+        gen_case("nmpc_n30_short", dict(controller="nmpc", N=30, n_steps=120), 64, 2)
+        gen_case("nmpc_n60_pert_short", dict(controller="nmpc", N=60, n_steps=120, perturb=True), 32, 1)
+        gen_case("nmpc_n120_short", dict(controller="nmpc", N=120, n_steps=60), 16, 1)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "all")
