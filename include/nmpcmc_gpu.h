@@ -200,6 +200,10 @@ int nmpcmc_gpu_normals(nmpcmc_gpu_ctx* ctx, uint64_t seed, uint64_t stream, int6
 /* fn: 0 exp, 1 log, 2 sin, 3 cos of x[n] with the device libm. */
 int nmpcmc_gpu_libm(nmpcmc_gpu_ctx* ctx, int32_t fn, const double* x, int64_t n, double* out);
 
+/* Measured FP64 throughput of the device (TFLOP/s): the roofline denominator
+ * for the FP64 closed-loop kernels (use_fma=1: DFMA, 2 flops each; 0: DADD). */
+int nmpcmc_gpu_fp64_peak(nmpcmc_gpu_ctx* ctx, int use_fma, double* tflops_out);
+
 #ifdef __cplusplus
 }
 #endif

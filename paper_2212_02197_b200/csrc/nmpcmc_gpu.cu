@@ -6,6 +6,7 @@
 // per sample), records land in index order exactly like McResult::sims.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -267,3 +268,59 @@ int nmpcmc_gpu_libm(nmpcmc_gpu_ctx* ctx, int32_t fn, const double* x, int64_t n,
 }
 
 }  // extern "C"
+
+// --------------------------------------------- FP64 peak (roofline denominator)
+// MEASURED_PEAKS.json carries HBM and bf16 only; the closed loop runs on the
+// FP64 CUDA cores, so its roofline denominator is measured here: independent
+// DFMA chains, grid = 8 x SMs x 256 threads, 2 flops per DFMA.
+namespace {
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, int use_fma) {
+    double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
+           a7 = a0 + 7;
+    const double b = 0.999999, c = 1e-7;
+    if (use_fma) {
+        for (int i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                a0 = __fma_rn(a0, b, c); a1 = __fma_rn(a1, b, c); a2 = __fma_rn(a2, b, c); a3 = __fma_rn(a3, b, c);
+                a4 = __fma_rn(a4, b, c); a5 = __fma_rn(a5, b, c); a6 = __fma_rn(a6, b, c); a7 = __fma_rn(a7, b, c);
+            }
+        }
+    } else {
+        for (int i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                a0 = __dadd_rn(a0, c); a1 = __dadd_rn(a1, c); a2 = __dadd_rn(a2, c); a3 = __dadd_rn(a3, c);
+                a4 = __dadd_rn(a4, c); a5 = __dadd_rn(a5, c); a6 = __dadd_rn(a6, c); a7 = __dadd_rn(a7, c);
+            }
+        }
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+}  // namespace
+
+extern "C" int nmpcmc_gpu_fp64_peak(nmpcmc_gpu_ctx* ctx, int use_fma, double* tflops_out) {
+    if (ctx == nullptr || tflops_out == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const int blocks = ctx->sm_count * 8, threads = 256, iters = 4096;
+    int rc = ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap, (size_t)blocks * threads * sizeof(double));
+    if (rc != NMPCMC_OK) return rc;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double best = 0.0;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(e0, ctx->stream);
+        fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(static_cast<double*>(ctx->d_scratch), iters, use_fma);
+        cudaEventRecord(e1, ctx->stream);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double ops = (double)blocks * threads * iters * 64.0 * (use_fma ? 2.0 : 1.0);
+        if (rep > 0) best = std::max(best, ops / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *tflops_out = best;
+    return cuda_check(ctx, cudaGetLastError(), "fp64 peak");
+}

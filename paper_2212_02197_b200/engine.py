@@ -101,6 +101,7 @@ def library():
     lib.nmpcmc_gpu_philox_blocks.argtypes = [P, C.POINTER(C.c_uint32), C.c_int64, C.POINTER(C.c_uint32)]
     lib.nmpcmc_gpu_normals.argtypes = [P, C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(C.c_double)]
     lib.nmpcmc_gpu_libm.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double)]
+    lib.nmpcmc_gpu_fp64_peak.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
     _lib = lib
     return lib
 
@@ -181,6 +182,12 @@ class Context:
         out = np.zeros(n)
         self._check(self.lib.nmpcmc_gpu_normals(self.handle, seed, stream, n, _ptr(out, C.c_double)))
         return out
+
+    def fp64_peak(self, use_fma: bool = True) -> float:
+        """Measured FP64 TFLOP/s of this device (roofline denominator)."""
+        out = C.c_double(0.0)
+        self._check(self.lib.nmpcmc_gpu_fp64_peak(self.handle, 1 if use_fma else 0, C.byref(out)))
+        return out.value
 
     def libm(self, fn: str, x: np.ndarray) -> np.ndarray:
         code = {"exp": 0, "log": 1, "sin": 2, "cos": 3}[fn]

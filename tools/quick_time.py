@@ -15,7 +15,7 @@ def main():
     cnt = torch.empty(n * 64, dtype=torch.uint8, device="cuda")
     s = torch.cuda.Stream()
     ctx.set_stream(s.cuda_stream)
-    for it in range(4):
+    for it in range(int(os.environ.get("ITERS", "4"))):
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(s)
