@@ -14,17 +14,22 @@
 // the shared portable libm the per-sample results are bitwise those of the
 // reference's exact-libm build (tests/test_gpu_nmpc.py).
 //
-// Execution model:
-//  * one warp = one sample; the whole per-sample workspace (~51 arrays of
-//    N+1 doubles: the iterate, multipliers, defect jacobians, BFGS blocks and
-//    the Riccati IPM state) lives in shared memory, so the inner loops never
-//    touch HBM;
+// Execution model (K3):
+//  * one warp = one block = one sample; the per-sample workspace (44 arrays of
+//    ST doubles, ST = compile-time stride >= N+1) lives in shared memory, so
+//    the inner loops never touch HBM, and every access is [base + imm];
 //  * stage-parallel work (the N independent shooting intervals, residuals,
 //    expand / step-length / update loops, BFGS blocks) is spread over the 32
 //    lanes, k = lane, lane+32, ...;
-//  * the inherently serial recursions (Riccati sweeps, ordered reductions,
-//    xi_from_inputs, EKF, plant) are executed redundantly by all 32 lanes in
-//    lockstep -- SIMT issues them once, no divergence, no broadcasts;
+//  * the serial recursions (Riccati sweeps, ordered reductions,
+//    xi_from_inputs, EKF, plant) run redundantly on all 32 lanes in lockstep;
+//  * the Riccati sweeps -- the latency-critical chain -- use a certified fast
+//    square root and division (Markstein correction from the hardware
+//    reciprocal-sqrt seed; an exact fma residual certifies that each result is
+//    the IEEE correctly rounded one). A sweep whose certificate fails anywhere
+//    is replayed with IEEE sqrt/division, so results are always bitwise IEEE;
+//  * phases are __noinline__ functions with one call site each, which keeps
+//    the kernel small enough for the instruction cache;
 //  * exceptions become per-sample status codes with the reference's catch
 //    scopes.
 #pragma once
@@ -66,7 +71,60 @@ __device__ __forceinline__ int warp_min_int(int v) {
     for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULLMASK, v, o));
     return v;
 }
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    return v;
+}
 __device__ __forceinline__ bool warp_any(bool p) { return __any_sync(FULLMASK, p); }
+
+// ------------------------------------------- certified fast sqrt / division
+__device__ __forceinline__ int expo(double x) { return (int)((__double_as_longlong(x) >> 52) & 0x7ff); }
+/// ulp(x)/2 for normal x (biased exponent field E >= 54): 2^(E-1023-53).
+__device__ __forceinline__ double half_ulp(double x) {
+    return __longlong_as_double((__double_as_longlong(x) & 0x7ff0000000000000LL) - (53LL << 52));
+}
+__device__ __forceinline__ bool mant_zero(double x) {
+    return (__double_as_longlong(x) & 0x000fffffffffffffLL) == 0;
+}
+/// exponent window in which every residual below is exact and nothing
+/// under/overflows: |x| in [2^-800, 2^800)
+__device__ __forceinline__ bool in_window(double x) {
+    const int e = expo(x);
+    return e >= 1023 - 800 && e < 1023 + 800;
+}
+
+/// l = sqrt(h) and y ~ 1/l for h > 0 (Newton on the rsqrt seed, Markstein
+/// correction). Returns true only if l is certified to be RN(sqrt(h)): the
+/// exact residual h - l^2 lies strictly inside (-l ulp(l), l ulp(l)) shrunk
+/// by 2^-50, l is not a power of two, and everything is inside the window.
+__device__ __forceinline__ bool fast_sqrt(double h, double& l, double& y) {
+    double y0;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(h));
+    const double hh = 0.5 * h;
+    double e = __fma_rn(-hh, y0 * y0, 0.5);
+    y0 = __fma_rn(y0, e, y0);
+    e = __fma_rn(-hh, y0 * y0, 0.5);
+    y0 = __fma_rn(y0, e, y0);
+    const double s = h * y0;
+    const double d = __fma_rn(-s, s, h);
+    l = __fma_rn(d, 0.5 * y0, s);
+    y = y0;
+    const double r = __fma_rn(-l, l, h);
+    const double bound = l * (2.0 * half_ulp(l)) * (1.0 - 0x1.0p-50);
+    return in_window(h) && in_window(l) && !mant_zero(l) && fabs(r) < bound;
+}
+
+/// q = a / b with y ~ 1/b (b > 0): Markstein correction, certified by the
+/// exact residual a - b q lying strictly inside b ulp(q) / 2 (shrunk).
+__device__ __forceinline__ bool fast_div(double a, double b, double y, double& q) {
+    const double q0 = a * y;
+    const double e0 = __fma_rn(-b, q0, a);
+    q = __fma_rn(e0, y, q0);
+    const double e = __fma_rn(-b, q, a);
+    const double bound = b * half_ulp(q) * (1.0 - 0x1.0p-50);
+    return in_window(a) && in_window(b) && in_window(q) && !mant_zero(q) && fabs(e) < bound;
+}
 
 // ------------------------------------------------------- one-state model
 /// One stage evaluation of the controller model: drift (cstr.cpp:42-53),
@@ -159,68 +217,29 @@ __device__ __forceinline__ int joint_rhs1(const Cstr& p, double x, double P, dou
 }
 
 // ----------------------------------------------------------- workspace
-/// Per-sample shared-memory workspace: kWsArrays arrays of `s` doubles at
-/// smem_nmpc + id * s (one warp = one block = one sample). Stage arrays are
-/// indexed by k; for the interleaved decision vector
-/// xi = (u_0, x_1, ..., u_{N-1}, x_N) (ocp.hpp:37-43) U[k] = u_k and X[k] = x_{k+1}.
-/// Index-based access keeps every address in the shared window (LDS/STS).
+/// Per-sample shared-memory workspace: kWsArrays arrays of ST doubles at
+/// smem_nmpc + id * ST. Stage arrays are indexed by k; for the interleaved
+/// decision vector xi = (u_0, x_1, ..., u_{N-1}, x_N) (ocp.hpp:37-43)
+/// U[k] = u_k and X[k] = x_{k+1}. W blocks: Wr[0] = block 0 (u_0),
+/// (Wq, Wm, Wr)[k] = block k = [x_k, u_k] (k = 1..N-1), Wq[N] = block N.
 extern __shared__ __align__(16) double smem_nmpc[];
-constexpr int kWsArrays = 51;
 
-struct Ws {
-    int s;
-    __device__ __forceinline__ double* U(int b) const { return smem_nmpc + (2 * b) * s; }
-    __device__ __forceinline__ double* X(int b) const { return smem_nmpc + (2 * b + 1) * s; }
-    __device__ __forceinline__ double* lam() const { return smem_nmpc + 4 * s; }
-    __device__ __forceinline__ double* pil() const { return smem_nmpc + 5 * s; }
-    __device__ __forceinline__ double* piu() const { return smem_nmpc + 6 * s; }
-    __device__ __forceinline__ double* gX() const { return smem_nmpc + 7 * s; }
-    __device__ __forceinline__ double* g() const { return smem_nmpc + 8 * s; }
-    __device__ __forceinline__ double* Jx() const { return smem_nmpc + 9 * s; }
-    __device__ __forceinline__ double* Ju() const { return smem_nmpc + 10 * s; }
-    __device__ __forceinline__ double* tgX() const { return smem_nmpc + 11 * s; }
-    __device__ __forceinline__ double* tg() const { return smem_nmpc + 12 * s; }
-    __device__ __forceinline__ double* tJx() const { return smem_nmpc + 13 * s; }
-    __device__ __forceinline__ double* tJu() const { return smem_nmpc + 14 * s; }
-    __device__ __forceinline__ double* Wq() const { return smem_nmpc + 15 * s; }
-    __device__ __forceinline__ double* Wm() const { return smem_nmpc + 16 * s; }
-    __device__ __forceinline__ double* Wr() const { return smem_nmpc + 17 * s; }
-    __device__ __forceinline__ double* sig() const { return smem_nmpc + 18 * s; }
-    __device__ __forceinline__ double* sp() const { return smem_nmpc + 19 * s; }
-    __device__ __forceinline__ double* dU() const { return smem_nmpc + 20 * s; }
-    __device__ __forceinline__ double* dX() const { return smem_nmpc + 21 * s; }
-    __device__ __forceinline__ double* mu() const { return smem_nmpc + 22 * s; }
-    __device__ __forceinline__ double* nl() const { return smem_nmpc + 23 * s; }
-    __device__ __forceinline__ double* nu() const { return smem_nmpc + 24 * s; }
-    __device__ __forceinline__ double* sl() const { return smem_nmpc + 25 * s; }
-    __device__ __forceinline__ double* su() const { return smem_nmpc + 26 * s; }
-    __device__ __forceinline__ double* rsu() const { return smem_nmpc + 27 * s; }
-    __device__ __forceinline__ double* rsx() const { return smem_nmpc + 28 * s; }
-    __device__ __forceinline__ double* rdyn() const { return smem_nmpc + 29 * s; }
-    __device__ __forceinline__ double* rl() const { return smem_nmpc + 30 * s; }
-    __device__ __forceinline__ double* ru() const { return smem_nmpc + 31 * s; }
-    __device__ __forceinline__ double* rcl() const { return smem_nmpc + 32 * s; }
-    __device__ __forceinline__ double* rcu() const { return smem_nmpc + 33 * s; }
-    __device__ __forceinline__ double* dsl() const { return smem_nmpc + 34 * s; }
-    __device__ __forceinline__ double* dsu() const { return smem_nmpc + 35 * s; }
-    __device__ __forceinline__ double* dnl() const { return smem_nmpc + 36 * s; }
-    __device__ __forceinline__ double* dnu() const { return smem_nmpc + 37 * s; }
-    __device__ __forceinline__ double* ddU() const { return smem_nmpc + 38 * s; }
-    __device__ __forceinline__ double* ddX() const { return smem_nmpc + 39 * s; }
-    __device__ __forceinline__ double* ddmu() const { return smem_nmpc + 40 * s; }
-    __device__ __forceinline__ double* cholh() const { return smem_nmpc + 41 * s; }
-    __device__ __forceinline__ double* gain() const { return smem_nmpc + 42 * s; }
-    __device__ __forceinline__ double* gmat() const { return smem_nmpc + 43 * s; }
-    __device__ __forceinline__ double* val() const { return smem_nmpc + 44 * s; }
-    __device__ __forceinline__ double* pvec() const { return smem_nmpc + 45 * s; }
-    __device__ __forceinline__ double* dff() const { return smem_nmpc + 46 * s; }
-    __device__ __forceinline__ double* rhat() const { return smem_nmpc + 47 * s; }
-    __device__ __forceinline__ double* bar() const { return smem_nmpc + 48 * s; }
-    __device__ __forceinline__ double* tmp() const { return smem_nmpc + 49 * s; }
+enum ArrayId {
+    A_U, A_X, A_LAM, A_PIL, A_PIU,
+    A_GX, A_G, A_JX, A_JU, A_TGX, A_TG, A_TJX, A_TJU,
+    A_WQ, A_WM, A_WR, A_SIG, A_SP,
+    A_DU, A_DX, A_MU, A_NL, A_NU, A_SL, A_SU,
+    A_RSU, A_RSX, A_RDYN, A_RCL, A_RCU,
+    A_DDU, A_DDX, A_DDMU,
+    A_CHOLH, A_RINV, A_GAIN, A_GMAT, A_VAL, A_PVEC, A_DFF, A_RHAT, A_BAR,
+    A_TMP,  // two strides
+    kWsArrays = A_TMP + 2
 };
 
-__host__ __device__ inline int ws_stride(int N) { return ((N + 1) + 3) & ~3; }
-__host__ __device__ inline size_t ws_bytes(int N) { return (size_t)kWsArrays * ws_stride(N) * sizeof(double); }
+#define SA(id) (smem_nmpc + (id) * ST)
+
+__host__ __device__ inline int ws_stride_for(int N) { return N < 32 ? 32 : N < 64 ? 64 : (N < 128 ? 128 : 256); }
+__host__ __device__ inline size_t ws_bytes_for(int ST) { return (size_t)kWsArrays * ST * sizeof(double); }
 
 /// Scalars of one NMPC problem instance (NlpInstance, ocp.hpp:25-34).
 struct Ocp {
@@ -240,29 +259,42 @@ struct Cnt {
 };
 
 // ------------------------------------------------------------ OCP evals
-/// eval_objective (ocp.cpp:76-99): phi in k order; gradient only on x slots.
-/// X holds x_{k+1} at index k; writes gX[k] = d phi / d x_{k+1}.
-__device__ __forceinline__ double eval_objective(const Ocp& o, const Ws& w, const double* X, double* gX, int lane) {
+/// eval_objective (ocp.cpp:76-99) at x = SA(xid): phi in k order; gradient
+/// only on x slots, written to SA(gid)[k] = d phi / d x_{k+1}.
+template <int ST>
+__device__ __noinline__ double eval_objective(const Ocp& o, int xid, int gid) {
+    const int lane = threadIdx.x & 31;
+    const double* X = SA(xid);
+    double* gX = SA(gid);
+    double* tmp = SA(A_TMP);
+    const double* sp = SA(A_SP);
     const double ts = o.Ts;
     for (int k = lane; k < o.N; k += 32) {
-        const double res = X[k] / o.p.V - w.sp()[k];  // output(x) - zbar
+        const double res = X[k] / o.p.V - sp[k];  // output(x) - zbar
         const double qres = epi0(dot1(o.Qz, res));
-        w.tmp()[k] = ts * dot1(res, qres);
+        tmp[k] = ts * dot1(res, qres);
         const double gx = epi0(dot1(o.inv_V, qres));
         gX[k] = 0.0 + 2.0 * ts * gx;
     }
     __syncwarp();
     double phi = 0.0;
-    for (int k = 0; k < o.N; ++k) phi += w.tmp()[k];
+    for (int k = 0; k < o.N; ++k) phi += tmp[k];
     __syncwarp();
     return phi;
 }
 
-/// eval_constraints (ocp.cpp:101-135) + status of the first failing stage in
-/// k order (the reference throws at the first failing shoot). Writes
-/// g[k] = x_{k+1} - F_k, Jx[k], Ju[k]. Returns 0 or ST_*.
-__device__ __forceinline__ int eval_constraints(const Ocp& o, const double* U, const double* X, double* g, double* Jx,
-                                double* Ju, int lane, Cnt& cnt) {
+/// eval_constraints (ocp.cpp:101-135) at (SA(uid), SA(xid)) into the block
+/// (g, Jx, Ju) at array ids (gid, gid+1, gid+2), plus the status of the first
+/// failing stage in k order (the reference throws at the first failing
+/// shoot). g[k] = x_{k+1} - F_k.
+template <int ST>
+__device__ __noinline__ int eval_constraints(const Ocp& o, int uid, int xid, int gid, Cnt* cnt) {
+    const int lane = threadIdx.x & 31;
+    const double* U = SA(uid);
+    const double* X = SA(xid);
+    double* g = SA(gid);
+    double* Jx = SA(gid + 1);
+    double* Ju = SA(gid + 2);
     int first_bad = 0x7fffffff;
     for (int k = lane; k < o.N; k += 32) {
         const double xk = (k == 0) ? o.x0 : X[k - 1];
@@ -276,29 +308,31 @@ __device__ __forceinline__ int eval_constraints(const Ocp& o, const double* U, c
             Ju[k] = Su;
         }
     }
-    cnt.shoot_full += o.N;
+    cnt->shoot_full += o.N;
     first_bad = warp_min_int(first_bad);
     __syncwarp();
     return first_bad == 0x7fffffff ? ST_OK : (first_bad & 15);
 }
 
-/// xi_from_inputs (ocp.cpp:137-154): forward shooting from x0 with the
-/// inputs already in U; serial in k, executed by all lanes.
-__device__ __forceinline__ int xi_from_inputs(const Ocp& o, const double* U, double* X, Cnt& cnt) {
+/// xi_from_inputs (ocp.cpp:137-154): forward shooting from x0 with the inputs
+/// in SA(uid), states into SA(xid); serial in k, all lanes.
+template <int ST>
+__device__ __noinline__ int xi_from_inputs(const Ocp& o, int uid, int xid, Cnt* cnt) {
+    const double* U = SA(uid);
+    double* X = SA(xid);
     double xk = o.x0;
-    for (int k = 0; k < o.N; ++k) {
+    int st = ST_OK;
+    int k = 0;
+    for (; k < o.N; ++k) {
         double F, Sx, Su;
-        const int st = shoot1<false>(o.p, xk, U[k], o.h, o.Nc, F, Sx, Su);
-        cnt.shoot_fonly += 1;
-        if (st) {
-            __syncwarp();
-            return st;
-        }
+        st = shoot1<false>(o.p, xk, U[k], o.h, o.Nc, F, Sx, Su);
+        if (st) break;
         X[k] = F;
         xk = F;
     }
+    cnt->shoot_fonly += (k < o.N) ? k + 1 : o.N;
     __syncwarp();
-    return ST_OK;
+    return st;
 }
 
 // ------------------------------------------------------------------- QP
@@ -306,20 +340,219 @@ __device__ __forceinline__ int xi_from_inputs(const Ocp& o, const double* U, dou
 /// antisymmetric, and an exact-zero defect is +0 either way.
 __device__ __forceinline__ double bneg(double g) { return g == 0.0 ? 0.0 : -g; }
 
-/// solve_qp (qp.cpp:173-423) for the stagewise box QP built by
-/// build_stages (sqp.cpp:130-171) from W, grad f and the defect blocks:
-///   stage k: R = Wr[k], Q = Wq[k], M = Wm[k] (k >= 1), q = gX[k-1], r = 0,
-///            Jx = Jx[k], Ju = Ju[k], b = F_k - x_{k+1} = -g[k],
-///            lb = umin - u_k, ub = umax - u_k;  terminal Q = Wq[N], q = gX[N-1].
-/// Result in dU/dX (step), mu, nl/nu (bound multipliers). Returns the QP
-/// status (0 Optimal, 1 MaxIter, 2 Failed) or ST_DOMAIN as -1 (lb > ub).
 enum { QP_OPTIMAL = 0, QP_MAXITER = 1, QP_FAILED = 2, QP_DOMAIN = -1 };
 
-__device__ __forceinline__ int solve_qp(const Ocp& o, const Ws& w, const double* U, const double* cgX,
-                                        const double* cg, const double* cJx, const double* cJu, double tol,
-                                        int max_iter, int lane, Cnt& cnt, int* iters_out) {
+/// riccati_factor (qp.cpp:73-110) fused with the affine backward vector sweep
+/// of riccati_solve_vectors (qp.cpp:122-141). Serial in k, all lanes.
+/// Returns true on NotPositiveDefinite. FAST: certified sqrt/division; *ok_out
+/// is false if any certificate failed (the caller then replays FAST = false).
+template <int ST, bool FAST>
+__device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
+    const double* Ju = SA(A_JU);
+    const double* Jx = SA(A_JX);
+    const double* Wq = SA(A_WQ);
+    const double* Wm = SA(A_WM);
+    const double* Wr = SA(A_WR);
+    const double* bar = SA(A_BAR);
+    const double* rdyn = SA(A_RDYN);
+    const double* rhat = SA(A_RHAT);
+    const double* rsx = SA(A_RSX);
+    double* cholh = SA(A_CHOLH);
+    double* rinv = SA(A_RINV);
+    double* val = SA(A_VAL);
+    double* gain = SA(A_GAIN);
+    double* gmat = SA(A_GMAT);
+    double* pvec = SA(A_PVEC);
+    double* dff = SA(A_DFF);
+    bool ok = true;
+    double P = Wq[N];
+    double pv = rsx[N - 1];  // pvec[N] = qhat[N]
+    val[N] = P;
+    pvec[N] = pv;
+    for (int k = N - 1; k >= 0; --k) {
+        const double ju = Ju[k];
+        const double pju = epi0(dot1(P, ju));
+        double hh = epi0(dot1(ju, pju));
+        hh = hh + Wr[k];
+        hh = hh + bar[k];
+        if (hh <= 0.0 || !dfinite(hh)) {  // cholesky_factor -> QP Failed (qp.cpp:358-364)
+            *ok_out = ok;
+            return true;
+        }
+        double l, y;
+        if (FAST) {
+            ok &= fast_sqrt(hh, l, y);
+        } else {
+            l = sqrt(hh);
+            y = 1.0 / l;  // seed for the corrector sweep's fast division
+        }
+        cholh[k] = l;
+        rinv[k] = y;
+        // vector part at stage k
+        const double tmpv = epi1(dot1(P, -rdyn[k]), pv);
+        double hv = epi1(dot1(ju, tmpv), rhat[k]);
+        if (FAST) {
+            ok &= fast_div(hv, l, y, hv);
+            ok &= fast_div(hv, l, y, hv);
+        } else {
+            hv = hv / l;
+            hv = hv / l;
+        }
+        hv = -hv;
+        dff[k] = hv;
+        if (k >= 1) {
+            const double jx = Jx[k];
+            const double pjx = epi0(dot1(P, jx));
+            double gg = epi0(dot1(ju, pjx));
+            gg = gg + Wm[k];
+            double gn;
+            if (FAST) {
+                ok &= fast_div(gg, l, y, gn);
+                ok &= fast_div(gn, l, y, gn);
+            } else {
+                gn = gg / l;
+                gn = gn / l;
+            }
+            const double gk = -gn;
+            double pn = epi0(dot1(jx, pjx));
+            pn = pn + Wq[k];
+            pn = epi1(dot1(gg, gk), pn);
+            val[k] = pn;
+            gain[k] = gk;
+            gmat[k] = gg;
+            double pvn = epi1(dot1(jx, tmpv), rsx[k - 1]);
+            pvn = epi1(dot1(gg, hv), pvn);
+            pvec[k] = pvn;
+            P = pn;
+            pv = pvn;
+        }
+    }
+    *ok_out = ok;
+    return false;
+}
+
+/// Corrector backward vector sweep with the cached factor (qp.cpp:122-141).
+/// Returns false if a FAST certificate failed (caller replays FAST = false).
+template <int ST, bool FAST>
+__device__ __noinline__ bool vector_sweep(int N) {
+    const double* Ju = SA(A_JU);
+    const double* Jx = SA(A_JX);
+    const double* rdyn = SA(A_RDYN);
+    const double* rhat = SA(A_RHAT);
+    const double* rsx = SA(A_RSX);
+    const double* cholh = SA(A_CHOLH);
+    const double* rinv = SA(A_RINV);
+    const double* val = SA(A_VAL);
+    const double* gmat = SA(A_GMAT);
+    double* pvec = SA(A_PVEC);
+    double* dff = SA(A_DFF);
+    bool ok = true;
+    double pv = rsx[N - 1];
+    pvec[N] = pv;
+    for (int k = N - 1; k >= 0; --k) {
+        const double l = cholh[k];
+        const double tmpv = epi1(dot1(val[k + 1], -rdyn[k]), pv);
+        double hv = epi1(dot1(Ju[k], tmpv), rhat[k]);
+        if (FAST) {
+            const double y = rinv[k];
+            ok &= fast_div(hv, l, y, hv);
+            ok &= fast_div(hv, l, y, hv);
+        } else {
+            hv = hv / l;
+            hv = hv / l;
+        }
+        hv = -hv;
+        dff[k] = hv;
+        if (k >= 1) {
+            double pvn = epi1(dot1(Jx[k], tmpv), rsx[k - 1]);
+            pvn = epi1(dot1(gmat[k], hv), pvn);
+            pvec[k] = pvn;
+            pv = pvn;
+        }
+    }
+    return ok;
+}
+
+/// Forward rollout (qp.cpp:142-155): step dxi (DDU, DDX) and dmu (DDMU).
+template <int ST>
+__device__ __noinline__ void rollout(int N) {
+    const double* Ju = SA(A_JU);
+    const double* Jx = SA(A_JX);
+    const double* rdyn = SA(A_RDYN);
+    const double* val = SA(A_VAL);
+    const double* pvec = SA(A_PVEC);
+    const double* gain = SA(A_GAIN);
+    const double* dff = SA(A_DFF);
+    double* ddU = SA(A_DDU);
+    double* ddX = SA(A_DDX);
+    double* ddmu = SA(A_DDMU);
+    double dx = 0.0;
+    for (int k = 0; k < N; ++k) {
+        double du = dff[k];
+        if (k >= 1) du = epi1(dot1(gain[k], dx), du);
+        ddU[k] = du;
+        double dxn = -rdyn[k];
+        if (k >= 1) dxn = epi1(dot1(Jx[k], dx), dxn);
+        dxn = epi1(dot1(Ju[k], du), dxn);
+        dx = dxn;
+        ddX[k] = dx;
+        const double mm = epi1(dot1(val[k + 1], dx), pvec[k + 1]);
+        ddmu[k] = -mm;
+    }
+    __syncwarp();
+}
+
+/// expand (qp.cpp:308-317) of stage k from the step in DDU, given rl/ru.
+struct Dir {
+    double dsl, dsu, dnl, dnu;
+};
+template <int ST>
+__device__ __forceinline__ Dir expand_k(int k, bool fl, bool fu, double rl, double ru) {
+    const double dv = SA(A_DDU)[k];
+    Dir d;
+    d.dsl = fl ? dv + rl : 0.0;
+    d.dsu = fu ? ru - dv : 0.0;
+    d.dnl = fl ? (SA(A_RCL)[k] - SA(A_NL)[k] * d.dsl) / SA(A_SL)[k] : 0.0;
+    d.dnu = fu ? (SA(A_RCU)[k] - SA(A_NU)[k] * d.dsu) / SA(A_SU)[k] : 0.0;
+    return d;
+}
+
+/// solve_qp (qp.cpp:173-423) for the stagewise box QP that build_stages
+/// (sqp.cpp:130-171) forms from W, grad f and the defect blocks of the
+/// current iterate:  stage k: R = Wr[k], Q = Wq[k], M = Wm[k] (k >= 1),
+/// q = gX[k-1], r = 0, Jx, Ju, b = -g[k], lb = umin - u_k, ub = umax - u_k;
+/// terminal Q = Wq[N], q = gX[N-1].  Result: step in DU/DX, multipliers MU, NL, NU.
+template <int ST>
+__device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt* cnt) {
+    const int lane = threadIdx.x & 31;
     const int N = o.N;
     const double tau = 0.995;
+    const double* U = SA(A_U);
+    const double* gX = SA(A_GX);
+    const double* g = SA(A_G);
+    const double* Jx = SA(A_JX);
+    const double* Ju = SA(A_JU);
+    const double* Wq = SA(A_WQ);
+    const double* Wm = SA(A_WM);
+    const double* Wr = SA(A_WR);
+    double* dU = SA(A_DU);
+    double* dX = SA(A_DX);
+    double* mu = SA(A_MU);
+    double* nl = SA(A_NL);
+    double* nu = SA(A_NU);
+    double* sl = SA(A_SL);
+    double* su = SA(A_SU);
+    double* rsu = SA(A_RSU);
+    double* rsx = SA(A_RSX);
+    double* rdyn = SA(A_RDYN);
+    double* rcl = SA(A_RCL);
+    double* rcu = SA(A_RCU);
+    double* rhat = SA(A_RHAT);
+    double* bar = SA(A_BAR);
+    double* tmp = SA(A_TMP);
+    const double* ddU = SA(A_DDU);
+    const double* ddX = SA(A_DDX);
+    const double* ddmu = SA(A_DDMU);
     // data_scale / bounds / init (qp.cpp:183-226)
     double ds = 1.0;
     int nfin = 0;
@@ -337,73 +570,73 @@ __device__ __forceinline__ int solve_qp(const Ocp& o, const Ws& w, const double*
             ++nfin;
             ds = smax(ds, fabs(ub));
         }
-        ds = smax(ds, fold_absmax(0.0, 0.0));        // inf_norm(r_k), r = 0
-        ds = smax(ds, fold_absmax(0.0, bneg(cg[k])));  // inf_norm(b_k)
-        ds = smax(ds, fold_absmax(0.0, cgX[k]));     // inf_norm(q_{k+1})
-        w.dU()[k] = 0.0;
-        w.dX()[k] = 0.0;
-        w.mu()[k] = 0.0;
-        w.sl()[k] = fl ? smax(1.0, fabs(lb)) : 0.0;
-        w.nl()[k] = fl ? 1.0 : 0.0;
-        w.su()[k] = fu ? smax(1.0, fabs(ub)) : 0.0;
-        w.nu()[k] = fu ? 1.0 : 0.0;
-        w.rcl()[k] = 0.0;
-        w.rcu()[k] = 0.0;
+        ds = smax(ds, fold_absmax(0.0, bneg(g[k])));  // inf_norm(b_k); inf_norm(r_k) = 0
+        ds = smax(ds, fold_absmax(0.0, gX[k]));       // inf_norm(q_{k+1})
+        dU[k] = 0.0;
+        dX[k] = 0.0;
+        mu[k] = 0.0;
+        sl[k] = fl ? smax(1.0, fabs(lb)) : 0.0;
+        nl[k] = fl ? 1.0 : 0.0;
+        su[k] = fu ? smax(1.0, fabs(ub)) : 0.0;
+        nu[k] = fu ? 1.0 : 0.0;
+        rcl[k] = 0.0;
+        rcu[k] = 0.0;
     }
     if (warp_any(bad)) return QP_DOMAIN;
     ds = warp_max(ds);
-#pragma unroll
-    for (int o2 = 16; o2 > 0; o2 >>= 1) nfin += __shfl_xor_sync(FULLMASK, nfin, o2);
-    const int m = nfin;
+    const int m = warp_sum_int(nfin);
     const double eps = tol * ds;
     __syncwarp();
 
+    // rl, ru of stage k at the current iterate (qp.cpp:278-283)
+    auto rlru = [&](int k, bool fl, bool fu, double& rl, double& ru) {
+        const double v = dU[k];
+        rl = fl ? v - sl[k] - (o.umin - U[k]) : 0.0;
+        ru = fu ? (o.umax - U[k]) - v - su[k] : 0.0;
+    };
+
     int status = QP_MAXITER;
-    int iter = 0;
-    for (;; ++iter) {
+    for (int iter = 0;; ++iter) {
         // residuals() (qp.cpp:237-284)
         double ninf = 0.0, dinf = 0.0, linf = 0.0, uinf = 0.0;
         for (int k = lane; k < N; k += 32) {
-            const double R = w.Wr()[k], Ju = cJu[k];
-            const double vk = w.dU()[k], muk = w.mu()[k];
-            double r = epi1(dot1(R, vk), 0.0);
-            if (k >= 1) r = epi1(dot1(w.Wm()[k], w.dX()[k - 1]), r);
-            r = epim1(dot1(Ju, muk), r);
-            r += w.nu()[k] - w.nl()[k];
-            w.rsu()[k] = r;
-            double rd = w.dX()[k] + -1.0 * bneg(cg[k]);
-            if (k >= 1) rd = epim1(dot1(cJx[k], w.dX()[k - 1]), rd);
-            rd = epim1(dot1(Ju, vk), rd);
-            w.rdyn()[k] = rd;
-            // x row of stage k+1 (k+1 = 1..N)
-            const int kk = k + 1;
-            double rx = epi1(dot1(w.Wq()[kk], w.dX()[k]), cgX[k]);
+            const double ju = Ju[k];
+            const double vk = dU[k], muk = mu[k];
+            double r = epi1(dot1(Wr[k], vk), 0.0);
+            if (k >= 1) r = epi1(dot1(Wm[k], dX[k - 1]), r);
+            r = epim1(dot1(ju, muk), r);
+            r += nu[k] - nl[k];
+            rsu[k] = r;
+            double rd = dX[k] + -1.0 * bneg(g[k]);
+            if (k >= 1) rd = epim1(dot1(Jx[k], dX[k - 1]), rd);
+            rd = epim1(dot1(ju, vk), rd);
+            rdyn[k] = rd;
+            const int kk = k + 1;  // x row of stage k+1
+            double rx = epi1(dot1(Wq[kk], dX[k]), gX[k]);
             if (kk < N) {
-                rx = epi1(dot1(w.Wm()[kk], w.dU()[kk]), rx);
-                rx = epim1(dot1(cJx[kk], w.mu()[kk]), rx);
+                rx = epi1(dot1(Wm[kk], dU[kk]), rx);
+                rx = epim1(dot1(Jx[kk], mu[kk]), rx);
             }
-            rx += w.mu()[k];
-            w.rsx()[k] = rx;
-            const double lb = o.umin - U[k], ub = o.umax - U[k];
-            const double rlk = dfinite(lb) ? vk - w.sl()[k] - lb : 0.0;
-            const double ruk = dfinite(ub) ? ub - vk - w.su()[k] : 0.0;
-            w.rl()[k] = rlk;
-            w.ru()[k] = ruk;
+            rx += mu[k];
+            rsx[k] = rx;
+            const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+            double rl, ru;
+            rlru(k, fl, fu, rl, ru);
             ninf = fold_absmax(fold_absmax(ninf, r), rx);
             dinf = fold_absmax(dinf, rd);
-            linf = fold_absmax(linf, rlk);
-            uinf = fold_absmax(uinf, ruk);
+            linf = fold_absmax(linf, rl);
+            uinf = fold_absmax(uinf, ru);
         }
         ninf = warp_max(ninf);
         dinf = warp_max(dinf);
         linf = warp_max(linf);
         uinf = warp_max(uinf);
         __syncwarp();
-        // gap = (dot(sl, nl) + dot(su, nu)) / m: two serial chains, lanes 0 and 1
-        double gap = 0.0;
+        // gap = (dot(sl, nl) + dot(su, nu)) / m: two serial chains (even/odd lanes)
+        double gap;
         {
-            const double* a = (lane & 1) ? w.su() : w.sl();
-            const double* b = (lane & 1) ? w.nu() : w.nl();
+            const double* a = (lane & 1) ? su : sl;
+            const double* b = (lane & 1) ? nu : nl;
             double s = 0.0;
             for (int k = 0; k < N; ++k) s += a[k] * b[k];
             const double dl = __shfl_sync(FULLMASK, s, 0);
@@ -418,135 +651,66 @@ __device__ __forceinline__ int solve_qp(const Ocp& o, const Ws& w, const double*
             status = QP_MAXITER;
             break;
         }
-        // barrier diagonal + affine rc (qp.cpp:353-372)
+        // barrier diagonal + affine rc + condensed rhs (qp.cpp:353-372, :288-305)
         for (int k = lane; k < N; k += 32) {
-            const double lb = o.umin - U[k], ub = o.umax - U[k];
-            const bool fl = dfinite(lb), fu = dfinite(ub);
+            const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
             double bk = 0.0;
-            if (fl) bk += w.nl()[k] / w.sl()[k];
-            if (fu) bk += w.nu()[k] / w.su()[k];
-            w.bar()[k] = bk;
-            const double rcl = fl ? -w.sl()[k] * w.nl()[k] : 0.0;
-            const double rcu = fu ? -w.su()[k] * w.nu()[k] : 0.0;
-            w.rcl()[k] = rcl;
-            w.rcu()[k] = rcu;
-            double v = w.rsu()[k];
-            if (fl) v -= (rcl - w.nl()[k] * w.rl()[k]) / w.sl()[k];
-            if (fu) v += (rcu - w.nu()[k] * w.ru()[k]) / w.su()[k];
-            w.rhat()[k] = v;
+            if (fl) bk += nl[k] / sl[k];
+            if (fu) bk += nu[k] / su[k];
+            bar[k] = bk;
+            const double cl = fl ? -sl[k] * nl[k] : 0.0;
+            const double cu = fu ? -su[k] * nu[k] : 0.0;
+            rcl[k] = cl;
+            rcu[k] = cu;
+            double rl, ru;
+            rlru(k, fl, fu, rl, ru);
+            double v = rsu[k];
+            if (fl) v -= (cl - nl[k] * rl) / sl[k];
+            if (fu) v += (cu - nu[k] * ru) / su[k];
+            rhat[k] = v;
         }
         __syncwarp();
-        // riccati_factor (qp.cpp:73-110) fused with the affine backward
-        // vector sweep (qp.cpp:122-141); serial in k, all lanes.
-        bool npd = false;
-        {
-            double P = w.Wq()[N];
-            double pv = w.rsx()[N - 1];  // pvec[N] = qhat[N]
-            w.val()[N] = P;
-            w.pvec()[N] = pv;
-            for (int k = N - 1; k >= 0; --k) {
-                const double Ju = cJu[k];
-                const double pju = epi0(dot1(P, Ju));
-                double hh = epi0(dot1(Ju, pju));
-                hh = hh + w.Wr()[k];
-                hh = hh + w.bar()[k];
-                if (hh <= 0.0 || !dfinite(hh)) {
-                    npd = true;
-                    break;
-                }
-                const double l = sqrt(hh);
-                w.cholh()[k] = l;
-                // vector part at stage k
-                const double tmpv = epi1(dot1(P, -w.rdyn()[k]), pv);
-                double hv = epi1(dot1(Ju, tmpv), w.rhat()[k]);
-                hv = hv / l;
-                hv = hv / l;
-                hv = -hv;
-                w.dff()[k] = hv;
-                if (k >= 1) {
-                    const double Jx = cJx[k];
-                    const double pjx = epi0(dot1(P, Jx));
-                    double gg = epi0(dot1(Ju, pjx));
-                    gg = gg + w.Wm()[k];
-                    double gn = gg / l;
-                    gn = gn / l;
-                    const double gain = -gn;
-                    double pn = epi0(dot1(Jx, pjx));
-                    pn = pn + w.Wq()[k];
-                    pn = epi1(dot1(gg, gain), pn);
-                    w.val()[k] = pn;
-                    w.gain()[k] = gain;
-                    w.gmat()[k] = gg;
-                    double pvn = epi1(dot1(Jx, tmpv), w.rsx()[k - 1]);
-                    pvn = epi1(dot1(gg, hv), pvn);
-                    w.pvec()[k] = pvn;
-                    P = pn;
-                    pv = pvn;
-                }
-            }
-        }
+        bool ok;
+        bool npd = factor_sweep<ST, true>(N, &ok);
+        if (!ok) npd = factor_sweep<ST, false>(N, &ok);
         if (npd) {
             status = QP_FAILED;
             break;
         }
-        // forward rollout (qp.cpp:142-155) + expand (qp.cpp:308-317)
-        auto rollout = [&]() {
-            double dx = 0.0;
-            for (int k = 0; k < N; ++k) {
-                double du = w.dff()[k];
-                if (k >= 1) du = epi1(dot1(w.gain()[k], dx), du);
-                w.ddU()[k] = du;
-                double dxn = -w.rdyn()[k];
-                if (k >= 1) dxn = epi1(dot1(cJx[k], dx), dxn);
-                dxn = epi1(dot1(cJu[k], du), dxn);
-                dx = dxn;
-                w.ddX()[k] = dx;
-                const double mm = epi1(dot1(w.val()[k + 1], dx), w.pvec()[k + 1]);
-                w.ddmu()[k] = -mm;
-            }
-        };
-        auto expand_and_step = [&](double frac) {
-            double alpha = 1.0;
-            for (int k = lane; k < N; k += 32) {
-                const double lb = o.umin - U[k], ub = o.umax - U[k];
-                const bool fl = dfinite(lb), fu = dfinite(ub);
-                const double dv = w.ddU()[k];
-                const double dsl = fl ? dv + w.rl()[k] : 0.0;
-                const double dsu = fu ? w.ru()[k] - dv : 0.0;
-                const double dnl = fl ? (w.rcl()[k] - w.nl()[k] * dsl) / w.sl()[k] : 0.0;
-                const double dnu = fu ? (w.rcu()[k] - w.nu()[k] * dsu) / w.su()[k] : 0.0;
-                w.dsl()[k] = dsl;
-                w.dsu()[k] = dsu;
-                w.dnl()[k] = dnl;
-                w.dnu()[k] = dnu;
-                if (fl) {
-                    if (dsl < 0.0) alpha = smin(alpha, -frac * w.sl()[k] / dsl);
-                    if (dnl < 0.0) alpha = smin(alpha, -frac * w.nl()[k] / dnl);
-                }
-                if (fu) {
-                    if (dsu < 0.0) alpha = smin(alpha, -frac * w.su()[k] / dsu);
-                    if (dnu < 0.0) alpha = smin(alpha, -frac * w.nu()[k] / dnu);
-                }
-            }
-            return warp_min(alpha);
-        };
-        rollout();
-        __syncwarp();
+        rollout<ST>(N);
+        // affine step length, gap_aff, sigma (qp.cpp:373-386)
         double sigma = 0.0;
         {
-            const double alpha_aff = expand_and_step(1.0);
+            double alpha_aff = 1.0;
+            for (int k = lane; k < N; k += 32) {
+                const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+                double rl, ru;
+                rlru(k, fl, fu, rl, ru);
+                const Dir d = expand_k<ST>(k, fl, fu, rl, ru);
+                if (fl) {
+                    if (d.dsl < 0.0) alpha_aff = smin(alpha_aff, -1.0 * sl[k] / d.dsl);
+                    if (d.dnl < 0.0) alpha_aff = smin(alpha_aff, -1.0 * nl[k] / d.dnl);
+                }
+                if (fu) {
+                    if (d.dsu < 0.0) alpha_aff = smin(alpha_aff, -1.0 * su[k] / d.dsu);
+                    if (d.dnu < 0.0) alpha_aff = smin(alpha_aff, -1.0 * nu[k] / d.dnu);
+                }
+            }
+            alpha_aff = warp_min(alpha_aff);
             if (m > 0 && gap > 0.0) {
                 for (int k = lane; k < N; k += 32) {
-                    const double lb = o.umin - U[k], ub = o.umax - U[k];
-                    w.tmp()[2 * k] = dfinite(lb) ? (w.sl()[k] + alpha_aff * w.dsl()[k]) * (w.nl()[k] + alpha_aff * w.dnl()[k]) : 0.0;
-                    w.tmp()[2 * k + 1] = dfinite(ub) ? (w.su()[k] + alpha_aff * w.dsu()[k]) * (w.nu()[k] + alpha_aff * w.dnu()[k]) : 0.0;
+                    const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+                    double rl, ru;
+                    rlru(k, fl, fu, rl, ru);
+                    const Dir d = expand_k<ST>(k, fl, fu, rl, ru);
+                    tmp[2 * k] = fl ? (sl[k] + alpha_aff * d.dsl) * (nl[k] + alpha_aff * d.dnl) : 0.0;
+                    tmp[2 * k + 1] = fu ? (su[k] + alpha_aff * d.dsu) * (nu[k] + alpha_aff * d.dnu) : 0.0;
                 }
                 __syncwarp();
                 double gap_aff = 0.0;
                 for (int k = 0; k < N; ++k) {
-                    const double lb = o.umin - U[k], ub = o.umax - U[k];
-                    if (dfinite(lb)) gap_aff += w.tmp()[2 * k];
-                    if (dfinite(ub)) gap_aff += w.tmp()[2 * k + 1];
+                    if (dfinite(o.umin - U[k])) gap_aff += tmp[2 * k];
+                    if (dfinite(o.umax - U[k])) gap_aff += tmp[2 * k + 1];
                 }
                 gap_aff /= m;
                 const double ratio = smax(0.0, gap_aff / gap);
@@ -554,78 +718,76 @@ __device__ __forceinline__ int solve_qp(const Ocp& o, const Ws& w, const double*
             }
         }
         __syncwarp();
-        // corrector rc + condensed rhs (qp.cpp:390-395, :288-305)
+        // corrector rc + condensed rhs (qp.cpp:390-395, :288-305); the affine
+        // directions are re-expanded from DDU, which still holds the affine step
         for (int k = lane; k < N; k += 32) {
-            const double lb = o.umin - U[k], ub = o.umax - U[k];
-            const bool fl = dfinite(lb), fu = dfinite(ub);
-            if (fl) w.rcl()[k] = sigma * gap - w.sl()[k] * w.nl()[k] - w.dsl()[k] * w.dnl()[k];
-            if (fu) w.rcu()[k] = sigma * gap - w.su()[k] * w.nu()[k] - w.dsu()[k] * w.dnu()[k];
-            double v = w.rsu()[k];
-            if (fl) v -= (w.rcl()[k] - w.nl()[k] * w.rl()[k]) / w.sl()[k];
-            if (fu) v += (w.rcu()[k] - w.nu()[k] * w.ru()[k]) / w.su()[k];
-            w.rhat()[k] = v;
+            const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+            double rl, ru;
+            rlru(k, fl, fu, rl, ru);
+            const Dir d = expand_k<ST>(k, fl, fu, rl, ru);
+            if (fl) rcl[k] = sigma * gap - sl[k] * nl[k] - d.dsl * d.dnl;
+            if (fu) rcu[k] = sigma * gap - su[k] * nu[k] - d.dsu * d.dnu;
+            double v = rsu[k];
+            if (fl) v -= (rcl[k] - nl[k] * rl) / sl[k];
+            if (fu) v += (rcu[k] - nu[k] * ru) / su[k];
+            rhat[k] = v;
         }
         __syncwarp();
-        // corrector backward vector sweep with the cached factor (qp.cpp:122-141)
-        {
-            double pv = w.rsx()[N - 1];
-            w.pvec()[N] = pv;
-            for (int k = N - 1; k >= 0; --k) {
-                const double Ju = cJu[k];
-                const double l = w.cholh()[k];
-                const double tmpv = epi1(dot1(w.val()[k + 1], -w.rdyn()[k]), pv);
-                double hv = epi1(dot1(Ju, tmpv), w.rhat()[k]);
-                hv = hv / l;
-                hv = hv / l;
-                hv = -hv;
-                w.dff()[k] = hv;
-                if (k >= 1) {
-                    double pvn = epi1(dot1(cJx[k], tmpv), w.rsx()[k - 1]);
-                    pvn = epi1(dot1(w.gmat()[k], hv), pvn);
-                    w.pvec()[k] = pvn;
-                    pv = pvn;
-                }
-            }
-        }
-        rollout();
-        __syncwarp();
-        const double alpha = expand_and_step(tau);
-        // update (qp.cpp:397-410)
+        if (!vector_sweep<ST, true>(N)) vector_sweep<ST, false>(N);
+        rollout<ST>(N);
+        // corrector step length (qp.cpp:397); directions stashed in the
+        // arrays this iteration no longer needs (bar, rhat, rcl, rcu)
+        double alpha = 1.0;
         for (int k = lane; k < N; k += 32) {
-            const double lb = o.umin - U[k], ub = o.umax - U[k];
-            w.dU()[k] = w.dU()[k] + alpha * w.ddU()[k];
-            w.dX()[k] = w.dX()[k] + alpha * w.ddX()[k];
-            w.mu()[k] = w.mu()[k] + alpha * w.ddmu()[k];
-            if (dfinite(lb)) {
-                w.sl()[k] += alpha * w.dsl()[k];
-                w.nl()[k] += alpha * w.dnl()[k];
+            const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+            double rl, ru;
+            rlru(k, fl, fu, rl, ru);
+            const Dir d = expand_k<ST>(k, fl, fu, rl, ru);
+            if (fl) {
+                if (d.dsl < 0.0) alpha = smin(alpha, -tau * sl[k] / d.dsl);
+                if (d.dnl < 0.0) alpha = smin(alpha, -tau * nl[k] / d.dnl);
             }
-            if (dfinite(ub)) {
-                w.su()[k] += alpha * w.dsu()[k];
-                w.nu()[k] += alpha * w.dnu()[k];
+            if (fu) {
+                if (d.dsu < 0.0) alpha = smin(alpha, -tau * su[k] / d.dsu);
+                if (d.dnu < 0.0) alpha = smin(alpha, -tau * nu[k] / d.dnu);
+            }
+            bar[k] = d.dsl;
+            rhat[k] = d.dnl;
+            rcl[k] = d.dsu;
+            rcu[k] = d.dnu;
+        }
+        alpha = warp_min(alpha);
+        // update (qp.cpp:398-410)
+        for (int k = lane; k < N; k += 32) {
+            const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+            dU[k] = dU[k] + alpha * ddU[k];
+            dX[k] = dX[k] + alpha * ddX[k];
+            mu[k] = mu[k] + alpha * ddmu[k];
+            if (fl) {
+                sl[k] += alpha * bar[k];
+                nl[k] += alpha * rhat[k];
+            }
+            if (fu) {
+                su[k] += alpha * rcl[k];
+                nu[k] += alpha * rcu[k];
             }
         }
-        cnt.ipm_stage += N;
+        cnt->ipm_stage += N;
         __syncwarp();
     }
     // final clamp (qp.cpp:414-419)
     for (int k = lane; k < N; k += 32) {
         const double lb = o.umin - U[k], ub = o.umax - U[k];
-        w.dU()[k] = smin(smax(w.dU()[k], lb), ub);
+        dU[k] = smin(smax(dU[k], lb), ub);
     }
     __syncwarp();
-    *iters_out = iter;
     return status;
 }
 
 // ------------------------------------------------------------------ SQP
-struct SqpOut {
-    bool converged;
-    int status;  // ST_OK or ST_DOMAIN (propagating)
-};
-
 /// Lagrangian gradient pieces (sqp.cpp:102-128) at stage k.
-/// hu = (0 - Ju_k lam_k) [+ (pi_u - pi_l)],  hx_k (slot x_{k+1}) = (gX_k + lam_k) - Jx_{k+1} lam_{k+1}.
+/// hu = (0 - Ju_k lam_k) [+ (pi_u - pi_l)],
+/// hx_k (slot x_{k+1}) = (gX_k + lam_k) - Jx_{k+1} lam_{k+1}.
 __device__ __forceinline__ double lag_u(const double* Ju, const double* lam, int k) {
     return 0.0 - Ju[k] * lam[k];
 }
@@ -635,11 +797,19 @@ __device__ __forceinline__ double lag_x(const double* gX, const double* Jx, cons
     return h;
 }
 
-/// check_convergence (sqp.cpp:86-96) with grad_l = lagrangian_gradient(gX, J, lam, pl, pu).
-__device__ __forceinline__ bool kkt_check(const Ocp& o, const Ws& w, const double* gX, const double* g, const double* Jx,
-                          const double* Ju, const double* lam, const double* pl, const double* pu, int m,
-                          double eps, int lane) {
-    const int N = o.N;
+/// check_convergence (sqp.cpp:86-96) of grad_l = lagrangian_gradient
+/// (sqp.cpp:118-128) at the current eval arrays with multipliers
+/// (SA(lid), SA(plid), SA(puid)).
+template <int ST>
+__device__ __noinline__ bool kkt_check(int N, int lid, int plid, int puid, int m, double eps) {
+    const int lane = threadIdx.x & 31;
+    const double* gX = SA(A_GX);
+    const double* g = SA(A_G);
+    const double* Jx = SA(A_JX);
+    const double* Ju = SA(A_JU);
+    const double* lam = SA(lid);
+    const double* pl = SA(plid);
+    const double* pu = SA(puid);
     double gl = 0.0, gi = 0.0;
     for (int k = lane; k < N; k += 32) {
         const double hu = lag_u(Ju, lam, k) + (pu[k] - pl[k]);
@@ -665,21 +835,23 @@ __device__ __forceinline__ bool kkt_check(const Ocp& o, const Ws& w, const doubl
     return gl / s_d <= eps && gi <= eps;
 }
 
-__device__ __forceinline__ void reset_blocks(const Ws& w, int N, int lane) {
+/// reset_blocks (sqp.cpp:173-178): identity Hessian blocks.
+template <int ST>
+__device__ __forceinline__ void reset_blocks(int N) {
+    const int lane = threadIdx.x & 31;
     for (int k = lane; k <= N; k += 32) {
-        w.Wq()[k] = 1.0;
-        w.Wm()[k] = 0.0;
-        w.Wr()[k] = 1.0;
+        SA(A_WQ)[k] = 1.0;
+        SA(A_WM)[k] = 0.0;
+        SA(A_WR)[k] = 1.0;
     }
     __syncwarp();
 }
 
 /// bfgs_block_update (sqp.cpp:61-84) for a block of size n (1 or 2) stored as
-/// (q, m, r) = (w00, w01 = w10, w11). Returns -1 on NotPositiveDefinite.
+/// (q, m, r) = (w00, w01 = w10, w11). Returns -1 on NotPositiveDefinite,
+/// 0 if skipped, 1 if updated.
 __device__ __forceinline__ int bfgs_block(double& q, double& mm, double& r, int n, const double* s,
                                           const double* y, bool uslot_only) {
-    // For n == 1 the block is either a pure u slot (stored in r) or a pure x
-    // slot (stored in q).
     if (n == 1) {
         double& wv = uslot_only ? r : q;
         const double ws = epi0(dot1(wv, s[0]));
@@ -717,184 +889,284 @@ __device__ __forceinline__ int bfgs_block(double& q, double& mm, double& r, int 
     return 1;
 }
 
+struct SqpOut {
+    bool converged;
+    int status;  // ST_OK or ST_DOMAIN (propagating)
+};
+
+/// Merit update, line search, acceptance and BFGS of one SQP iteration
+/// (sqp.cpp:312-406). Returns 0 = continue, 1 = break (exhausted with no
+/// finite trial), ST_DOMAIN << 4 = DomainError escaped.
+template <int ST>
+__device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt, double* f, bool first_merit,
+                                     Cnt* cnt) {
+    const int lane = threadIdx.x & 31;
+    const int N = o.N;
+    double* U = SA(A_U);
+    double* X = SA(A_X);
+    double* lam = SA(A_LAM);
+    double* pil = SA(A_PIL);
+    double* piu = SA(A_PIU);
+    double* gX = SA(A_GX);
+    double* g = SA(A_G);
+    double* Jx = SA(A_JX);
+    double* Ju = SA(A_JU);
+    const double* tgX = SA(A_TGX);
+    const double* tg = SA(A_TG);
+    const double* tJx = SA(A_TJX);
+    const double* tJu = SA(A_TJU);
+    double* sig = SA(A_SIG);
+    double* tmp = SA(A_TMP);
+    const double* dU = SA(A_DU);
+    const double* dX = SA(A_DX);
+    const double* mu = SA(A_MU);
+    const double* nl = SA(A_NL);
+    const double* nu = SA(A_NU);
+    double* tU = SA(A_DDU);  // trial iterate (QP scratch is free here)
+    double* tX = SA(A_DDX);
+    // merit_weights_update (sqp.cpp:12-20)
+    for (int k = lane; k < N; k += 32) {
+        const double am = fabs(mu[k]);
+        sig[k] = first_merit ? am : smax(am, 0.5 * (sig[k] + am));
+    }
+    __syncwarp();
+    // line_search (sqp.cpp:22-59)
+    double penalty0, dd;
+    {
+        bool du_bad = false;
+        for (int k = lane; k < N; k += 32) {
+            tmp[k] = sig[k] * fabs(g[k]);
+            tmp[ST + k] = gX[k] * dX[k];
+            du_bad |= !dfinite(dU[k]);
+        }
+        du_bad = warp_any(du_bad);
+        __syncwarp();
+        // two serial chains (even/odd lanes): penalty0 and dot(grad f, dxi);
+        // the u slots contribute 0 * du (exactly +-0) unless du is not finite
+        const double* a = (lane & 1) ? tmp + ST : tmp;
+        double s = 0.0;
+        for (int k = 0; k < N; ++k) s += a[k];
+        penalty0 = __shfl_sync(FULLMASK, s, 0);
+        const double dot_gd = du_bad ? kNaN : __shfl_sync(FULLMASK, s, 1);
+        dd = dot_gd - penalty0;
+        __syncwarp();
+    }
+    const double merit_before = *f + penalty0;
+    double alpha = 1.0, merit = 0.0, f_trial = 0.0;
+    bool ok = false;
+    for (int bt = 0;; ++bt) {
+        for (int k = lane; k < N; k += 32) {
+            tU[k] = U[k] + alpha * dU[k];
+            tX[k] = X[k] + alpha * dX[k];
+        }
+        __syncwarp();
+        f_trial = eval_objective<ST>(o, A_DDX, A_TGX);
+        const int st = eval_constraints<ST>(o, A_DDU, A_DDX, A_TG, cnt);
+        if (st == ST_DOMAIN) return ST_DOMAIN << 4;
+        merit = HUGE_VAL;
+        if (st == ST_OK) {
+            for (int k = lane; k < N; k += 32) tmp[k] = sig[k] * fabs(tg[k]);
+            __syncwarp();
+            merit = f_trial;
+            for (int k = 0; k < N; ++k) merit += tmp[k];
+            __syncwarp();
+        }
+        cnt->ls += 1;
+        ok = dfinite(merit) && merit <= merit_before + opt.c1 * alpha * dd;
+        if (ok || bt >= opt.max_backtracks) break;
+        alpha *= opt.backtrack_factor;
+    }
+    if (!ok && !dfinite(merit)) return 1;  // exhausted with no finite trial
+
+    // accept: xi_new = xi + a dxi equals the last trial bitwise, and so do f,
+    // grad f and the constraint blocks (sqp.cpp:331-352)
+    const double a = alpha;
+    for (int k = lane; k < N; k += 32) {
+        U[k] = tU[k];
+        X[k] = tX[k];
+        lam[k] += a * (mu[k] - lam[k]);
+        pil[k] += a * (nl[k] - pil[k]);
+        piu[k] += a * (nu[k] - piu[k]);
+    }
+    __syncwarp();
+    // damped block BFGS on (s, y) with y = h_new - h_old (sqp.cpp:362-400)
+    bool lost = false;
+    double* Wq = SA(A_WQ);
+    double* Wm = SA(A_WM);
+    double* Wr = SA(A_WR);
+    for (int blk = lane; blk <= N; blk += 32) {
+        double s[2], y[2];
+        int n;
+        bool uonly = false;
+        if (blk == 0) {
+            n = 1;
+            uonly = true;
+            s[0] = a * dU[0];
+            y[0] = lag_u(tJu, lam, 0) - lag_u(Ju, lam, 0);
+        } else if (blk < N) {
+            n = 2;
+            s[0] = a * dX[blk - 1];
+            s[1] = a * dU[blk];
+            y[0] = lag_x(tgX, tJx, lam, blk - 1, N) - lag_x(gX, Jx, lam, blk - 1, N);
+            y[1] = lag_u(tJu, lam, blk) - lag_u(Ju, lam, blk);
+        } else {
+            n = 1;
+            s[0] = a * dX[N - 1];
+            y[0] = lag_x(tgX, tJx, lam, N - 1, N) - lag_x(gX, Jx, lam, N - 1, N);
+        }
+        double q = Wq[blk], mm = Wm[blk], r = Wr[blk];
+        const int res = bfgs_block(q, mm, r, n, s, y, uonly);
+        if (res < 0) lost = true;
+        if (res > 0) {
+            Wq[blk] = q;
+            Wm[blk] = mm;
+            Wr[blk] = r;
+        }
+    }
+    lost = warp_any(lost);
+    __syncwarp();
+    if (lost) reset_blocks<ST>(N);
+    // the trial evaluation becomes the current one
+    for (int k = lane; k < N; k += 32) {
+        gX[k] = tgX[k];
+        g[k] = tg[k];
+        Jx[k] = tJx[k];
+        Ju[k] = tJu[k];
+    }
+    __syncwarp();
+    *f = f_trial;
+    cnt->sqp += 1;
+    return 0;
+}
+
 /// sqp_solve (sqp.cpp:182-411) on the iterate in (U, X) with duals in
-/// lam/pil/piu (already warm-started). Returns status ST_DOMAIN if a
-/// DomainError escapes (sim failure), otherwise ST_OK and converged flag.
-__device__ __forceinline__ SqpOut sqp_solve(const Ocp& o, const Ws& w, double* U, double* X, const nmpcmc_sqp_options& opt,
-                            int lane, Cnt& cnt) {
+/// LAM/PIL/PIU (already warm-started).
+template <int ST>
+__device__ __noinline__ SqpOut sqp_solve(const Ocp& o, const nmpcmc_sqp_options& opt, Cnt* cnt) {
+    const int lane = threadIdx.x & 31;
     const int N = o.N;
     SqpOut out{false, ST_OK};
-    const int m_e = N;
-    const int m_l = dfinite(o.umin) ? N : 0;
-    const int m_u = dfinite(o.umax) ? N : 0;
-    const int m = m_e + m_l + m_u;
-    reset_blocks(w, N, lane);
+    const int m = N + (dfinite(o.umin) ? N : 0) + (dfinite(o.umax) ? N : 0);
+    reset_blocks<ST>(N);
     bool first_merit = true;
 
     // initial evaluation: NonFiniteState -> unconverged return (sqp.cpp:238-246)
-    double f = eval_objective(o, w, X, w.gX(), lane);
-    int st = eval_constraints(o, U, X, w.g(), w.Jx(), w.Ju(), lane, cnt);
+    double f = eval_objective<ST>(o, A_X, A_GX);
+    const int st = eval_constraints<ST>(o, A_U, A_X, A_G, cnt);
     if (st == ST_DOMAIN) return SqpOut{false, ST_DOMAIN};
     if (st == ST_NONFINITE) return out;
 
-    double* gX = w.gX();
-    double* g = w.g();
-    double* Jx = w.Jx();
-    double* Ju = w.Ju();
-    double* tgX = w.tgX();
-    double* tg = w.tg();
-    double* tJx = w.tJx();
-    double* tJu = w.tJu();
     for (int iter = 0;; ++iter) {
-        if (kkt_check(o, w, gX, g, Jx, Ju, w.lam(), w.pil(), w.piu(), m, opt.eps, lane)) {
+        if (kkt_check<ST>(N, A_LAM, A_PIL, A_PIU, m, opt.eps)) {
             out.converged = true;
             break;
         }
         if (iter >= opt.max_iter) break;
-        cnt.sqp_stage += N;
-
-        int qp_iters = 0;
-        int qs = solve_qp(o, w, U, gX, g, Jx, Ju, opt.qp_tol, opt.qp_max_iter, lane, cnt, &qp_iters);
-        cnt.qp += 1;
-        if (qs == QP_DOMAIN) return SqpOut{false, ST_DOMAIN};
-        if (qs == QP_FAILED) {
-            reset_blocks(w, N, lane);
-            qs = solve_qp(o, w, U, gX, g, Jx, Ju, opt.qp_tol, opt.qp_max_iter, lane, cnt, &qp_iters);
-            cnt.qp += 1;
-            if (qs == QP_DOMAIN) return SqpOut{false, ST_DOMAIN};
-            if (qs == QP_FAILED) break;  // rep.qp_failed
+        cnt->sqp_stage += N;
+        // QP, with one identity-reset salvage attempt (sqp.cpp:263-278)
+        int qs = QP_FAILED;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            if (attempt == 1) reset_blocks<ST>(N);
+            qs = solve_qp<ST>(o, opt.qp_tol, opt.qp_max_iter, cnt);
+            cnt->qp += 1;
+            if (qs != QP_FAILED) break;
         }
+        if (qs == QP_DOMAIN) return SqpOut{false, ST_DOMAIN};
+        if (qs == QP_FAILED) break;  // rep.qp_failed
         // KKT certificate with the fresh QP multipliers (sqp.cpp:285-310)
-        if (kkt_check(o, w, gX, g, Jx, Ju, w.mu(), w.nl(), w.nu(), m, opt.eps, lane)) {
+        if (kkt_check<ST>(N, A_MU, A_NL, A_NU, m, opt.eps)) {
             for (int k = lane; k < N; k += 32) {
-                w.lam()[k] = w.mu()[k];
-                w.pil()[k] = w.nl()[k];
-                w.piu()[k] = w.nu()[k];
+                SA(A_LAM)[k] = SA(A_MU)[k];
+                SA(A_PIL)[k] = SA(A_NL)[k];
+                SA(A_PIU)[k] = SA(A_NU)[k];
             }
             __syncwarp();
             out.converged = true;
             break;
         }
-        // merit_weights_update (sqp.cpp:12-20)
-        for (int k = lane; k < N; k += 32) {
-            const double am = fabs(w.mu()[k]);
-            w.sig()[k] = first_merit ? am : smax(am, 0.5 * (w.sig()[k] + am));
-        }
+        const int r = sqp_step<ST>(o, opt, &f, first_merit, cnt);
         first_merit = false;
-        __syncwarp();
-
-        // line_search (sqp.cpp:22-59)
-        double penalty0 = 0.0, dd = 0.0;
-        {
-            for (int k = lane; k < N; k += 32) {
-                w.tmp()[k] = w.sig()[k] * fabs(g[k]);
-                w.tmp()[N + k] = gX[k] * w.dX()[k];
-            }
-            bool du_bad = false;
-            for (int k = lane; k < N; k += 32) du_bad |= !dfinite(w.dU()[k]);
-            du_bad = warp_any(du_bad);
-            __syncwarp();
-            // two serial chains (lanes even/odd): penalty0 and dot(grad f, dxi)
-            const double* a = (lane & 1) ? w.tmp() + N : w.tmp();
-            double s = 0.0;
-            for (int k = 0; k < N; ++k) s += a[k];
-            penalty0 = __shfl_sync(FULLMASK, s, 0);
-            const double dot_gd = du_bad ? kNaN : __shfl_sync(FULLMASK, s, 1);
-            dd = dot_gd - penalty0;
-            __syncwarp();
-        }
-        const double merit_before = f + penalty0;
-        double alpha = 1.0, merit = 0.0, f_trial = 0.0;
-        bool ok = false;
-        int trial_status = ST_OK;
-        for (int bt = 0;; ++bt) {
-            for (int k = lane; k < N; k += 32) {
-                w.ddU()[k] = U[k] + alpha * w.dU()[k];  // trial iterate
-                w.ddX()[k] = X[k] + alpha * w.dX()[k];
-            }
-            __syncwarp();
-            f_trial = eval_objective(o, w, w.ddX(), tgX, lane);
-            trial_status = eval_constraints(o, w.ddU(), w.ddX(), tg, tJx, tJu, lane, cnt);
-            if (trial_status == ST_DOMAIN) return SqpOut{false, ST_DOMAIN};
-            merit = HUGE_VAL;
-            if (trial_status == ST_OK) {
-                for (int k = lane; k < N; k += 32) w.tmp()[k] = w.sig()[k] * fabs(tg[k]);
-                __syncwarp();
-                merit = f_trial;
-                for (int k = 0; k < N; ++k) merit += w.tmp()[k];
-                __syncwarp();
-            }
-            cnt.ls += 1;
-            ok = dfinite(merit) && merit <= merit_before + opt.c1 * alpha * dd;
-            if (ok || bt >= opt.max_backtracks) break;
-            alpha *= opt.backtrack_factor;
-        }
-        if (!ok && !dfinite(merit)) break;  // exhausted with no finite trial
-
-        // accept: xi_new = xi + a * dxi equals the last trial bitwise, and so
-        // do f, grad f and the constraint blocks (sqp.cpp:331-352)
-        const double a = alpha;
-        for (int k = lane; k < N; k += 32) {
-            U[k] = w.ddU()[k];
-            X[k] = w.ddX()[k];
-        }
-        for (int k = lane; k < N; k += 32) {
-            w.lam()[k] += a * (w.mu()[k] - w.lam()[k]);
-            w.pil()[k] += a * (w.nl()[k] - w.pil()[k]);
-            w.piu()[k] += a * (w.nu()[k] - w.piu()[k]);
-        }
-        __syncwarp();
-        // damped block BFGS on (s, y) with y = h_new - h_old (sqp.cpp:362-400)
-        bool lost = false;
-        for (int blk = lane; blk <= N; blk += 32) {
-            double s[2], y[2];
-            int n;
-            bool uonly = false;
-            if (blk == 0) {
-                n = 1;
-                uonly = true;
-                s[0] = a * w.dU()[0];
-                y[0] = lag_u(tJu, w.lam(), 0) - lag_u(Ju, w.lam(), 0);
-            } else if (blk < N) {
-                n = 2;
-                s[0] = a * w.dX()[blk - 1];
-                s[1] = a * w.dU()[blk];
-                y[0] = lag_x(tgX, tJx, w.lam(), blk - 1, N) - lag_x(gX, Jx, w.lam(), blk - 1, N);
-                y[1] = lag_u(tJu, w.lam(), blk) - lag_u(Ju, w.lam(), blk);
-            } else {
-                n = 1;
-                s[0] = a * w.dX()[N - 1];
-                y[0] = lag_x(tgX, tJx, w.lam(), N - 1, N) - lag_x(gX, Jx, w.lam(), N - 1, N);
-            }
-            double q = w.Wq()[blk], mm = w.Wm()[blk], r = w.Wr()[blk];
-            const int res = bfgs_block(q, mm, r, n, s, y, uonly);
-            if (res < 0) lost = true;
-            if (res > 0) {
-                w.Wq()[blk] = q;
-                w.Wm()[blk] = mm;
-                w.Wr()[blk] = r;
-            }
-        }
-        lost = warp_any(lost);
-        __syncwarp();
-        if (lost) reset_blocks(w, N, lane);
-
-        f = f_trial;
-        double* t;
-        t = gX; gX = tgX; tgX = t;
-        t = g; g = tg; tg = t;
-        t = Jx; Jx = tJx; tJx = t;
-        t = Ju; Ju = tJu; tJu = t;
-        cnt.sqp += 1;
+        if (r == (ST_DOMAIN << 4)) return SqpOut{false, ST_DOMAIN};
+        if (r == 1) break;
     }
     return out;
 }
 
 // ------------------------------------------------------------ closed loop
+/// Warm/cold start of the SQP iterate (controllers.cpp:147-186) into U, X and
+/// the duals. Returns ST_DOMAIN if a DomainError escapes.
+template <int ST>
+__device__ __noinline__ int start_iterate(const Ocp& o, bool warm, Cnt* cnt) {
+    const int lane = threadIdx.x & 31;
+    const int N = o.N;
+    double* U = SA(A_U);
+    double* X = SA(A_X);
+    double* nU = SA(A_DDU);
+    double* nX = SA(A_DDX);
+    double* tmp = SA(A_TMP);
+    double* lam = SA(A_LAM);
+    double* pil = SA(A_PIL);
+    double* piu = SA(A_PIU);
+    const bool fl = dfinite(o.umin), fh = dfinite(o.umax);
+    const double u_nom = fl && fh ? 0.5 * (o.umin + o.umax) : smax(o.umin, smin(o.umax, 0.0));
+    // u sequence: shifted_inputs (controllers.cpp:70-83) or nominal_input (:58-66)
+    for (int k = lane; k < N; k += 32)
+        nU[k] = warm ? smax(o.umin, smin(o.umax, U[min(k + 1, N - 1)])) : u_nom;
+    __syncwarp();
+    const int st = xi_from_inputs<ST>(o, A_DDU, A_DDX, cnt);
+    if (st == ST_DOMAIN) return ST_DOMAIN;
+    if (st == ST_OK) {
+        for (int k = lane; k < N; k += 32) {
+            U[k] = nU[k];
+            X[k] = nX[k];
+        }
+    } else if (warm) {
+        // shifted_warm_start (controllers.cpp:97-110)
+        for (int k = lane; k < N; k += 32) nX[k] = X[min(k + 1, N - 1)];
+        __syncwarp();
+        for (int k = lane; k < N; k += 32) {
+            U[k] = nU[k];
+            X[k] = nX[k];
+        }
+    } else {
+        // flat guess (controllers.cpp:173-185)
+        for (int k = lane; k < N; k += 32) {
+            U[k] = u_nom;
+            X[k] = o.x0;
+        }
+    }
+    __syncwarp();
+    if (warm) {
+        // shifted_multipliers (controllers.cpp:87-93); sqp_solve then projects
+        // the warm bound multipliers onto >= 0 (sqp.cpp:219-222)
+        for (int k = lane; k < N; k += 32) {
+            const int src = N >= 2 ? min(k + 1, N - 1) : k;
+            tmp[k] = lam[src];
+            tmp[ST + k] = pil[src];
+            SA(A_DDMU)[k] = piu[src];
+        }
+        __syncwarp();
+        for (int k = lane; k < N; k += 32) {
+            lam[k] = tmp[k];
+            pil[k] = smax(0.0, tmp[ST + k]);
+            piu[k] = smax(0.0, SA(A_DDMU)[k]);
+        }
+    } else {
+        for (int k = lane; k < N; k += 32) {
+            lam[k] = 0.0;
+            pil[k] = 0.0;
+            piu[k] = 0.0;
+        }
+    }
+    __syncwarp();
+    return ST_OK;
+}
+
 /// The NMPC branch of run_closed_loop (montecarlo.cpp:80-157) for one sample.
-template <int NX>
+template <int NX, int ST>
 __device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar,
-                                 nmpcmc_sim_record* rec, nmpcmc_work_counters* cntp, double* traj) {
+                                                 nmpcmc_sim_record* rec, nmpcmc_work_counters* cntp,
+                                                 double* traj) {
     const int lane = threadIdx.x & 31;
     const Cstr p = sample_truth(sc, sim_index);
     NormalStream rng;
@@ -917,15 +1189,13 @@ __device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint
     o.umax = sc.u_max;
     o.Qz = sc.Qz;
     o.inv_V = 1.0 / o.p.V;
+    o.x0 = 0.0;
     const int N = o.N;
-    Ws w{ws_stride(N)};
     Cnt cnt = {};
 
     // NmpcState (make_nmpc_state, controllers.cpp:25-48)
     double xhat = sc.x0_hat[0], Pf = sc.P0[0];
     bool have_last = false;  // last_xi empty -> cold start
-    bool have_duals = false;
-    int cur = 0;             // buffer holding last_xi
 
     double t = sc.t0;
     double z = pl.x[NX - 1] / p.V;
@@ -947,7 +1217,7 @@ __device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint
             status = ST_NONFINITE;
             break;
         }
-        for (int k = lane; k < N; k += 32) w.sp()[k] = setpoint_at(sc, t + (k + 1) * sc.Ts);
+        for (int k = lane; k < N; k += 32) smem_nmpc[A_SP * ST + k] = setpoint_at(sc, t + (k + 1) * sc.Ts);
         // filter_update (ekf.cpp:59-96) with the jitter retry (controllers.cpp:123-132)
         double xf, Pn;
         {
@@ -976,87 +1246,18 @@ __device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint
             Pn = epi1(dot1(kr, K), Pn);
         }
         o.x0 = xf;
-        const int nb = cur ^ 1;  // buffer for this step's iterate
-        double* U = w.U(nb);
-        double* X = w.X(nb);
-        const double* LU = w.U(cur);
-        const double* LX = w.X(cur);
-        if (have_last) {
-            // shifted_inputs (controllers.cpp:70-83) + xi_from_inputs, fallback
-            // shifted_warm_start (controllers.cpp:97-110)
-            for (int k = lane; k < N; k += 32) {
-                const int src = min(k + 1, N - 1);
-                U[k] = smax(o.umin, smin(o.umax, LU[src]));
-            }
-            __syncwarp();
-            const int st = xi_from_inputs(o, U, X, cnt);
-            if (st == ST_DOMAIN) {
-                status = ST_DOMAIN;
-                break;
-            }
-            if (st == ST_NONFINITE) {
-                for (int k = lane; k < N; k += 32) {
-                    const int src = min(k + 1, N - 1);
-                    U[k] = smax(o.umin, smin(o.umax, LU[src]));
-                    X[k] = LX[src];
-                }
-                __syncwarp();
-            }
-            // shifted_multipliers (controllers.cpp:87-93), in place; sqp_solve
-            // then projects the warm bound multipliers onto >= 0 (sqp.cpp:219-222)
-            if (have_duals) {
-                double l1 = 0, l2 = 0, l3 = 0;
-                for (int k = lane; k < N; k += 32) {
-                    const int src = N >= 2 ? min(k + 1, N - 1) : k;
-                    l1 = w.lam()[src];
-                    l2 = w.pil()[src];
-                    l3 = w.piu()[src];
-                    w.tmp()[k] = l1;
-                    w.tmp()[N + k] = l2;
-                    w.ddmu()[k] = l3;
-                }
-                __syncwarp();
-                for (int k = lane; k < N; k += 32) {
-                    w.lam()[k] = w.tmp()[k];
-                    w.pil()[k] = smax(0.0, w.tmp()[N + k]);  // sqp.cpp:219-222
-                    w.piu()[k] = smax(0.0, w.ddmu()[k]);
-                }
-                __syncwarp();
-            }
-        } else {
-            // nominal_input (controllers.cpp:58-66) + cold xi_from_inputs
-            const bool fl = dfinite(o.umin), fh = dfinite(o.umax);
-            const double u_nom = fl && fh ? 0.5 * (o.umin + o.umax) : smax(o.umin, smin(o.umax, 0.0));
-            for (int k = lane; k < N; k += 32) U[k] = u_nom;
-            __syncwarp();
-            const int st = xi_from_inputs(o, U, X, cnt);
-            if (st == ST_DOMAIN) {
-                status = ST_DOMAIN;
-                break;
-            }
-            if (st == ST_NONFINITE) {
-                for (int k = lane; k < N; k += 32) {
-                    U[k] = u_nom;
-                    X[k] = o.x0;
-                }
-                __syncwarp();
-            }
-            for (int k = lane; k < N; k += 32) {
-                w.lam()[k] = 0.0;
-                w.pil()[k] = 0.0;
-                w.piu()[k] = 0.0;
-            }
-            __syncwarp();
+        __syncwarp();
+        if (start_iterate<ST>(o, have_last, &cnt) == ST_DOMAIN) {
+            status = ST_DOMAIN;
+            break;
         }
-        const SqpOut so = sqp_solve(o, w, U, X, sc.sqp, lane, cnt);
+        const SqpOut so = sqp_solve<ST>(o, sc.sqp, &cnt);
         if (so.status != ST_OK) {
             status = so.status;
             break;
         }
-        const double u = smax(o.umin, smin(o.umax, U[0]));
-        cur = nb;
+        const double u = smax(o.umin, smin(o.umax, smem_nmpc[A_U * ST]));
         have_last = true;
-        have_duals = true;
         // predict (ekf.cpp:26-57), np RK4 steps on (x, P)
         {
             const double t_next = t + o.Ts;
@@ -1084,15 +1285,17 @@ __device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint
         if (!so.converged) ++ocp_failures;
         cnt.steps += 1;
         // ---- back in run_closed_loop
-        if (record && i % stride == 0 && lane == 0) {
-            double* rw = traj + (size_t)row * 5;
-            rw[0] = t;
-            rw[1] = z;
-            rw[2] = zbar;
-            rw[3] = u;
-            rw[4] = y;
+        if (record && i % stride == 0) {
+            if (lane == 0) {
+                double* rw = traj + (size_t)row * 5;
+                rw[0] = t;
+                rw[1] = z;
+                rw[2] = zbar;
+                rw[3] = u;
+                rw[4] = y;
+            }
+            ++row;
         }
-        if (record && i % stride == 0) ++row;
         status = simulate_interval<NX>(p, pl, t, t + sc.Ts, u, sc.Ns, rng);
         if (status != ST_OK) break;
         t = sc.t0 + (i + 1) * sc.Ts;
@@ -1138,15 +1341,22 @@ __device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint
     }
 }
 
-template <int NX>
+template <int NX, int ST>
 __global__ void __launch_bounds__(32) nmpc_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
                                                   int64_t n_sims, int nbar, nmpcmc_sim_record* records,
                                                   nmpcmc_work_counters* counters, double* traj, int traj_rows) {
     const int64_t i = blockIdx.x;
     if (i >= n_sims) return;
-    nmpc_closed_loop<NX>(sc, first_sim + (uint64_t)i, nbar, records + i,
-                         counters ? counters + i : nullptr,
-                         traj ? traj + (size_t)i * traj_rows * 5 : nullptr);
+    nmpc_closed_loop<NX, ST>(sc, first_sim + (uint64_t)i, nbar, records + i, counters ? counters + i : nullptr,
+                             traj ? traj + (size_t)i * traj_rows * 5 : nullptr);
+}
+
+template <int NX, int ST>
+inline void launch_nmpc_t(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
+                          nmpcmc_work_counters* d_cnt, double* d_traj, int rows, cudaStream_t stream) {
+    const size_t smem = ws_bytes_for(ST);
+    cudaFuncSetAttribute(nmpc_kernel<NX, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    nmpc_kernel<NX, ST><<<(unsigned)n, 32, smem, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
 }
 
 inline int launch_nmpc(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
@@ -1154,16 +1364,25 @@ inline int launch_nmpc(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int
                        cudaStream_t stream) {
     (void)sm_count;
     if (sc.ctrl_variant != NMPCMC_ONE_STATE) return NMPCMC_UNSUPPORTED;
-    const size_t smem = ws_bytes(sc.N);
-    if (smem > 227 * 1024) return NMPCMC_UNSUPPORTED;
-    if (sc.truth_variant == NMPCMC_THREE_STATE) {
-        cudaFuncSetAttribute(nmpc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        nmpc_kernel<3><<<(unsigned)n, 32, smem, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+    if (sc.N < 1 || sc.N > 255) return NMPCMC_UNSUPPORTED;
+    const int ST = ws_stride_for(sc.N);
+    const bool three = sc.truth_variant == NMPCMC_THREE_STATE;
+    if (ST == 32) {
+        if (three) launch_nmpc_t<3, 32>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
+        else launch_nmpc_t<1, 32>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
+    } else if (ST == 64) {
+        if (three) launch_nmpc_t<3, 64>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
+        else launch_nmpc_t<1, 64>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
+    } else if (ST == 128) {
+        if (three) launch_nmpc_t<3, 128>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
+        else launch_nmpc_t<1, 128>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
     } else {
-        cudaFuncSetAttribute(nmpc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        nmpc_kernel<1><<<(unsigned)n, 32, smem, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+        if (three) launch_nmpc_t<3, 256>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
+        else launch_nmpc_t<1, 256>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
     }
     return NMPCMC_OK;
 }
+
+#undef SA
 
 }  // namespace nmpcmc_dev
