@@ -12,6 +12,7 @@
 #include <string>
 
 #include "nmpc_kernel.cuh"
+#include "nmpc_tps_kernel.cuh"
 #include "nmpcmc_gpu.h"
 #include "pi_kernel.cuh"
 
@@ -27,7 +28,11 @@ struct nmpcmc_gpu_ctx {
     size_t traj_cap = 0;
     void* d_scratch = nullptr;
     size_t scratch_cap = 0;
+    void* d_ws = nullptr;  // K3b structure-of-arrays workspace
+    size_t ws_cap = 0;
     int sm_count = 0;
+    int nmpc_kernel = NMPCMC_NMPC_KERNEL_THREAD;  // which NMPC kernel to launch
+    int tps_warps_per_sm = 8;                     // K3b resident warps per SM
 };
 
 namespace {
@@ -68,8 +73,17 @@ int launch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario& sc, uint64_t first, int64
                 sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
         return cuda_check(ctx, cudaGetLastError(), "pi_kernel launch");
     }
-    const int rc = nmpcmc_dev::launch_nmpc(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
-                                           ctx->sm_count, ctx->stream);
+    int rc;
+    if (ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_WARP) {
+        rc = nmpcmc_dev::launch_nmpc(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ctx->sm_count, ctx->stream);
+    } else {
+        int64_t slots = (int64_t)ctx->sm_count * ctx->tps_warps_per_sm * 32;
+        if (slots > n) slots = ((n + 31) / 32) * 32;
+        const size_t need = nmpcmc_dev::tps_ws_bytes(sc.N, slots);
+        if ((rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, need)) != NMPCMC_OK) return rc;
+        rc = nmpcmc_dev::launch_nmpc_tps(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
+                                         static_cast<double*>(ctx->d_ws), slots, ctx->stream);
+    }
     if (rc != NMPCMC_OK) return fail(ctx, rc, "nmpc launch: unsupported configuration");
     return cuda_check(ctx, cudaGetLastError(), "nmpc_kernel launch");
 }
@@ -103,13 +117,29 @@ void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx) {
     if (ctx == nullptr) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
-    for (void* p : {ctx->d_rec, ctx->d_cnt, ctx->d_traj, ctx->d_scratch})
+    for (void* p : {ctx->d_rec, ctx->d_cnt, ctx->d_traj, ctx->d_scratch, ctx->d_ws})
         if (p) cudaFree(p);
     delete ctx;
 }
 
 const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx) {
     return ctx ? ctx->err.c_str() : "null context";
+}
+
+int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value) {
+    if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    switch (option) {
+        case NMPCMC_OPT_NMPC_KERNEL:
+            if (value != NMPCMC_NMPC_KERNEL_WARP && value != NMPCMC_NMPC_KERNEL_THREAD) return NMPCMC_INVALID_ARGUMENT;
+            ctx->nmpc_kernel = (int)value;
+            return NMPCMC_OK;
+        case NMPCMC_OPT_TPS_WARPS_PER_SM:
+            if (value < 1 || value > 64) return NMPCMC_INVALID_ARGUMENT;
+            ctx->tps_warps_per_sm = (int)value;
+            return NMPCMC_OK;
+        default:
+            return NMPCMC_INVALID_ARGUMENT;
+    }
 }
 
 int nmpcmc_gpu_set_stream(nmpcmc_gpu_ctx* ctx, void* stream) {

@@ -90,6 +90,7 @@ def library():
     lib.nmpcmc_gpu_last_error.argtypes = [P]
     lib.nmpcmc_gpu_last_error.restype = C.c_char_p
     lib.nmpcmc_gpu_set_stream.argtypes = [P, P]
+    lib.nmpcmc_gpu_set_option.argtypes = [P, C.c_int32, C.c_int64]
     lib.nmpcmc_gpu_run.argtypes = [P, S, C.c_uint64, C.c_int64, R, W, A]
     lib.nmpcmc_gpu_run_device.argtypes = [P, S, C.c_uint64, C.c_int64, P, P]
     lib.nmpcmc_gpu_traj_rows.argtypes = [S]
@@ -141,6 +142,15 @@ class Context:
     def _check(self, rc):
         if rc != 0:
             _raise(rc, self.lib.nmpcmc_gpu_last_error(self.handle).decode())
+
+    KERNELS = {"warp": 1, "thread": 2}
+
+    def set_nmpc_kernel(self, kind: str):
+        """'thread' (K3b, default) or 'warp' (K3): bitwise-identical results."""
+        self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 1, self.KERNELS[kind]))
+
+    def set_tps_warps_per_sm(self, w: int):
+        self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 2, w))
 
     def set_stream(self, stream_ptr: int):
         self._check(self.lib.nmpcmc_gpu_set_stream(self.handle, C.c_void_p(stream_ptr)))

@@ -12,34 +12,43 @@ from paper_2212_02197_b200 import configs, engine
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(params=["thread", "warp"])
+def nctx(request, gpu_ctx):
+    """The context with one of the two NMPC kernels selected (K3b / K3):
+    both must reproduce the reference bitwise."""
+    gpu_ctx.set_nmpc_kernel(request.param)
+    yield gpu_ctx
+    gpu_ctx.set_nmpc_kernel("thread")
+
 NMPC_CASES = ["nmpc_n30_short", "nmpc_n60_pert_short", "nmpc_n120_short", "nmpc_cfg2"]
 
 
 @pytest.mark.parametrize("name", NMPC_CASES)
-def test_nmpc_records_bitwise_vs_exact_libm_reference(gpu_ctx, name):
+def test_nmpc_records_bitwise_vs_exact_libm_reference(nctx, name):
     d, _, sc = load_golden(name)
     want = d["rec_xlibm"]
-    got, _ = gpu_ctx.run(sc, int(d["first"]), len(want))
+    got, _ = nctx.run(sc, int(d["first"]), len(want))
     assert_records_equal(got, want)
 
 
 @pytest.mark.parametrize("name", NMPC_CASES)
-def test_nmpc_trajectories_bitwise(gpu_ctx, name):
+def test_nmpc_trajectories_bitwise(nctx, name):
     d, kw, _ = load_golden(name)
     sct = configs.make_scenario(**kw, record=True)
     want = d["traj_xlibm"]
-    _, traj = gpu_ctx.run_traj(sct, int(d["first"]), want.shape[0])
+    _, traj = nctx.run_traj(sct, int(d["first"]), want.shape[0])
     np.testing.assert_array_equal(traj, want)
 
 
 @pytest.mark.parametrize("name", NMPC_CASES)
-def test_nmpc_vs_glibc_reference_distribution(gpu_ctx, name):
+def test_nmpc_vs_glibc_reference_distribution(nctx, name):
     """Against the reference as shipped (glibc libm) per-sample agreement is
     limited by libm rounding amplified through iteration-capped SQP solves
     (SURVEY.md §0.5); report it and require the bulk to agree."""
     d, _, sc = load_golden(name)
     want = d["rec_glibc"]
-    got, _ = gpu_ctx.run(sc, int(d["first"]), len(want))
+    got, _ = nctx.run(sc, int(d["first"]), len(want))
     same_flag = np.mean(got["failed"] == want["failed"])
     both = (got["failed"] == 0) & (want["failed"] == 0)
     rel = np.abs(got["phi"][both] - want["phi"][both]) / np.abs(want["phi"][both])
@@ -49,21 +58,33 @@ def test_nmpc_vs_glibc_reference_distribution(gpu_ctx, name):
     assert np.mean(rel <= 1e-5) >= 0.5
 
 
-def test_nmpc_sharding_invariance(gpu_ctx):
+def test_nmpc_sharding_invariance(nctx):
     sc = configs.make_scenario("nmpc", N=30, n_steps=30, perturb=True)
-    full, _ = gpu_ctx.run(sc, 0, 300)
-    a, _ = gpu_ctx.run(sc, 0, 137)
-    b, _ = gpu_ctx.run(sc, 137, 163)
+    full, _ = nctx.run(sc, 0, 300)
+    a, _ = nctx.run(sc, 0, 137)
+    b, _ = nctx.run(sc, 137, 163)
     assert_records_equal(np.concatenate([a, b]), full)
 
 
-def test_nmpc_counters_consistent(gpu_ctx):
+def test_nmpc_counters_consistent(nctx):
     sc = configs.make_scenario("nmpc", N=30, n_steps=30)
-    rec, cnt = gpu_ctx.run(sc, 0, 64, counters=True)
+    rec, cnt = nctx.run(sc, 0, 64, counters=True)
     ok = rec["failed"] == 0
     assert np.all(cnt["control_steps"][ok] == 30)
     assert np.all(cnt["control_steps"] == rec["ocp_solves"])
     assert np.all(cnt["qp_solves"] >= cnt["sqp_iterations"])
     assert np.all(cnt["ls_evals"] >= cnt["sqp_iterations"])
-    # every OCP evaluates the initial point plus one sweep per line-search trial
-    assert np.all(cnt["shoot_full"] == 30 * (cnt["ls_evals"] + rec["ocp_solves"]) ) or True
+    assert np.all(cnt["shoot_full"] <= 30 * (cnt["ls_evals"] + rec["ocp_solves"]))
+
+
+def test_nmpc_kernels_agree_at_scale(gpu_ctx):
+    """K3 (warp per sample) and K3b (thread per sample) on 600 perturbed
+    config-3 samples, 60 control steps: identical records."""
+    sc = configs.make_scenario("nmpc", N=60, n_steps=60, perturb=True)
+    gpu_ctx.set_nmpc_kernel("warp")
+    a, ca = gpu_ctx.run(sc, 1000, 600, counters=True)
+    gpu_ctx.set_nmpc_kernel("thread")
+    b, cb = gpu_ctx.run(sc, 1000, 600, counters=True)
+    assert_records_equal(a, b)
+    for f in ("control_steps", "ipm_stage_iters", "sqp_iterations", "qp_solves", "ls_evals"):
+        np.testing.assert_array_equal(ca[f], cb[f])
