@@ -161,8 +161,8 @@ int nmpcmc_gpu_ctx_create(int device, nmpcmc_gpu_ctx** out);
 void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx);
 const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx);
 /* Context options. NMPCMC_OPT_NMPC_KERNEL selects the NMPC kernel:
- * THREAD (default) = one thread per sample, workspace in HBM (K3b);
- * WARP = one warp per sample, workspace in shared memory (K3). Results are
+ * WARP (default) = one warp per sample, workspace in shared memory (K3);
+ * THREAD = one thread per sample, workspace in HBM (K3b). Results are
  * bitwise identical; only speed differs. NMPCMC_OPT_TPS_WARPS_PER_SM = resident
  * warps per SM for K3b (default 8). */
 enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2 };

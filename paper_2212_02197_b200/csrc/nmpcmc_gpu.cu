@@ -31,7 +31,7 @@ struct nmpcmc_gpu_ctx {
     void* d_ws = nullptr;  // K3b structure-of-arrays workspace
     size_t ws_cap = 0;
     int sm_count = 0;
-    int nmpc_kernel = NMPCMC_NMPC_KERNEL_THREAD;  // which NMPC kernel to launch
+    int nmpc_kernel = NMPCMC_NMPC_KERNEL_WARP;    // which NMPC kernel to launch
     int tps_warps_per_sm = 8;                     // K3b resident warps per SM
 };
 

@@ -146,7 +146,7 @@ class Context:
     KERNELS = {"warp": 1, "thread": 2}
 
     def set_nmpc_kernel(self, kind: str):
-        """'thread' (K3b, default) or 'warp' (K3): bitwise-identical results."""
+        """'warp' (K3, default) or 'thread' (K3b): bitwise-identical results."""
         self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 1, self.KERNELS[kind]))
 
     def set_tps_warps_per_sm(self, w: int):

@@ -19,7 +19,7 @@ def nctx(request, gpu_ctx):
     both must reproduce the reference bitwise."""
     gpu_ctx.set_nmpc_kernel(request.param)
     yield gpu_ctx
-    gpu_ctx.set_nmpc_kernel("thread")
+    gpu_ctx.set_nmpc_kernel("warp")
 
 NMPC_CASES = ["nmpc_n30_short", "nmpc_n60_pert_short", "nmpc_n120_short", "nmpc_cfg2"]
 
@@ -85,6 +85,7 @@ def test_nmpc_kernels_agree_at_scale(gpu_ctx):
     a, ca = gpu_ctx.run(sc, 1000, 600, counters=True)
     gpu_ctx.set_nmpc_kernel("thread")
     b, cb = gpu_ctx.run(sc, 1000, 600, counters=True)
+    gpu_ctx.set_nmpc_kernel("warp")
     assert_records_equal(a, b)
     for f in ("control_steps", "ipm_stage_iters", "sqp_iterations", "qp_solves", "ls_evals"):
         np.testing.assert_array_equal(ca[f], cb[f])

@@ -11,7 +11,7 @@ def main():
     kw = json.loads(sys.argv[3]) if len(sys.argv) > 3 else {}
     sc = configs.make_scenario(ctl, perturb=True, **kw)
     ctx = engine.Context(0)
-    ctx.set_nmpc_kernel(os.environ.get('KERNEL', 'thread'))
+    ctx.set_nmpc_kernel(os.environ.get('KERNEL', 'warp'))
     if 'WPS' in os.environ: ctx.set_tps_warps_per_sm(int(os.environ['WPS']))
     rec = torch.empty(n * 24, dtype=torch.uint8, device="cuda")
     cnt = torch.empty(n * 64, dtype=torch.uint8, device="cuda")
