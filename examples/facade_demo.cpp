@@ -1,0 +1,51 @@
+// Minimal C++ client of the facade: a reference-style program that runs the
+// PI case study through nmpcmc::gpu (build: see tests/test_cpp_facade.py).
+#include <cstdio>
+#include <cstring>
+
+#include "nmpcmc_gpu.hpp"
+
+int main(int argc, char** argv) {
+    nmpcmc::gpu::Scenario sc;
+    std::memset(&sc, 0, sizeof sc);
+    sc.controller = NMPCMC_CTRL_PI;
+    sc.truth_variant = NMPCMC_THREE_STATE;
+    sc.ctrl_variant = NMPCMC_ONE_STATE;
+    const nmpcmc_cstr_params p = {0.105, 0x1.679cb6b1d419cp+35, 8500.0, 560.0 / 4.186, 0.8, 1.2, 273.65,
+                                  0.0, 0.0, 2.5, 0.0, 1000.0};
+    sc.truth = p;
+    sc.ctrl = p;
+    sc.has_noise_R = 1;
+    sc.noise_R = 0.01;
+    sc.R_filter = 0.01;
+    sc.Qz = 1.0;
+    sc.horizon_Ts = 10.0;
+    sc.N = 60;
+    sc.Nc = 5;
+    sc.np = 5;
+    sc.Ns = 10;
+    sc.sqp = {1e-6, 1e-4, 0.5, 1e-12, 20, 30, 50, 0};
+    sc.pi = {-10.0, -0.1, -0.1, 600.0, 0.0};
+    sc.u_min = 0.0;
+    sc.u_max = 1000.0;
+    sc.t0 = 0.0;
+    sc.tf = 7200.0;
+    sc.Ts = 10.0;
+    sc.n_setpoints = 1;
+    sc.sp_times[0] = 0.0;
+    sc.sp_values[0] = 335.0;
+    const double T0 = 335.0;
+    sc.x0[0] = (p.cA_in - (T0 - p.cT_in) / p.beta) * p.V;
+    sc.x0[1] = (p.cB_in - 2.0 * (T0 - p.cT_in) / p.beta) * p.V;
+    sc.x0[2] = T0 * p.V;
+    sc.x0_hat[0] = T0 * p.V;
+    sc.P0[0] = 1e-6;
+    sc.base_seed = 12345;
+    sc.record_stride = 1;
+    std::printf("N_bar = %d\n", nmpcmc::gpu::validate_scenario(sc));
+    if (argc > 1 && std::strcmp(argv[1], "--validate-only") == 0) return 0;
+    nmpcmc::gpu::Context ctx(0);
+    const auto r = nmpcmc::gpu::run_monte_carlo(ctx, sc, 1000);
+    std::printf("mean phi %.6f, failed %d\n", r.aggregate.mean, r.aggregate.n_failed);
+    return 0;
+}
