@@ -43,13 +43,19 @@ def ref(libm="xlibm"):
     return lib
 
 
-def port():
-    path = os.path.join(HERE, "_build", "libnmpcmc_port.so")
+def port(libm="xlibm"):
+    """The C++ restatement (oracle/port/nmpcmc_port.cpp); symbol prefix
+    nmpcmc_portx_ (exact-libm build) or nmpcmc_port_ (glibc build)."""
+    path = os.path.join(HERE, "_build", f"libnmpcmc_port_{libm}.so")
     if not os.path.exists(path):
         build("port")
     lib = _load(path)
-    _sig(lib, "nmpcmc_port")
+    _sig(lib, port_prefix(libm))
     return lib
+
+
+def port_prefix(libm="xlibm"):
+    return "nmpcmc_portx" if libm == "xlibm" else "nmpcmc_port"
 
 
 def xlibm():
