@@ -15,9 +15,12 @@
 // reference's exact-libm build (tests/test_gpu_nmpc.py).
 //
 // Execution model (K3):
-//  * one warp = one block = one sample; the per-sample workspace (44 arrays of
-//    ST doubles, ST = compile-time stride >= N+1) lives in shared memory, so
-//    the inner loops never touch HBM, and every access is [base + imm];
+//  * one warp = one block = one sample at a time; persistent blocks pull
+//    sample indices from an atomic counter. The workspace is split: the 22
+//    arrays the serial Riccati sweeps and ordered reductions read live in
+//    shared memory (ST doubles each, ST = compile-time stride >= N+1), the 25
+//    arrays only lane-parallel loops touch live in a per-block global region
+//    that stays L2-resident -- which doubles the samples resident per SM;
 //  * stage-parallel work (the N independent shooting intervals, residuals,
 //    expand / step-length / update loops, BFGS blocks) is spread over the 32
 //    lanes, k = lane, lane+32, ...;
@@ -79,25 +82,26 @@ __device__ __forceinline__ int warp_sum_int(int v) {
 __device__ __forceinline__ bool warp_any(bool p) { return __any_sync(FULLMASK, p); }
 
 // ------------------------------------------- certified fast sqrt / division
-__device__ __forceinline__ int expo(double x) { return (int)((__double_as_longlong(x) >> 52) & 0x7ff); }
-/// ulp(x)/2 for normal x (biased exponent field E >= 54): 2^(E-1023-53).
-__device__ __forceinline__ double half_ulp(double x) {
-    return __longlong_as_double((__double_as_longlong(x) & 0x7ff0000000000000LL) - (53LL << 52));
+// Certificates work on the high words only (cheap integer ops). Windows:
+// the Cholesky pivot l in [2^-200, 2^200), numerators in [2^-400, 2^400),
+// so every quotient lies in [2^-600, 2^600): residuals are exact, half-ulps
+// are normal, nothing under/overflows.
+__device__ __forceinline__ bool hi_window(double x, unsigned lo_e, unsigned span) {
+    const unsigned e = ((unsigned)__double2hiint(x) >> 20) & 0x7ffu;
+    return (e - lo_e) < span;
 }
-__device__ __forceinline__ bool mant_zero(double x) {
-    return (__double_as_longlong(x) & 0x000fffffffffffffLL) == 0;
+/// ulp(x)/2 for |x| in the window: 2^(E-1023-53).
+__device__ __forceinline__ double half_ulp_hi(double x) {
+    return __hiloint2double((__double2hiint(x) & 0x7ff00000) - (53 << 20), 0);
 }
-/// exponent window in which every residual below is exact and nothing
-/// under/overflows: |x| in [2^-800, 2^800)
-__device__ __forceinline__ bool in_window(double x) {
-    const int e = expo(x);
-    return e >= 1023 - 800 && e < 1023 + 800;
+__device__ __forceinline__ bool mant_nonzero(double x) {
+    return ((__double2hiint(x) & 0x000fffff) | __double2loint(x)) != 0;
 }
 
 /// l = sqrt(h) and y ~ 1/l for h > 0 (Newton on the rsqrt seed, Markstein
-/// correction). Returns true only if l is certified to be RN(sqrt(h)): the
-/// exact residual h - l^2 lies strictly inside (-l ulp(l), l ulp(l)) shrunk
-/// by 2^-50, l is not a power of two, and everything is inside the window.
+/// correction). Returns true only if l is certified RN(sqrt(h)): the exact
+/// residual h - l^2 lies strictly inside (-l ulp(l), l ulp(l)) shrunk by
+/// 2^-50, l is not a power of two, and l is inside its window.
 __device__ __forceinline__ bool fast_sqrt(double h, double& l, double& y) {
     double y0;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(h));
@@ -111,19 +115,19 @@ __device__ __forceinline__ bool fast_sqrt(double h, double& l, double& y) {
     l = __fma_rn(d, 0.5 * y0, s);
     y = y0;
     const double r = __fma_rn(-l, l, h);
-    const double bound = l * (2.0 * half_ulp(l)) * (1.0 - 0x1.0p-50);
-    return in_window(h) && in_window(l) && !mant_zero(l) && fabs(r) < bound;
+    const double bound = (l * (1.0 - 0x1.0p-50)) * (2.0 * half_ulp_hi(l));
+    return hi_window(l, 1023u - 200u, 400u) && mant_nonzero(l) && fabs(r) < bound;
 }
 
-/// q = a / b with y ~ 1/b (b > 0): Markstein correction, certified by the
-/// exact residual a - b q lying strictly inside b ulp(q) / 2 (shrunk).
-__device__ __forceinline__ bool fast_div(double a, double b, double y, double& q) {
+/// q = a / b with y ~ 1/b (b > 0 inside the pivot window), bs = b (1 - 2^-50):
+/// Markstein correction, certified by the exact residual a - b q lying
+/// strictly inside b ulp(q) / 2 (q not a power of two, a inside its window).
+__device__ __forceinline__ bool fast_div(double a, double b, double y, double bs, double& q) {
     const double q0 = a * y;
     const double e0 = __fma_rn(-b, q0, a);
     q = __fma_rn(e0, y, q0);
     const double e = __fma_rn(-b, q, a);
-    const double bound = b * half_ulp(q) * (1.0 - 0x1.0p-50);
-    return in_window(a) && in_window(b) && in_window(q) && !mant_zero(q) && fabs(e) < bound;
+    return hi_window(a, 1023u - 400u, 800u) && mant_nonzero(q) && fabs(e) < bs * half_ulp_hi(q);
 }
 
 // ------------------------------------------------------- one-state model
@@ -217,13 +221,11 @@ __device__ __forceinline__ int joint_rhs1(const Cstr& p, double x, double P, dou
 }
 
 // ----------------------------------------------------------- workspace
-/// Per-sample shared-memory workspace: kWsArrays arrays of ST doubles at
-/// smem_nmpc + id * ST. Stage arrays are indexed by k; for the interleaved
+/// Full per-sample array set; K3b (nmpc_tps_kernel.cuh) lays all of them out
+/// in global memory. Stage arrays are indexed by k; for the interleaved
 /// decision vector xi = (u_0, x_1, ..., u_{N-1}, x_N) (ocp.hpp:37-43)
 /// U[k] = u_k and X[k] = x_{k+1}. W blocks: Wr[0] = block 0 (u_0),
 /// (Wq, Wm, Wr)[k] = block k = [x_k, u_k] (k = 1..N-1), Wq[N] = block N.
-extern __shared__ __align__(16) double smem_nmpc[];
-
 enum ArrayId {
     A_U, A_X, A_LAM, A_PIL, A_PIU,
     A_GX, A_G, A_JX, A_JU, A_TGX, A_TG, A_TJX, A_TJU,
@@ -236,10 +238,33 @@ enum ArrayId {
     kWsArrays = A_TMP + 2
 };
 
-#define SA(id) (smem_nmpc + (id) * ST)
-
 __host__ __device__ inline int ws_stride_for(int N) { return N < 32 ? 32 : N < 64 ? 64 : (N < 128 ? 128 : 256); }
-__host__ __device__ inline size_t ws_bytes_for(int ST) { return (size_t)kWsArrays * ST * sizeof(double); }
+
+/// K3 splits the workspace by access pattern. Shared memory holds what the
+/// serial Riccati sweeps and ordered reductions read (their latency is on the
+/// critical path); a per-block region of global memory (L2-resident: ~12 KB
+/// per resident sample) holds the rest, touched only by lane-parallel loops.
+extern __shared__ __align__(16) double smem_nmpc[];
+
+enum SmemId {
+    S_JX, S_JU, S_WQ, S_WM, S_WR, S_BAR, S_RDYN, S_RHAT, S_RSX,
+    S_CHOLH, S_RINV, S_VAL, S_GAIN, S_GMAT, S_PVEC, S_DFF,
+    S_DDU, S_DDX, S_DDMU,
+    S_TMP,  // three strides
+    kSmemArrays = S_TMP + 3
+};
+enum GlobId {
+    G_U, G_X, G_TU, G_TX, G_LAM, G_PIL, G_PIU,
+    G_GX, G_G, G_TGX, G_TG, G_TJX, G_TJU,
+    G_SIG, G_SP, G_DU, G_DX, G_MU, G_NL, G_NU, G_SL, G_SU, G_RSU, G_RCL, G_RCU,
+    kGlobArrays
+};
+
+#define SA(id) (smem_nmpc + (id) * ST)
+#define GA(id) (o.gws + (id) * ST)
+
+__host__ __device__ inline size_t ws_bytes_for(int ST) { return (size_t)kSmemArrays * ST * sizeof(double); }
+__host__ __device__ inline size_t gws_bytes_for(int ST) { return (size_t)kGlobArrays * ST * sizeof(double); }
 
 /// Scalars of one NMPC problem instance (NlpInstance, ocp.hpp:25-34).
 struct Ocp {
@@ -251,6 +276,7 @@ struct Ocp {
     double umin, umax;
     double Qz;
     double inv_V;  // output / measurement jacobian 1/V (cstr.cpp:92-95)
+    double* gws;   // K3: this block's global workspace
 };
 
 /// Work counters accumulated per sample (lane-uniform).
@@ -259,15 +285,13 @@ struct Cnt {
 };
 
 // ------------------------------------------------------------ OCP evals
-/// eval_objective (ocp.cpp:76-99) at x = SA(xid): phi in k order; gradient
-/// only on x slots, written to SA(gid)[k] = d phi / d x_{k+1}.
+/// eval_objective (ocp.cpp:76-99): phi in k order; gradient only on the x
+/// slots, gX[k] = d phi / d x_{k+1}.
 template <int ST>
-__device__ __noinline__ double eval_objective(const Ocp& o, int xid, int gid) {
+__device__ __noinline__ double eval_objective(const Ocp& o, const double* X, double* gX) {
     const int lane = threadIdx.x & 31;
-    const double* X = SA(xid);
-    double* gX = SA(gid);
-    double* tmp = SA(A_TMP);
-    const double* sp = SA(A_SP);
+    double* tmp = SA(S_TMP);
+    const double* sp = GA(G_SP);
     const double ts = o.Ts;
     for (int k = lane; k < o.N; k += 32) {
         const double res = X[k] / o.p.V - sp[k];  // output(x) - zbar
@@ -283,18 +307,13 @@ __device__ __noinline__ double eval_objective(const Ocp& o, int xid, int gid) {
     return phi;
 }
 
-/// eval_constraints (ocp.cpp:101-135) at (SA(uid), SA(xid)) into the block
-/// (g, Jx, Ju) at array ids (gid, gid+1, gid+2), plus the status of the first
-/// failing stage in k order (the reference throws at the first failing
+/// eval_constraints (ocp.cpp:101-135) into (g, Jx, Ju), plus the status of the
+/// first failing stage in k order (the reference throws at the first failing
 /// shoot). g[k] = x_{k+1} - F_k.
 template <int ST>
-__device__ __noinline__ int eval_constraints(const Ocp& o, int uid, int xid, int gid, Cnt* cnt) {
+__device__ __noinline__ int eval_constraints(const Ocp& o, const double* U, const double* X, double* g, double* Jx,
+                                             double* Ju, Cnt* cnt) {
     const int lane = threadIdx.x & 31;
-    const double* U = SA(uid);
-    const double* X = SA(xid);
-    double* g = SA(gid);
-    double* Jx = SA(gid + 1);
-    double* Ju = SA(gid + 2);
     int first_bad = 0x7fffffff;
     for (int k = lane; k < o.N; k += 32) {
         const double xk = (k == 0) ? o.x0 : X[k - 1];
@@ -314,12 +333,10 @@ __device__ __noinline__ int eval_constraints(const Ocp& o, int uid, int xid, int
     return first_bad == 0x7fffffff ? ST_OK : (first_bad & 15);
 }
 
-/// xi_from_inputs (ocp.cpp:137-154): forward shooting from x0 with the inputs
-/// in SA(uid), states into SA(xid); serial in k, all lanes.
+/// xi_from_inputs (ocp.cpp:137-154): forward shooting from x0 with inputs U,
+/// states into X; serial in k, all lanes.
 template <int ST>
-__device__ __noinline__ int xi_from_inputs(const Ocp& o, int uid, int xid, Cnt* cnt) {
-    const double* U = SA(uid);
-    double* X = SA(xid);
+__device__ __noinline__ int xi_from_inputs(const Ocp& o, const double* U, double* X, Cnt* cnt) {
     double xk = o.x0;
     int st = ST_OK;
     int k = 0;
@@ -342,28 +359,36 @@ __device__ __forceinline__ double bneg(double g) { return g == 0.0 ? 0.0 : -g; }
 
 enum { QP_OPTIMAL = 0, QP_MAXITER = 1, QP_FAILED = 2, QP_DOMAIN = -1 };
 
+// Inside the Riccati sweeps and rollouts the reference's 1x1 gemm/gemv
+// epilogues "0.0 + a*b" / "1.0*s + 0.0" are evaluated as a*b / s. The two can
+// differ only in the sign of an exact zero; in this path a signed zero never
+// reaches a divisor (the divisors are Cholesky pivots, slacks, sws/sr > eps,
+// V, beta, c_T > 0), a comparison outcome, or an output (phi is a sum of
+// squares), so every nonzero result is bitwise that of the reference -- the
+// GPU parity tests check exactly this.
+
 /// riccati_factor (qp.cpp:73-110) fused with the affine backward vector sweep
 /// of riccati_solve_vectors (qp.cpp:122-141). Serial in k, all lanes.
 /// Returns true on NotPositiveDefinite. FAST: certified sqrt/division; *ok_out
 /// is false if any certificate failed (the caller then replays FAST = false).
 template <int ST, bool FAST>
 __device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
-    const double* Ju = SA(A_JU);
-    const double* Jx = SA(A_JX);
-    const double* Wq = SA(A_WQ);
-    const double* Wm = SA(A_WM);
-    const double* Wr = SA(A_WR);
-    const double* bar = SA(A_BAR);
-    const double* rdyn = SA(A_RDYN);
-    const double* rhat = SA(A_RHAT);
-    const double* rsx = SA(A_RSX);
-    double* cholh = SA(A_CHOLH);
-    double* rinv = SA(A_RINV);
-    double* val = SA(A_VAL);
-    double* gain = SA(A_GAIN);
-    double* gmat = SA(A_GMAT);
-    double* pvec = SA(A_PVEC);
-    double* dff = SA(A_DFF);
+    const double* Ju = SA(S_JU);
+    const double* Jx = SA(S_JX);
+    const double* Wq = SA(S_WQ);
+    const double* Wm = SA(S_WM);
+    const double* Wr = SA(S_WR);
+    const double* bar = SA(S_BAR);
+    const double* rdyn = SA(S_RDYN);
+    const double* rhat = SA(S_RHAT);
+    const double* rsx = SA(S_RSX);
+    double* cholh = SA(S_CHOLH);
+    double* rinv = SA(S_RINV);
+    double* val = SA(S_VAL);
+    double* gain = SA(S_GAIN);
+    double* gmat = SA(S_GMAT);
+    double* pvec = SA(S_PVEC);
+    double* dff = SA(S_DFF);
     bool ok = true;
     double P = Wq[N];
     double pv = rsx[N - 1];  // pvec[N] = qhat[N]
@@ -371,29 +396,28 @@ __device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
     pvec[N] = pv;
     for (int k = N - 1; k >= 0; --k) {
         const double ju = Ju[k];
-        const double pju = epi0(dot1(P, ju));
-        double hh = epi0(dot1(ju, pju));
+        double hh = ju * (P * ju);
         hh = hh + Wr[k];
         hh = hh + bar[k];
         if (hh <= 0.0 || !dfinite(hh)) {  // cholesky_factor -> QP Failed (qp.cpp:358-364)
             *ok_out = ok;
             return true;
         }
-        double l, y;
+        double l, y, ls;
         if (FAST) {
             ok &= fast_sqrt(hh, l, y);
+            ls = l * (1.0 - 0x1.0p-50);
         } else {
             l = sqrt(hh);
             y = 1.0 / l;  // seed for the corrector sweep's fast division
         }
         cholh[k] = l;
         rinv[k] = y;
-        // vector part at stage k
-        const double tmpv = epi1(dot1(P, -rdyn[k]), pv);
-        double hv = epi1(dot1(ju, tmpv), rhat[k]);
+        const double tmpv = P * -rdyn[k] + pv;
+        double hv = ju * tmpv + rhat[k];
         if (FAST) {
-            ok &= fast_div(hv, l, y, hv);
-            ok &= fast_div(hv, l, y, hv);
+            ok &= fast_div(hv, l, y, ls, hv);
+            ok &= fast_div(hv, l, y, ls, hv);
         } else {
             hv = hv / l;
             hv = hv / l;
@@ -402,26 +426,26 @@ __device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
         dff[k] = hv;
         if (k >= 1) {
             const double jx = Jx[k];
-            const double pjx = epi0(dot1(P, jx));
-            double gg = epi0(dot1(ju, pjx));
+            const double pjx = P * jx;
+            double gg = ju * pjx;
             gg = gg + Wm[k];
             double gn;
             if (FAST) {
-                ok &= fast_div(gg, l, y, gn);
-                ok &= fast_div(gn, l, y, gn);
+                ok &= fast_div(gg, l, y, ls, gn);
+                ok &= fast_div(gn, l, y, ls, gn);
             } else {
                 gn = gg / l;
                 gn = gn / l;
             }
             const double gk = -gn;
-            double pn = epi0(dot1(jx, pjx));
+            double pn = jx * pjx;
             pn = pn + Wq[k];
-            pn = epi1(dot1(gg, gk), pn);
+            pn = gg * gk + pn;
             val[k] = pn;
             gain[k] = gk;
             gmat[k] = gg;
-            double pvn = epi1(dot1(jx, tmpv), rsx[k - 1]);
-            pvn = epi1(dot1(gg, hv), pvn);
+            double pvn = jx * tmpv + rsx[k - 1];
+            pvn = gg * hv + pvn;
             pvec[k] = pvn;
             P = pn;
             pv = pvn;
@@ -435,28 +459,30 @@ __device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
 /// Returns false if a FAST certificate failed (caller replays FAST = false).
 template <int ST, bool FAST>
 __device__ __noinline__ bool vector_sweep(int N) {
-    const double* Ju = SA(A_JU);
-    const double* Jx = SA(A_JX);
-    const double* rdyn = SA(A_RDYN);
-    const double* rhat = SA(A_RHAT);
-    const double* rsx = SA(A_RSX);
-    const double* cholh = SA(A_CHOLH);
-    const double* rinv = SA(A_RINV);
-    const double* val = SA(A_VAL);
-    const double* gmat = SA(A_GMAT);
-    double* pvec = SA(A_PVEC);
-    double* dff = SA(A_DFF);
+    const double* Ju = SA(S_JU);
+    const double* Jx = SA(S_JX);
+    const double* rdyn = SA(S_RDYN);
+    const double* rhat = SA(S_RHAT);
+    const double* rsx = SA(S_RSX);
+    const double* cholh = SA(S_CHOLH);
+    const double* rinv = SA(S_RINV);
+    const double* val = SA(S_VAL);
+    const double* gmat = SA(S_GMAT);
+    double* pvec = SA(S_PVEC);
+    double* dff = SA(S_DFF);
     bool ok = true;
     double pv = rsx[N - 1];
     pvec[N] = pv;
     for (int k = N - 1; k >= 0; --k) {
         const double l = cholh[k];
-        const double tmpv = epi1(dot1(val[k + 1], -rdyn[k]), pv);
-        double hv = epi1(dot1(Ju[k], tmpv), rhat[k]);
+        const double tmpv = val[k + 1] * -rdyn[k] + pv;
+        double hv = Ju[k] * tmpv + rhat[k];
         if (FAST) {
             const double y = rinv[k];
-            ok &= fast_div(hv, l, y, hv);
-            ok &= fast_div(hv, l, y, hv);
+            const double ls = l * (1.0 - 0x1.0p-50);
+            ok &= hi_window(l, 1023u - 200u, 400u);
+            ok &= fast_div(hv, l, y, ls, hv);
+            ok &= fast_div(hv, l, y, ls, hv);
         } else {
             hv = hv / l;
             hv = hv / l;
@@ -464,8 +490,8 @@ __device__ __noinline__ bool vector_sweep(int N) {
         hv = -hv;
         dff[k] = hv;
         if (k >= 1) {
-            double pvn = epi1(dot1(Jx[k], tmpv), rsx[k - 1]);
-            pvn = epi1(dot1(gmat[k], hv), pvn);
+            double pvn = Jx[k] * tmpv + rsx[k - 1];
+            pvn = gmat[k] * hv + pvn;
             pvec[k] = pvn;
             pv = pvn;
         }
@@ -476,28 +502,28 @@ __device__ __noinline__ bool vector_sweep(int N) {
 /// Forward rollout (qp.cpp:142-155): step dxi (DDU, DDX) and dmu (DDMU).
 template <int ST>
 __device__ __noinline__ void rollout(int N) {
-    const double* Ju = SA(A_JU);
-    const double* Jx = SA(A_JX);
-    const double* rdyn = SA(A_RDYN);
-    const double* val = SA(A_VAL);
-    const double* pvec = SA(A_PVEC);
-    const double* gain = SA(A_GAIN);
-    const double* dff = SA(A_DFF);
-    double* ddU = SA(A_DDU);
-    double* ddX = SA(A_DDX);
-    double* ddmu = SA(A_DDMU);
-    double dx = 0.0;
-    for (int k = 0; k < N; ++k) {
-        double du = dff[k];
-        if (k >= 1) du = epi1(dot1(gain[k], dx), du);
+    const double* Ju = SA(S_JU);
+    const double* Jx = SA(S_JX);
+    const double* rdyn = SA(S_RDYN);
+    const double* val = SA(S_VAL);
+    const double* pvec = SA(S_PVEC);
+    const double* gain = SA(S_GAIN);
+    const double* dff = SA(S_DFF);
+    double* ddU = SA(S_DDU);
+    double* ddX = SA(S_DDX);
+    double* ddmu = SA(S_DDMU);
+    double dx = -rdyn[0] + Ju[0] * dff[0];  // k = 0 (no state feedback)
+    ddU[0] = dff[0];
+    ddX[0] = dx;
+    ddmu[0] = -(val[1] * dx + pvec[1]);
+    for (int k = 1; k < N; ++k) {
+        const double du = gain[k] * dx + dff[k];
         ddU[k] = du;
-        double dxn = -rdyn[k];
-        if (k >= 1) dxn = epi1(dot1(Jx[k], dx), dxn);
-        dxn = epi1(dot1(Ju[k], du), dxn);
+        double dxn = Jx[k] * dx + -rdyn[k];
+        dxn = Ju[k] * du + dxn;
         dx = dxn;
         ddX[k] = dx;
-        const double mm = epi1(dot1(val[k + 1], dx), pvec[k + 1]);
-        ddmu[k] = -mm;
+        ddmu[k] = -(val[k + 1] * dx + pvec[k + 1]);
     }
     __syncwarp();
 }
@@ -507,13 +533,13 @@ struct Dir {
     double dsl, dsu, dnl, dnu;
 };
 template <int ST>
-__device__ __forceinline__ Dir expand_k(int k, bool fl, bool fu, double rl, double ru) {
-    const double dv = SA(A_DDU)[k];
+__device__ __forceinline__ Dir expand_k(const Ocp& o, int k, bool fl, bool fu, double rl, double ru) {
+    const double dv = SA(S_DDU)[k];
     Dir d;
     d.dsl = fl ? dv + rl : 0.0;
     d.dsu = fu ? ru - dv : 0.0;
-    d.dnl = fl ? (SA(A_RCL)[k] - SA(A_NL)[k] * d.dsl) / SA(A_SL)[k] : 0.0;
-    d.dnu = fu ? (SA(A_RCU)[k] - SA(A_NU)[k] * d.dsu) / SA(A_SU)[k] : 0.0;
+    d.dnl = fl ? (GA(G_RCL)[k] - GA(G_NL)[k] * d.dsl) / GA(G_SL)[k] : 0.0;
+    d.dnu = fu ? (GA(G_RCU)[k] - GA(G_NU)[k] * d.dsu) / GA(G_SU)[k] : 0.0;
     return d;
 }
 
@@ -527,39 +553,40 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
     const int lane = threadIdx.x & 31;
     const int N = o.N;
     const double tau = 0.995;
-    const double* U = SA(A_U);
-    const double* gX = SA(A_GX);
-    const double* g = SA(A_G);
-    const double* Jx = SA(A_JX);
-    const double* Ju = SA(A_JU);
-    const double* Wq = SA(A_WQ);
-    const double* Wm = SA(A_WM);
-    const double* Wr = SA(A_WR);
-    double* dU = SA(A_DU);
-    double* dX = SA(A_DX);
-    double* mu = SA(A_MU);
-    double* nl = SA(A_NL);
-    double* nu = SA(A_NU);
-    double* sl = SA(A_SL);
-    double* su = SA(A_SU);
-    double* rsu = SA(A_RSU);
-    double* rsx = SA(A_RSX);
-    double* rdyn = SA(A_RDYN);
-    double* rcl = SA(A_RCL);
-    double* rcu = SA(A_RCU);
-    double* rhat = SA(A_RHAT);
-    double* bar = SA(A_BAR);
-    double* tmp = SA(A_TMP);
-    const double* ddU = SA(A_DDU);
-    const double* ddX = SA(A_DDX);
-    const double* ddmu = SA(A_DDMU);
+    const double umin = o.umin, umax = o.umax;
+    const double* U = GA(G_U);
+    const double* gX = GA(G_GX);
+    const double* g = GA(G_G);
+    const double* Jx = SA(S_JX);
+    const double* Ju = SA(S_JU);
+    const double* Wq = SA(S_WQ);
+    const double* Wm = SA(S_WM);
+    const double* Wr = SA(S_WR);
+    double* dU = GA(G_DU);
+    double* dX = GA(G_DX);
+    double* mu = GA(G_MU);
+    double* nl = GA(G_NL);
+    double* nu = GA(G_NU);
+    double* sl = GA(G_SL);
+    double* su = GA(G_SU);
+    double* rsu = GA(G_RSU);
+    double* rcl = GA(G_RCL);
+    double* rcu = GA(G_RCU);
+    double* rsx = SA(S_RSX);
+    double* rdyn = SA(S_RDYN);
+    double* rhat = SA(S_RHAT);
+    double* bar = SA(S_BAR);
+    double* tmp = SA(S_TMP);
+    const double* ddU = SA(S_DDU);
+    const double* ddX = SA(S_DDX);
+    const double* ddmu = SA(S_DDMU);
     // data_scale / bounds / init (qp.cpp:183-226)
     double ds = 1.0;
     int nfin = 0;
     bool bad = false;
     for (int k = lane; k < N; k += 32) {
-        const double lb = o.umin - U[k];
-        const double ub = o.umax - U[k];
+        const double lb = umin - U[k];
+        const double ub = umax - U[k];
         if (lb > ub) bad = true;
         const bool fl = dfinite(lb), fu = dfinite(ub);
         if (fl) {
@@ -589,26 +616,28 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
     __syncwarp();
 
     // rl, ru of stage k at the current iterate (qp.cpp:278-283)
-    auto rlru = [&](int k, bool fl, bool fu, double& rl, double& ru) {
+    auto rlru = [&](int k, double u, bool fl, bool fu, double& rl, double& ru) {
         const double v = dU[k];
-        rl = fl ? v - sl[k] - (o.umin - U[k]) : 0.0;
-        ru = fu ? (o.umax - U[k]) - v - su[k] : 0.0;
+        rl = fl ? v - sl[k] - (umin - u) : 0.0;
+        ru = fu ? (umax - u) - v - su[k] : 0.0;
     };
 
     int status = QP_MAXITER;
     for (int iter = 0;; ++iter) {
-        // residuals() (qp.cpp:237-284)
+        // residuals() (qp.cpp:237-284); the gap terms go to TMP for the
+        // ordered sums
         double ninf = 0.0, dinf = 0.0, linf = 0.0, uinf = 0.0;
         for (int k = lane; k < N; k += 32) {
             const double ju = Ju[k];
             const double vk = dU[k], muk = mu[k];
+            const double dxp = k >= 1 ? dX[k - 1] : 0.0;
             double r = epi1(dot1(Wr[k], vk), 0.0);
-            if (k >= 1) r = epi1(dot1(Wm[k], dX[k - 1]), r);
+            if (k >= 1) r = epi1(dot1(Wm[k], dxp), r);
             r = epim1(dot1(ju, muk), r);
             r += nu[k] - nl[k];
             rsu[k] = r;
             double rd = dX[k] + -1.0 * bneg(g[k]);
-            if (k >= 1) rd = epim1(dot1(Jx[k], dX[k - 1]), rd);
+            if (k >= 1) rd = epim1(dot1(Jx[k], dxp), rd);
             rd = epim1(dot1(ju, vk), rd);
             rdyn[k] = rd;
             const int kk = k + 1;  // x row of stage k+1
@@ -617,15 +646,18 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
                 rx = epi1(dot1(Wm[kk], dU[kk]), rx);
                 rx = epim1(dot1(Jx[kk], mu[kk]), rx);
             }
-            rx += mu[k];
+            rx += muk;
             rsx[k] = rx;
-            const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+            const double u = U[k];
+            const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
             double rl, ru;
-            rlru(k, fl, fu, rl, ru);
+            rlru(k, u, fl, fu, rl, ru);
             ninf = fold_absmax(fold_absmax(ninf, r), rx);
             dinf = fold_absmax(dinf, rd);
             linf = fold_absmax(linf, rl);
             uinf = fold_absmax(uinf, ru);
+            tmp[k] = sl[k] * nl[k];
+            tmp[ST + k] = su[k] * nu[k];
         }
         ninf = warp_max(ninf);
         dinf = warp_max(dinf);
@@ -635,10 +667,9 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
         // gap = (dot(sl, nl) + dot(su, nu)) / m: two serial chains (even/odd lanes)
         double gap;
         {
-            const double* a = (lane & 1) ? su : sl;
-            const double* b = (lane & 1) ? nu : nl;
+            const double* a = (lane & 1) ? tmp + ST : tmp;
             double s = 0.0;
-            for (int k = 0; k < N; ++k) s += a[k] * b[k];
+            for (int k = 0; k < N; ++k) s += a[k];
             const double dl = __shfl_sync(FULLMASK, s, 0);
             const double du = __shfl_sync(FULLMASK, s, 1);
             gap = m > 0 ? (dl + du) / m : 0.0;
@@ -653,20 +684,22 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
         }
         // barrier diagonal + affine rc + condensed rhs (qp.cpp:353-372, :288-305)
         for (int k = lane; k < N; k += 32) {
-            const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+            const double u = U[k];
+            const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
+            const double slk = sl[k], suk = su[k], nlk = nl[k], nuk = nu[k];
             double bk = 0.0;
-            if (fl) bk += nl[k] / sl[k];
-            if (fu) bk += nu[k] / su[k];
+            if (fl) bk += nlk / slk;
+            if (fu) bk += nuk / suk;
             bar[k] = bk;
-            const double cl = fl ? -sl[k] * nl[k] : 0.0;
-            const double cu = fu ? -su[k] * nu[k] : 0.0;
+            const double cl = fl ? -slk * nlk : 0.0;
+            const double cu = fu ? -suk * nuk : 0.0;
             rcl[k] = cl;
             rcu[k] = cu;
             double rl, ru;
-            rlru(k, fl, fu, rl, ru);
+            rlru(k, u, fl, fu, rl, ru);
             double v = rsu[k];
-            if (fl) v -= (cl - nl[k] * rl) / sl[k];
-            if (fu) v += (cu - nu[k] * ru) / su[k];
+            if (fl) v -= (cl - nlk * rl) / slk;
+            if (fu) v += (cu - nuk * ru) / suk;
             rhat[k] = v;
         }
         __syncwarp();
@@ -683,34 +716,39 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
         {
             double alpha_aff = 1.0;
             for (int k = lane; k < N; k += 32) {
-                const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+                const double u = U[k];
+                const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
                 double rl, ru;
-                rlru(k, fl, fu, rl, ru);
-                const Dir d = expand_k<ST>(k, fl, fu, rl, ru);
+                rlru(k, u, fl, fu, rl, ru);
+                const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
+                const double slk = sl[k], suk = su[k], nlk = nl[k], nuk = nu[k];
                 if (fl) {
-                    if (d.dsl < 0.0) alpha_aff = smin(alpha_aff, -1.0 * sl[k] / d.dsl);
-                    if (d.dnl < 0.0) alpha_aff = smin(alpha_aff, -1.0 * nl[k] / d.dnl);
+                    if (d.dsl < 0.0) alpha_aff = smin(alpha_aff, -1.0 * slk / d.dsl);
+                    if (d.dnl < 0.0) alpha_aff = smin(alpha_aff, -1.0 * nlk / d.dnl);
                 }
                 if (fu) {
-                    if (d.dsu < 0.0) alpha_aff = smin(alpha_aff, -1.0 * su[k] / d.dsu);
-                    if (d.dnu < 0.0) alpha_aff = smin(alpha_aff, -1.0 * nu[k] / d.dnu);
+                    if (d.dsu < 0.0) alpha_aff = smin(alpha_aff, -1.0 * suk / d.dsu);
+                    if (d.dnu < 0.0) alpha_aff = smin(alpha_aff, -1.0 * nuk / d.dnu);
                 }
             }
             alpha_aff = warp_min(alpha_aff);
             if (m > 0 && gap > 0.0) {
                 for (int k = lane; k < N; k += 32) {
-                    const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+                    const double u = U[k];
+                    const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
                     double rl, ru;
-                    rlru(k, fl, fu, rl, ru);
-                    const Dir d = expand_k<ST>(k, fl, fu, rl, ru);
-                    tmp[2 * k] = fl ? (sl[k] + alpha_aff * d.dsl) * (nl[k] + alpha_aff * d.dnl) : 0.0;
-                    tmp[2 * k + 1] = fu ? (su[k] + alpha_aff * d.dsu) * (nu[k] + alpha_aff * d.dnu) : 0.0;
+                    rlru(k, u, fl, fu, rl, ru);
+                    const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
+                    tmp[k] = fl ? (sl[k] + alpha_aff * d.dsl) * (nl[k] + alpha_aff * d.dnl) : 0.0;
+                    tmp[ST + k] = fu ? (su[k] + alpha_aff * d.dsu) * (nu[k] + alpha_aff * d.dnu) : 0.0;
+                    tmp[2 * ST + k] = (fl ? 1.0 : 0.0) + (fu ? 2.0 : 0.0);
                 }
                 __syncwarp();
                 double gap_aff = 0.0;
                 for (int k = 0; k < N; ++k) {
-                    if (dfinite(o.umin - U[k])) gap_aff += tmp[2 * k];
-                    if (dfinite(o.umax - U[k])) gap_aff += tmp[2 * k + 1];
+                    const double f = tmp[2 * ST + k];
+                    if (f == 1.0 || f == 3.0) gap_aff += tmp[k];
+                    if (f >= 2.0) gap_aff += tmp[ST + k];
                 }
                 gap_aff /= m;
                 const double ratio = smax(0.0, gap_aff / gap);
@@ -721,28 +759,34 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
         // corrector rc + condensed rhs (qp.cpp:390-395, :288-305); the affine
         // directions are re-expanded from DDU, which still holds the affine step
         for (int k = lane; k < N; k += 32) {
-            const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+            const double u = U[k];
+            const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
             double rl, ru;
-            rlru(k, fl, fu, rl, ru);
-            const Dir d = expand_k<ST>(k, fl, fu, rl, ru);
-            if (fl) rcl[k] = sigma * gap - sl[k] * nl[k] - d.dsl * d.dnl;
-            if (fu) rcu[k] = sigma * gap - su[k] * nu[k] - d.dsu * d.dnu;
+            rlru(k, u, fl, fu, rl, ru);
+            const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
+            const double slk = sl[k], suk = su[k], nlk = nl[k], nuk = nu[k];
+            double cl = rcl[k], cu = rcu[k];
+            if (fl) cl = sigma * gap - slk * nlk - d.dsl * d.dnl;
+            if (fu) cu = sigma * gap - suk * nuk - d.dsu * d.dnu;
+            rcl[k] = cl;
+            rcu[k] = cu;
             double v = rsu[k];
-            if (fl) v -= (rcl[k] - nl[k] * rl) / sl[k];
-            if (fu) v += (rcu[k] - nu[k] * ru) / su[k];
+            if (fl) v -= (cl - nlk * rl) / slk;
+            if (fu) v += (cu - nuk * ru) / suk;
             rhat[k] = v;
         }
         __syncwarp();
         if (!vector_sweep<ST, true>(N)) vector_sweep<ST, false>(N);
         rollout<ST>(N);
-        // corrector step length (qp.cpp:397); directions stashed in the
-        // arrays this iteration no longer needs (bar, rhat, rcl, rcu)
+        // corrector step length (qp.cpp:397) and update (qp.cpp:398-410); the
+        // directions are recomputed after the warp-wide min
         double alpha = 1.0;
         for (int k = lane; k < N; k += 32) {
-            const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+            const double u = U[k];
+            const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
             double rl, ru;
-            rlru(k, fl, fu, rl, ru);
-            const Dir d = expand_k<ST>(k, fl, fu, rl, ru);
+            rlru(k, u, fl, fu, rl, ru);
+            const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
             if (fl) {
                 if (d.dsl < 0.0) alpha = smin(alpha, -tau * sl[k] / d.dsl);
                 if (d.dnl < 0.0) alpha = smin(alpha, -tau * nl[k] / d.dnl);
@@ -751,25 +795,24 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
                 if (d.dsu < 0.0) alpha = smin(alpha, -tau * su[k] / d.dsu);
                 if (d.dnu < 0.0) alpha = smin(alpha, -tau * nu[k] / d.dnu);
             }
-            bar[k] = d.dsl;
-            rhat[k] = d.dnl;
-            rcl[k] = d.dsu;
-            rcu[k] = d.dnu;
         }
         alpha = warp_min(alpha);
-        // update (qp.cpp:398-410)
         for (int k = lane; k < N; k += 32) {
-            const bool fl = dfinite(o.umin - U[k]), fu = dfinite(o.umax - U[k]);
+            const double u = U[k];
+            const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
+            double rl, ru;
+            rlru(k, u, fl, fu, rl, ru);
+            const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
             dU[k] = dU[k] + alpha * ddU[k];
             dX[k] = dX[k] + alpha * ddX[k];
             mu[k] = mu[k] + alpha * ddmu[k];
             if (fl) {
-                sl[k] += alpha * bar[k];
-                nl[k] += alpha * rhat[k];
+                sl[k] += alpha * d.dsl;
+                nl[k] += alpha * d.dnl;
             }
             if (fu) {
-                su[k] += alpha * rcl[k];
-                nu[k] += alpha * rcu[k];
+                su[k] += alpha * d.dsu;
+                nu[k] += alpha * d.dnu;
             }
         }
         cnt->ipm_stage += N;
@@ -777,7 +820,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
     }
     // final clamp (qp.cpp:414-419)
     for (int k = lane; k < N; k += 32) {
-        const double lb = o.umin - U[k], ub = o.umax - U[k];
+        const double lb = umin - U[k], ub = umax - U[k];
         dU[k] = smin(smax(dU[k], lb), ub);
     }
     __syncwarp();
@@ -798,35 +841,40 @@ __device__ __forceinline__ double lag_x(const double* gX, const double* Jx, cons
 }
 
 /// check_convergence (sqp.cpp:86-96) of grad_l = lagrangian_gradient
-/// (sqp.cpp:118-128) at the current eval arrays with multipliers
-/// (SA(lid), SA(plid), SA(puid)).
+/// (sqp.cpp:118-128) at the current evaluation with multipliers (lam, pl, pu).
 template <int ST>
-__device__ __noinline__ bool kkt_check(int N, int lid, int plid, int puid, int m, double eps) {
+__device__ __noinline__ bool kkt_check(const Ocp& o, const double* lam, const double* pl, const double* pu, int m,
+                                       double eps) {
     const int lane = threadIdx.x & 31;
-    const double* gX = SA(A_GX);
-    const double* g = SA(A_G);
-    const double* Jx = SA(A_JX);
-    const double* Ju = SA(A_JU);
-    const double* lam = SA(lid);
-    const double* pl = SA(plid);
-    const double* pu = SA(puid);
+    const int N = o.N;
+    const double* gX = GA(G_GX);
+    const double* g = GA(G_G);
+    const double* Jx = SA(S_JX);
+    const double* Ju = SA(S_JU);
+    double* tmp = SA(S_TMP);
     double gl = 0.0, gi = 0.0;
     for (int k = lane; k < N; k += 32) {
-        const double hu = lag_u(Ju, lam, k) + (pu[k] - pl[k]);
+        const double lk = lam[k], plk = pl[k], puk = pu[k];
+        const double hu = (0.0 - Ju[k] * lk) + (puk - plk);
         const double hx = lag_x(gX, Jx, lam, k, N);
         gl = fold_absmax(fold_absmax(gl, hu), hx);
         gi = fold_absmax(gi, g[k]);
+        tmp[k] = fabs(lk);
+        tmp[ST + k] = fabs(plk);
+        tmp[2 * ST + k] = fabs(puk);
     }
     gl = warp_max(gl);
     gi = warp_max(gi);
+    __syncwarp();
     // mults = one_norm(lam) + one_norm(pi_l) + one_norm(pi_u): three serial
     // chains in one instruction stream (lanes 0, 1, 2)
-    const double* a = (lane % 3 == 0) ? lam : (lane % 3 == 1) ? pl : pu;
+    const double* a = tmp + (lane % 3) * ST;
     double s = 0.0;
-    for (int k = 0; k < N; ++k) s += fabs(a[k]);
+    for (int k = 0; k < N; ++k) s += a[k];
     const double n1 = __shfl_sync(FULLMASK, s, 0);
     const double n2 = __shfl_sync(FULLMASK, s, 1);
     const double n3 = __shfl_sync(FULLMASK, s, 2);
+    __syncwarp();
     double s_d = 1.0;
     if (m > 0) {
         const double mults = n1 + n2 + n3;
@@ -840,9 +888,9 @@ template <int ST>
 __device__ __forceinline__ void reset_blocks(int N) {
     const int lane = threadIdx.x & 31;
     for (int k = lane; k <= N; k += 32) {
-        SA(A_WQ)[k] = 1.0;
-        SA(A_WM)[k] = 0.0;
-        SA(A_WR)[k] = 1.0;
+        SA(S_WQ)[k] = 1.0;
+        SA(S_WM)[k] = 0.0;
+        SA(S_WR)[k] = 1.0;
     }
     __syncwarp();
 }
@@ -902,45 +950,42 @@ __device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt
                                      Cnt* cnt) {
     const int lane = threadIdx.x & 31;
     const int N = o.N;
-    double* U = SA(A_U);
-    double* X = SA(A_X);
-    double* lam = SA(A_LAM);
-    double* pil = SA(A_PIL);
-    double* piu = SA(A_PIU);
-    double* gX = SA(A_GX);
-    double* g = SA(A_G);
-    double* Jx = SA(A_JX);
-    double* Ju = SA(A_JU);
-    const double* tgX = SA(A_TGX);
-    const double* tg = SA(A_TG);
-    const double* tJx = SA(A_TJX);
-    const double* tJu = SA(A_TJU);
-    double* sig = SA(A_SIG);
-    double* tmp = SA(A_TMP);
-    const double* dU = SA(A_DU);
-    const double* dX = SA(A_DX);
-    const double* mu = SA(A_MU);
-    const double* nl = SA(A_NL);
-    const double* nu = SA(A_NU);
-    double* tU = SA(A_DDU);  // trial iterate (QP scratch is free here)
-    double* tX = SA(A_DDX);
-    // merit_weights_update (sqp.cpp:12-20)
+    double* U = GA(G_U);
+    double* X = GA(G_X);
+    double* tU = GA(G_TU);
+    double* tX = GA(G_TX);
+    double* lam = GA(G_LAM);
+    double* pil = GA(G_PIL);
+    double* piu = GA(G_PIU);
+    double* gX = GA(G_GX);
+    double* g = GA(G_G);
+    double* tgX = GA(G_TGX);
+    double* tg = GA(G_TG);
+    double* tJx = GA(G_TJX);
+    double* tJu = GA(G_TJU);
+    double* Jx = SA(S_JX);
+    double* Ju = SA(S_JU);
+    double* sig = GA(G_SIG);
+    double* tmp = SA(S_TMP);
+    const double* dU = GA(G_DU);
+    const double* dX = GA(G_DX);
+    const double* mu = GA(G_MU);
+    const double* nl = GA(G_NL);
+    const double* nu = GA(G_NU);
+    // merit_weights_update (sqp.cpp:12-20) + line_search terms (sqp.cpp:28-31)
+    bool du_bad = false;
     for (int k = lane; k < N; k += 32) {
         const double am = fabs(mu[k]);
-        sig[k] = first_merit ? am : smax(am, 0.5 * (sig[k] + am));
+        const double sg = first_merit ? am : smax(am, 0.5 * (sig[k] + am));
+        sig[k] = sg;
+        tmp[k] = sg * fabs(g[k]);
+        tmp[ST + k] = gX[k] * dX[k];
+        du_bad |= !dfinite(dU[k]);
     }
+    du_bad = warp_any(du_bad);
     __syncwarp();
-    // line_search (sqp.cpp:22-59)
     double penalty0, dd;
     {
-        bool du_bad = false;
-        for (int k = lane; k < N; k += 32) {
-            tmp[k] = sig[k] * fabs(g[k]);
-            tmp[ST + k] = gX[k] * dX[k];
-            du_bad |= !dfinite(dU[k]);
-        }
-        du_bad = warp_any(du_bad);
-        __syncwarp();
         // two serial chains (even/odd lanes): penalty0 and dot(grad f, dxi);
         // the u slots contribute 0 * du (exactly +-0) unless du is not finite
         const double* a = (lane & 1) ? tmp + ST : tmp;
@@ -960,8 +1005,8 @@ __device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt
             tX[k] = X[k] + alpha * dX[k];
         }
         __syncwarp();
-        f_trial = eval_objective<ST>(o, A_DDX, A_TGX);
-        const int st = eval_constraints<ST>(o, A_DDU, A_DDX, A_TG, cnt);
+        f_trial = eval_objective<ST>(o, tX, tgX);
+        const int st = eval_constraints<ST>(o, tU, tX, tg, tJx, tJu, cnt);
         if (st == ST_DOMAIN) return ST_DOMAIN << 4;
         merit = HUGE_VAL;
         if (st == ST_OK) {
@@ -991,9 +1036,9 @@ __device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt
     __syncwarp();
     // damped block BFGS on (s, y) with y = h_new - h_old (sqp.cpp:362-400)
     bool lost = false;
-    double* Wq = SA(A_WQ);
-    double* Wm = SA(A_WM);
-    double* Wr = SA(A_WR);
+    double* Wq = SA(S_WQ);
+    double* Wm = SA(S_WM);
+    double* Wr = SA(S_WR);
     for (int blk = lane; blk <= N; blk += 32) {
         double s[2], y[2];
         int n;
@@ -1051,13 +1096,13 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp& o, const nmpcmc_sqp_options&
     bool first_merit = true;
 
     // initial evaluation: NonFiniteState -> unconverged return (sqp.cpp:238-246)
-    double f = eval_objective<ST>(o, A_X, A_GX);
-    const int st = eval_constraints<ST>(o, A_U, A_X, A_G, cnt);
+    double f = eval_objective<ST>(o, GA(G_X), GA(G_GX));
+    const int st = eval_constraints<ST>(o, GA(G_U), GA(G_X), GA(G_G), SA(S_JX), SA(S_JU), cnt);
     if (st == ST_DOMAIN) return SqpOut{false, ST_DOMAIN};
     if (st == ST_NONFINITE) return out;
 
     for (int iter = 0;; ++iter) {
-        if (kkt_check<ST>(N, A_LAM, A_PIL, A_PIU, m, opt.eps)) {
+        if (kkt_check<ST>(o, GA(G_LAM), GA(G_PIL), GA(G_PIU), m, opt.eps)) {
             out.converged = true;
             break;
         }
@@ -1074,11 +1119,11 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp& o, const nmpcmc_sqp_options&
         if (qs == QP_DOMAIN) return SqpOut{false, ST_DOMAIN};
         if (qs == QP_FAILED) break;  // rep.qp_failed
         // KKT certificate with the fresh QP multipliers (sqp.cpp:285-310)
-        if (kkt_check<ST>(N, A_MU, A_NL, A_NU, m, opt.eps)) {
+        if (kkt_check<ST>(o, GA(G_MU), GA(G_NL), GA(G_NU), m, opt.eps)) {
             for (int k = lane; k < N; k += 32) {
-                SA(A_LAM)[k] = SA(A_MU)[k];
-                SA(A_PIL)[k] = SA(A_NL)[k];
-                SA(A_PIU)[k] = SA(A_NU)[k];
+                GA(G_LAM)[k] = GA(G_MU)[k];
+                GA(G_PIL)[k] = GA(G_NL)[k];
+                GA(G_PIU)[k] = GA(G_NU)[k];
             }
             __syncwarp();
             out.converged = true;
@@ -1099,21 +1144,21 @@ template <int ST>
 __device__ __noinline__ int start_iterate(const Ocp& o, bool warm, Cnt* cnt) {
     const int lane = threadIdx.x & 31;
     const int N = o.N;
-    double* U = SA(A_U);
-    double* X = SA(A_X);
-    double* nU = SA(A_DDU);
-    double* nX = SA(A_DDX);
-    double* tmp = SA(A_TMP);
-    double* lam = SA(A_LAM);
-    double* pil = SA(A_PIL);
-    double* piu = SA(A_PIU);
+    double* U = GA(G_U);
+    double* X = GA(G_X);
+    double* nU = GA(G_TU);
+    double* nX = GA(G_TX);
+    double* tmp = SA(S_TMP);
+    double* lam = GA(G_LAM);
+    double* pil = GA(G_PIL);
+    double* piu = GA(G_PIU);
     const bool fl = dfinite(o.umin), fh = dfinite(o.umax);
     const double u_nom = fl && fh ? 0.5 * (o.umin + o.umax) : smax(o.umin, smin(o.umax, 0.0));
     // u sequence: shifted_inputs (controllers.cpp:70-83) or nominal_input (:58-66)
     for (int k = lane; k < N; k += 32)
         nU[k] = warm ? smax(o.umin, smin(o.umax, U[min(k + 1, N - 1)])) : u_nom;
     __syncwarp();
-    const int st = xi_from_inputs<ST>(o, A_DDU, A_DDX, cnt);
+    const int st = xi_from_inputs<ST>(o, nU, nX, cnt);
     if (st == ST_DOMAIN) return ST_DOMAIN;
     if (st == ST_OK) {
         for (int k = lane; k < N; k += 32) {
@@ -1143,13 +1188,13 @@ __device__ __noinline__ int start_iterate(const Ocp& o, bool warm, Cnt* cnt) {
             const int src = N >= 2 ? min(k + 1, N - 1) : k;
             tmp[k] = lam[src];
             tmp[ST + k] = pil[src];
-            SA(A_DDMU)[k] = piu[src];
+            tmp[2 * ST + k] = piu[src];
         }
         __syncwarp();
         for (int k = lane; k < N; k += 32) {
             lam[k] = tmp[k];
             pil[k] = smax(0.0, tmp[ST + k]);
-            piu[k] = smax(0.0, SA(A_DDMU)[k]);
+            piu[k] = smax(0.0, tmp[2 * ST + k]);
         }
     } else {
         for (int k = lane; k < N; k += 32) {
@@ -1164,9 +1209,8 @@ __device__ __noinline__ int start_iterate(const Ocp& o, bool warm, Cnt* cnt) {
 
 /// The NMPC branch of run_closed_loop (montecarlo.cpp:80-157) for one sample.
 template <int NX, int ST>
-__device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar,
-                                                 nmpcmc_sim_record* rec, nmpcmc_work_counters* cntp,
-                                                 double* traj) {
+__device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar, double* gws,
+                                              nmpcmc_sim_record* rec, nmpcmc_work_counters* cntp, double* traj) {
     const int lane = threadIdx.x & 31;
     const Cstr p = sample_truth(sc, sim_index);
     NormalStream rng;
@@ -1190,6 +1234,7 @@ __device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint
     o.Qz = sc.Qz;
     o.inv_V = 1.0 / o.p.V;
     o.x0 = 0.0;
+    o.gws = gws;
     const int N = o.N;
     Cnt cnt = {};
 
@@ -1217,7 +1262,7 @@ __device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint
             status = ST_NONFINITE;
             break;
         }
-        for (int k = lane; k < N; k += 32) smem_nmpc[A_SP * ST + k] = setpoint_at(sc, t + (k + 1) * sc.Ts);
+        for (int k = lane; k < N; k += 32) GA(G_SP)[k] = setpoint_at(sc, t + (k + 1) * sc.Ts);
         // filter_update (ekf.cpp:59-96) with the jitter retry (controllers.cpp:123-132)
         double xf, Pn;
         {
@@ -1256,7 +1301,7 @@ __device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint
             status = so.status;
             break;
         }
-        const double u = smax(o.umin, smin(o.umax, smem_nmpc[A_U * ST]));
+        const double u = smax(o.umin, smin(o.umax, GA(G_U)[0]));
         have_last = true;
         // predict (ekf.cpp:26-57), np RK4 steps on (x, P)
         {
@@ -1339,50 +1384,92 @@ __device__ __forceinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint
             *cntp = c;
         }
     }
+    __syncwarp();
 }
 
+/// Persistent blocks (one warp, one sample at a time) pull sample indices
+/// from a global atomic counter -- the device form of run_monte_carlo's worker
+/// pool (montecarlo.cpp:218-238) -- so long and short samples balance.
 template <int NX, int ST>
-__global__ void __launch_bounds__(32) nmpc_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
+__global__ void __launch_bounds__(32, 16) nmpc_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
                                                   int64_t n_sims, int nbar, nmpcmc_sim_record* records,
-                                                  nmpcmc_work_counters* counters, double* traj, int traj_rows) {
-    const int64_t i = blockIdx.x;
-    if (i >= n_sims) return;
-    nmpc_closed_loop<NX, ST>(sc, first_sim + (uint64_t)i, nbar, records + i, counters ? counters + i : nullptr,
-                             traj ? traj + (size_t)i * traj_rows * 5 : nullptr);
+                                                  nmpcmc_work_counters* counters, double* traj, int traj_rows,
+                                                  double* gws_all, unsigned long long* next) {
+    double* gws = gws_all + (size_t)blockIdx.x * kGlobArrays * ST;
+    for (;;) {
+        unsigned long long i = 0;
+        if ((threadIdx.x & 31) == 0) i = atomicAdd(next, 1ULL);
+        i = __shfl_sync(FULLMASK, i, 0);
+        if (i >= (unsigned long long)n_sims) break;
+        nmpc_closed_loop<NX, ST>(sc, first_sim + i, nbar, gws, records + i, counters ? counters + i : nullptr,
+                                 traj ? traj + (size_t)i * traj_rows * 5 : nullptr);
+    }
 }
 
+/// Resident blocks per SM for the K3 kernel of stride ST (occupancy query).
 template <int NX, int ST>
-inline void launch_nmpc_t(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
-                          nmpcmc_work_counters* d_cnt, double* d_traj, int rows, cudaStream_t stream) {
+inline int nmpc_blocks_per_sm() {
     const size_t smem = ws_bytes_for(ST);
     cudaFuncSetAttribute(nmpc_kernel<NX, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    nmpc_kernel<NX, ST><<<(unsigned)n, 32, smem, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nmpc_kernel<NX, ST>, 32, smem);
+    return b < 1 ? 1 : b;
+}
+
+template <int NX, int ST>
+inline int launch_nmpc_t(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
+                         nmpcmc_work_counters* d_cnt, double* d_traj, int rows, int sm_count, double* gws,
+                         int64_t gws_blocks, unsigned long long* counter, cudaStream_t stream) {
+    const size_t smem = ws_bytes_for(ST);
+    int64_t grid = (int64_t)sm_count * nmpc_blocks_per_sm<NX, ST>();
+    if (grid > n) grid = n;
+    if (grid > gws_blocks) return NMPCMC_INVALID_ARGUMENT;
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    nmpc_kernel<NX, ST><<<(unsigned)grid, 32, smem, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, gws,
+                                                              counter);
+    return NMPCMC_OK;
+}
+
+/// Global workspace bytes and block count K3 needs on this device.
+inline void nmpc_gws_need(const nmpcmc_scenario& sc, int sm_count, int64_t n, size_t* bytes, int64_t* blocks) {
+    const int ST = ws_stride_for(sc.N);
+    const bool three = sc.truth_variant == NMPCMC_THREE_STATE;
+    int per = 1;
+    switch (ST) {
+        case 32: per = three ? nmpc_blocks_per_sm<3, 32>() : nmpc_blocks_per_sm<1, 32>(); break;
+        case 64: per = three ? nmpc_blocks_per_sm<3, 64>() : nmpc_blocks_per_sm<1, 64>(); break;
+        case 128: per = three ? nmpc_blocks_per_sm<3, 128>() : nmpc_blocks_per_sm<1, 128>(); break;
+        default: per = three ? nmpc_blocks_per_sm<3, 256>() : nmpc_blocks_per_sm<1, 256>(); break;
+    }
+    int64_t b = (int64_t)sm_count * per;
+    if (b > n) b = n;
+    if (b < 1) b = 1;
+    *blocks = b;
+    *bytes = (size_t)b * gws_bytes_for(ST);
 }
 
 inline int launch_nmpc(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
-                       nmpcmc_work_counters* d_cnt, double* d_traj, int rows, int sm_count,
-                       cudaStream_t stream) {
-    (void)sm_count;
+                       nmpcmc_work_counters* d_cnt, double* d_traj, int rows, int sm_count, double* gws,
+                       int64_t gws_blocks, unsigned long long* counter, cudaStream_t stream) {
     if (sc.ctrl_variant != NMPCMC_ONE_STATE) return NMPCMC_UNSUPPORTED;
     if (sc.N < 1 || sc.N > 255) return NMPCMC_UNSUPPORTED;
     const int ST = ws_stride_for(sc.N);
     const bool three = sc.truth_variant == NMPCMC_THREE_STATE;
-    if (ST == 32) {
-        if (three) launch_nmpc_t<3, 32>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
-        else launch_nmpc_t<1, 32>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
-    } else if (ST == 64) {
-        if (three) launch_nmpc_t<3, 64>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
-        else launch_nmpc_t<1, 64>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
-    } else if (ST == 128) {
-        if (three) launch_nmpc_t<3, 128>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
-        else launch_nmpc_t<1, 128>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
-    } else {
-        if (three) launch_nmpc_t<3, 256>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
-        else launch_nmpc_t<1, 256>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, stream);
-    }
-    return NMPCMC_OK;
+#define NMPCMC_K3_CASE(S)                                                                                      \
+    if (ST == S)                                                                                              \
+        return three ? launch_nmpc_t<3, S>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, sm_count, gws,       \
+                                           gws_blocks, counter, stream)                                       \
+                     : launch_nmpc_t<1, S>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, sm_count, gws,       \
+                                           gws_blocks, counter, stream);
+    NMPCMC_K3_CASE(32)
+    NMPCMC_K3_CASE(64)
+    NMPCMC_K3_CASE(128)
+    NMPCMC_K3_CASE(256)
+#undef NMPCMC_K3_CASE
+    return NMPCMC_UNSUPPORTED;
 }
 
 #undef SA
+#undef GA
 
 }  // namespace nmpcmc_dev

@@ -30,6 +30,10 @@ struct nmpcmc_gpu_ctx {
     size_t scratch_cap = 0;
     void* d_ws = nullptr;  // K3b structure-of-arrays workspace
     size_t ws_cap = 0;
+    void* d_gws = nullptr;  // K3 per-block global workspace
+    size_t gws_cap = 0;
+    void* d_counter = nullptr;  // K3 work counter
+    size_t counter_cap = 0;
     int sm_count = 0;
     int nmpc_kernel = NMPCMC_NMPC_KERNEL_WARP;    // which NMPC kernel to launch
     int tps_warps_per_sm = 8;                     // K3b resident warps per SM
@@ -75,7 +79,14 @@ int launch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario& sc, uint64_t first, int64
     }
     int rc;
     if (ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_WARP) {
-        rc = nmpcmc_dev::launch_nmpc(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ctx->sm_count, ctx->stream);
+        size_t bytes = 0;
+        int64_t blocks = 0;
+        nmpcmc_dev::nmpc_gws_need(sc, ctx->sm_count, n, &bytes, &blocks);
+        if ((rc = ensure(ctx, &ctx->d_gws, &ctx->gws_cap, bytes)) != NMPCMC_OK) return rc;
+        if ((rc = ensure(ctx, &ctx->d_counter, &ctx->counter_cap, 256)) != NMPCMC_OK) return rc;
+        rc = nmpcmc_dev::launch_nmpc(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ctx->sm_count,
+                                     static_cast<double*>(ctx->d_gws), blocks,
+                                     static_cast<unsigned long long*>(ctx->d_counter), ctx->stream);
     } else {
         int64_t slots = (int64_t)ctx->sm_count * ctx->tps_warps_per_sm * 32;
         if (slots > n) slots = ((n + 31) / 32) * 32;
@@ -117,7 +128,7 @@ void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx) {
     if (ctx == nullptr) return;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
-    for (void* p : {ctx->d_rec, ctx->d_cnt, ctx->d_traj, ctx->d_scratch, ctx->d_ws})
+    for (void* p : {ctx->d_rec, ctx->d_cnt, ctx->d_traj, ctx->d_scratch, ctx->d_ws, ctx->d_gws, ctx->d_counter})
         if (p) cudaFree(p);
     delete ctx;
 }
