@@ -78,7 +78,7 @@ struct NormalStream {
 
     /// rng.cpp:78-91: u1 = 1 - U, u2 = U, r = sqrt(-2 ln u1), a = 2 pi u2,
     /// return r cos a, cache r sin a (GCC emits one sincos call).
-    __device__ double normal() {
+    __device__ __noinline__ double normal() {
         if (have_spare) {
             have_spare = false;
             return spare;

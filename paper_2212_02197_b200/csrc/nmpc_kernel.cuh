@@ -69,16 +69,8 @@ __device__ __forceinline__ double warp_min(double m) {
     }
     return m;
 }
-__device__ __forceinline__ int warp_min_int(int v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULLMASK, v, o));
-    return v;
-}
-__device__ __forceinline__ int warp_sum_int(int v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
-    return v;
-}
+__device__ __forceinline__ int warp_min_int(int v) { return __reduce_min_sync(FULLMASK, v); }
+__device__ __forceinline__ int warp_sum_int(int v) { return __reduce_add_sync(FULLMASK, v); }
 __device__ __forceinline__ bool warp_any(bool p) { return __any_sync(FULLMASK, p); }
 
 // ------------------------------------------- certified fast sqrt / division
@@ -169,37 +161,53 @@ __device__ __forceinline__ int shoot1(const Cstr& p, double x, double u, double 
     Su = 0.0;
     const double h2 = 0.5 * h;
     const double h6 = h / 6.0;
+#pragma unroll 1
     for (int step = 0; step < nc; ++step) {
-        Stage1 s1, s2, s3, s4;
-        int st = eval1(p, F, u, s1, WITH_SENS);
-        if (st) return st;
-        double kx1 = 0, ku1 = 0, kx2 = 0, ku2 = 0, kx3 = 0, ku3 = 0, kx4 = 0, ku4 = 0;
-        if (WITH_SENS) {
-            kx1 = epi0(dot1(s1.a, Sx));
-            ku1 = epi1(dot1(s1.a, Su), s1.b);
+        // stage j evaluates at (F, Sx, Su) + c_j h (k, kx, ku)_{j-1} with
+        // c_j h = 0, h/2, h/2, 1.0*h (advanced / advanced_sens, ocp.cpp:39-46);
+        // the weighted sum k1 + 2 k2 + 2 k3 + k4 accumulates left to right,
+        // exactly the reference's expression order (ocp.cpp:51-60)
+        double pk = 0.0, pkx = 0.0, pku = 0.0, acc = 0.0, accx = 0.0, accu = 0.0;
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+            double xs = F, sx = Sx, su = Su;
+            if (j > 0) {
+                const double ch = (j == 3) ? 1.0 * h : h2;
+                xs = F + ch * pk;
+                if (WITH_SENS) {
+                    sx = Sx + ch * pkx;
+                    su = Su + ch * pku;
+                }
+            }
+            Stage1 s;
+            const int st = eval1(p, xs, u, s, WITH_SENS);
+            if (st) return st;
+            double kx = 0.0, ku = 0.0;
+            if (WITH_SENS) {
+                kx = epi0(dot1(s.a, sx));
+                ku = epi1(dot1(s.a, su), s.b);
+            }
+            if (j == 0) {
+                acc = s.k;
+                accx = kx;
+                accu = ku;
+            } else if (j < 3) {
+                acc = acc + 2.0 * s.k;
+                accx = accx + 2.0 * kx;
+                accu = accu + 2.0 * ku;
+            } else {
+                acc = acc + s.k;
+                accx = accx + kx;
+                accu = accu + ku;
+            }
+            pk = s.k;
+            pkx = kx;
+            pku = ku;
         }
-        st = eval1(p, F + h2 * s1.k, u, s2, WITH_SENS);
-        if (st) return st;
+        F += h6 * acc;
         if (WITH_SENS) {
-            kx2 = epi0(dot1(s2.a, Sx + h2 * kx1));
-            ku2 = epi1(dot1(s2.a, Su + h2 * ku1), s2.b);
-        }
-        st = eval1(p, F + h2 * s2.k, u, s3, WITH_SENS);
-        if (st) return st;
-        if (WITH_SENS) {
-            kx3 = epi0(dot1(s3.a, Sx + h2 * kx2));
-            ku3 = epi1(dot1(s3.a, Su + h2 * ku2), s3.b);
-        }
-        st = eval1(p, F + 1.0 * h * s3.k, u, s4, WITH_SENS);
-        if (st) return st;
-        if (WITH_SENS) {
-            kx4 = epi0(dot1(s4.a, Sx + 1.0 * h * kx3));
-            ku4 = epi1(dot1(s4.a, Su + 1.0 * h * ku3), s4.b);
-        }
-        F += h6 * (s1.k + 2.0 * s2.k + 2.0 * s3.k + s4.k);
-        if (WITH_SENS) {
-            Sx += h6 * (kx1 + 2.0 * kx2 + 2.0 * kx3 + kx4);
-            Su += h6 * (ku1 + 2.0 * ku2 + 2.0 * ku3 + ku4);
+            Sx += h6 * accx;
+            Su += h6 * accu;
         }
     }
     if (!dfinite(F)) return ST_NONFINITE;
@@ -257,8 +265,14 @@ enum GlobId {
     G_U, G_X, G_TU, G_TX, G_LAM, G_PIL, G_PIU,
     G_GX, G_G, G_TGX, G_TG, G_TJX, G_TJU,
     G_SIG, G_SP, G_DU, G_DX, G_MU, G_NL, G_NU, G_SL, G_SU, G_RSU, G_RCL, G_RCU,
+    G_DSL, G_DSU, G_DNL, G_DNU,
     kGlobArrays
 };
+
+/// Out-of-line IEEE division for the lane-parallel loops: one call site per
+/// use instead of an inlined ~25-instruction sequence keeps the hot code small
+/// (the kernel is instruction-cache bound; see profiles/).
+__device__ __noinline__ double qdiv(double a, double b) { return a / b; }
 
 #define SA(id) (smem_nmpc + (id) * ST)
 #define GA(id) (o.gws + (id) * ST)
@@ -293,6 +307,7 @@ __device__ __noinline__ double eval_objective(const Ocp& o, const double* X, dou
     double* tmp = SA(S_TMP);
     const double* sp = GA(G_SP);
     const double ts = o.Ts;
+#pragma unroll 1
     for (int k = lane; k < o.N; k += 32) {
         const double res = X[k] / o.p.V - sp[k];  // output(x) - zbar
         const double qres = epi0(dot1(o.Qz, res));
@@ -302,6 +317,7 @@ __device__ __noinline__ double eval_objective(const Ocp& o, const double* X, dou
     }
     __syncwarp();
     double phi = 0.0;
+#pragma unroll 1
     for (int k = 0; k < o.N; ++k) phi += tmp[k];
     __syncwarp();
     return phi;
@@ -315,6 +331,7 @@ __device__ __noinline__ int eval_constraints(const Ocp& o, const double* U, cons
                                              double* Ju, Cnt* cnt) {
     const int lane = threadIdx.x & 31;
     int first_bad = 0x7fffffff;
+#pragma unroll 1
     for (int k = lane; k < o.N; k += 32) {
         const double xk = (k == 0) ? o.x0 : X[k - 1];
         double F, Sx, Su;
@@ -340,6 +357,7 @@ __device__ __noinline__ int xi_from_inputs(const Ocp& o, const double* U, double
     double xk = o.x0;
     int st = ST_OK;
     int k = 0;
+#pragma unroll 1
     for (; k < o.N; ++k) {
         double F, Sx, Su;
         st = shoot1<false>(o.p, xk, U[k], o.h, o.Nc, F, Sx, Su);
@@ -394,6 +412,7 @@ __device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
     double pv = rsx[N - 1];  // pvec[N] = qhat[N]
     val[N] = P;
     pvec[N] = pv;
+#pragma unroll 1
     for (int k = N - 1; k >= 0; --k) {
         const double ju = Ju[k];
         double hh = ju * (P * ju);
@@ -473,6 +492,7 @@ __device__ __noinline__ bool vector_sweep(int N) {
     bool ok = true;
     double pv = rsx[N - 1];
     pvec[N] = pv;
+#pragma unroll 1
     for (int k = N - 1; k >= 0; --k) {
         const double l = cholh[k];
         const double tmpv = val[k + 1] * -rdyn[k] + pv;
@@ -516,6 +536,7 @@ __device__ __noinline__ void rollout(int N) {
     ddU[0] = dff[0];
     ddX[0] = dx;
     ddmu[0] = -(val[1] * dx + pvec[1]);
+#pragma unroll 1
     for (int k = 1; k < N; ++k) {
         const double du = gain[k] * dx + dff[k];
         ddU[k] = du;
@@ -528,7 +549,8 @@ __device__ __noinline__ void rollout(int N) {
     __syncwarp();
 }
 
-/// expand (qp.cpp:308-317) of stage k from the step in DDU, given rl/ru.
+/// expand (qp.cpp:308-317) of stage k from the step in DDU, given rl/ru;
+/// stored in G_DSL.. for the later loops of the iteration.
 struct Dir {
     double dsl, dsu, dnl, dnu;
 };
@@ -538,9 +560,32 @@ __device__ __forceinline__ Dir expand_k(const Ocp& o, int k, bool fl, bool fu, d
     Dir d;
     d.dsl = fl ? dv + rl : 0.0;
     d.dsu = fu ? ru - dv : 0.0;
-    d.dnl = fl ? (GA(G_RCL)[k] - GA(G_NL)[k] * d.dsl) / GA(G_SL)[k] : 0.0;
-    d.dnu = fu ? (GA(G_RCU)[k] - GA(G_NU)[k] * d.dsu) / GA(G_SU)[k] : 0.0;
+    d.dnl = fl ? qdiv(GA(G_RCL)[k] - GA(G_NL)[k] * d.dsl, GA(G_SL)[k]) : 0.0;
+    d.dnu = fu ? qdiv(GA(G_RCU)[k] - GA(G_NU)[k] * d.dsu, GA(G_SU)[k]) : 0.0;
+    GA(G_DSL)[k] = d.dsl;
+    GA(G_DSU)[k] = d.dsu;
+    GA(G_DNL)[k] = d.dnl;
+    GA(G_DNU)[k] = d.dnu;
     return d;
+}
+template <int ST>
+__device__ __forceinline__ Dir load_dir(const Ocp& o, int k) {
+    return Dir{GA(G_DSL)[k], GA(G_DSU)[k], GA(G_DNL)[k], GA(G_DNU)[k]};
+}
+/// max_step's cap (qp.cpp:321-337) for the four (value, direction) pairs of
+/// stage k: alpha = min(alpha, -frac value / dir) over dir < 0.
+template <int ST>
+__device__ __forceinline__ double step_caps(const Ocp& o, int k, bool fl, bool fu, const Dir& d, double frac,
+                                            double alpha) {
+    if (fl) {
+        if (d.dsl < 0.0) alpha = smin(alpha, qdiv(-frac * GA(G_SL)[k], d.dsl));
+        if (d.dnl < 0.0) alpha = smin(alpha, qdiv(-frac * GA(G_NL)[k], d.dnl));
+    }
+    if (fu) {
+        if (d.dsu < 0.0) alpha = smin(alpha, qdiv(-frac * GA(G_SU)[k], d.dsu));
+        if (d.dnu < 0.0) alpha = smin(alpha, qdiv(-frac * GA(G_NU)[k], d.dnu));
+    }
+    return alpha;
 }
 
 /// solve_qp (qp.cpp:173-423) for the stagewise box QP that build_stages
@@ -584,6 +629,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
     double ds = 1.0;
     int nfin = 0;
     bool bad = false;
+#pragma unroll 1
     for (int k = lane; k < N; k += 32) {
         const double lb = umin - U[k];
         const double ub = umax - U[k];
@@ -623,10 +669,12 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
     };
 
     int status = QP_MAXITER;
+#pragma unroll 1
     for (int iter = 0;; ++iter) {
         // residuals() (qp.cpp:237-284); the gap terms go to TMP for the
         // ordered sums
         double ninf = 0.0, dinf = 0.0, linf = 0.0, uinf = 0.0;
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             const double ju = Ju[k];
             const double vk = dU[k], muk = mu[k];
@@ -659,22 +707,23 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             tmp[k] = sl[k] * nl[k];
             tmp[ST + k] = su[k] * nu[k];
         }
-        ninf = warp_max(ninf);
-        dinf = warp_max(dinf);
-        linf = warp_max(linf);
-        uinf = warp_max(uinf);
+        // the inf-norms only meet "<= eps": max over lanes <= eps iff every
+        // lane's partial max is (partials never hold NaN) -- one vote
+        const bool res_ok = __all_sync(FULLMASK, ninf <= eps && dinf <= eps && linf <= eps && uinf <= eps);
         __syncwarp();
-        // gap = (dot(sl, nl) + dot(su, nu)) / m: two serial chains (even/odd lanes)
+        // gap = (dot(sl, nl) + dot(su, nu)) / m: two serial chains, each lane
+        // runs both (no shuffles)
         double gap;
         {
-            const double* a = (lane & 1) ? tmp + ST : tmp;
-            double s = 0.0;
-            for (int k = 0; k < N; ++k) s += a[k];
-            const double dl = __shfl_sync(FULLMASK, s, 0);
-            const double du = __shfl_sync(FULLMASK, s, 1);
+            double dl = 0.0, du = 0.0;
+#pragma unroll 1
+            for (int k = 0; k < N; ++k) {
+                dl += tmp[k];
+                du += tmp[ST + k];
+            }
             gap = m > 0 ? (dl + du) / m : 0.0;
         }
-        if (ninf <= eps && dinf <= eps && linf <= eps && uinf <= eps && gap <= eps) {
+        if (res_ok && gap <= eps) {
             status = QP_OPTIMAL;
             break;
         }
@@ -683,13 +732,14 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             break;
         }
         // barrier diagonal + affine rc + condensed rhs (qp.cpp:353-372, :288-305)
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             const double u = U[k];
             const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
             const double slk = sl[k], suk = su[k], nlk = nl[k], nuk = nu[k];
             double bk = 0.0;
-            if (fl) bk += nlk / slk;
-            if (fu) bk += nuk / suk;
+            if (fl) bk += qdiv(nlk, slk);
+            if (fu) bk += qdiv(nuk, suk);
             bar[k] = bk;
             const double cl = fl ? -slk * nlk : 0.0;
             const double cu = fu ? -suk * nuk : 0.0;
@@ -698,8 +748,8 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             double rl, ru;
             rlru(k, u, fl, fu, rl, ru);
             double v = rsu[k];
-            if (fl) v -= (cl - nlk * rl) / slk;
-            if (fu) v += (cu - nuk * ru) / suk;
+            if (fl) v -= qdiv(cl - nlk * rl, slk);
+            if (fu) v += qdiv(cu - nuk * ru, suk);
             rhat[k] = v;
         }
         __syncwarp();
@@ -711,40 +761,33 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             break;
         }
         rollout<ST>(N);
-        // affine step length, gap_aff, sigma (qp.cpp:373-386)
+        // affine directions + step length, gap_aff, sigma (qp.cpp:367-386)
         double sigma = 0.0;
         {
             double alpha_aff = 1.0;
+#pragma unroll 1
             for (int k = lane; k < N; k += 32) {
                 const double u = U[k];
                 const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
                 double rl, ru;
                 rlru(k, u, fl, fu, rl, ru);
                 const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
-                const double slk = sl[k], suk = su[k], nlk = nl[k], nuk = nu[k];
-                if (fl) {
-                    if (d.dsl < 0.0) alpha_aff = smin(alpha_aff, -1.0 * slk / d.dsl);
-                    if (d.dnl < 0.0) alpha_aff = smin(alpha_aff, -1.0 * nlk / d.dnl);
-                }
-                if (fu) {
-                    if (d.dsu < 0.0) alpha_aff = smin(alpha_aff, -1.0 * suk / d.dsu);
-                    if (d.dnu < 0.0) alpha_aff = smin(alpha_aff, -1.0 * nuk / d.dnu);
-                }
+                alpha_aff = step_caps<ST>(o, k, fl, fu, d, 1.0, alpha_aff);
             }
             alpha_aff = warp_min(alpha_aff);
             if (m > 0 && gap > 0.0) {
+#pragma unroll 1
                 for (int k = lane; k < N; k += 32) {
                     const double u = U[k];
                     const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
-                    double rl, ru;
-                    rlru(k, u, fl, fu, rl, ru);
-                    const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
+                    const Dir d = load_dir<ST>(o, k);
                     tmp[k] = fl ? (sl[k] + alpha_aff * d.dsl) * (nl[k] + alpha_aff * d.dnl) : 0.0;
                     tmp[ST + k] = fu ? (su[k] + alpha_aff * d.dsu) * (nu[k] + alpha_aff * d.dnu) : 0.0;
                     tmp[2 * ST + k] = (fl ? 1.0 : 0.0) + (fu ? 2.0 : 0.0);
                 }
                 __syncwarp();
                 double gap_aff = 0.0;
+#pragma unroll 1
                 for (int k = 0; k < N; ++k) {
                     const double f = tmp[2 * ST + k];
                     if (f == 1.0 || f == 3.0) gap_aff += tmp[k];
@@ -756,14 +799,15 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             }
         }
         __syncwarp();
-        // corrector rc + condensed rhs (qp.cpp:390-395, :288-305); the affine
-        // directions are re-expanded from DDU, which still holds the affine step
+        // corrector rc + condensed rhs (qp.cpp:390-395, :288-305) from the
+        // stored affine directions
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             const double u = U[k];
             const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
             double rl, ru;
             rlru(k, u, fl, fu, rl, ru);
-            const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
+            const Dir d = load_dir<ST>(o, k);
             const double slk = sl[k], suk = su[k], nlk = nl[k], nuk = nu[k];
             double cl = rcl[k], cu = rcu[k];
             if (fl) cl = sigma * gap - slk * nlk - d.dsl * d.dnl;
@@ -771,38 +815,31 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             rcl[k] = cl;
             rcu[k] = cu;
             double v = rsu[k];
-            if (fl) v -= (cl - nlk * rl) / slk;
-            if (fu) v += (cu - nuk * ru) / suk;
+            if (fl) v -= qdiv(cl - nlk * rl, slk);
+            if (fu) v += qdiv(cu - nuk * ru, suk);
             rhat[k] = v;
         }
         __syncwarp();
         if (!vector_sweep<ST, true>(N)) vector_sweep<ST, false>(N);
         rollout<ST>(N);
-        // corrector step length (qp.cpp:397) and update (qp.cpp:398-410); the
-        // directions are recomputed after the warp-wide min
+        // corrector directions + step length (qp.cpp:396-397)
         double alpha = 1.0;
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             const double u = U[k];
             const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
             double rl, ru;
             rlru(k, u, fl, fu, rl, ru);
             const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
-            if (fl) {
-                if (d.dsl < 0.0) alpha = smin(alpha, -tau * sl[k] / d.dsl);
-                if (d.dnl < 0.0) alpha = smin(alpha, -tau * nl[k] / d.dnl);
-            }
-            if (fu) {
-                if (d.dsu < 0.0) alpha = smin(alpha, -tau * su[k] / d.dsu);
-                if (d.dnu < 0.0) alpha = smin(alpha, -tau * nu[k] / d.dnu);
-            }
+            alpha = step_caps<ST>(o, k, fl, fu, d, tau, alpha);
         }
         alpha = warp_min(alpha);
+        // update (qp.cpp:398-410)
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             const double u = U[k];
             const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
-            double rl, ru;
-            rlru(k, u, fl, fu, rl, ru);
-            const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
+            const Dir d = load_dir<ST>(o, k);
             dU[k] = dU[k] + alpha * ddU[k];
             dX[k] = dX[k] + alpha * ddX[k];
             mu[k] = mu[k] + alpha * ddmu[k];
@@ -819,6 +856,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
         __syncwarp();
     }
     // final clamp (qp.cpp:414-419)
+#pragma unroll 1
     for (int k = lane; k < N; k += 32) {
         const double lb = umin - U[k], ub = umax - U[k];
         dU[k] = smin(smax(dU[k], lb), ub);
@@ -853,6 +891,7 @@ __device__ __noinline__ bool kkt_check(const Ocp& o, const double* lam, const do
     const double* Ju = SA(S_JU);
     double* tmp = SA(S_TMP);
     double gl = 0.0, gi = 0.0;
+#pragma unroll 1
     for (int k = lane; k < N; k += 32) {
         const double lk = lam[k], plk = pl[k], puk = pu[k];
         const double hu = (0.0 - Ju[k] * lk) + (puk - plk);
@@ -863,30 +902,32 @@ __device__ __noinline__ bool kkt_check(const Ocp& o, const double* lam, const do
         tmp[ST + k] = fabs(plk);
         tmp[2 * ST + k] = fabs(puk);
     }
-    gl = warp_max(gl);
-    gi = warp_max(gi);
     __syncwarp();
     // mults = one_norm(lam) + one_norm(pi_l) + one_norm(pi_u): three serial
-    // chains in one instruction stream (lanes 0, 1, 2)
-    const double* a = tmp + (lane % 3) * ST;
-    double s = 0.0;
-    for (int k = 0; k < N; ++k) s += a[k];
-    const double n1 = __shfl_sync(FULLMASK, s, 0);
-    const double n2 = __shfl_sync(FULLMASK, s, 1);
-    const double n3 = __shfl_sync(FULLMASK, s, 2);
+    // chains, all on every lane (no shuffles)
+    double n1 = 0.0, n2 = 0.0, n3 = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) {
+        n1 += tmp[k];
+        n2 += tmp[ST + k];
+        n3 += tmp[2 * ST + k];
+    }
     __syncwarp();
     double s_d = 1.0;
     if (m > 0) {
         const double mults = n1 + n2 + n3;
         s_d = smax(100.0, mults / m) / 100.0;
     }
-    return gl / s_d <= eps && gi <= eps;
+    // max over lanes of gl, divided by s_d > 0, is <= eps iff every lane's is
+    // (division by a positive number is monotone under rounding)
+    return __all_sync(FULLMASK, gl / s_d <= eps && gi <= eps);
 }
 
 /// reset_blocks (sqp.cpp:173-178): identity Hessian blocks.
 template <int ST>
 __device__ __forceinline__ void reset_blocks(int N) {
     const int lane = threadIdx.x & 31;
+#pragma unroll 1
     for (int k = lane; k <= N; k += 32) {
         SA(S_WQ)[k] = 1.0;
         SA(S_WM)[k] = 0.0;
@@ -974,6 +1015,7 @@ __device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt
     const double* nu = GA(G_NU);
     // merit_weights_update (sqp.cpp:12-20) + line_search terms (sqp.cpp:28-31)
     bool du_bad = false;
+#pragma unroll 1
     for (int k = lane; k < N; k += 32) {
         const double am = fabs(mu[k]);
         const double sg = first_merit ? am : smax(am, 0.5 * (sig[k] + am));
@@ -988,18 +1030,23 @@ __device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt
     {
         // two serial chains (even/odd lanes): penalty0 and dot(grad f, dxi);
         // the u slots contribute 0 * du (exactly +-0) unless du is not finite
-        const double* a = (lane & 1) ? tmp + ST : tmp;
-        double s = 0.0;
-        for (int k = 0; k < N; ++k) s += a[k];
-        penalty0 = __shfl_sync(FULLMASK, s, 0);
-        const double dot_gd = du_bad ? kNaN : __shfl_sync(FULLMASK, s, 1);
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll 1
+        for (int k = 0; k < N; ++k) {
+            s0 += tmp[k];
+            s1 += tmp[ST + k];
+        }
+        penalty0 = s0;
+        const double dot_gd = du_bad ? kNaN : s1;
         dd = dot_gd - penalty0;
         __syncwarp();
     }
     const double merit_before = *f + penalty0;
     double alpha = 1.0, merit = 0.0, f_trial = 0.0;
     bool ok = false;
+#pragma unroll 1
     for (int bt = 0;; ++bt) {
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             tU[k] = U[k] + alpha * dU[k];
             tX[k] = X[k] + alpha * dX[k];
@@ -1010,9 +1057,11 @@ __device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt
         if (st == ST_DOMAIN) return ST_DOMAIN << 4;
         merit = HUGE_VAL;
         if (st == ST_OK) {
+#pragma unroll 1
             for (int k = lane; k < N; k += 32) tmp[k] = sig[k] * fabs(tg[k]);
             __syncwarp();
             merit = f_trial;
+#pragma unroll 1
             for (int k = 0; k < N; ++k) merit += tmp[k];
             __syncwarp();
         }
@@ -1026,6 +1075,7 @@ __device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt
     // accept: xi_new = xi + a dxi equals the last trial bitwise, and so do f,
     // grad f and the constraint blocks (sqp.cpp:331-352)
     const double a = alpha;
+#pragma unroll 1
     for (int k = lane; k < N; k += 32) {
         U[k] = tU[k];
         X[k] = tX[k];
@@ -1039,6 +1089,7 @@ __device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt
     double* Wq = SA(S_WQ);
     double* Wm = SA(S_WM);
     double* Wr = SA(S_WR);
+#pragma unroll 1
     for (int blk = lane; blk <= N; blk += 32) {
         double s[2], y[2];
         int n;
@@ -1072,6 +1123,7 @@ __device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt
     __syncwarp();
     if (lost) reset_blocks<ST>(N);
     // the trial evaluation becomes the current one
+#pragma unroll 1
     for (int k = lane; k < N; k += 32) {
         gX[k] = tgX[k];
         g[k] = tg[k];
@@ -1101,6 +1153,7 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp& o, const nmpcmc_sqp_options&
     if (st == ST_DOMAIN) return SqpOut{false, ST_DOMAIN};
     if (st == ST_NONFINITE) return out;
 
+#pragma unroll 1
     for (int iter = 0;; ++iter) {
         if (kkt_check<ST>(o, GA(G_LAM), GA(G_PIL), GA(G_PIU), m, opt.eps)) {
             out.converged = true;
@@ -1110,6 +1163,7 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp& o, const nmpcmc_sqp_options&
         cnt->sqp_stage += N;
         // QP, with one identity-reset salvage attempt (sqp.cpp:263-278)
         int qs = QP_FAILED;
+#pragma unroll 1
         for (int attempt = 0; attempt < 2; ++attempt) {
             if (attempt == 1) reset_blocks<ST>(N);
             qs = solve_qp<ST>(o, opt.qp_tol, opt.qp_max_iter, cnt);
@@ -1120,6 +1174,7 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp& o, const nmpcmc_sqp_options&
         if (qs == QP_FAILED) break;  // rep.qp_failed
         // KKT certificate with the fresh QP multipliers (sqp.cpp:285-310)
         if (kkt_check<ST>(o, GA(G_MU), GA(G_NL), GA(G_NU), m, opt.eps)) {
+#pragma unroll 1
             for (int k = lane; k < N; k += 32) {
                 GA(G_LAM)[k] = GA(G_MU)[k];
                 GA(G_PIL)[k] = GA(G_NL)[k];
@@ -1155,26 +1210,31 @@ __device__ __noinline__ int start_iterate(const Ocp& o, bool warm, Cnt* cnt) {
     const bool fl = dfinite(o.umin), fh = dfinite(o.umax);
     const double u_nom = fl && fh ? 0.5 * (o.umin + o.umax) : smax(o.umin, smin(o.umax, 0.0));
     // u sequence: shifted_inputs (controllers.cpp:70-83) or nominal_input (:58-66)
+#pragma unroll 1
     for (int k = lane; k < N; k += 32)
         nU[k] = warm ? smax(o.umin, smin(o.umax, U[min(k + 1, N - 1)])) : u_nom;
     __syncwarp();
     const int st = xi_from_inputs<ST>(o, nU, nX, cnt);
     if (st == ST_DOMAIN) return ST_DOMAIN;
     if (st == ST_OK) {
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             U[k] = nU[k];
             X[k] = nX[k];
         }
     } else if (warm) {
         // shifted_warm_start (controllers.cpp:97-110)
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) nX[k] = X[min(k + 1, N - 1)];
         __syncwarp();
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             U[k] = nU[k];
             X[k] = nX[k];
         }
     } else {
         // flat guess (controllers.cpp:173-185)
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             U[k] = u_nom;
             X[k] = o.x0;
@@ -1184,6 +1244,7 @@ __device__ __noinline__ int start_iterate(const Ocp& o, bool warm, Cnt* cnt) {
     if (warm) {
         // shifted_multipliers (controllers.cpp:87-93); sqp_solve then projects
         // the warm bound multipliers onto >= 0 (sqp.cpp:219-222)
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             const int src = N >= 2 ? min(k + 1, N - 1) : k;
             tmp[k] = lam[src];
@@ -1191,12 +1252,14 @@ __device__ __noinline__ int start_iterate(const Ocp& o, bool warm, Cnt* cnt) {
             tmp[2 * ST + k] = piu[src];
         }
         __syncwarp();
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             lam[k] = tmp[k];
             pil[k] = smax(0.0, tmp[ST + k]);
             piu[k] = smax(0.0, tmp[2 * ST + k]);
         }
     } else {
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) {
             lam[k] = 0.0;
             pil[k] = 0.0;
@@ -1255,6 +1318,7 @@ __device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_
     int ocp_solves = 0, ocp_failures = 0;
     int row = 0;
 
+#pragma unroll 1
     for (int i = 0; i < nbar; ++i) {
         const double y = measure<NX>(p, pl, has_R, lR, rng);
         // ---- nmpc_step (controllers.cpp:114-212)
@@ -1262,6 +1326,7 @@ __device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_
             status = ST_NONFINITE;
             break;
         }
+#pragma unroll 1
         for (int k = lane; k < N; k += 32) GA(G_SP)[k] = setpoint_at(sc, t + (k + 1) * sc.Ts);
         // filter_update (ekf.cpp:59-96) with the jitter retry (controllers.cpp:123-132)
         double xf, Pn;
@@ -1309,6 +1374,7 @@ __device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_
             const double h = (t_next - t) / sc.np;
             double x = xf, P = Pn;
             int st = ST_OK;
+#pragma unroll 1
             for (int s = 0; s < sc.np && st == ST_OK; ++s) {
                 double k1x, k1p, k2x, k2p, k3x, k3p, k4x, k4p;
                 if ((st = joint_rhs1(o.p, x, P, u, k1x, k1p))) break;
@@ -1396,6 +1462,7 @@ __global__ void __launch_bounds__(32, 16) nmpc_kernel(const __grid_constant__ nm
                                                   nmpcmc_work_counters* counters, double* traj, int traj_rows,
                                                   double* gws_all, unsigned long long* next) {
     double* gws = gws_all + (size_t)blockIdx.x * kGlobArrays * ST;
+#pragma unroll 1
     for (;;) {
         unsigned long long i = 0;
         if ((threadIdx.x & 31) == 0) i = atomicAdd(next, 1ULL);
