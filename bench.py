@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sims-per-step", type=int, default=2960, help="NMPC (and PI) samples per rank per step")
+    ap.add_argument("--sims-per-step", type=int, default=9472,
+                    help="NMPC (and PI) samples per rank per step (9,472 = 4 waves of 148 SMs x 16 resident samples)")
     ap.add_argument("--horizon", type=int, default=60)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="NMPC samples for the CPU baseline (0 = host cores)")

@@ -72,6 +72,21 @@ __device__ __forceinline__ double warp_min(double m) {
 __device__ __forceinline__ int warp_min_int(int v) { return __reduce_min_sync(FULLMASK, v); }
 __device__ __forceinline__ int warp_sum_int(int v) { return __reduce_add_sync(FULLMASK, v); }
 __device__ __forceinline__ bool warp_any(bool p) { return __any_sync(FULLMASK, p); }
+/// Exact warp min / max of NON-NEGATIVE doubles via REDUX on the bit
+/// patterns (IEEE order is the unsigned order of the words for x >= 0):
+/// two single-instruction reductions instead of ten shuffles.
+__device__ __forceinline__ double warp_min_pos(double a) {
+    const unsigned hi = (unsigned)__double2hiint(a), lo = (unsigned)__double2loint(a);
+    const unsigned mh = __reduce_min_sync(FULLMASK, hi);
+    const unsigned ml = __reduce_min_sync(FULLMASK, hi == mh ? lo : 0xffffffffu);
+    return __hiloint2double((int)mh, (int)ml);
+}
+__device__ __forceinline__ double warp_max_pos(double a) {
+    const unsigned hi = (unsigned)__double2hiint(a), lo = (unsigned)__double2loint(a);
+    const unsigned mh = __reduce_max_sync(FULLMASK, hi);
+    const unsigned ml = __reduce_max_sync(FULLMASK, hi == mh ? lo : 0u);
+    return __hiloint2double((int)mh, (int)ml);
+}
 
 // ------------------------------------------- certified fast sqrt / division
 // Certificates work on the high words only (cheap integer ops). Windows:
@@ -656,7 +671,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
         rcu[k] = 0.0;
     }
     if (warp_any(bad)) return QP_DOMAIN;
-    ds = warp_max(ds);
+    ds = warp_max_pos(ds);  // ds >= 1
     const int m = warp_sum_int(nfin);
     const double eps = tol * ds;
     __syncwarp();
@@ -774,7 +789,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
                 const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
                 alpha_aff = step_caps<ST>(o, k, fl, fu, d, 1.0, alpha_aff);
             }
-            alpha_aff = warp_min(alpha_aff);
+            alpha_aff = warp_min_pos(alpha_aff);  // step lengths lie in (0, 1]
             if (m > 0 && gap > 0.0) {
 #pragma unroll 1
                 for (int k = lane; k < N; k += 32) {
@@ -833,7 +848,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
             alpha = step_caps<ST>(o, k, fl, fu, d, tau, alpha);
         }
-        alpha = warp_min(alpha);
+        alpha = warp_min_pos(alpha);
         // update (qp.cpp:398-410)
 #pragma unroll 1
         for (int k = lane; k < N; k += 32) {
@@ -936,6 +951,8 @@ __device__ __forceinline__ void reset_blocks(int N) {
     __syncwarp();
 }
 
+__device__ __noinline__ double qdiv(double a, double b);
+
 /// bfgs_block_update (sqp.cpp:61-84) for a block of size n (1 or 2) stored as
 /// (q, m, r) = (w00, w01 = w10, w11). Returns -1 on NotPositiveDefinite,
 /// 0 if skipped, 1 if updated.
@@ -947,11 +964,11 @@ __device__ __forceinline__ int bfgs_block(double& q, double& mm, double& r, int 
         const double sws = dot1(s[0], ws);
         if (!(sws > kEpsMach)) return 0;
         const double sy = dot1(s[0], y[0]);
-        const double theta = sy >= 0.2 * sws ? 1.0 : 0.8 * sws / (sws - sy);
+        const double theta = sy >= 0.2 * sws ? 1.0 : qdiv(0.8 * sws, sws - sy);
         const double rr = theta * y[0] + (1.0 - theta) * ws;
         const double sr = dot1(s[0], rr);
         if (!(smin(sws, sr) > kEpsMach)) return 0;
-        wv += rr * rr / sr - ws * ws / sws;
+        wv += qdiv(rr * rr, sr) - qdiv(ws * ws, sws);
         if (wv <= 0.0 || !dfinite(wv)) return -1;
         return 1;
     }
@@ -960,19 +977,19 @@ __device__ __forceinline__ int bfgs_block(double& q, double& mm, double& r, int 
     const double sws = 0.0 + s[0] * ws0 + s[1] * ws1;
     if (!(sws > kEpsMach)) return 0;
     const double sy = 0.0 + s[0] * y[0] + s[1] * y[1];
-    const double theta = sy >= 0.2 * sws ? 1.0 : 0.8 * sws / (sws - sy);
+    const double theta = sy >= 0.2 * sws ? 1.0 : qdiv(0.8 * sws, sws - sy);
     const double r0 = theta * y[0] + (1.0 - theta) * ws0;
     const double r1 = theta * y[1] + (1.0 - theta) * ws1;
     const double sr = 0.0 + s[0] * r0 + s[1] * r1;
     if (!(smin(sws, sr) > kEpsMach)) return 0;
-    q += r0 * r0 / sr - ws0 * ws0 / sws;
-    mm += r1 * r0 / sr - ws1 * ws0 / sws;  // w(1,0) == w(0,1): same products, commuted
-    r += r1 * r1 / sr - ws1 * ws1 / sws;
+    q += qdiv(r0 * r0, sr) - qdiv(ws0 * ws0, sws);
+    mm += qdiv(r1 * r0, sr) - qdiv(ws1 * ws0, sws);  // w(1,0) == w(0,1): same products, commuted
+    r += qdiv(r1 * r1, sr) - qdiv(ws1 * ws1, sws);
     mm = 0.5 * (mm + mm);                  // symmetrize
     // cholesky_factor audit (linalg.cpp:69-103)
     if (q <= 0.0 || !dfinite(q)) return -1;
     const double l00 = sqrt(q);
-    const double l10 = mm / l00;
+    const double l10 = qdiv(mm, l00);
     const double d = r - l10 * l10;
     if (d <= 0.0 || !dfinite(d)) return -1;
     return 1;
@@ -1376,13 +1393,38 @@ __device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_
             int st = ST_OK;
 #pragma unroll 1
             for (int s = 0; s < sc.np && st == ST_OK; ++s) {
-                double k1x, k1p, k2x, k2p, k3x, k3p, k4x, k4p;
-                if ((st = joint_rhs1(o.p, x, P, u, k1x, k1p))) break;
-                if ((st = joint_rhs1(o.p, x + 0.5 * h * k1x, P + 0.5 * h * k1p, u, k2x, k2p))) break;
-                if ((st = joint_rhs1(o.p, x + 0.5 * h * k2x, P + 0.5 * h * k2p, u, k3x, k3p))) break;
-                if ((st = joint_rhs1(o.p, x + h * k3x, P + h * k3p, u, k4x, k4p))) break;
-                x += (h / 6.0) * (k1x + 2.0 * k2x + 2.0 * k3x + k4x);
-                P += (h / 6.0) * (k1p + 2.0 * k2p + 2.0 * k3p + k4p);
+                // RK4 stages at (x, P) + c h k_{j-1}, c = 0, 1/2, 1/2, 1, with
+                // 0.5 * h * k formed as (0.5 * h) * k (ekf.cpp:38-44); the
+                // weighted sum accumulates left to right (ekf.cpp:46-50)
+                double pkx = 0.0, pkp = 0.0, ax = 0.0, ap = 0.0;
+#pragma unroll 1
+                for (int j = 0; j < 4 && st == ST_OK; ++j) {
+                    double xs = x, ps = P;
+                    if (j == 1 || j == 2) {
+                        xs = x + 0.5 * h * pkx;
+                        ps = P + 0.5 * h * pkp;
+                    } else if (j == 3) {
+                        xs = x + h * pkx;
+                        ps = P + h * pkp;
+                    }
+                    double kx, kp;
+                    st = joint_rhs1(o.p, xs, ps, u, kx, kp);
+                    if (j == 0) {
+                        ax = kx;
+                        ap = kp;
+                    } else if (j < 3) {
+                        ax = ax + 2.0 * kx;
+                        ap = ap + 2.0 * kp;
+                    } else {
+                        ax = ax + kx;
+                        ap = ap + kp;
+                    }
+                    pkx = kx;
+                    pkp = kp;
+                }
+                if (st != ST_OK) break;
+                x += (h / 6.0) * ax;
+                P += (h / 6.0) * ap;
                 if (!dfinite(x) || !dfinite(P)) st = ST_NONFINITE;
             }
             if (st != ST_OK) {
