@@ -105,11 +105,9 @@ __device__ __forceinline__ bool mant_nonzero(double x) {
     return ((__double2hiint(x) & 0x000fffff) | __double2loint(x)) != 0;
 }
 
-/// l = sqrt(h) and y ~ 1/l for h > 0 (Newton on the rsqrt seed, Markstein
-/// correction). Returns true only if l is certified RN(sqrt(h)): the exact
-/// residual h - l^2 lies strictly inside (-l ulp(l), l ulp(l)) shrunk by
-/// 2^-50, l is not a power of two, and l is inside its window.
-__device__ __forceinline__ bool fast_sqrt(double h, double& l, double& y) {
+/// l ~ sqrt(h) and y ~ 1/l for h > 0: Newton on the hardware rsqrt seed and
+/// a Markstein correction. Not yet certified (see cert_sqrt).
+__device__ __forceinline__ void fast_sqrt(double h, double& l, double& y) {
     double y0;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(h));
     const double hh = 0.5 * h;
@@ -121,20 +119,29 @@ __device__ __forceinline__ bool fast_sqrt(double h, double& l, double& y) {
     const double d = __fma_rn(-s, s, h);
     l = __fma_rn(d, 0.5 * y0, s);
     y = y0;
+}
+/// q ~ a / b from y ~ 1/b (Markstein correction); 3 dependent operations.
+/// Not yet certified (see cert_div).
+__device__ __forceinline__ double fast_div(double a, double b, double y) {
+    const double q0 = a * y;
+    const double e0 = __fma_rn(-b, q0, a);
+    return __fma_rn(e0, y, q0);
+}
+/// True only if l is RN(sqrt(h)): the exact residual h - l^2 lies strictly
+/// inside (-l ulp(l), l ulp(l)) shrunk by 2^-50, l is not a power of two and
+/// inside its window.
+__device__ __forceinline__ bool cert_sqrt(double h, double l) {
     const double r = __fma_rn(-l, l, h);
     const double bound = (l * (1.0 - 0x1.0p-50)) * (2.0 * half_ulp_hi(l));
     return hi_window(l, 1023u - 200u, 400u) && mant_nonzero(l) && fabs(r) < bound;
 }
-
-/// q = a / b with y ~ 1/b (b > 0 inside the pivot window), bs = b (1 - 2^-50):
-/// Markstein correction, certified by the exact residual a - b q lying
-/// strictly inside b ulp(q) / 2 (q not a power of two, a inside its window).
-__device__ __forceinline__ bool fast_div(double a, double b, double y, double bs, double& q) {
-    const double q0 = a * y;
-    const double e0 = __fma_rn(-b, q0, a);
-    q = __fma_rn(e0, y, q0);
+/// True only if q is RN(a / b) for b > 0: the exact residual a - b q lies
+/// strictly inside b ulp(q) / 2 (shrunk), q not a power of two, a and b
+/// inside their windows.
+__device__ __forceinline__ bool cert_div(double a, double b, double q) {
     const double e = __fma_rn(-b, q, a);
-    return hi_window(a, 1023u - 400u, 800u) && mant_nonzero(q) && fabs(e) < bs * half_ulp_hi(q);
+    return hi_window(a, 1023u - 400u, 800u) && hi_window(b, 1023u - 200u, 400u) && mant_nonzero(q) &&
+           fabs(e) < (b * (1.0 - 0x1.0p-50)) * half_ulp_hi(q);
 }
 
 // ------------------------------------------------------- one-state model
@@ -281,6 +288,7 @@ enum GlobId {
     G_GX, G_G, G_TGX, G_TG, G_TJX, G_TJU,
     G_SIG, G_SP, G_DU, G_DX, G_MU, G_NL, G_NU, G_SL, G_SU, G_RSU, G_RCL, G_RCU,
     G_DSL, G_DSU, G_DNL, G_DNU,
+    G_CHH, G_CA1, G_CQ1, G_CG1,  // certificate inputs of the fast Riccati sweeps
     kGlobArrays
 };
 
@@ -402,10 +410,13 @@ enum { QP_OPTIMAL = 0, QP_MAXITER = 1, QP_FAILED = 2, QP_DOMAIN = -1 };
 
 /// riccati_factor (qp.cpp:73-110) fused with the affine backward vector sweep
 /// of riccati_solve_vectors (qp.cpp:122-141). Serial in k, all lanes.
-/// Returns true on NotPositiveDefinite. FAST: certified sqrt/division; *ok_out
-/// is false if any certificate failed (the caller then replays FAST = false).
+/// Returns true on NotPositiveDefinite. FAST: sqrt and the four divisions by
+/// each pivot use the 3-operation fast forms; their inputs are stashed so that
+/// certify_factor() can prove every result is the IEEE one afterwards (the
+/// caller replays FAST = false otherwise).
 template <int ST, bool FAST>
-__device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
+__device__ __noinline__ bool factor_sweep(const Ocp& o) {
+    const int N = o.N;
     const double* Ju = SA(S_JU);
     const double* Jx = SA(S_JX);
     const double* Wq = SA(S_WQ);
@@ -422,7 +433,10 @@ __device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
     double* gmat = SA(S_GMAT);
     double* pvec = SA(S_PVEC);
     double* dff = SA(S_DFF);
-    bool ok = true;
+    double* chh = GA(G_CHH);
+    double* ca1 = GA(G_CA1);
+    double* cq1 = GA(G_CQ1);
+    double* cg1 = GA(G_CG1);
     double P = Wq[N];
     double pv = rsx[N - 1];  // pvec[N] = qhat[N]
     val[N] = P;
@@ -433,14 +447,11 @@ __device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
         double hh = ju * (P * ju);
         hh = hh + Wr[k];
         hh = hh + bar[k];
-        if (hh <= 0.0 || !dfinite(hh)) {  // cholesky_factor -> QP Failed (qp.cpp:358-364)
-            *ok_out = ok;
-            return true;
-        }
-        double l, y, ls;
+        if (hh <= 0.0 || !dfinite(hh)) return true;  // cholesky_factor -> QP Failed (qp.cpp:358-364)
+        double l, y;
         if (FAST) {
-            ok &= fast_sqrt(hh, l, y);
-            ls = l * (1.0 - 0x1.0p-50);
+            fast_sqrt(hh, l, y);
+            chh[k] = hh;
         } else {
             l = sqrt(hh);
             y = 1.0 / l;  // seed for the corrector sweep's fast division
@@ -450,8 +461,10 @@ __device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
         const double tmpv = P * -rdyn[k] + pv;
         double hv = ju * tmpv + rhat[k];
         if (FAST) {
-            ok &= fast_div(hv, l, y, ls, hv);
-            ok &= fast_div(hv, l, y, ls, hv);
+            ca1[k] = hv;
+            hv = fast_div(hv, l, y);
+            cq1[k] = hv;
+            hv = fast_div(hv, l, y);
         } else {
             hv = hv / l;
             hv = hv / l;
@@ -465,8 +478,9 @@ __device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
             gg = gg + Wm[k];
             double gn;
             if (FAST) {
-                ok &= fast_div(gg, l, y, ls, gn);
-                ok &= fast_div(gn, l, y, ls, gn);
+                gn = fast_div(gg, l, y);
+                cg1[k] = gn;
+                gn = fast_div(gn, l, y);
             } else {
                 gn = gg / l;
                 gn = gn / l;
@@ -485,14 +499,33 @@ __device__ __noinline__ bool factor_sweep(int N, bool* ok_out) {
             pv = pvn;
         }
     }
-    *ok_out = ok;
     return false;
 }
 
-/// Corrector backward vector sweep with the cached factor (qp.cpp:122-141).
-/// Returns false if a FAST certificate failed (caller replays FAST = false).
+/// Lane-parallel certificate of a FAST factor_sweep: every sqrt and division
+/// of every stage is the IEEE correctly rounded result (cert_sqrt/cert_div).
+template <int ST>
+__device__ __noinline__ bool certify_factor(const Ocp& o) {
+    const int lane = threadIdx.x & 31;
+    bool ok = true;
+#pragma unroll 1
+    for (int k = lane; k < o.N; k += 32) {
+        const double l = SA(S_CHOLH)[k];
+        const double q1 = GA(G_CQ1)[k];
+        ok = ok && cert_sqrt(GA(G_CHH)[k], l) && cert_div(GA(G_CA1)[k], l, q1) && cert_div(q1, l, -SA(S_DFF)[k]);
+        if (k >= 1) {
+            const double g1 = GA(G_CG1)[k];
+            ok = ok && cert_div(SA(S_GMAT)[k], l, g1) && cert_div(g1, l, -SA(S_GAIN)[k]);
+        }
+    }
+    return __all_sync(FULLMASK, ok);
+}
+
+/// Corrector backward vector sweep with the cached factor (qp.cpp:122-141);
+/// FAST stashes the division inputs for certify_vector().
 template <int ST, bool FAST>
-__device__ __noinline__ bool vector_sweep(int N) {
+__device__ __noinline__ void vector_sweep(const Ocp& o) {
+    const int N = o.N;
     const double* Ju = SA(S_JU);
     const double* Jx = SA(S_JX);
     const double* rdyn = SA(S_RDYN);
@@ -504,7 +537,8 @@ __device__ __noinline__ bool vector_sweep(int N) {
     const double* gmat = SA(S_GMAT);
     double* pvec = SA(S_PVEC);
     double* dff = SA(S_DFF);
-    bool ok = true;
+    double* ca1 = GA(G_CA1);
+    double* cq1 = GA(G_CQ1);
     double pv = rsx[N - 1];
     pvec[N] = pv;
 #pragma unroll 1
@@ -514,10 +548,10 @@ __device__ __noinline__ bool vector_sweep(int N) {
         double hv = Ju[k] * tmpv + rhat[k];
         if (FAST) {
             const double y = rinv[k];
-            const double ls = l * (1.0 - 0x1.0p-50);
-            ok &= hi_window(l, 1023u - 200u, 400u);
-            ok &= fast_div(hv, l, y, ls, hv);
-            ok &= fast_div(hv, l, y, ls, hv);
+            ca1[k] = hv;
+            hv = fast_div(hv, l, y);
+            cq1[k] = hv;
+            hv = fast_div(hv, l, y);
         } else {
             hv = hv / l;
             hv = hv / l;
@@ -531,7 +565,19 @@ __device__ __noinline__ bool vector_sweep(int N) {
             pv = pvn;
         }
     }
-    return ok;
+}
+
+template <int ST>
+__device__ __noinline__ bool certify_vector(const Ocp& o) {
+    const int lane = threadIdx.x & 31;
+    bool ok = true;
+#pragma unroll 1
+    for (int k = lane; k < o.N; k += 32) {
+        const double l = SA(S_CHOLH)[k];
+        const double q1 = GA(G_CQ1)[k];
+        ok = ok && cert_div(GA(G_CA1)[k], l, q1) && cert_div(q1, l, -SA(S_DFF)[k]);
+    }
+    return __all_sync(FULLMASK, ok);
 }
 
 /// Forward rollout (qp.cpp:142-155): step dxi (DDU, DDX) and dmu (DDMU).
@@ -768,9 +814,12 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             rhat[k] = v;
         }
         __syncwarp();
-        bool ok;
-        bool npd = factor_sweep<ST, true>(N, &ok);
-        if (!ok) npd = factor_sweep<ST, false>(N, &ok);
+        __syncwarp();
+        bool npd = factor_sweep<ST, true>(o);
+        __syncwarp();
+        // a pivot the fast sqrt got wrong could also change the NPD decision
+        // downstream, so any failed certificate replays the whole sweep
+        if (!certify_factor<ST>(o)) npd = factor_sweep<ST, false>(o);
         if (npd) {
             status = QP_FAILED;
             break;
@@ -798,15 +847,15 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
                     const Dir d = load_dir<ST>(o, k);
                     tmp[k] = fl ? (sl[k] + alpha_aff * d.dsl) * (nl[k] + alpha_aff * d.dnl) : 0.0;
                     tmp[ST + k] = fu ? (su[k] + alpha_aff * d.dsu) * (nu[k] + alpha_aff * d.dnu) : 0.0;
-                    tmp[2 * ST + k] = (fl ? 1.0 : 0.0) + (fu ? 2.0 : 0.0);
                 }
                 __syncwarp();
+                // terms of infinite bounds are stored as +0: adding +0 to this
+                // sum of non-negative products (never -0) changes nothing
                 double gap_aff = 0.0;
 #pragma unroll 1
                 for (int k = 0; k < N; ++k) {
-                    const double f = tmp[2 * ST + k];
-                    if (f == 1.0 || f == 3.0) gap_aff += tmp[k];
-                    if (f >= 2.0) gap_aff += tmp[ST + k];
+                    gap_aff += tmp[k];
+                    gap_aff += tmp[ST + k];
                 }
                 gap_aff /= m;
                 const double ratio = smax(0.0, gap_aff / gap);
@@ -835,7 +884,9 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             rhat[k] = v;
         }
         __syncwarp();
-        if (!vector_sweep<ST, true>(N)) vector_sweep<ST, false>(N);
+        vector_sweep<ST, true>(o);
+        __syncwarp();
+        if (!certify_vector<ST>(o)) vector_sweep<ST, false>(o);
         rollout<ST>(N);
         // corrector directions + step length (qp.cpp:396-397)
         double alpha = 1.0;
