@@ -276,21 +276,42 @@ __host__ __device__ inline int ws_stride_for(int N) { return N < 32 ? 32 : N < 6
 /// per resident sample) holds the rest, touched only by lane-parallel loops.
 extern __shared__ __align__(16) double smem_nmpc[];
 
+// NMPCMC_IPM_SMEM = 1 places the interior-point state and direction arrays
+// (touched by every lane-parallel IPM phase) in shared memory, 0 in L2.
+#ifndef NMPCMC_IPM_SMEM
+#define NMPCMC_IPM_SMEM 0
+#endif
 enum SmemId {
     S_JX, S_JU, S_WQ, S_WM, S_WR, S_BAR, S_RDYN, S_RHAT, S_RSX,
     S_CHOLH, S_RINV, S_VAL, S_GAIN, S_GMAT, S_PVEC, S_DFF,
     S_DDU, S_DDX, S_DDMU,
     S_TMP,  // three strides
-    kSmemArrays = S_TMP + 3
+    S_IPM0 = S_TMP + 3,
+#if NMPCMC_IPM_SMEM
+    kSmemArrays = S_IPM0 + 14
+#else
+    kSmemArrays = S_IPM0
+#endif
 };
 enum GlobId {
     G_U, G_X, G_TU, G_TX, G_LAM, G_PIL, G_PIU,
     G_GX, G_G, G_TGX, G_TG, G_TJX, G_TJU,
-    G_SIG, G_SP, G_DU, G_DX, G_MU, G_NL, G_NU, G_SL, G_SU, G_RSU, G_RCL, G_RCU,
-    G_DSL, G_DSU, G_DNL, G_DNU,
+    G_SIG, G_SP,
     G_CHH, G_CA1, G_CQ1, G_CG1,  // certificate inputs of the fast Riccati sweeps
-    kGlobArrays
+    G_IPM0,
+#if NMPCMC_IPM_SMEM
+    kGlobArrays = G_IPM0
+#else
+    kGlobArrays = G_IPM0 + 14
+#endif
 };
+/// interior-point arrays: DU DX MU NL NU SL SU RSU RCL RCU DSL DSU DNL DNU
+enum IpmId { I_DU, I_DX, I_MU, I_NL, I_NU, I_SL, I_SU, I_RSU, I_RCL, I_RCU, I_DSL, I_DSU, I_DNL, I_DNU };
+#if NMPCMC_IPM_SMEM
+#define IA(id) (smem_nmpc + (S_IPM0 + (id)) * ST)
+#else
+#define IA(id) (o.gws + (G_IPM0 + (id)) * ST)
+#endif
 
 /// Out-of-line IEEE division for the lane-parallel loops: one call site per
 /// use instead of an inlined ~25-instruction sequence keeps the hot code small
@@ -621,17 +642,17 @@ __device__ __forceinline__ Dir expand_k(const Ocp& o, int k, bool fl, bool fu, d
     Dir d;
     d.dsl = fl ? dv + rl : 0.0;
     d.dsu = fu ? ru - dv : 0.0;
-    d.dnl = fl ? qdiv(GA(G_RCL)[k] - GA(G_NL)[k] * d.dsl, GA(G_SL)[k]) : 0.0;
-    d.dnu = fu ? qdiv(GA(G_RCU)[k] - GA(G_NU)[k] * d.dsu, GA(G_SU)[k]) : 0.0;
-    GA(G_DSL)[k] = d.dsl;
-    GA(G_DSU)[k] = d.dsu;
-    GA(G_DNL)[k] = d.dnl;
-    GA(G_DNU)[k] = d.dnu;
+    d.dnl = fl ? qdiv(IA(I_RCL)[k] - IA(I_NL)[k] * d.dsl, IA(I_SL)[k]) : 0.0;
+    d.dnu = fu ? qdiv(IA(I_RCU)[k] - IA(I_NU)[k] * d.dsu, IA(I_SU)[k]) : 0.0;
+    IA(I_DSL)[k] = d.dsl;
+    IA(I_DSU)[k] = d.dsu;
+    IA(I_DNL)[k] = d.dnl;
+    IA(I_DNU)[k] = d.dnu;
     return d;
 }
 template <int ST>
 __device__ __forceinline__ Dir load_dir(const Ocp& o, int k) {
-    return Dir{GA(G_DSL)[k], GA(G_DSU)[k], GA(G_DNL)[k], GA(G_DNU)[k]};
+    return Dir{IA(I_DSL)[k], IA(I_DSU)[k], IA(I_DNL)[k], IA(I_DNU)[k]};
 }
 /// max_step's cap (qp.cpp:321-337) for the four (value, direction) pairs of
 /// stage k: alpha = min(alpha, -frac value / dir) over dir < 0.
@@ -639,12 +660,12 @@ template <int ST>
 __device__ __forceinline__ double step_caps(const Ocp& o, int k, bool fl, bool fu, const Dir& d, double frac,
                                             double alpha) {
     if (fl) {
-        if (d.dsl < 0.0) alpha = smin(alpha, qdiv(-frac * GA(G_SL)[k], d.dsl));
-        if (d.dnl < 0.0) alpha = smin(alpha, qdiv(-frac * GA(G_NL)[k], d.dnl));
+        if (d.dsl < 0.0) alpha = smin(alpha, qdiv(-frac * IA(I_SL)[k], d.dsl));
+        if (d.dnl < 0.0) alpha = smin(alpha, qdiv(-frac * IA(I_NL)[k], d.dnl));
     }
     if (fu) {
-        if (d.dsu < 0.0) alpha = smin(alpha, qdiv(-frac * GA(G_SU)[k], d.dsu));
-        if (d.dnu < 0.0) alpha = smin(alpha, qdiv(-frac * GA(G_NU)[k], d.dnu));
+        if (d.dsu < 0.0) alpha = smin(alpha, qdiv(-frac * IA(I_SU)[k], d.dsu));
+        if (d.dnu < 0.0) alpha = smin(alpha, qdiv(-frac * IA(I_NU)[k], d.dnu));
     }
     return alpha;
 }
@@ -668,16 +689,16 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
     const double* Wq = SA(S_WQ);
     const double* Wm = SA(S_WM);
     const double* Wr = SA(S_WR);
-    double* dU = GA(G_DU);
-    double* dX = GA(G_DX);
-    double* mu = GA(G_MU);
-    double* nl = GA(G_NL);
-    double* nu = GA(G_NU);
-    double* sl = GA(G_SL);
-    double* su = GA(G_SU);
-    double* rsu = GA(G_RSU);
-    double* rcl = GA(G_RCL);
-    double* rcu = GA(G_RCU);
+    double* dU = IA(I_DU);
+    double* dX = IA(I_DX);
+    double* mu = IA(I_MU);
+    double* nl = IA(I_NL);
+    double* nu = IA(I_NU);
+    double* sl = IA(I_SL);
+    double* su = IA(I_SU);
+    double* rsu = IA(I_RSU);
+    double* rcl = IA(I_RCL);
+    double* rcu = IA(I_RCU);
     double* rsx = SA(S_RSX);
     double* rdyn = SA(S_RDYN);
     double* rhat = SA(S_RHAT);
@@ -1076,11 +1097,11 @@ __device__ __noinline__ int sqp_step(const Ocp& o, const nmpcmc_sqp_options& opt
     double* Ju = SA(S_JU);
     double* sig = GA(G_SIG);
     double* tmp = SA(S_TMP);
-    const double* dU = GA(G_DU);
-    const double* dX = GA(G_DX);
-    const double* mu = GA(G_MU);
-    const double* nl = GA(G_NL);
-    const double* nu = GA(G_NU);
+    const double* dU = IA(I_DU);
+    const double* dX = IA(I_DX);
+    const double* mu = IA(I_MU);
+    const double* nl = IA(I_NL);
+    const double* nu = IA(I_NU);
     // merit_weights_update (sqp.cpp:12-20) + line_search terms (sqp.cpp:28-31)
     bool du_bad = false;
 #pragma unroll 1
@@ -1241,12 +1262,12 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp& o, const nmpcmc_sqp_options&
         if (qs == QP_DOMAIN) return SqpOut{false, ST_DOMAIN};
         if (qs == QP_FAILED) break;  // rep.qp_failed
         // KKT certificate with the fresh QP multipliers (sqp.cpp:285-310)
-        if (kkt_check<ST>(o, GA(G_MU), GA(G_NL), GA(G_NU), m, opt.eps)) {
+        if (kkt_check<ST>(o, IA(I_MU), IA(I_NL), IA(I_NU), m, opt.eps)) {
 #pragma unroll 1
             for (int k = lane; k < N; k += 32) {
-                GA(G_LAM)[k] = GA(G_MU)[k];
-                GA(G_PIL)[k] = GA(G_NL)[k];
-                GA(G_PIU)[k] = GA(G_NU)[k];
+                GA(G_LAM)[k] = IA(I_MU)[k];
+                GA(G_PIL)[k] = IA(I_NL)[k];
+                GA(G_PIU)[k] = IA(I_NU)[k];
             }
             __syncwarp();
             out.converged = true;
@@ -1631,5 +1652,6 @@ inline int launch_nmpc(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int
 
 #undef SA
 #undef GA
+#undef IA
 
 }  // namespace nmpcmc_dev

@@ -19,7 +19,7 @@ import numpy as np
 
 from . import abi
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libnmpcmc_gpu.so")
+_LIB_PATH = os.environ.get("NMPCMC_GPU_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libnmpcmc_gpu.so")
 _lib = None
 
 
