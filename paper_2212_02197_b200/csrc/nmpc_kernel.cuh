@@ -284,7 +284,7 @@ extern __shared__ __align__(16) double smem_nmpc[];
 enum SmemId {
     S_JX, S_JU, S_WQ, S_WM, S_WR, S_BAR, S_RDYN, S_RHAT, S_RSX,
     S_CHOLH, S_RINV, S_VAL, S_GAIN, S_GMAT, S_PVEC, S_DFF,
-    S_DDU, S_DDX, S_DDMU,
+    S_DDU, S_DDX,
     S_TMP,  // three strides
     S_IPM0 = S_TMP + 3,
 #if NMPCMC_IPM_SMEM
@@ -462,13 +462,19 @@ __device__ __noinline__ bool factor_sweep(const Ocp& o) {
     double pv = rsx[N - 1];  // pvec[N] = qhat[N]
     val[N] = P;
     pvec[N] = pv;
+    // the head of the P chain (ju, Wr, bar) is loaded one stage ahead
+    double ju = Ju[N - 1], wr = Wr[N - 1], br = bar[N - 1];
 #pragma unroll 1
     for (int k = N - 1; k >= 0; --k) {
-        const double ju = Ju[k];
+        const int kn = k > 0 ? k - 1 : 0;
+        const double jun = Ju[kn], wrn = Wr[kn], brn = bar[kn];
         double hh = ju * (P * ju);
-        hh = hh + Wr[k];
-        hh = hh + bar[k];
-        if (hh <= 0.0 || !dfinite(hh)) return true;  // cholesky_factor -> QP Failed (qp.cpp:358-364)
+        hh = hh + wr;
+        hh = hh + br;
+        // cholesky_factor -> QP Failed (qp.cpp:358-364); tested at the end of
+        // the stage so the branch does not sit on the chain (a failing stage's
+        // values are never used)
+        const bool npd = hh <= 0.0 || !dfinite(hh);
         double l, y;
         if (FAST) {
             fast_sqrt(hh, l, y);
@@ -519,6 +525,10 @@ __device__ __noinline__ bool factor_sweep(const Ocp& o) {
             P = pn;
             pv = pvn;
         }
+        if (npd) return true;
+        ju = jun;
+        wr = wrn;
+        br = brn;
     }
     return false;
 }
@@ -542,6 +552,26 @@ __device__ __noinline__ bool certify_factor(const Ocp& o) {
     return __all_sync(FULLMASK, ok);
 }
 
+/// Certificate of stage k of a FAST factor_sweep (fused into a later loop).
+template <int ST>
+__device__ __forceinline__ bool certify_factor_k(const Ocp& o, int k) {
+    const double l = SA(S_CHOLH)[k];
+    const double q1 = GA(G_CQ1)[k];
+    bool ok = cert_sqrt(GA(G_CHH)[k], l) && cert_div(GA(G_CA1)[k], l, q1) && cert_div(q1, l, -SA(S_DFF)[k]);
+    if (k >= 1) {
+        const double g1 = GA(G_CG1)[k];
+        ok = ok && cert_div(SA(S_GMAT)[k], l, g1) && cert_div(g1, l, -SA(S_GAIN)[k]);
+    }
+    return ok;
+}
+/// Certificate of stage k of a FAST vector_sweep.
+template <int ST>
+__device__ __forceinline__ bool certify_vector_k(const Ocp& o, int k) {
+    const double l = SA(S_CHOLH)[k];
+    const double q1 = GA(G_CQ1)[k];
+    return cert_div(GA(G_CA1)[k], l, q1) && cert_div(q1, l, -SA(S_DFF)[k]);
+}
+
 /// Corrector backward vector sweep with the cached factor (qp.cpp:122-141);
 /// FAST stashes the division inputs for certify_vector().
 template <int ST, bool FAST>
@@ -562,11 +592,15 @@ __device__ __noinline__ void vector_sweep(const Ocp& o) {
     double* cq1 = GA(G_CQ1);
     double pv = rsx[N - 1];
     pvec[N] = pv;
+    // operands at the head of the pv chain are loaded one stage ahead
+    double vl = val[N], rd = rdyn[N - 1], ju = Ju[N - 1], rh = rhat[N - 1];
 #pragma unroll 1
     for (int k = N - 1; k >= 0; --k) {
+        const int kn = k > 0 ? k - 1 : 0;
+        const double vln = val[kn + 1], rdn = rdyn[kn], jun = Ju[kn], rhn = rhat[kn];
         const double l = cholh[k];
-        const double tmpv = val[k + 1] * -rdyn[k] + pv;
-        double hv = Ju[k] * tmpv + rhat[k];
+        const double tmpv = vl * -rd + pv;
+        double hv = ju * tmpv + rh;
         if (FAST) {
             const double y = rinv[k];
             ca1[k] = hv;
@@ -585,6 +619,10 @@ __device__ __noinline__ void vector_sweep(const Ocp& o) {
             pvec[k] = pvn;
             pv = pvn;
         }
+        vl = vln;
+        rd = rdn;
+        ju = jun;
+        rh = rhn;
     }
 }
 
@@ -601,32 +639,39 @@ __device__ __noinline__ bool certify_vector(const Ocp& o) {
     return __all_sync(FULLMASK, ok);
 }
 
-/// Forward rollout (qp.cpp:142-155): step dxi (DDU, DDX) and dmu (DDMU).
+/// Forward rollout (qp.cpp:142-155): step dxi (DDU, DDX). The multiplier step
+/// dmu_k = -(P_{k+1} dx_k + p_{k+1}) (qp.cpp:153) is off the dx chain and is
+/// formed where it is consumed (the update loop of solve_qp).
 template <int ST>
 __device__ __noinline__ void rollout(int N) {
     const double* Ju = SA(S_JU);
     const double* Jx = SA(S_JX);
     const double* rdyn = SA(S_RDYN);
-    const double* val = SA(S_VAL);
-    const double* pvec = SA(S_PVEC);
     const double* gain = SA(S_GAIN);
     const double* dff = SA(S_DFF);
     double* ddU = SA(S_DDU);
     double* ddX = SA(S_DDX);
-    double* ddmu = SA(S_DDMU);
     double dx = -rdyn[0] + Ju[0] * dff[0];  // k = 0 (no state feedback)
     ddU[0] = dff[0];
     ddX[0] = dx;
-    ddmu[0] = -(val[1] * dx + pvec[1]);
+    // the loop is latency-bound on the dx chain: stage k+1's operands are
+    // loaded while stage k computes, so no shared-memory latency sits on it
+    double g = gain[1], f = dff[1], jx = Jx[1], rd = rdyn[1], ju = Ju[1];
 #pragma unroll 1
     for (int k = 1; k < N; ++k) {
-        const double du = gain[k] * dx + dff[k];
-        ddU[k] = du;
-        double dxn = Jx[k] * dx + -rdyn[k];
-        dxn = Ju[k] * du + dxn;
+        const int kn = k + 1 < N ? k + 1 : k;
+        const double gn = gain[kn], fn = dff[kn], jxn = Jx[kn], rdn = rdyn[kn], jun = Ju[kn];
+        const double du = g * dx + f;
+        double dxn = jx * dx + -rd;
+        dxn = ju * du + dxn;
         dx = dxn;
+        ddU[k] = du;
         ddX[k] = dx;
-        ddmu[k] = -(val[k + 1] * dx + pvec[k + 1]);
+        g = gn;
+        f = fn;
+        jx = jxn;
+        rd = rdn;
+        ju = jun;
     }
     __syncwarp();
 }
@@ -706,7 +751,8 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
     double* tmp = SA(S_TMP);
     const double* ddU = SA(S_DDU);
     const double* ddX = SA(S_DDX);
-    const double* ddmu = SA(S_DDMU);
+    const double* val = SA(S_VAL);
+    const double* pvec = SA(S_PVEC);
     // data_scale / bounds / init (qp.cpp:183-226)
     double ds = 1.0;
     int nfin = 0;
@@ -786,8 +832,24 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             dinf = fold_absmax(dinf, rd);
             linf = fold_absmax(linf, rl);
             uinf = fold_absmax(uinf, ru);
-            tmp[k] = sl[k] * nl[k];
-            tmp[ST + k] = su[k] * nu[k];
+            const double slk = sl[k], suk = su[k], nlk = nl[k], nuk = nu[k];
+            tmp[k] = slk * nlk;
+            tmp[ST + k] = suk * nuk;
+            // barrier diagonal + affine rc + condensed rhs of the next step
+            // (qp.cpp:353-372, :288-305), computed speculatively: unused when
+            // the iteration stops below
+            double bk = 0.0;
+            if (fl) bk += qdiv(nlk, slk);
+            if (fu) bk += qdiv(nuk, suk);
+            bar[k] = bk;
+            const double cl = fl ? -slk * nlk : 0.0;
+            const double cu = fu ? -suk * nuk : 0.0;
+            rcl[k] = cl;
+            rcu[k] = cu;
+            double v = r;
+            if (fl) v -= qdiv(cl - nlk * rl, slk);
+            if (fu) v += qdiv(cu - nuk * ru, suk);
+            rhat[k] = v;
         }
         // the inf-norms only meet "<= eps": max over lanes <= eps iff every
         // lane's partial max is (partials never hold NaN) -- one vote
@@ -798,7 +860,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
         double gap;
         {
             double dl = 0.0, du = 0.0;
-#pragma unroll 1
+#pragma unroll 4
             for (int k = 0; k < N; ++k) {
                 dl += tmp[k];
                 du += tmp[ST + k];
@@ -813,34 +875,11 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             status = QP_MAXITER;
             break;
         }
-        // barrier diagonal + affine rc + condensed rhs (qp.cpp:353-372, :288-305)
-#pragma unroll 1
-        for (int k = lane; k < N; k += 32) {
-            const double u = U[k];
-            const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
-            const double slk = sl[k], suk = su[k], nlk = nl[k], nuk = nu[k];
-            double bk = 0.0;
-            if (fl) bk += qdiv(nlk, slk);
-            if (fu) bk += qdiv(nuk, suk);
-            bar[k] = bk;
-            const double cl = fl ? -slk * nlk : 0.0;
-            const double cu = fu ? -suk * nuk : 0.0;
-            rcl[k] = cl;
-            rcu[k] = cu;
-            double rl, ru;
-            rlru(k, u, fl, fu, rl, ru);
-            double v = rsu[k];
-            if (fl) v -= qdiv(cl - nlk * rl, slk);
-            if (fu) v += qdiv(cu - nuk * ru, suk);
-            rhat[k] = v;
-        }
-        __syncwarp();
-        __syncwarp();
+        // riccati_factor + affine solve (qp.cpp:358-372); the fast sweep's
+        // certificate is checked inside the affine expand loop below
         bool npd = factor_sweep<ST, true>(o);
-        __syncwarp();
-        // a pivot the fast sqrt got wrong could also change the NPD decision
-        // downstream, so any failed certificate replays the whole sweep
-        if (!certify_factor<ST>(o)) npd = factor_sweep<ST, false>(o);
+        bool fast_ok = !npd;
+        if (npd) npd = factor_sweep<ST, false>(o);  // confirm a fast NPD with IEEE ops
         if (npd) {
             status = QP_FAILED;
             break;
@@ -850,14 +889,33 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
         double sigma = 0.0;
         {
             double alpha_aff = 1.0;
+            for (int pass = 0;; ++pass) {
+                bool cert = true;
+                alpha_aff = 1.0;
 #pragma unroll 1
-            for (int k = lane; k < N; k += 32) {
-                const double u = U[k];
-                const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
-                double rl, ru;
-                rlru(k, u, fl, fu, rl, ru);
-                const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
-                alpha_aff = step_caps<ST>(o, k, fl, fu, d, 1.0, alpha_aff);
+                for (int k = lane; k < N; k += 32) {
+                    if (fast_ok) cert = cert && certify_factor_k<ST>(o, k);
+                    const double u = U[k];
+                    const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
+                    double rl, ru;
+                    rlru(k, u, fl, fu, rl, ru);
+                    const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
+                    alpha_aff = step_caps<ST>(o, k, fl, fu, d, 1.0, alpha_aff);
+                }
+                if (!fast_ok || __all_sync(FULLMASK, cert)) break;
+                // a fast sqrt/division was not the IEEE one: replay the
+                // factor with IEEE ops (an NPD there is genuine) and redo
+                __syncwarp();
+                fast_ok = false;
+                if (factor_sweep<ST, false>(o)) {
+                    npd = true;
+                    break;
+                }
+                rollout<ST>(N);
+            }
+            if (npd) {
+                status = QP_FAILED;
+                break;
             }
             alpha_aff = warp_min_pos(alpha_aff);  // step lengths lie in (0, 1]
             if (m > 0 && gap > 0.0) {
@@ -873,7 +931,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
                 // terms of infinite bounds are stored as +0: adding +0 to this
                 // sum of non-negative products (never -0) changes nothing
                 double gap_aff = 0.0;
-#pragma unroll 1
+#pragma unroll 4
                 for (int k = 0; k < N; ++k) {
                     gap_aff += tmp[k];
                     gap_aff += tmp[ST + k];
@@ -906,19 +964,27 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
         }
         __syncwarp();
         vector_sweep<ST, true>(o);
-        __syncwarp();
-        if (!certify_vector<ST>(o)) vector_sweep<ST, false>(o);
         rollout<ST>(N);
-        // corrector directions + step length (qp.cpp:396-397)
+        // corrector directions + step length (qp.cpp:396-397), with the
+        // certificate of the fast vector sweep
         double alpha = 1.0;
+        for (bool vfast = true;; vfast = false) {
+            bool cert = true;
+            alpha = 1.0;
 #pragma unroll 1
-        for (int k = lane; k < N; k += 32) {
-            const double u = U[k];
-            const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
-            double rl, ru;
-            rlru(k, u, fl, fu, rl, ru);
-            const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
-            alpha = step_caps<ST>(o, k, fl, fu, d, tau, alpha);
+            for (int k = lane; k < N; k += 32) {
+                if (vfast) cert = cert && certify_vector_k<ST>(o, k);
+                const double u = U[k];
+                const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
+                double rl, ru;
+                rlru(k, u, fl, fu, rl, ru);
+                const Dir d = expand_k<ST>(o, k, fl, fu, rl, ru);
+                alpha = step_caps<ST>(o, k, fl, fu, d, tau, alpha);
+            }
+            if (!vfast || __all_sync(FULLMASK, cert)) break;
+            __syncwarp();
+            vector_sweep<ST, false>(o);
+            rollout<ST>(N);
         }
         alpha = warp_min_pos(alpha);
         // update (qp.cpp:398-410)
@@ -929,7 +995,8 @@ __device__ __noinline__ int solve_qp(const Ocp& o, double tol, int max_iter, Cnt
             const Dir d = load_dir<ST>(o, k);
             dU[k] = dU[k] + alpha * ddU[k];
             dX[k] = dX[k] + alpha * ddX[k];
-            mu[k] = mu[k] + alpha * ddmu[k];
+            const double dmu = -(val[k + 1] * ddX[k] + pvec[k + 1]);  // qp.cpp:153
+            mu[k] = mu[k] + alpha * dmu;
             if (fl) {
                 sl[k] += alpha * d.dsl;
                 nl[k] += alpha * d.dnl;
