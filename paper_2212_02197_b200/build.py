@@ -34,13 +34,17 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+    """Compile the library. Experiments only: NMPCMC_NVCC_EXTRA adds flags
+    (e.g. -DNMPCMC_IPM_SMEM=1) and NMPCMC_BUILD_OUT redirects the output."""
+    out = os.environ.get("NMPCMC_BUILD_OUT") or LIB
+    extra = os.environ.get("NMPCMC_NVCC_EXTRA", "").split()
+    if not force and not extra and out == LIB and not _stale():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB]
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+           *[os.path.join(CSRC, s) for s in SOURCES], "-o", out]
     res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(LIBDIR, "build.log")
+    log = os.path.join(LIBDIR, "build.log") if out == LIB else out + ".build.log"
     with open(log, "w") as fh:
         fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
@@ -48,9 +52,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stdout.write(res.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True))

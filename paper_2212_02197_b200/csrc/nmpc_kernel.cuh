@@ -433,7 +433,7 @@ enum { QP_OPTIMAL = 0, QP_MAXITER = 1, QP_FAILED = 2, QP_DOMAIN = -1 };
 /// of riccati_solve_vectors (qp.cpp:122-141). Serial in k, all lanes.
 /// Returns true on NotPositiveDefinite. FAST: sqrt and the four divisions by
 /// each pivot use the 3-operation fast forms; their inputs are stashed so that
-/// certify_factor() can prove every result is the IEEE one afterwards (the
+/// certify_factor_k() can prove every result is the IEEE one afterwards (the
 /// caller replays FAST = false otherwise).
 template <int ST, bool FAST>
 __device__ __noinline__ bool factor_sweep(const Ocp& o) {
@@ -533,25 +533,6 @@ __device__ __noinline__ bool factor_sweep(const Ocp& o) {
     return false;
 }
 
-/// Lane-parallel certificate of a FAST factor_sweep: every sqrt and division
-/// of every stage is the IEEE correctly rounded result (cert_sqrt/cert_div).
-template <int ST>
-__device__ __noinline__ bool certify_factor(const Ocp& o) {
-    const int lane = threadIdx.x & 31;
-    bool ok = true;
-#pragma unroll 1
-    for (int k = lane; k < o.N; k += 32) {
-        const double l = SA(S_CHOLH)[k];
-        const double q1 = GA(G_CQ1)[k];
-        ok = ok && cert_sqrt(GA(G_CHH)[k], l) && cert_div(GA(G_CA1)[k], l, q1) && cert_div(q1, l, -SA(S_DFF)[k]);
-        if (k >= 1) {
-            const double g1 = GA(G_CG1)[k];
-            ok = ok && cert_div(SA(S_GMAT)[k], l, g1) && cert_div(g1, l, -SA(S_GAIN)[k]);
-        }
-    }
-    return __all_sync(FULLMASK, ok);
-}
-
 /// Certificate of stage k of a FAST factor_sweep (fused into a later loop).
 template <int ST>
 __device__ __forceinline__ bool certify_factor_k(const Ocp& o, int k) {
@@ -573,7 +554,7 @@ __device__ __forceinline__ bool certify_vector_k(const Ocp& o, int k) {
 }
 
 /// Corrector backward vector sweep with the cached factor (qp.cpp:122-141);
-/// FAST stashes the division inputs for certify_vector().
+/// FAST stashes the division inputs for certify_vector_k().
 template <int ST, bool FAST>
 __device__ __noinline__ void vector_sweep(const Ocp& o) {
     const int N = o.N;
@@ -624,19 +605,6 @@ __device__ __noinline__ void vector_sweep(const Ocp& o) {
         ju = jun;
         rh = rhn;
     }
-}
-
-template <int ST>
-__device__ __noinline__ bool certify_vector(const Ocp& o) {
-    const int lane = threadIdx.x & 31;
-    bool ok = true;
-#pragma unroll 1
-    for (int k = lane; k < o.N; k += 32) {
-        const double l = SA(S_CHOLH)[k];
-        const double q1 = GA(G_CQ1)[k];
-        ok = ok && cert_div(GA(G_CA1)[k], l, q1) && cert_div(q1, l, -SA(S_DFF)[k]);
-    }
-    return __all_sync(FULLMASK, ok);
 }
 
 /// Forward rollout (qp.cpp:142-155): step dxi (DDU, DDX). The multiplier step
@@ -1638,7 +1606,10 @@ __device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_
 /// from a global atomic counter -- the device form of run_monte_carlo's worker
 /// pool (montecarlo.cpp:218-238) -- so long and short samples balance.
 template <int NX, int ST>
-__global__ void __launch_bounds__(32, 16) nmpc_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
+#ifndef NMPCMC_MIN_BLOCKS
+#define NMPCMC_MIN_BLOCKS 16
+#endif
+__global__ void __launch_bounds__(32, NMPCMC_MIN_BLOCKS) nmpc_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
                                                   int64_t n_sims, int nbar, nmpcmc_sim_record* records,
                                                   nmpcmc_work_counters* counters, double* traj, int traj_rows,
                                                   double* gws_all, unsigned long long* next) {
