@@ -78,7 +78,7 @@ typedef struct nmpcmc_pi_gains {
 typedef struct nmpcmc_scenario {
     int32_t controller;      /* NMPCMC_CTRL_* */
     int32_t truth_variant;   /* NMPCMC_THREE_STATE | NMPCMC_ONE_STATE */
-    int32_t ctrl_variant;    /* NMPC controller model; device supports ONE_STATE */
+    int32_t ctrl_variant;    /* NMPC controller model: THREE_STATE (K3g) or ONE_STATE */
     int32_t has_noise_R;     /* NoiseSpec::R has rows (model.cpp:41) */
     nmpcmc_cstr_params truth;
     nmpcmc_cstr_params ctrl;
@@ -160,13 +160,16 @@ int nmpcmc_gpu_validate(const nmpcmc_scenario* sc, int32_t* nbar_out);
 int nmpcmc_gpu_ctx_create(int device, nmpcmc_gpu_ctx** out);
 void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx);
 const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx);
-/* Context options. NMPCMC_OPT_NMPC_KERNEL selects the NMPC kernel:
+/* Context options. NMPCMC_OPT_NMPC_KERNEL selects the NMPC kernel for a
+ * one-state controller model with N <= 255:
  * WARP (default) = one warp per sample, workspace in shared memory (K3);
- * THREAD = one thread per sample, workspace in HBM (K3b). Results are
+ * THREAD = one thread per sample, workspace in HBM (K3b);
+ * GENERIC = one thread per sample, any controller state dimension (K3g).
+ * A three-state controller model or N > 255 always runs K3g. Results are
  * bitwise identical; only speed differs. NMPCMC_OPT_TPS_WARPS_PER_SM = resident
  * warps per SM for K3b (default 8). */
 enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2 };
-enum { NMPCMC_NMPC_KERNEL_WARP = 1, NMPCMC_NMPC_KERNEL_THREAD = 2 };
+enum { NMPCMC_NMPC_KERNEL_WARP = 1, NMPCMC_NMPC_KERNEL_THREAD = 2, NMPCMC_NMPC_KERNEL_GENERIC = 3 };
 int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value);
 /* CUDA stream the context launches on (as void*; 0 = legacy default). */
 int nmpcmc_gpu_set_stream(nmpcmc_gpu_ctx* ctx, void* stream);

@@ -70,8 +70,9 @@ int nmpcmc_gpu_validate(const nmpcmc_scenario* sc, int32_t* nbar_out) {
         if (std::fabs(sc->horizon_Ts - sc->Ts) > 1e-12) return NMPCMC_DOMAIN_ERROR;
         if (sc->N <= 0 || sc->horizon_Ts <= 0.0 || sc->Nc <= 0 || sc->np <= 0)
             return NMPCMC_DOMAIN_ERROR;
-        if (sc->ctrl_variant != NMPCMC_ONE_STATE) return NMPCMC_UNSUPPORTED;
-        if (sc->N > 256) return NMPCMC_UNSUPPORTED;
+        if (sc->ctrl_variant != NMPCMC_ONE_STATE && sc->ctrl_variant != NMPCMC_THREE_STATE)
+            return NMPCMC_DOMAIN_ERROR;
+        if (sc->N > 4096) return NMPCMC_UNSUPPORTED;  // workspace sanity bound
         if (sc->sqp.max_iter < 0 || sc->sqp.qp_max_iter < 0 || sc->sqp.max_backtracks < 0)
             return NMPCMC_DOMAIN_ERROR;
     } else if (sc->controller == NMPCMC_CTRL_PI) {

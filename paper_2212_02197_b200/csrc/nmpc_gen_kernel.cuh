@@ -1,0 +1,1479 @@
+// nmpc_gen_kernel.cuh -- K3g: NMPC closed loop for a controller model of any
+// state dimension NX (compile time), one thread per sample.
+//
+// K3 (nmpc_kernel.cuh) is the one-state fast path. K3g covers the
+// three-state controller model: the literal "CD-EKF on the 3-state model"
+// reading of BASELINE config 2, and SURVEY.md §8(f) row 3. It restates the
+// reference's NMPC branch for general n_x with n_u = n_y = n_z = 1:
+//   run_closed_loop      montecarlo.cpp:80-157
+//   nmpc_step            controllers.cpp:114-212
+//   filter_update        ekf.cpp:59-96      predict / joint_rhs  ekf.cpp:12-57
+//   drift / jacobians    cstr.cpp:36-53, :99-127
+//   shoot                ocp.cpp:9-74       eval_objective / eval_constraints  ocp.cpp:76-135
+//   xi_from_inputs       ocp.cpp:137-154
+//   sqp_solve            sqp.cpp:12-411     solve_qp  qp.cpp:66-423
+//   gemm/gemv/cholesky   linalg.cpp:69-235 (loop orders and epilogues)
+// keeping every floating-point operation in the reference's order, so the
+// records are bitwise those of the exact-libm reference (tests/test_gpu_gen.py).
+//
+// Layout: a per-sample workspace of ~9k doubles (N = 60, NX = 3) in global
+// memory, element e of slot t at ws[e * T + t] (T = resident slots), so the
+// 32 lanes of a warp touch 32 consecutive doubles. Small matrices (NX x NX)
+// live in registers. Reference exceptions become status codes returned to
+// exactly the callers that catch them.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace nmpcmc_dev {
+namespace gen {
+
+enum : int { G_OK = 0, G_NPD = ST_NPD, G_NONFINITE = ST_NONFINITE, G_DOMAIN = ST_DOMAIN };
+
+/// Per-thread view of the SoA workspace.
+struct Ws {
+    double* p;
+    int64_t T;
+    __device__ __forceinline__ double& operator[](int64_t e) const { return p[e * T]; }
+};
+
+/// Element offsets of the per-sample arrays for horizon N (NX compile time).
+/// Two evaluation sets (iterate / trial) are swapped by index, not copied.
+template <int NX>
+struct Layout {
+    static constexpr int W = 1 + NX;  // stride of xi (n_u + n_x)
+    static constexpr int B = (NX + 1) * (NX + 1);
+    int N, L, NN;
+    int64_t XI[2], GF[2], G[2], FX[2], FU[2], BB[2];
+    int64_t LAM, PL, PU, QDXI, QMU, QNL, QNU, SL, SU, RS, RD, RL, RU, CL, CU, DSL, DSU, DNL, DNU, BAR, DXI,
+        DMU, RH, FP, FLL, FK, FG, PV, DFF, WB, SIG, HO, HN, LXI, LLAM, LPL, LPU, SP, US, total;
+    __host__ __device__ explicit Layout(int n) : N(n), L(n * W), NN(n * NX) {
+        int64_t o = 0;
+        auto take = [&](int64_t len) {
+            const int64_t at = o;
+            o += len;
+            return at;
+        };
+        for (int s = 0; s < 2; ++s) {
+            XI[s] = take(L);
+            GF[s] = take(L);
+            G[s] = take(NN);
+            FX[s] = take((int64_t)NN * NX);
+            FU[s] = take(NN);
+            BB[s] = take(NN);
+        }
+        LAM = take(NN), PL = take(N), PU = take(N);
+        QDXI = take(L), QMU = take(NN), QNL = take(N), QNU = take(N);
+        SL = take(N), SU = take(N), RS = take(L), RD = take(NN), RL = take(N), RU = take(N);
+        CL = take(N), CU = take(N), DSL = take(N), DSU = take(N), DNL = take(N), DNU = take(N);
+        BAR = take(N), DXI = take(L), DMU = take(NN), RH = take(N);
+        FP = take((int64_t)(N + 1) * NX * NX), FLL = take(N), FK = take(NN), FG = take(NN);
+        PV = take((int64_t)(N + 1) * NX), DFF = take(N);
+        WB = take((int64_t)(N + 1) * B);
+        SIG = take(NN), HO = take(L), HN = take(L);
+        LXI = take(L), LLAM = take(NN), LPL = take(N), LPU = take(N);
+        SP = take(N), US = take(N);
+        total = o;
+    }
+    __host__ __device__ int uo(int k) const { return k * W; }            // u slot of stage k
+    __host__ __device__ int xo(int k) const { return (k - 1) * W + 1; }  // x_k, k >= 1
+};
+
+/// Work counters (K3's units: stage intervals shot, IPM stage-iterations,
+/// completed SQP steps, ...), for the roofline.
+struct Cnt {
+    int64_t steps, shoot_full, shoot_fonly, ipm_stage, sqp_stage, qp, sqp, ls;
+};
+
+// ------------------------------------------------------------------ model
+/// One CSTR variant (cstr.cpp:21-34 stoichiometry, cstr.hpp:21-34 params).
+template <int NX>
+struct Model {
+    Cstr p;
+    double S[NX], Cin[NX], sb[NX];
+};
+template <int NX>
+__device__ Model<NX> make_model(const nmpcmc_cstr_params& q) {
+    Model<NX> m;
+    m.p = load_cstr(q);
+    if (NX == 3) {
+        m.S[0] = -1.0, m.S[1] = -2.0, m.S[NX - 1] = q.beta;
+        m.Cin[0] = q.cA_in, m.Cin[1] = q.cB_in, m.Cin[NX - 1] = q.cT_in;
+        m.sb[0] = q.sigmaA, m.sb[1] = q.sigmaB, m.sb[NX - 1] = q.sigmaT;
+    } else {
+        m.S[0] = q.beta;
+        m.Cin[0] = q.cT_in;
+        m.sb[0] = q.sigmaT;
+    }
+    return m;
+}
+
+/// drift (cstr.cpp:42-53) and, when J != nullptr, drift_jacobian_x
+/// (cstr.cpp:99-119); both evaluate exp(-EaR/cT) of the same argument, so it
+/// is computed once. Returns G_DOMAIN when c_T <= 0 (cstr.cpp:38).
+template <int NX>
+__device__ __forceinline__ int drift_jac(const Model<NX>& m, const double* x, double u, double* d, double* J) {
+    const double f = u * kMlMinToLs;
+    double c[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) c[i] = x[i] / m.p.V;
+    double cA, cB, cT;
+    if (NX == 3) {
+        cA = c[0], cB = c[1], cT = c[NX - 1];
+    } else {
+        cT = c[0];
+        cA = m.p.cA_in - (cT - m.p.cT_in) / m.p.beta;
+        cB = m.p.cB_in - 2.0 * (cT - m.p.cT_in) / m.p.beta;
+    }
+    if (cT <= 0.0) return G_DOMAIN;
+    const double k = m.p.k0 * xlibm_exp(-m.p.EaR / cT);
+    const double r = k * cA * cB;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) d[i] = m.Cin[i] * f - c[i] * f + m.S[i] * r * m.p.V;
+    if (J != nullptr) {
+        if (NX == 3) {
+            const double g[3] = {k * cB, k * cA, k * (m.p.EaR / (cT * cT)) * cA * cB};
+            const double dg = -f / m.p.V;
+#pragma unroll
+            for (int j = 0; j < NX; ++j)
+#pragma unroll
+                for (int i = 0; i < NX; ++i) J[j * NX + i] = (i == j ? dg : 0.0) + m.S[i] * g[j];
+        } else {
+            const double g = k * (m.p.EaR / (cT * cT)) * cA * cB + k * (-cB / m.p.beta - 2.0 * cA / m.p.beta);
+            J[0] = -f / m.p.V + m.p.beta * g;
+        }
+    }
+    return G_OK;
+}
+/// drift_jacobian_u (cstr.cpp:120-127).
+template <int NX>
+__device__ __forceinline__ void jac_u(const Model<NX>& m, const double* x, double* B) {
+#pragma unroll
+    for (int i = 0; i < NX; ++i) B[i] = (m.Cin[i] - x[i] / m.p.V) * kMlMinToLs;
+}
+
+// ------------------------------------------------------------------ shoot
+/// shoot (ocp.cpp:9-74): Nc RK4 steps of (F, Fx, Fu). Column-major Fx.
+/// The RK4 weighted sum a + 2b + 2c + d accumulates left to right.
+template <int NX, bool SENS>
+__device__ __noinline__ int shoot(const Model<NX>& m, const double* x, double u, double h, int nc, double* F,
+                                  double* Fx, double* Fu) {
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+        F[i] = x[i];
+        if (SENS) {
+            Fu[i] = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) Fx[j * NX + i] = (i == j) ? 1.0 : 0.0;
+        }
+    }
+#pragma unroll 1
+    for (int step = 0; step < nc; ++step) {
+        double pk[NX], pkx[NX * NX], pku[NX], ak[NX], akx[NX * NX], aku[NX];
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+            double xs[NX], sx[NX * NX], su[NX];
+            const double c = (j == 3) ? 1.0 : 0.5;
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                xs[i] = j == 0 ? F[i] : F[i] + c * h * pk[i];
+                if (SENS) {
+                    su[i] = j == 0 ? Fu[i] : Fu[i] + c * h * pku[i];
+#pragma unroll
+                    for (int l = 0; l < NX; ++l)
+                        sx[l * NX + i] = j == 0 ? Fx[l * NX + i] : Fx[l * NX + i] + c * h * pkx[l * NX + i];
+                }
+            }
+            double k[NX], A[NX * NX], B[NX];
+            const int st = drift_jac<NX>(m, xs, u, k, SENS ? A : nullptr);
+            if (st) return st;
+            double kx[NX * NX], ku[NX];
+            if (SENS) {
+                jac_u<NX>(m, xs, B);
+#pragma unroll
+                for (int jj = 0; jj < NX; ++jj)  // kx = A sx (gemm, beta 0)
+#pragma unroll
+                    for (int i = 0; i < NX; ++i) {
+                        double s = 0.0;
+#pragma unroll
+                        for (int l = 0; l < NX; ++l) s += A[l * NX + i] * sx[jj * NX + l];
+                        kx[jj * NX + i] = 1.0 * s + 0.0;
+                    }
+#pragma unroll
+                for (int i = 0; i < NX; ++i) {  // ku = B; gemm(1, A, su, 1, ku)
+                    double s = 0.0;
+#pragma unroll
+                    for (int l = 0; l < NX; ++l) s += A[l * NX + i] * su[l];
+                    ku[i] = 1.0 * s + 1.0 * B[i];
+                }
+            }
+            const double w = (j == 1 || j == 2) ? 2.0 : 1.0;
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                ak[i] = j == 0 ? k[i] : (j < 3 ? ak[i] + w * k[i] : ak[i] + k[i]);
+                pk[i] = k[i];
+                if (SENS) {
+                    aku[i] = j == 0 ? ku[i] : (j < 3 ? aku[i] + w * ku[i] : aku[i] + ku[i]);
+                    pku[i] = ku[i];
+#pragma unroll
+                    for (int l = 0; l < NX; ++l) {
+                        const int e = l * NX + i;
+                        akx[e] = j == 0 ? kx[e] : (j < 3 ? akx[e] + w * kx[e] : akx[e] + kx[e]);
+                        pkx[e] = kx[e];
+                    }
+                }
+            }
+        }
+        const double h6 = h / 6.0;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            F[i] += h6 * ak[i];
+            if (SENS) {
+                Fu[i] += h6 * aku[i];
+#pragma unroll
+                for (int l = 0; l < NX; ++l) Fx[l * NX + i] += h6 * akx[l * NX + i];
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NX; ++i)
+        if (!dfinite(F[i])) return G_NONFINITE;
+    return G_OK;
+}
+
+// -------------------------------------------------------------------- OCP
+template <int NX>
+struct Ocp {
+    Model<NX> m;
+    Layout<NX> lay;
+    Ws ws;
+    int N, Nc;
+    double Ts, h, umin, umax, Qz, invV;
+    double x0[NX];
+    Cnt* cnt;
+};
+
+/// eval_objective (ocp.cpp:76-99) of xi set s; gradient into GF[s] if grad.
+template <int NX>
+__device__ __noinline__ double objective(const Ocp<NX>& o, int s, bool grad) {
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+    double phi = 0.0;
+    if (grad)
+        for (int i = 0; i < L.L; ++i) w[L.GF[s] + i] = 0.0;
+#pragma unroll 1
+    for (int k = 1; k <= o.N; ++k) {
+        const double res = w[L.XI[s] + L.xo(k) + NX - 1] / o.m.p.V - w[L.SP + k - 1];
+        const double qres = 1.0 * (0.0 + o.Qz * res) + 0.0;
+        phi += o.Ts * (0.0 + res * qres);
+        if (grad) {
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                const double hi = (i == NX - 1) ? o.invV : 0.0;
+                const double g = 1.0 * (0.0 + hi * qres) + 0.0;
+                w[L.GF[s] + L.xo(k) + i] += 2.0 * o.Ts * g;
+            }
+        }
+    }
+    return phi;
+}
+
+/// eval_constraints (ocp.cpp:101-135) of xi set s into G/FX/FU/BB[s].
+template <int NX>
+__device__ __noinline__ int constraints(const Ocp<NX>& o, int s) {
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+    double xk[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) xk[i] = o.x0[i];
+#pragma unroll 1
+    for (int k = 0; k < o.N; ++k) {
+        double F[NX], Fx[NX * NX], Fu[NX];
+        const int st = shoot<NX, true>(o.m, xk, w[L.XI[s] + L.uo(k)], o.h, o.Nc, F, Fx, Fu);
+        o.cnt->shoot_full += 1;  // one stage interval (workmodel.SHOOT_FULL)
+        if (st) return st;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            const double nx = w[L.XI[s] + L.xo(k + 1) + i];
+            w[L.BB[s] + k * NX + i] = F[i] - nx;
+            w[L.G[s] + k * NX + i] = nx - F[i];
+            w[L.FU[s] + k * NX + i] = Fu[i];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) w[L.FX[s] + (k * NX + j) * NX + i] = Fx[j * NX + i];
+            xk[i] = nx;
+        }
+    }
+    return G_OK;
+}
+
+/// xi_from_inputs (ocp.cpp:137-154): u from US, result into XI[s].
+template <int NX>
+__device__ __noinline__ int xi_from_u(const Ocp<NX>& o, int s) {
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+    double xk[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) xk[i] = o.x0[i];
+#pragma unroll 1
+    for (int k = 0; k < o.N; ++k) {
+        const double u = w[L.US + k];
+        w[L.XI[s] + L.uo(k)] = u;
+        double F[NX];
+        const int st = shoot<NX, false>(o.m, xk, u, o.h, o.Nc, F, nullptr, nullptr);
+        o.cnt->shoot_fonly += 1;
+        if (st) return st;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            w[L.XI[s] + L.xo(k + 1) + i] = F[i];
+            xk[i] = F[i];
+        }
+    }
+    return G_OK;
+}
+
+// --------------------------------------------------------------------- QP
+// Stage data (build_stages, sqp.cpp:130-171) is read in place: R_0 = W_0;
+// for k >= 1, Q = W_k[0:nx,0:nx], M = W_k[0:nx,nx], R = W_k[nx,nx],
+// q = gf(x_k); r = gf(u_k); Jx/Ju/b = the constraint blocks of set s;
+// terminal Q = W_N, q = gf(x_N); lb/ub = umin/umax - u_k.
+template <int NX>
+struct QpView {
+    const Ocp<NX>* o;
+    int s;  // evaluation set of the current iterate
+    __device__ double W(int k, int i, int j) const {
+        const int ld = k == 0 ? 1 : (k < o->N ? NX + 1 : NX);
+        return o->ws[o->lay.WB + (int64_t)k * Layout<NX>::B + j * ld + i];
+    }
+    __device__ double R(int k) const { return k == 0 ? W(0, 0, 0) : W(k, NX, NX); }
+    __device__ double Q(int k, int i, int j) const { return W(k, i, j); }
+    __device__ double M(int k, int i) const { return W(k, i, NX); }
+    __device__ double q(int k, int i) const { return o->ws[o->lay.GF[s] + o->lay.xo(k) + i]; }
+    __device__ double r(int k) const { return o->ws[o->lay.GF[s] + o->lay.uo(k)]; }
+    __device__ double Jx(int k, int i, int j) const { return o->ws[o->lay.FX[s] + ((int64_t)k * NX + j) * NX + i]; }
+    __device__ double Ju(int k, int i) const { return o->ws[o->lay.FU[s] + k * NX + i]; }
+    __device__ double b(int k, int i) const { return o->ws[o->lay.BB[s] + k * NX + i]; }
+    __device__ double u(int k) const { return o->ws[o->lay.XI[s] + o->lay.uo(k)]; }
+    __device__ double lb(int k) const { return o->umin - u(k); }
+    __device__ double ub(int k) const { return o->umax - u(k); }
+};
+
+/// riccati_factor (qp.cpp:73-110) with barrier diagonal BAR. Returns true on
+/// NotPositiveDefinite.
+template <int NX>
+__device__ __noinline__ bool rfactor(const QpView<NX>& v) {
+    const Ocp<NX>& o = *v.o;
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+    const int N = o.N;
+    auto P = [&](int k, int i, int j) -> double& { return w[L.FP + ((int64_t)k * NX + j) * NX + i]; };
+#pragma unroll
+    for (int j = 0; j < NX; ++j)
+#pragma unroll
+        for (int i = 0; i < NX; ++i) P(N, i, j) = v.Q(N, i, j);
+#pragma unroll 1
+    for (int k = N - 1; k >= 0; --k) {
+        double Pn[NX * NX], ju[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+            ju[j] = v.Ju(k, j);
+#pragma unroll
+            for (int i = 0; i < NX; ++i) Pn[j * NX + i] = P(k + 1, i, j);
+        }
+        double PJu[NX];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < NX; ++l) s += Pn[l * NX + i] * ju[l];
+            PJu[i] = 1.0 * s + 0.0;
+        }
+        double H;
+        {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < NX; ++l) s += ju[l] * PJu[l];
+            H = 1.0 * s + 0.0;
+        }
+        H += v.R(k);
+        H += w[L.BAR + k];
+        if (H <= 0.0 || !dfinite(H)) return true;  // cholesky_factor (linalg.cpp:69-103)
+        const double l = sqrt(H);
+        w[L.FLL + k] = l;
+        if (k >= 1) {
+            double PJx[NX * NX], G[NX], K[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j)
+#pragma unroll
+                for (int i = 0; i < NX; ++i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int m = 0; m < NX; ++m) s += Pn[m * NX + i] * v.Jx(k, m, j);
+                    PJx[j * NX + i] = 1.0 * s + 0.0;
+                }
+#pragma unroll
+            for (int j = 0; j < NX; ++j) {
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m < NX; ++m) s += ju[m] * PJx[j * NX + m];
+                G[j] = 1.0 * s + 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < NX; ++j) G[j] += v.M(k, j);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) {  // cholesky_solve of the 1x1 factor, then negate
+                double t = G[j] / l;
+                t = t / l;
+                K[j] = -t;
+            }
+            double Pk[NX * NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j)
+#pragma unroll
+                for (int i = 0; i < NX; ++i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int m = 0; m < NX; ++m) s += v.Jx(k, m, i) * PJx[j * NX + m];
+                    Pk[j * NX + i] = 1.0 * s + 0.0;
+                }
+#pragma unroll
+            for (int j = 0; j < NX; ++j)
+#pragma unroll
+                for (int i = 0; i < NX; ++i) Pk[j * NX + i] += v.Q(k, i, j);
+#pragma unroll
+            for (int j = 0; j < NX; ++j)
+#pragma unroll
+                for (int i = 0; i < NX; ++i) Pk[j * NX + i] = 1.0 * (0.0 + G[i] * K[j]) + 1.0 * Pk[j * NX + i];
+#pragma unroll
+            for (int j = 0; j < NX; ++j)  // symmetrize (linalg.cpp:227-235)
+#pragma unroll
+                for (int i = j + 1; i < NX; ++i) {
+                    const double mm = 0.5 * (Pk[j * NX + i] + Pk[i * NX + j]);
+                    Pk[j * NX + i] = mm;
+                    Pk[i * NX + j] = mm;
+                }
+#pragma unroll
+            for (int j = 0; j < NX; ++j) {
+                w[L.FK + k * NX + j] = K[j];
+                w[L.FG + k * NX + j] = G[j];
+#pragma unroll
+                for (int i = 0; i < NX; ++i) P(k, i, j) = Pk[j * NX + i];
+            }
+        }
+    }
+    return false;
+}
+
+/// riccati_solve_vectors (qp.cpp:116-155) for the condensed right-hand side
+/// rh = RH, qhat_k = rs(x_k), bhat_k = -rd_k; step into DXI, DMU.
+template <int NX>
+__device__ __noinline__ void rsolve(const QpView<NX>& v) {
+    const Ocp<NX>& o = *v.o;
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+    const int N = o.N;
+    auto P = [&](int k, int i, int j) -> double { return w[L.FP + ((int64_t)k * NX + j) * NX + i]; };
+    auto bh = [&](int k, int i) -> double { return -w[L.RD + k * NX + i]; };
+#pragma unroll
+    for (int i = 0; i < NX; ++i) w[L.PV + N * NX + i] = w[L.RS + L.xo(N) + i];
+#pragma unroll 1
+    for (int k = N - 1; k >= 0; --k) {
+        double t[NX];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += P(k + 1, i, j) * bh(k, j);
+            t[i] = 1.0 * s + 1.0 * w[L.PV + (k + 1) * NX + i];
+        }
+        double hv;
+        {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += v.Ju(k, j) * t[j];
+            hv = 1.0 * s + 1.0 * w[L.RH + k];
+        }
+        const double l = w[L.FLL + k];
+        hv = hv / l;
+        hv = hv / l;
+        const double dff = -hv;
+        w[L.DFF + k] = dff;
+        if (k >= 1) {
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int j = 0; j < NX; ++j) s += v.Jx(k, j, i) * t[j];
+                double p = 1.0 * s + 1.0 * w[L.RS + L.xo(k) + i];
+                p = 1.0 * (0.0 + w[L.FG + k * NX + i] * dff) + 1.0 * p;
+                w[L.PV + k * NX + i] = p;
+            }
+        }
+    }
+    double dx[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) dx[i] = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) {
+        double du = w[L.DFF + k];
+        if (k >= 1) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += w[L.FK + k * NX + j] * dx[j];
+            du = 1.0 * s + 1.0 * du;
+        }
+        w[L.DXI + L.uo(k)] = du;
+        double dn[NX];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) dn[i] = bh(k, i);
+        if (k >= 1) {
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int j = 0; j < NX; ++j) s += v.Jx(k, i, j) * dx[j];
+                dn[i] = 1.0 * s + 1.0 * dn[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NX; ++i) dn[i] = 1.0 * (0.0 + v.Ju(k, i) * du) + 1.0 * dn[i];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            dx[i] = dn[i];
+            w[L.DXI + L.uo(k) + 1 + i] = dx[i];
+        }
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += P(k + 1, i, j) * dx[j];
+            const double mv = 1.0 * s + 1.0 * w[L.PV + (k + 1) * NX + i];
+            w[L.DMU + k * NX + i] = -mv;
+        }
+    }
+}
+
+enum : int { QP_OPTIMAL = 0, QP_MAXITER = 1, QP_FAILED = 2, QP_DOMAIN = 3 };
+
+/// residuals (qp.cpp:237-284) into RS, RD, RL, RU.
+template <int NX>
+__device__ __noinline__ void qp_resid(const QpView<NX>& v) {
+    const Ocp<NX>& o = *v.o;
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+    const int N = o.N;
+    auto dxi = [&](int e) -> double { return w[L.QDXI + e]; };
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) {
+        const double vk = dxi(L.uo(k));
+        double r = 1.0 * (0.0 + v.R(k) * vk) + 1.0 * v.r(k);
+        if (k >= 1) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += v.M(k, j) * dxi(L.xo(k) + j);
+            r = 1.0 * s + 1.0 * r;
+        }
+        {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += v.Ju(k, j) * w[L.QMU + k * NX + j];
+            r = -1.0 * s + 1.0 * r;
+        }
+        r += w[L.QNU + k] - w[L.QNL + k];
+        w[L.RS + L.uo(k)] = r;
+        double d[NX];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) d[i] = dxi(L.xo(k + 1) + i) + -1.0 * v.b(k, i);
+        if (k >= 1) {
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int j = 0; j < NX; ++j) s += v.Jx(k, i, j) * dxi(L.xo(k) + j);
+                d[i] = -1.0 * s + 1.0 * d[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NX; ++i) w[L.RD + k * NX + i] = -1.0 * (0.0 + v.Ju(k, i) * vk) + 1.0 * d[i];
+    }
+#pragma unroll 1
+    for (int k = 1; k <= N; ++k) {
+        double x[NX];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += v.Q(k, i, j) * dxi(L.xo(k) + j);
+            x[i] = 1.0 * s + 1.0 * v.q(k, i);
+        }
+        if (k < N) {
+            const double uk = dxi(L.uo(k));
+#pragma unroll
+            for (int i = 0; i < NX; ++i) x[i] = 1.0 * (0.0 + v.M(k, i) * uk) + 1.0 * x[i];
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                double s = 0.0;
+#pragma unroll
+                for (int j = 0; j < NX; ++j) s += v.Jx(k, j, i) * w[L.QMU + k * NX + j];
+                x[i] = -1.0 * s + 1.0 * x[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < NX; ++i) w[L.RS + L.xo(k) + i] = x[i] + w[L.QMU + (k - 1) * NX + i];
+    }
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) {
+        const double vk = dxi(L.uo(k));
+        const double lb = v.lb(k), ub = v.ub(k);
+        w[L.RL + k] = dfinite(lb) ? vk - w[L.SL + k] - lb : 0.0;
+        w[L.RU + k] = dfinite(ub) ? ub - vk - w[L.SU + k] : 0.0;
+    }
+}
+
+/// Condensed right-hand side (qp.cpp:288-305) into RH, then the vector solve.
+template <int NX>
+__device__ __forceinline__ void qp_csolve(const QpView<NX>& v) {
+    const Ocp<NX>& o = *v.o;
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+#pragma unroll 1
+    for (int k = 0; k < o.N; ++k) {
+        double x = w[L.RS + L.uo(k)];
+        if (dfinite(v.lb(k))) x -= (w[L.CL + k] - w[L.QNL + k] * w[L.RL + k]) / w[L.SL + k];
+        if (dfinite(v.ub(k))) x += (w[L.CU + k] - w[L.QNU + k] * w[L.RU + k]) / w[L.SU + k];
+        w[L.RH + k] = x;
+    }
+    rsolve<NX>(v);
+}
+/// expand (qp.cpp:308-317) of the step in DXI.
+template <int NX>
+__device__ __forceinline__ void qp_expand(const QpView<NX>& v) {
+    const Ocp<NX>& o = *v.o;
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+#pragma unroll 1
+    for (int k = 0; k < o.N; ++k) {
+        const double dv = w[L.DXI + L.uo(k)];
+        const bool fl = dfinite(v.lb(k)), fu = dfinite(v.ub(k));
+        const double dsl = fl ? dv + w[L.RL + k] : 0.0;
+        const double dsu = fu ? w[L.RU + k] - dv : 0.0;
+        w[L.DSL + k] = dsl;
+        w[L.DSU + k] = dsu;
+        w[L.DNL + k] = fl ? (w[L.CL + k] - w[L.QNL + k] * dsl) / w[L.SL + k] : 0.0;
+        w[L.DNU + k] = fu ? (w[L.CU + k] - w[L.QNU + k] * dsu) / w[L.SU + k] : 0.0;
+    }
+}
+/// max_step (qp.cpp:321-337).
+template <int NX>
+__device__ __forceinline__ double qp_step(const QpView<NX>& v, double frac) {
+    const Ocp<NX>& o = *v.o;
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+    double a = 1.0;
+    auto cap = [&](double val, double dir) {
+        if (dir < 0.0) a = smin(a, -frac * val / dir);
+    };
+#pragma unroll 1
+    for (int k = 0; k < o.N; ++k) {
+        if (dfinite(v.lb(k))) cap(w[L.SL + k], w[L.DSL + k]), cap(w[L.QNL + k], w[L.DNL + k]);
+        if (dfinite(v.ub(k))) cap(w[L.SU + k], w[L.DSU + k]), cap(w[L.QNU + k], w[L.DNU + k]);
+    }
+    return a;
+}
+
+__device__ __forceinline__ double inf_fold(double m, double x) { return smax(m, fabs(x)); }
+
+/// solve_qp (qp.cpp:173-423): Mehrotra predictor-corrector interior point.
+/// Result in QDXI, QMU, QNL, QNU.
+template <int NX>
+__device__ __noinline__ int solve_qp(const QpView<NX>& v, double tol, int max_iter) {
+    const Ocp<NX>& o = *v.o;
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+    const int N = o.N;
+    int m = 0;
+    double scale = 1.0;
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) {
+        const double lb = v.lb(k), ub = v.ub(k);
+        if (lb > ub) return QP_DOMAIN;
+        if (dfinite(lb)) ++m, scale = smax(scale, fabs(lb));
+        if (dfinite(ub)) ++m, scale = smax(scale, fabs(ub));
+        scale = smax(scale, inf_fold(0.0, v.r(k)));
+        double nb = 0.0;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) nb = inf_fold(nb, v.b(k, i));
+        scale = smax(scale, nb);
+    }
+#pragma unroll 1
+    for (int k = 1; k <= N; ++k) {
+        double nq = 0.0;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) nq = inf_fold(nq, v.q(k, i));
+        scale = smax(scale, nq);
+    }
+    const double eps = tol * scale;
+    for (int e = 0; e < L.L; ++e) w[L.QDXI + e] = 0.0;
+    for (int e = 0; e < L.NN; ++e) w[L.QMU + e] = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) {
+        const double lb = v.lb(k), ub = v.ub(k);
+        const bool fl = dfinite(lb), fu = dfinite(ub);
+        w[L.SL + k] = fl ? smax(1.0, fabs(lb)) : 0.0;
+        w[L.QNL + k] = fl ? 1.0 : 0.0;
+        w[L.SU + k] = fu ? smax(1.0, fabs(ub)) : 0.0;
+        w[L.QNU + k] = fu ? 1.0 : 0.0;
+        w[L.CL + k] = 0.0;
+        w[L.CU + k] = 0.0;
+    }
+    int status = QP_FAILED;
+#pragma unroll 1
+    for (int it = 0;; ++it) {
+        qp_resid<NX>(v);
+        double gap = 0.0;
+        if (m > 0) {
+            double dl = 0.0, du = 0.0;
+#pragma unroll 1
+            for (int k = 0; k < N; ++k) dl += w[L.SL + k] * w[L.QNL + k];
+#pragma unroll 1
+            for (int k = 0; k < N; ++k) du += w[L.SU + k] * w[L.QNU + k];
+            gap = (dl + du) / m;
+        }
+        double ns = 0.0, nd = 0.0, nl = 0.0, nu = 0.0;
+        for (int e = 0; e < L.L; ++e) ns = inf_fold(ns, w[L.RS + e]);
+        for (int e = 0; e < L.NN; ++e) nd = inf_fold(nd, w[L.RD + e]);
+#pragma unroll 1
+        for (int k = 0; k < N; ++k) {
+            nl = inf_fold(nl, w[L.RL + k]);
+            nu = inf_fold(nu, w[L.RU + k]);
+        }
+        if (ns <= eps && nd <= eps && nl <= eps && nu <= eps && gap <= eps) {
+            status = QP_OPTIMAL;
+            break;
+        }
+        if (it >= max_iter) {
+            status = QP_MAXITER;
+            break;
+        }
+#pragma unroll 1
+        for (int k = 0; k < N; ++k) {
+            double b = 0.0;
+            if (dfinite(v.lb(k))) b += w[L.QNL + k] / w[L.SL + k];
+            if (dfinite(v.ub(k))) b += w[L.QNU + k] / w[L.SU + k];
+            w[L.BAR + k] = b;
+        }
+        if (rfactor<NX>(v)) {
+            status = QP_FAILED;
+            break;
+        }
+#pragma unroll 1
+        for (int k = 0; k < N; ++k) {
+            w[L.CL + k] = dfinite(v.lb(k)) ? -w[L.SL + k] * w[L.QNL + k] : 0.0;
+            w[L.CU + k] = dfinite(v.ub(k)) ? -w[L.SU + k] * w[L.QNU + k] : 0.0;
+        }
+        qp_csolve<NX>(v);
+        qp_expand<NX>(v);
+        double sig = 0.0;
+        if (m > 0 && gap > 0.0) {
+            const double aa = qp_step<NX>(v, 1.0);
+            double ga = 0.0;
+#pragma unroll 1
+            for (int k = 0; k < N; ++k) {
+                if (dfinite(v.lb(k)))
+                    ga += (w[L.SL + k] + aa * w[L.DSL + k]) * (w[L.QNL + k] + aa * w[L.DNL + k]);
+                if (dfinite(v.ub(k)))
+                    ga += (w[L.SU + k] + aa * w[L.DSU + k]) * (w[L.QNU + k] + aa * w[L.DNU + k]);
+            }
+            ga /= m;
+            const double ratio = smax(0.0, ga / gap);
+            sig = smin(1.0, ratio * ratio * ratio);
+        }
+#pragma unroll 1
+        for (int k = 0; k < N; ++k) {
+            if (dfinite(v.lb(k)))
+                w[L.CL + k] = sig * gap - w[L.SL + k] * w[L.QNL + k] - w[L.DSL + k] * w[L.DNL + k];
+            if (dfinite(v.ub(k)))
+                w[L.CU + k] = sig * gap - w[L.SU + k] * w[L.QNU + k] - w[L.DSU + k] * w[L.DNU + k];
+        }
+        qp_csolve<NX>(v);
+        qp_expand<NX>(v);
+        const double a = qp_step<NX>(v, 0.995);
+        for (int e = 0; e < L.L; ++e) w[L.QDXI + e] += a * w[L.DXI + e];
+        for (int e = 0; e < L.NN; ++e) w[L.QMU + e] += a * w[L.DMU + e];
+#pragma unroll 1
+        for (int k = 0; k < N; ++k) {
+            if (dfinite(v.lb(k))) {
+                w[L.SL + k] += a * w[L.DSL + k];
+                w[L.QNL + k] += a * w[L.DNL + k];
+            }
+            if (dfinite(v.ub(k))) {
+                w[L.SU + k] += a * w[L.DSU + k];
+                w[L.QNU + k] += a * w[L.DNU + k];
+            }
+        }
+        o.cnt->ipm_stage += N;
+    }
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) {
+        double& x = w[L.QDXI + L.uo(k)];
+        x = smin(smax(x, v.lb(k)), v.ub(k));
+    }
+    return status;
+}
+
+// -------------------------------------------------------------------- SQP
+/// h += J_g' lam (add_constraint_term, sqp.cpp:102-116) on the blocks of
+/// set s; h at element offset H.
+template <int NX>
+__device__ void add_jt(const Ocp<NX>& o, int s, int64_t LAMo, int64_t H) {
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+#pragma unroll 1
+    for (int k = 0; k < o.N; ++k) {
+#pragma unroll
+        for (int i = 0; i < NX; ++i) w[H + L.xo(k + 1) + i] += w[LAMo + k * NX + i];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) w[H + L.uo(k)] -= w[L.FU[s] + k * NX + j] * w[LAMo + k * NX + j];
+        if (k >= 1) {
+#pragma unroll
+            for (int i = 0; i < NX; ++i)
+#pragma unroll
+                for (int j = 0; j < NX; ++j)
+                    w[H + L.xo(k) + i] -= w[L.FX[s] + ((int64_t)k * NX + i) * NX + j] * w[LAMo + k * NX + j];
+        }
+    }
+}
+
+/// lagrangian_gradient (sqp.cpp:118-128) into HO for duals (LAMo, PLo, PUo),
+/// then check_convergence (sqp.cpp:86-96).
+template <int NX>
+__device__ __noinline__ bool kkt_ok(const Ocp<NX>& o, int s, int64_t LAMo, int64_t PLo, int64_t PUo, int m,
+                                    double eps) {
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+    for (int e = 0; e < L.L; ++e) w[L.HO + e] = w[L.GF[s] + e];
+    add_jt<NX>(o, s, LAMo, L.HO);
+#pragma unroll 1
+    for (int k = 0; k < o.N; ++k) w[L.HO + L.uo(k)] += w[PUo + k] - w[PLo + k];
+    double sd = 1.0;
+    if (m > 0) {
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int e = 0; e < L.NN; ++e) a += fabs(w[LAMo + e]);
+#pragma unroll 1
+        for (int k = 0; k < o.N; ++k) b += fabs(w[PLo + k]);
+#pragma unroll 1
+        for (int k = 0; k < o.N; ++k) c += fabs(w[PUo + k]);
+        sd = smax(100.0, (a + b + c) / m) / 100.0;
+    }
+    double gl = 0.0, gg = 0.0;
+    for (int e = 0; e < L.L; ++e) gl = inf_fold(gl, w[L.HO + e]);
+    for (int e = 0; e < L.NN; ++e) gg = inf_fold(gg, w[L.G[s] + e]);
+    return gl / sd <= eps && gg <= eps;
+}
+
+/// reset_blocks (sqp.cpp:173-178): identities of size 1, nx+1, ..., nx.
+template <int NX>
+__device__ void identity_blocks(const Ocp<NX>& o) {
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+#pragma unroll 1
+    for (int k = 0; k <= o.N; ++k) {
+        const int n = k == 0 ? 1 : (k < o.N ? NX + 1 : NX);
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) w[L.WB + (int64_t)k * Layout<NX>::B + j * n + i] = (i == j) ? 1.0 : 0.0;
+    }
+}
+
+/// bfgs_block_update (sqp.cpp:61-84) of block k with s, y of length n.
+/// Returns true on NotPositiveDefinite (the Cholesky audit).
+template <int NX>
+__device__ bool bfgs_block(const Ocp<NX>& o, int k, int n, const double* s, const double* y) {
+    const Ws& w = o.ws;
+    const int64_t base = o.lay.WB + (int64_t)k * Layout<NX>::B;
+    auto Wm = [&](int i, int j) -> double& { return w[base + j * n + i]; };
+    double Ws_[NX + 1];
+    for (int i = 0; i < n; ++i) {
+        double a = 0.0;
+        for (int j = 0; j < n; ++j) a += Wm(i, j) * s[j];
+        Ws_[i] = 1.0 * a + 0.0;
+    }
+    const double tiny = 0x1.0p-52;
+    double sWs = 0.0;
+    for (int i = 0; i < n; ++i) sWs += s[i] * Ws_[i];
+    if (!(sWs > tiny)) return false;
+    double sy = 0.0;
+    for (int i = 0; i < n; ++i) sy += s[i] * y[i];
+    const double th = sy >= 0.2 * sWs ? 1.0 : 0.8 * sWs / (sWs - sy);
+    double r[NX + 1];
+    for (int i = 0; i < n; ++i) r[i] = th * y[i] + (1.0 - th) * Ws_[i];
+    double sr = 0.0;
+    for (int i = 0; i < n; ++i) sr += s[i] * r[i];
+    if (!(smin(sWs, sr) > tiny)) return false;
+    for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i) Wm(i, j) += r[i] * r[j] / sr - Ws_[i] * Ws_[j] / sWs;
+    for (int j = 0; j < n; ++j)
+        for (int i = j + 1; i < n; ++i) {
+            const double mm = 0.5 * (Wm(i, j) + Wm(j, i));
+            Wm(i, j) = mm;
+            Wm(j, i) = mm;
+        }
+    // cholesky_factor audit (linalg.cpp:69-103)
+    double Lc[(NX + 1) * (NX + 1)];
+    for (int e = 0; e < n * n; ++e) Lc[e] = 0.0;
+    for (int j = 0; j < n; ++j) {
+        double d = Wm(j, j);
+        for (int q = 0; q < j; ++q) d -= Lc[q * n + j] * Lc[q * n + j];
+        if (d <= 0.0 || !dfinite(d)) return true;
+        const double p = sqrt(d);
+        Lc[j * n + j] = p;
+        for (int i = j + 1; i < n; ++i) {
+            double a = Wm(i, j);
+            for (int q = 0; q < j; ++q) a -= Lc[q * n + i] * Lc[q * n + j];
+            Lc[j * n + i] = a / p;
+        }
+    }
+    return false;
+}
+
+struct SqpOut {
+    bool converged;
+    int status;  // G_DOMAIN escapes sqp_solve
+};
+
+/// sqp_solve (sqp.cpp:182-411) from the iterate in XI[0] and duals LAM/PL/PU.
+/// On return the iterate is in XI[*cur].
+template <int NX>
+__device__ __noinline__ SqpOut sqp_solve(const Ocp<NX>& o, const nmpcmc_sqp_options& op, int* cur) {
+    const Ws& w = o.ws;
+    const Layout<NX>& L = o.lay;
+    const int N = o.N;
+    const int m = N * NX + (dfinite(o.umin) ? N : 0) + (dfinite(o.umax) ? N : 0);
+    int s = 0;
+    *cur = 0;
+    identity_blocks<NX>(o);
+    double f = objective<NX>(o, s, true);
+    {
+        const int st = constraints<NX>(o, s);
+        if (st == G_DOMAIN) return SqpOut{false, G_DOMAIN};
+        if (st != G_OK) return SqpOut{false, G_OK};
+    }
+    bool first = true;
+#pragma unroll 1
+    for (int it = 0;; ++it) {
+        if (kkt_ok<NX>(o, s, L.LAM, L.PL, L.PU, m, op.eps)) return SqpOut{true, G_OK};
+        if (it >= op.max_iter) break;
+        o.cnt->sqp_stage += N;
+        const QpView<NX> v{&o, s};
+        int qs = solve_qp<NX>(v, op.qp_tol, op.qp_max_iter);
+        o.cnt->qp += 1;
+        if (qs == QP_DOMAIN) return SqpOut{false, G_DOMAIN};
+        if (qs == QP_FAILED) {
+            identity_blocks<NX>(o);
+            qs = solve_qp<NX>(v, op.qp_tol, op.qp_max_iter);
+            o.cnt->qp += 1;
+            if (qs == QP_DOMAIN) return SqpOut{false, G_DOMAIN};
+            if (qs == QP_FAILED) break;
+        }
+        if (kkt_ok<NX>(o, s, L.QMU, L.QNL, L.QNU, m, op.eps)) {
+            for (int e = 0; e < L.NN; ++e) w[L.LAM + e] = w[L.QMU + e];
+#pragma unroll 1
+            for (int k = 0; k < N; ++k) {
+                w[L.PL + k] = w[L.QNL + k];
+                w[L.PU + k] = w[L.QNU + k];
+            }
+            return SqpOut{true, G_OK};
+        }
+        // merit_weights_update (sqp.cpp:12-20)
+        for (int e = 0; e < L.NN; ++e) {
+            const double am = fabs(w[L.QMU + e]);
+            w[L.SIG + e] = first ? am : smax(am, 0.5 * (w[L.SIG + e] + am));
+        }
+        first = false;
+        // line_search (sqp.cpp:22-59); the trial of the accepted step is the
+        // new iterate (identical by construction, sqp.cpp:331-352)
+        double pen = 0.0;
+        for (int e = 0; e < L.NN; ++e) pen += w[L.SIG + e] * fabs(w[L.G[s] + e]);
+        const double m0 = f + pen;
+        double gd = 0.0;
+        for (int e = 0; e < L.L; ++e) gd += w[L.GF[s] + e] * w[L.QDXI + e];
+        const double dd = gd - pen;
+        const int t = 1 - s;
+        double a = 1.0, merit = 0.0, ft = 0.0;
+        bool ok = false, tfin = false;
+#pragma unroll 1
+        for (int bt = 0;; ++bt) {
+            for (int e = 0; e < L.L; ++e) w[L.XI[t] + e] = w[L.XI[s] + e] + a * w[L.QDXI + e];
+            o.cnt->ls += 1;
+            merit = __longlong_as_double(0x7ff0000000000000LL);
+            ft = objective<NX>(o, t, true);
+            const int st = constraints<NX>(o, t);
+            if (st == G_DOMAIN) return SqpOut{false, G_DOMAIN};
+            tfin = st == G_OK;
+            if (tfin) {
+                merit = ft;
+                for (int e = 0; e < L.NN; ++e) merit += w[L.SIG + e] * fabs(w[L.G[t] + e]);
+            }
+            ok = dfinite(merit) && merit <= m0 + op.c1 * a * dd;
+            if (ok || bt >= op.max_backtracks) break;
+            a *= op.backtrack_factor;
+        }
+        if (!ok && !dfinite(merit)) break;
+        if (!tfin) break;  // the re-evaluation at xn would throw NonFiniteState
+        // duals (sqp.cpp:355-364)
+        for (int e = 0; e < L.NN; ++e) w[L.LAM + e] += a * (w[L.QMU + e] - w[L.LAM + e]);
+#pragma unroll 1
+        for (int k = 0; k < N; ++k) {
+            w[L.PL + k] += a * (w[L.QNL + k] - w[L.PL + k]);
+            w[L.PU + k] += a * (w[L.QNU + k] - w[L.PU + k]);
+        }
+        // BFGS on the Lagrangian gradients with the new multipliers (sqp.cpp:366-396)
+        for (int e = 0; e < L.L; ++e) {
+            w[L.HO + e] = w[L.GF[s] + e];
+            w[L.HN + e] = w[L.GF[t] + e];
+        }
+        add_jt<NX>(o, s, L.LAM, L.HO);
+        add_jt<NX>(o, t, L.LAM, L.HN);
+        bool lost = false;
+#pragma unroll 1
+        for (int blk = 0; blk <= N && !lost; ++blk) {
+            const int off = blk == 0 ? 0 : (blk < N ? L.xo(blk) : L.xo(N));
+            const int len = blk == 0 ? 1 : (blk < N ? NX + 1 : NX);
+            double sv[NX + 1], yv[NX + 1];
+            for (int i = 0; i < len; ++i) {
+                sv[i] = a * w[L.QDXI + off + i];
+                yv[i] = w[L.HN + off + i] - w[L.HO + off + i];
+            }
+            lost = bfgs_block<NX>(o, blk, len, sv, yv);
+        }
+        if (lost) identity_blocks<NX>(o);
+        f = ft;
+        s = t;
+        *cur = s;
+        o.cnt->sqp += 1;  // completed SQP steps, as K3 counts them
+    }
+    return SqpOut{false, G_OK};
+}
+
+// ------------------------------------------------------------------- EKF
+/// predict (ekf.cpp:26-57): np RK4 steps on (x, P), P symmetrised per step.
+template <int NX>
+__device__ __noinline__ int ekf_predict(const Model<NX>& m, double* x, double* P, double u, double t, double tn,
+                                        int np) {
+    const double h = (tn - t) / np;
+    const double f = u * kMlMinToLs;
+    double sd[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) sd[i] = f * m.sb[i];
+#pragma unroll 1
+    for (int step = 0; step < np; ++step) {
+        double ax[NX], aP[NX * NX], pk[NX], pP[NX * NX];
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+            double xs[NX], Ps[NX * NX];
+            const double c = (j == 3) ? 1.0 : 0.5;
+#pragma unroll
+            for (int i = 0; i < NX; ++i) xs[i] = j == 0 ? x[i] : (j == 3 ? x[i] + h * pk[i] : x[i] + c * h * pk[i]);
+#pragma unroll
+            for (int e = 0; e < NX * NX; ++e)
+                Ps[e] = j == 0 ? P[e] : (j == 3 ? P[e] + h * pP[e] : P[e] + c * h * pP[e]);
+            double dx[NX], A[NX * NX], dP[NX * NX];
+            const int st = drift_jac<NX>(m, xs, u, dx, A);
+            if (st) return st;
+#pragma unroll
+            for (int jj = 0; jj < NX; ++jj)  // dP = A P
+#pragma unroll
+                for (int i = 0; i < NX; ++i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int l = 0; l < NX; ++l) s += A[l * NX + i] * Ps[jj * NX + l];
+                    dP[jj * NX + i] = 1.0 * s + 0.0;
+                }
+#pragma unroll
+            for (int jj = 0; jj < NX; ++jj)  // + P A'
+#pragma unroll
+                for (int i = 0; i < NX; ++i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int l = 0; l < NX; ++l) s += Ps[l * NX + i] * A[l * NX + jj];
+                    dP[jj * NX + i] = 1.0 * s + 1.0 * dP[jj * NX + i];
+                }
+#pragma unroll
+            for (int jj = 0; jj < NX; ++jj)  // + s s' (diagonal s, all terms)
+#pragma unroll
+                for (int i = 0; i < NX; ++i) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int l = 0; l < NX; ++l) s += (i == l ? sd[i] : 0.0) * (jj == l ? sd[jj] : 0.0);
+                    dP[jj * NX + i] = 1.0 * s + 1.0 * dP[jj * NX + i];
+                }
+            const double wgt = (j == 1 || j == 2) ? 2.0 : 1.0;
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                ax[i] = j == 0 ? dx[i] : ax[i] + wgt * dx[i];
+                pk[i] = dx[i];
+            }
+#pragma unroll
+            for (int e = 0; e < NX * NX; ++e) {
+                aP[e] = j == 0 ? dP[e] : aP[e] + wgt * dP[e];
+                pP[e] = dP[e];
+            }
+        }
+        const double h6 = h / 6.0;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) x[i] += h6 * ax[i];
+#pragma unroll
+        for (int e = 0; e < NX * NX; ++e) P[e] += h6 * aP[e];
+#pragma unroll
+        for (int jj = 0; jj < NX; ++jj)
+#pragma unroll
+            for (int i = jj + 1; i < NX; ++i) {
+                const double mm = 0.5 * (P[jj * NX + i] + P[i * NX + jj]);
+                P[jj * NX + i] = mm;
+                P[i * NX + jj] = mm;
+            }
+        bool fin = true;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) fin = fin && dfinite(x[i]);
+#pragma unroll
+        for (int e = 0; e < NX * NX; ++e) fin = fin && dfinite(P[e]);
+        if (!fin) return G_NONFINITE;
+    }
+    return G_OK;
+}
+
+/// filter_update (ekf.cpp:59-96), Joseph form, n_y = 1. Returns true on
+/// NotPositiveDefinite of R_e.
+template <int NX>
+__device__ __noinline__ bool ekf_update(const Model<NX>& m, double* x, double* P, double y, double R) {
+    const double cv = 1.0 / m.p.V;
+    double C[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) C[i] = (i == NX - 1) ? cv : 0.0;
+    const double e = y - x[NX - 1] / m.p.V;
+    double PC[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NX; ++k) s += P[k * NX + i] * C[k];
+        PC[i] = 1.0 * s + 0.0;
+    }
+    double Re;
+    {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NX; ++k) s += C[k] * PC[k];
+        Re = 1.0 * s + 1.0 * R;
+    }
+    if (Re <= 0.0 || !dfinite(Re)) return true;
+    const double l = sqrt(Re);
+    double K[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+        double t = PC[i] / l;
+        K[i] = t / l;
+    }
+#pragma unroll
+    for (int i = 0; i < NX; ++i) x[i] = 1.0 * (0.0 + K[i] * e) + 1.0 * x[i];
+    double IKC[NX * NX];
+#pragma unroll
+    for (int j = 0; j < NX; ++j)
+#pragma unroll
+        for (int i = 0; i < NX; ++i) IKC[j * NX + i] = -1.0 * (0.0 + K[i] * C[j]) + 1.0 * ((i == j) ? 1.0 : 0.0);
+    double T[NX * NX], Pn[NX * NX];
+#pragma unroll
+    for (int j = 0; j < NX; ++j)
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < NX; ++k) s += IKC[k * NX + i] * P[j * NX + k];
+            T[j * NX + i] = 1.0 * s + 0.0;
+        }
+#pragma unroll
+    for (int j = 0; j < NX; ++j)
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < NX; ++k) s += T[k * NX + i] * IKC[k * NX + j];
+            Pn[j * NX + i] = 1.0 * s + 0.0;
+        }
+    double KR[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) KR[i] = 1.0 * (0.0 + K[i] * R) + 0.0;
+#pragma unroll
+    for (int j = 0; j < NX; ++j)
+#pragma unroll
+        for (int i = 0; i < NX; ++i) Pn[j * NX + i] = 1.0 * (0.0 + KR[i] * K[j]) + 1.0 * Pn[j * NX + i];
+#pragma unroll
+    for (int j = 0; j < NX; ++j)
+#pragma unroll
+        for (int i = j + 1; i < NX; ++i) {
+            const double mm = 0.5 * (Pn[j * NX + i] + Pn[i * NX + j]);
+            Pn[j * NX + i] = mm;
+            Pn[i * NX + j] = mm;
+        }
+#pragma unroll
+    for (int e2 = 0; e2 < NX * NX; ++e2) P[e2] = Pn[e2];
+    return false;
+}
+
+// ------------------------------------------------------------ closed loop
+/// The NMPC branch of run_closed_loop (montecarlo.cpp:80-157) for one sample
+/// with a controller model of NX states and a truth plant of TX states.
+template <int TX, int NX>
+__device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar, const Ws& ws,
+                                         nmpcmc_sim_record* rec, nmpcmc_work_counters* cntp, double* traj) {
+    const Cstr p = sample_truth(sc, sim_index);
+    NormalStream rng;
+    rng.init(sc.base_seed, sim_index);
+    Plant<TX> pl;
+#pragma unroll
+    for (int i = 0; i < TX; ++i) pl.x[i] = sc.x0[i];
+    const bool has_R = sc.has_noise_R != 0;
+    const double lR = has_R ? chol_semidef_1x1(sc.noise_R) : 0.0;
+    const int stride = sc.record_stride < 1 ? 1 : sc.record_stride;
+    Cnt cnt = {};
+    Ocp<NX> o{make_model<NX>(sc.ctrl), Layout<NX>(sc.N), ws, sc.N, sc.Nc, sc.horizon_Ts, sc.horizon_Ts / sc.Nc,
+              sc.u_min, sc.u_max, sc.Qz, 0.0, {}, &cnt};
+    o.invV = 1.0 / o.m.p.V;
+    const Layout<NX>& L = o.lay;
+    const int N = o.N;
+    // make_nmpc_state (controllers.cpp:25-48)
+    double xhat[NX], Pf[NX * NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) xhat[i] = sc.x0_hat[i];
+#pragma unroll
+    for (int e = 0; e < NX * NX; ++e) Pf[e] = sc.P0[e];
+    bool have_last = false;
+    double t = sc.t0;
+    double z = pl.x[TX - 1] / p.V, zbar = setpoint_at(sc, t);
+    double acc = 0.0;
+    {
+        const double r = z - zbar;
+        acc += r * r;
+    }
+    int status = G_OK, solves = 0, fails = 0, row = 0;
+    bool counts_lost = false;
+    const bool fl = dfinite(o.umin), fh = dfinite(o.umax);
+    auto clampu = [&](double u) { return smax(o.umin, smin(o.umax, u)); };
+#pragma unroll 1
+    for (int i = 0; i < nbar; ++i) {
+        const double y = measure<TX>(p, pl, has_R, lR, rng);
+        // ---- nmpc_step (controllers.cpp:114-212)
+        if (!dfinite(y)) {
+            status = G_NONFINITE;
+            break;
+        }
+#pragma unroll 1
+        for (int k = 0; k < N; ++k) ws[L.SP + k] = setpoint_at(sc, t + (k + 1) * sc.Ts);
+        double xf[NX], Pn[NX * NX];
+#pragma unroll
+        for (int e = 0; e < NX; ++e) xf[e] = xhat[e];
+#pragma unroll
+        for (int e = 0; e < NX * NX; ++e) Pn[e] = Pf[e];
+        if (ekf_update<NX>(o.m, xf, Pn, y, sc.R_filter)) {  // jitter retry (controllers.cpp:123-132)
+#pragma unroll
+            for (int e = 0; e < NX; ++e) xf[e] = xhat[e];
+#pragma unroll
+            for (int e = 0; e < NX * NX; ++e) Pn[e] = Pf[e];
+            if (ekf_update<NX>(o.m, xf, Pn, y, sc.R_filter + 1e-10)) {
+                status = G_NPD;
+                counts_lost = true;
+                break;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < NX; ++e) o.x0[e] = xf[e];
+        // warm / cold start (controllers.cpp:147-186)
+        if (have_last) {
+#pragma unroll 1
+            for (int k = 0; k < N; ++k) ws[L.US + k] = clampu(ws[L.LXI + L.uo(k + 1 < N ? k + 1 : N - 1)]);
+            const int st = xi_from_u<NX>(o, 0);
+            if (st == G_DOMAIN) {
+                status = G_DOMAIN;
+                break;
+            }
+            if (st != G_OK) {  // shifted_warm_start (controllers.cpp:97-110)
+                const int w = Layout<NX>::W;
+                for (int e = 0; e < L.L; ++e) ws[L.XI[0] + e] = 0.0;
+                for (int e = w; e < L.L; ++e) ws[L.XI[0] + e - w] = ws[L.LXI + e];
+                for (int e = L.L - w; e < L.L; ++e) ws[L.XI[0] + e] = ws[L.LXI + e];
+#pragma unroll 1
+                for (int k = 0; k < N; ++k) ws[L.XI[0] + L.uo(k)] = clampu(ws[L.XI[0] + L.uo(k)]);
+            }
+            // shifted_multipliers (controllers.cpp:87-93), projected (sqp.cpp:219-222)
+            if (L.NN >= 2 * NX) {
+                for (int e = 0; e < L.NN - NX; ++e) ws[L.LAM + e] = ws[L.LLAM + e + NX];
+                for (int e = L.NN - NX; e < L.NN; ++e) ws[L.LAM + e] = ws[L.LLAM + e];
+            } else {
+                for (int e = 0; e < L.NN; ++e) ws[L.LAM + e] = ws[L.LLAM + e];
+            }
+            if (N >= 2) {
+#pragma unroll 1
+                for (int k = 0; k < N - 1; ++k) {
+                    ws[L.PL + k] = ws[L.LPL + k + 1];
+                    ws[L.PU + k] = ws[L.LPU + k + 1];
+                }
+                ws[L.PL + N - 1] = ws[L.LPL + N - 1];
+                ws[L.PU + N - 1] = ws[L.LPU + N - 1];
+            } else {
+                ws[L.PL] = ws[L.LPL];
+                ws[L.PU] = ws[L.LPU];
+            }
+#pragma unroll 1
+            for (int k = 0; k < N; ++k) {
+                ws[L.PL + k] = smax(0.0, ws[L.PL + k]);
+                ws[L.PU + k] = smax(0.0, ws[L.PU + k]);
+            }
+        } else {
+            const double un = fl && fh ? 0.5 * (o.umin + o.umax) : clampu(0.0);
+#pragma unroll 1
+            for (int k = 0; k < N; ++k) ws[L.US + k] = un;
+            const int st = xi_from_u<NX>(o, 0);
+            if (st == G_DOMAIN) {
+                status = G_DOMAIN;
+                break;
+            }
+            if (st != G_OK) {
+#pragma unroll 1
+                for (int k = 0; k < N; ++k) {
+                    ws[L.XI[0] + L.uo(k)] = un;
+#pragma unroll
+                    for (int e = 0; e < NX; ++e) ws[L.XI[0] + L.xo(k + 1) + e] = xf[e];
+                }
+            }
+            for (int e = 0; e < L.NN; ++e) ws[L.LAM + e] = 0.0;
+#pragma unroll 1
+            for (int k = 0; k < N; ++k) ws[L.PL + k] = 0.0, ws[L.PU + k] = 0.0;
+        }
+        int cur = 0;
+        const SqpOut so = sqp_solve<NX>(o, sc.sqp, &cur);
+        if (so.status != G_OK) {
+            status = so.status;
+            break;
+        }
+        const double u = clampu(ws[L.XI[cur] + L.uo(0)]);
+        for (int e = 0; e < L.L; ++e) ws[L.LXI + e] = ws[L.XI[cur] + e];
+        for (int e = 0; e < L.NN; ++e) ws[L.LLAM + e] = ws[L.LAM + e];
+#pragma unroll 1
+        for (int k = 0; k < N; ++k) ws[L.LPL + k] = ws[L.PL + k], ws[L.LPU + k] = ws[L.PU + k];
+        have_last = true;
+        {
+            const int st = ekf_predict<NX>(o.m, xf, Pn, u, t, t + sc.horizon_Ts, sc.np);
+            if (st != G_OK) {
+                status = st;
+                break;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < NX; ++e) xhat[e] = xf[e];
+#pragma unroll
+        for (int e = 0; e < NX * NX; ++e) Pf[e] = Pn[e];
+        ++solves;
+        if (!so.converged) ++fails;
+        cnt.steps += 1;
+        if (traj != nullptr && i % stride == 0) {
+            double* rw = traj + (size_t)row * 5;
+            rw[0] = t, rw[1] = z, rw[2] = zbar, rw[3] = u, rw[4] = y;
+            ++row;
+        }
+        status = simulate_interval<TX>(p, pl, t, t + sc.Ts, u, sc.Ns, rng);
+        if (status != G_OK) break;
+        t = sc.t0 + (i + 1) * sc.Ts;
+        z = pl.x[TX - 1] / p.V;
+        zbar = setpoint_at(sc, t);
+        const double r = z - zbar;
+        acc += r * r;
+    }
+    if (status == G_OK) {
+        rec->phi = acc / (double)(nbar + 1);
+        rec->failed = 0;
+        if (traj != nullptr) {
+            double* rw = traj + (size_t)row * 5;
+            rw[0] = t, rw[1] = z, rw[2] = zbar;
+        }
+    } else {
+        rec->phi = kNaN;
+        rec->failed = 1;
+    }
+    rec->ocp_solves = counts_lost ? 0 : solves;
+    rec->ocp_failures = counts_lost ? 0 : fails;
+    rec->status = status;
+    if (cntp != nullptr) {
+        nmpcmc_work_counters c;
+        c.control_steps = cnt.steps;
+        c.shoot_full = cnt.shoot_full;
+        c.shoot_fonly = cnt.shoot_fonly;
+        c.ipm_stage_iters = cnt.ipm_stage;
+        c.sqp_stage_iters = cnt.sqp_stage;
+        c.qp_solves = cnt.qp;
+        c.sqp_iterations = cnt.sqp;
+        c.ls_evals = cnt.ls;
+        *cntp = c;
+    }
+}
+
+constexpr int kGenBlock = 64;
+
+/// One thread per sample; threads pull sample indices from an atomic counter
+/// (run_monte_carlo's worker pool, montecarlo.cpp:218-238). Slot t of the
+/// workspace belongs to global thread t.
+template <int TX, int NX>
+__global__ void __launch_bounds__(kGenBlock) nmpc_gen_kernel(const __grid_constant__ nmpcmc_scenario sc,
+                                                             uint64_t first_sim, int64_t n_sims, int nbar,
+                                                             nmpcmc_sim_record* records,
+                                                             nmpcmc_work_counters* counters, double* traj,
+                                                             int traj_rows, double* ws_all, int64_t slots,
+                                                             unsigned long long* next) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= slots) return;
+    const Ws ws{ws_all + tid, slots};
+#pragma unroll 1
+    for (;;) {
+        const unsigned long long i = atomicAdd(next, 1ULL);
+        if (i >= (unsigned long long)n_sims) break;
+        closed_loop<TX, NX>(sc, first_sim + i, nbar, ws, records + i, counters ? counters + i : nullptr,
+                            traj ? traj + (size_t)i * traj_rows * 5 : nullptr);
+    }
+}
+
+/// Doubles of workspace per slot.
+inline int64_t gen_ws_doubles(const nmpcmc_scenario& sc) {
+    return sc.ctrl_variant == NMPCMC_THREE_STATE ? Layout<3>(sc.N).total : Layout<1>(sc.N).total;
+}
+
+/// Resident slots: SMs x resident 64-thread blocks, at most n.
+template <int TX, int NX>
+inline int64_t gen_slots_t(int sm_count, int64_t n) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nmpc_gen_kernel<TX, NX>, kGenBlock, 0);
+    if (b < 1) b = 1;
+    int64_t slots = (int64_t)sm_count * b * kGenBlock;
+    return slots < n ? slots : n;
+}
+inline int64_t gen_slots(const nmpcmc_scenario& sc, int sm_count, int64_t n) {
+    const bool t3 = sc.truth_variant == NMPCMC_THREE_STATE, c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
+    if (t3) return c3 ? gen_slots_t<3, 3>(sm_count, n) : gen_slots_t<3, 1>(sm_count, n);
+    return c3 ? gen_slots_t<1, 3>(sm_count, n) : gen_slots_t<1, 1>(sm_count, n);
+}
+
+inline int launch_gen(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
+                      nmpcmc_work_counters* d_cnt, double* d_traj, int rows, double* ws, int64_t slots,
+                      unsigned long long* counter, cudaStream_t stream) {
+    if (slots < 1) return NMPCMC_INVALID_ARGUMENT;
+    const unsigned grid = (unsigned)((slots + kGenBlock - 1) / kGenBlock);
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    const bool t3 = sc.truth_variant == NMPCMC_THREE_STATE, c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
+#define NMPCMC_GEN_LAUNCH(T, C) \
+    nmpc_gen_kernel<T, C><<<grid, kGenBlock, 0, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ws, slots, counter)
+    if (t3 && c3) NMPCMC_GEN_LAUNCH(3, 3);
+    else if (t3) NMPCMC_GEN_LAUNCH(3, 1);
+    else if (c3) NMPCMC_GEN_LAUNCH(1, 3);
+    else NMPCMC_GEN_LAUNCH(1, 1);
+#undef NMPCMC_GEN_LAUNCH
+    return NMPCMC_OK;
+}
+
+}  // namespace gen
+}  // namespace nmpcmc_dev

@@ -13,6 +13,7 @@
 
 #include "nmpc_kernel.cuh"
 #include "nmpc_tps_kernel.cuh"
+#include "nmpc_gen_kernel.cuh"
 #include "nmpcmc_gpu.h"
 #include "pi_kernel.cuh"
 
@@ -78,7 +79,17 @@ int launch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario& sc, uint64_t first, int64
         return cuda_check(ctx, cudaGetLastError(), "pi_kernel launch");
     }
     int rc;
-    if (ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_WARP) {
+    const bool generic = sc.ctrl_variant != NMPCMC_ONE_STATE || sc.N > 255 ||
+                         ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC;
+    if (generic) {
+        const int64_t slots = nmpcmc_dev::gen::gen_slots(sc, ctx->sm_count, n);
+        const size_t need = (size_t)slots * (size_t)nmpcmc_dev::gen::gen_ws_doubles(sc) * sizeof(double);
+        if ((rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, need)) != NMPCMC_OK) return rc;
+        if ((rc = ensure(ctx, &ctx->d_counter, &ctx->counter_cap, 256)) != NMPCMC_OK) return rc;
+        rc = nmpcmc_dev::gen::launch_gen(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
+                                         static_cast<double*>(ctx->d_ws), slots,
+                                         static_cast<unsigned long long*>(ctx->d_counter), ctx->stream);
+    } else if (ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_WARP) {
         size_t bytes = 0;
         int64_t blocks = 0;
         nmpcmc_dev::nmpc_gws_need(sc, ctx->sm_count, n, &bytes, &blocks);
@@ -141,7 +152,9 @@ int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value) {
     if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
     switch (option) {
         case NMPCMC_OPT_NMPC_KERNEL:
-            if (value != NMPCMC_NMPC_KERNEL_WARP && value != NMPCMC_NMPC_KERNEL_THREAD) return NMPCMC_INVALID_ARGUMENT;
+            if (value != NMPCMC_NMPC_KERNEL_WARP && value != NMPCMC_NMPC_KERNEL_THREAD &&
+                value != NMPCMC_NMPC_KERNEL_GENERIC)
+                return NMPCMC_INVALID_ARGUMENT;
             ctx->nmpc_kernel = (int)value;
             return NMPCMC_OK;
         case NMPCMC_OPT_TPS_WARPS_PER_SM:

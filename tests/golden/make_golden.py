@@ -87,6 +87,15 @@ def main(which):
         gen_case("nmpc_n30_short", dict(controller="nmpc", N=30, n_steps=120), 64, 2)
         gen_case("nmpc_n60_pert_short", dict(controller="nmpc", N=60, n_steps=120, perturb=True), 32, 1)
         gen_case("nmpc_n120_short", dict(controller="nmpc", N=120, n_steps=60), 16, 1)
+    if which in ("nmpc3", "all"):
+        # three-state controller model (config 2 read literally: CD-EKF and
+        # OCP on the 3-state CSTR; ctrl_variant 0 = THREE_STATE) -> kernel K3g
+        gen_case("nmpc3_cfg2", dict(controller="nmpc", N=60, ctrl_variant=0), 8, 1)
+        gen_case("nmpc3_n30_short", dict(controller="nmpc", N=30, n_steps=120, ctrl_variant=0), 32, 1)
+        gen_case("nmpc3_n60_pert_short", dict(controller="nmpc", N=60, n_steps=60, perturb=True, ctrl_variant=0),
+                 16, 1)
+        # one-state horizon beyond K3's shared-memory strides (N > 255) -> K3g
+        gen_case("nmpc_n256_short", dict(controller="nmpc", N=256, n_steps=20), 8, 1)
 
 
 if __name__ == "__main__":

@@ -51,8 +51,14 @@ def test_validate_matches_reference_rules():
     with pytest.raises(engine.DomainError):
         engine.validate_scenario(bad)
     three = configs.make_scenario("nmpc", ctrl_variant=abi.THREE_STATE)
+    assert engine.validate_scenario(three) == 720  # runs on K3g
+    bad = configs.make_scenario("nmpc", ctrl_variant=abi.THREE_STATE)
+    bad.ctrl_variant = 7
+    with pytest.raises(engine.DomainError):
+        engine.validate_scenario(bad)
+    big = configs.make_scenario("nmpc", N=5000)
     with pytest.raises(engine.Unsupported):
-        engine.validate_scenario(three)
+        engine.validate_scenario(big)
     neg = configs.make_scenario("pi", noise_R=-1.0)
     with pytest.raises(engine.NotPositiveDefinite):
         engine.validate_scenario(neg)

@@ -1,6 +1,6 @@
 """The oracle's C++ restatement (oracle/port/nmpcmc_port.cpp) against the
-compiled reference: bitwise on the golden fixtures in both libm modes, and on
-the three-state controller model (which the device does not run yet)."""
+compiled reference: bitwise on the golden fixtures in both libm modes,
+three-state controller model included (the device runs it on K3g)."""
 import os
 
 import numpy as np
@@ -11,7 +11,7 @@ from oracle import lib as O
 from paper_2212_02197_b200 import abi, configs
 
 CASES = [("pi_cfg0", 256), ("pi_cfg1", 256), ("pi_onestate", 64), ("pi_quiet", 16),
-         ("nmpc_n30_short", 8), ("nmpc_n120_short", 2)]
+         ("nmpc_n30_short", 8), ("nmpc_n120_short", 2), ("nmpc3_n30_short", 8), ("nmpc3_n60_pert_short", 4)]
 
 
 @pytest.mark.parametrize("libm", ["xlibm", "glibc"])
