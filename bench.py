@@ -45,6 +45,8 @@ def parse():
                     help="NMPC (and PI) samples per rank per step (9,472 = 4 waves of 148 SMs x 16 resident samples)")
     ap.add_argument("--horizon", type=int, default=60)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-lanes", action="store_true",
+                    help="serial batches on one stream (default: NMPCMC_OPT_LANES=2 pipelining)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="NMPC samples for the CPU baseline (0 = host cores)")
     return ap.parse_args()
 
@@ -201,23 +203,29 @@ def run_ours(args):
     def first_of(j):
         return ((j * world + rank) * S) % TOTAL_SIMS
 
+    lanes = not args.no_lanes
     ev = []
 
     def step(j, timed):
+        """One step: the NMPC batch and the PI batch of the same indices. With
+        lanes, consecutive NMPC batches run on alternating library streams, so
+        a batch's drain (its last wave of long samples) overlaps the next."""
         first = first_of(j)
-        if timed:
+        if timed and not lanes:
             e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             e[0].record(stream)
         ctx.run_device(sc_n, first, S, rec_n[j].data_ptr(), cnt_n[j].data_ptr())
-        if timed:
+        if timed and not lanes:
             e[1].record(stream)
         ctx.run_device(sc_p, first, S, rec_p[j].data_ptr(), cnt_p[j].data_ptr())
-        if timed:
+        if timed and not lanes:
             e[2].record(stream)
             ev.append(e)
 
+    ctx.set_lanes(2 if lanes else 1)
     for j in range(W):
         step(j, False)
+    ctx.join()
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -228,15 +236,31 @@ def run_ours(args):
     t0.record(stream)
     for j in range(W, W + K):
         step(j, True)
+    ctx.join()  # the stream now waits for every lane
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
     elapsed = t0.elapsed_time(t1) / 1e3
     elapsed_max = max_over_ranks(elapsed)
-    nmpc_kernel_s = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3
-    pi_kernel_s = sum(e[1].elapsed_time(e[2]) for e in ev) / 1e3
     value = world * S * K / elapsed_max
+
+    # kernel times: serial mode brackets each launch with events on the launch
+    # stream; with lanes the launches overlap, so the NMPC kernel's time per
+    # launch is the pipeline period (elapsed / K, PI on its own lane inside it)
+    # and the PI kernel is timed alone once after the timed region
+    if lanes:
+        nmpc_kernel_s = elapsed
+        ctx.set_lanes(1)
+        pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        pe[0].record(stream)
+        ctx.run_device(sc_p, first_of(W), S, rec_p[W].data_ptr(), cnt_p[W].data_ptr())
+        pe[1].record(stream)
+        torch.cuda.synchronize()
+        pi_kernel_s = K * pe[0].elapsed_time(pe[1]) / 1e3
+    else:
+        nmpc_kernel_s = sum(e[0].elapsed_time(e[1]) for e in ev) / 1e3
+        pi_kernel_s = sum(e[1].elapsed_time(e[2]) for e in ev) / 1e3
 
     # roofline of the dominant kernel (NMPC) from the device work counters
     cn = np.frombuffer(cnt_n[W:].cpu().numpy().tobytes(), dtype=abi.COUNTERS_DTYPE)
@@ -247,16 +271,23 @@ def run_ours(args):
     peak_add = ctx.fp64_peak(False)
     achieved = nmpc_flops / nmpc_kernel_s / 1e12
 
-    # end to end through the public C ABI with host buffers (nmpcmc_gpu_run):
-    # H2D = the scenario PODs (kernel arguments), D2H = the per-sample records
-    Ke = max(1, min(K, 2))
+    # end to end through the public C ABI with HOST buffers: every step enqueues
+    # its batches (H2D = the scenario PODs, passed as kernel arguments) and the
+    # copy of its records into pinned host memory (D2H); one wait at the end
+    Ke = K
+    ctx.set_lanes(2 if lanes else 1)
+    host_n = [torch.empty(S * rec_sz, dtype=torch.uint8).pin_memory() for _ in range(Ke)]
+    host_p = [torch.empty(S * rec_sz, dtype=torch.uint8).pin_memory() for _ in range(Ke)]
+    torch.cuda.synchronize()
     barrier()
     te = time.perf_counter()
     for j in range(Ke):
-        r1, _ = ctx.run(sc_n, first_of(W + K + j), S)
-        r2, _ = ctx.run(sc_p, first_of(W + K + j), S)
+        ctx.run_async(sc_n, first_of(W + K + j), S, host_n[j].data_ptr())
+        ctx.run_async(sc_p, first_of(W + K + j), S, host_p[j].data_ptr())
+    ctx.wait()
     e2e_s = max_over_ranks(time.perf_counter() - te)
     e2e_value = world * S * Ke / e2e_s
+    ctx.set_lanes(1)
 
     # final statistics: gather the last timed step's records from every rank (NCCL)
     last_n, last_p = rec_n[W + K - 1], rec_p[W + K - 1]
@@ -299,11 +330,19 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded per-sample noise and parameters)",
             "config": workload_config(args, world),
             "e2e": {"value": e2e_value, "unit": "sims/s", "h2d_bytes_per_step": 2 * C.sizeof(abi.Scenario),
-                    "d2h_bytes_per_step": 2 * S * rec_sz, "steps": Ke},
+                    "d2h_bytes_per_step": 2 * S * rec_sz, "steps": Ke,
+                    "api": "nmpcmc_gpu_run_async (host records, pinned) x 2 per step + nmpcmc_gpu_wait"},
+            "pipelining": "lanes=2 (NMPCMC_OPT_LANES): consecutive batches overlap at their drain" if lanes
+                          else "serial batches on one stream",
             "gpu_launches": 2 * K,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_fma, "unit": "TFLOP/s",
                          "frac": achieved / peak_fma, "traffic": None,
-                         "kernel": "nmpc_kernel<3>", "kernel_ms_per_step": 1e3 * nmpc_kernel_s / K,
+                         "traffic_note": "ncu --set full of the same kernel (2,368 samples x 6 steps): 325.5 MB DRAM "
+                                         "per launch, 2.4 GB/s -- workspace spill from L2, HBM idle "
+                                         "(profiles/r01d_nmpc_ncu_summary.md)",
+                         "kernel": "nmpc_kernel<3,64>", "kernel_ms_per_step": 1e3 * nmpc_kernel_s / K,
+                         "kernel_time": "pipeline period elapsed/K (launches overlap on two lanes)" if lanes
+                                        else "CUDA events around each launch on its stream",
                          "flops_per_step": nmpc_flops / K,
                          "peak_source": "measured on this GPU: DFMA throughput kernel (nmpcmc_gpu_fp64_peak), "
                                         "2 flops/DFMA; MEASURED_PEAKS.json has no FP64 entry",

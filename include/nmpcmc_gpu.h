@@ -168,7 +168,15 @@ const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx);
  * A three-state controller model or N > 255 always runs K3g. Results are
  * bitwise identical; only speed differs. NMPCMC_OPT_TPS_WARPS_PER_SM = resident
  * warps per SM for K3b (default 8). */
-enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2 };
+enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2, NMPCMC_OPT_LANES = 3 };
+/* NMPCMC_OPT_LANES = 2 pipelines back-to-back batches: NMPC launches alternate
+ * between two internal streams with their own workspace (PI launches use a
+ * third), each forked from the context stream, so one batch's drain (its last
+ * wave of long samples) overlaps the next batch. Work on a lane is ordered
+ * after everything enqueued on the context stream before the call; later work
+ * on the context stream is ordered after the lanes only through
+ * nmpcmc_gpu_join / nmpcmc_gpu_wait. 1 (default) = everything on the context
+ * stream. */
 enum { NMPCMC_NMPC_KERNEL_WARP = 1, NMPCMC_NMPC_KERNEL_THREAD = 2, NMPCMC_NMPC_KERNEL_GENERIC = 3 };
 int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value);
 /* CUDA stream the context launches on (as void*; 0 = legacy default). */
@@ -182,8 +190,22 @@ int nmpcmc_gpu_run(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t firs
                    int64_t n_sims, nmpcmc_sim_record* records_out,
                    nmpcmc_work_counters* counters_out, nmpcmc_aggregate* agg_out);
 
+/* Asynchronous form: enqueue the batch and the copy of its records (and
+ * counters, may be NULL) into HOST buffers, which must stay valid until
+ * nmpcmc_gpu_wait. With pinned host memory and NMPCMC_OPT_LANES = 2,
+ * consecutive calls overlap. */
+int nmpcmc_gpu_run_async(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
+                         int64_t n_sims, nmpcmc_sim_record* records_out,
+                         nmpcmc_work_counters* counters_out);
+/* Order the context stream after all work enqueued on the lanes (no host
+ * wait); no-op without lanes. */
+int nmpcmc_gpu_join(nmpcmc_gpu_ctx* ctx);
+/* join + wait on the host for the context stream; reports kernel errors. */
+int nmpcmc_gpu_wait(nmpcmc_gpu_ctx* ctx);
+
 /* Same, DEVICE-resident outputs (records_dev[n_sims], counters_dev may be
- * NULL), enqueued on the context stream; returns after the launch. */
+ * NULL), enqueued on the context stream (or a lane, NMPCMC_OPT_LANES);
+ * returns after the launch. */
 int nmpcmc_gpu_run_device(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
                           int64_t n_sims, nmpcmc_sim_record* records_dev,
                           nmpcmc_work_counters* counters_dev);

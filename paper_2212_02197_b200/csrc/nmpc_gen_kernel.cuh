@@ -1002,11 +1002,11 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX>& o, const nmpcmc_sqp_opti
 #pragma unroll 1
         for (int bt = 0;; ++bt) {
             for (int e = 0; e < L.L; ++e) w[L.XI[t] + e] = w[L.XI[s] + e] + a * w[L.QDXI + e];
-            o.cnt->ls += 1;
             merit = __longlong_as_double(0x7ff0000000000000LL);
             ft = objective<NX>(o, t, true);
             const int st = constraints<NX>(o, t);
             if (st == G_DOMAIN) return SqpOut{false, G_DOMAIN};
+            o.cnt->ls += 1;  // counted like K3: a trial that raises DomainError ends the solve uncounted
             tfin = st == G_OK;
             if (tfin) {
                 merit = ft;

@@ -17,6 +17,26 @@
 #include "nmpcmc_gpu.h"
 #include "pi_kernel.cuh"
 
+/// Where one launch runs and the workspace it owns. The context's own target
+/// uses ctx->stream; with NMPCMC_OPT_LANES = 2, NMPC launches alternate
+/// between two lanes and PI launches use a third, each lane with its own
+/// stream and workspace, so a batch's drain overlaps the next batch.
+struct Lane {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+    bool pending = false;
+    void* d_gws = nullptr;
+    size_t gws_cap = 0;
+    void* d_counter = nullptr;
+    size_t counter_cap = 0;
+    void* d_ws = nullptr;
+    size_t ws_cap = 0;
+    void* d_rec = nullptr;
+    size_t rec_cap = 0;
+    void* d_cnt = nullptr;
+    size_t cnt_cap = 0;
+};
+
 struct nmpcmc_gpu_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -38,6 +58,11 @@ struct nmpcmc_gpu_ctx {
     int sm_count = 0;
     int nmpc_kernel = NMPCMC_NMPC_KERNEL_WARP;    // which NMPC kernel to launch
     int tps_warps_per_sm = 8;                     // K3b resident warps per SM
+    cudaStream_t own = nullptr;                   // the stream ctx_create made (set_stream may replace ctx->stream)
+    int lanes = 1;                                // NMPCMC_OPT_LANES
+    int next_nmpc_lane = 0;
+    Lane lane[3];
+    cudaEvent_t fork = nullptr;
 };
 
 namespace {
@@ -63,18 +88,36 @@ int ensure(nmpcmc_gpu_ctx* ctx, void** buf, size_t* cap, size_t need) {
     return NMPCMC_OK;
 }
 
-/// Enqueue the closed-loop kernel for [first, first+n) on ctx->stream.
-int launch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar,
+/// Launch target: a stream and the workspace buffers the launch may use.
+struct Target {
+    cudaStream_t stream;
+    void** d_gws;
+    size_t* gws_cap;
+    void** d_counter;
+    size_t* counter_cap;
+    void** d_ws;
+    size_t* ws_cap;
+};
+Target main_target(nmpcmc_gpu_ctx* ctx) {
+    return Target{ctx->stream, &ctx->d_gws, &ctx->gws_cap, &ctx->d_counter, &ctx->counter_cap, &ctx->d_ws,
+                  &ctx->ws_cap};
+}
+Target lane_target(Lane& l) {
+    return Target{l.stream, &l.d_gws, &l.gws_cap, &l.d_counter, &l.counter_cap, &l.d_ws, &l.ws_cap};
+}
+
+/// Enqueue the closed-loop kernel for [first, first+n) on target tg.
+int launch(nmpcmc_gpu_ctx* ctx, const Target& tg, const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar,
            nmpcmc_sim_record* d_rec, nmpcmc_work_counters* d_cnt, double* d_traj, int rows) {
     if (n == 0) return NMPCMC_OK;
     if (sc.controller == NMPCMC_CTRL_PI) {
         const int block = 128;
         const int64_t grid = (n + block - 1) / block;
         if (sc.truth_variant == NMPCMC_THREE_STATE)
-            nmpcmc_dev::pi_kernel<3><<<(unsigned)grid, block, 0, ctx->stream>>>(
+            nmpcmc_dev::pi_kernel<3><<<(unsigned)grid, block, 0, tg.stream>>>(
                 sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
         else
-            nmpcmc_dev::pi_kernel<1><<<(unsigned)grid, block, 0, ctx->stream>>>(
+            nmpcmc_dev::pi_kernel<1><<<(unsigned)grid, block, 0, tg.stream>>>(
                 sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
         return cuda_check(ctx, cudaGetLastError(), "pi_kernel launch");
     }
@@ -84,30 +127,57 @@ int launch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario& sc, uint64_t first, int64
     if (generic) {
         const int64_t slots = nmpcmc_dev::gen::gen_slots(sc, ctx->sm_count, n);
         const size_t need = (size_t)slots * (size_t)nmpcmc_dev::gen::gen_ws_doubles(sc) * sizeof(double);
-        if ((rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, need)) != NMPCMC_OK) return rc;
-        if ((rc = ensure(ctx, &ctx->d_counter, &ctx->counter_cap, 256)) != NMPCMC_OK) return rc;
+        if ((rc = ensure(ctx, tg.d_ws, tg.ws_cap, need)) != NMPCMC_OK) return rc;
+        if ((rc = ensure(ctx, tg.d_counter, tg.counter_cap, 256)) != NMPCMC_OK) return rc;
         rc = nmpcmc_dev::gen::launch_gen(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
-                                         static_cast<double*>(ctx->d_ws), slots,
-                                         static_cast<unsigned long long*>(ctx->d_counter), ctx->stream);
+                                         static_cast<double*>(*tg.d_ws), slots,
+                                         static_cast<unsigned long long*>(*tg.d_counter), tg.stream);
     } else if (ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_WARP) {
         size_t bytes = 0;
         int64_t blocks = 0;
         nmpcmc_dev::nmpc_gws_need(sc, ctx->sm_count, n, &bytes, &blocks);
-        if ((rc = ensure(ctx, &ctx->d_gws, &ctx->gws_cap, bytes)) != NMPCMC_OK) return rc;
-        if ((rc = ensure(ctx, &ctx->d_counter, &ctx->counter_cap, 256)) != NMPCMC_OK) return rc;
+        if ((rc = ensure(ctx, tg.d_gws, tg.gws_cap, bytes)) != NMPCMC_OK) return rc;
+        if ((rc = ensure(ctx, tg.d_counter, tg.counter_cap, 256)) != NMPCMC_OK) return rc;
         rc = nmpcmc_dev::launch_nmpc(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ctx->sm_count,
-                                     static_cast<double*>(ctx->d_gws), blocks,
-                                     static_cast<unsigned long long*>(ctx->d_counter), ctx->stream);
+                                     static_cast<double*>(*tg.d_gws), blocks,
+                                     static_cast<unsigned long long*>(*tg.d_counter), tg.stream);
     } else {
         int64_t slots = (int64_t)ctx->sm_count * ctx->tps_warps_per_sm * 32;
         if (slots > n) slots = ((n + 31) / 32) * 32;
         const size_t need = nmpcmc_dev::tps_ws_bytes(sc.N, slots);
-        if ((rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, need)) != NMPCMC_OK) return rc;
+        if ((rc = ensure(ctx, tg.d_ws, tg.ws_cap, need)) != NMPCMC_OK) return rc;
         rc = nmpcmc_dev::launch_nmpc_tps(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
-                                         static_cast<double*>(ctx->d_ws), slots, ctx->stream);
+                                         static_cast<double*>(*tg.d_ws), slots, tg.stream);
     }
     if (rc != NMPCMC_OK) return fail(ctx, rc, "nmpc launch: unsupported configuration");
     return cuda_check(ctx, cudaGetLastError(), "nmpc_kernel launch");
+}
+
+/// Pick the lane of the next launch (lane mode): NMPC launches alternate
+/// between lanes 0 and 1, PI uses lane 2. The lane first waits for all work
+/// enqueued so far on ctx->stream.
+int lane_begin(nmpcmc_gpu_ctx* ctx, int controller, Lane** out) {
+    int rc;
+    if (ctx->fork == nullptr &&
+        (rc = cuda_check(ctx, cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming), "event")) != NMPCMC_OK)
+        return rc;
+    const int i = controller == NMPCMC_CTRL_PI ? 2 : (ctx->next_nmpc_lane++ & 1);
+    Lane& l = ctx->lane[i];
+    if (l.stream == nullptr) {
+        if ((rc = cuda_check(ctx, cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking), "lane stream")) !=
+            NMPCMC_OK)
+            return rc;
+        if ((rc = cuda_check(ctx, cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming), "event")) != NMPCMC_OK)
+            return rc;
+    }
+    cudaEventRecord(ctx->fork, ctx->stream);
+    cudaStreamWaitEvent(l.stream, ctx->fork, 0);
+    *out = &l;
+    return NMPCMC_OK;
+}
+void lane_end(Lane* l) {
+    cudaEventRecord(l->done, l->stream);
+    l->pending = true;
 }
 
 }  // namespace
@@ -131,6 +201,7 @@ int nmpcmc_gpu_ctx_create(int device, nmpcmc_gpu_ctx** out) {
         delete ctx;
         return NMPCMC_CUDA_ERROR;
     }
+    ctx->own = ctx->stream;
     *out = ctx;
     return NMPCMC_OK;
 }
@@ -138,7 +209,17 @@ int nmpcmc_gpu_ctx_create(int device, nmpcmc_gpu_ctx** out) {
 void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx) {
     if (ctx == nullptr) return;
     cudaSetDevice(ctx->device);
-    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    for (Lane& l : ctx->lane) {
+        if (l.stream) {
+            cudaStreamSynchronize(l.stream);
+            cudaStreamDestroy(l.stream);
+        }
+        if (l.done) cudaEventDestroy(l.done);
+        for (void* p : {l.d_gws, l.d_counter, l.d_ws, l.d_rec, l.d_cnt})
+            if (p) cudaFree(p);
+    }
+    if (ctx->fork) cudaEventDestroy(ctx->fork);
+    if (ctx->own) cudaStreamDestroy(ctx->own);
     for (void* p : {ctx->d_rec, ctx->d_cnt, ctx->d_traj, ctx->d_scratch, ctx->d_ws, ctx->d_gws, ctx->d_counter})
         if (p) cudaFree(p);
     delete ctx;
@@ -157,6 +238,11 @@ int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value) {
                 return NMPCMC_INVALID_ARGUMENT;
             ctx->nmpc_kernel = (int)value;
             return NMPCMC_OK;
+        case NMPCMC_OPT_LANES:
+            if (value != 1 && value != 2) return NMPCMC_INVALID_ARGUMENT;
+            nmpcmc_gpu_join(ctx);
+            ctx->lanes = (int)value;
+            return NMPCMC_OK;
         case NMPCMC_OPT_TPS_WARPS_PER_SM:
             if (value < 1 || value > 64) return NMPCMC_INVALID_ARGUMENT;
             ctx->tps_warps_per_sm = (int)value;
@@ -168,6 +254,7 @@ int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value) {
 
 int nmpcmc_gpu_set_stream(nmpcmc_gpu_ctx* ctx, void* stream) {
     if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    nmpcmc_gpu_join(ctx);  // lanes stay ordered before later work on the old stream
     ctx->stream = static_cast<cudaStream_t>(stream);
     return NMPCMC_OK;
 }
@@ -181,35 +268,72 @@ int nmpcmc_gpu_run_device(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64
     int rc = nmpcmc_gpu_validate(sc, &nbar);
     if (rc != NMPCMC_OK) return fail(ctx, rc, "scenario validation failed");
     cudaSetDevice(ctx->device);
-    return launch(ctx, *sc, first_sim, n_sims, nbar, records_dev, counters_dev, nullptr, 0);
+    if (ctx->lanes > 1) {
+        Lane* l = nullptr;
+        if ((rc = lane_begin(ctx, sc->controller, &l)) != NMPCMC_OK) return rc;
+        rc = launch(ctx, lane_target(*l), *sc, first_sim, n_sims, nbar, records_dev, counters_dev, nullptr, 0);
+        lane_end(l);
+        return rc;
+    }
+    return launch(ctx, main_target(ctx), *sc, first_sim, n_sims, nbar, records_dev, counters_dev, nullptr, 0);
 }
 
-int nmpcmc_gpu_run(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
-                   int64_t n_sims, nmpcmc_sim_record* records_out,
-                   nmpcmc_work_counters* counters_out, nmpcmc_aggregate* agg_out) {
+int nmpcmc_gpu_run_async(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
+                         int64_t n_sims, nmpcmc_sim_record* records_out,
+                         nmpcmc_work_counters* counters_out) {
     if (ctx == nullptr || sc == nullptr || records_out == nullptr || n_sims < 1)
         return NMPCMC_INVALID_ARGUMENT;
     int32_t nbar = 0;
     int rc = nmpcmc_gpu_validate(sc, &nbar);
     if (rc != NMPCMC_OK) return fail(ctx, rc, "scenario validation failed");
     cudaSetDevice(ctx->device);
+    Lane* l = nullptr;
+    if (ctx->lanes > 1 && (rc = lane_begin(ctx, sc->controller, &l)) != NMPCMC_OK) return rc;
+    const Target tg = l ? lane_target(*l) : main_target(ctx);
+    void** rec_buf = l ? &l->d_rec : &ctx->d_rec;
+    size_t* rec_cap = l ? &l->rec_cap : &ctx->rec_cap;
+    void** cnt_buf = l ? &l->d_cnt : &ctx->d_cnt;
+    size_t* cnt_cap = l ? &l->cnt_cap : &ctx->cnt_cap;
     const size_t nrec = (size_t)n_sims * sizeof(nmpcmc_sim_record);
-    if ((rc = ensure(ctx, &ctx->d_rec, &ctx->rec_cap, nrec)) != NMPCMC_OK) return rc;
-    nmpcmc_work_counters* d_cnt = nullptr;
-    if (counters_out) {
-        if ((rc = ensure(ctx, &ctx->d_cnt, &ctx->cnt_cap, (size_t)n_sims * sizeof(nmpcmc_work_counters))) != NMPCMC_OK)
-            return rc;
-        d_cnt = static_cast<nmpcmc_work_counters*>(ctx->d_cnt);
-    }
-    auto* d_rec = static_cast<nmpcmc_sim_record*>(ctx->d_rec);
-    if ((rc = launch(ctx, *sc, first_sim, n_sims, nbar, d_rec, d_cnt, nullptr, 0)) != NMPCMC_OK) return rc;
-    if ((rc = cuda_check(ctx, cudaMemcpyAsync(records_out, d_rec, nrec, cudaMemcpyDeviceToHost, ctx->stream), "D2H records")) != NMPCMC_OK)
-        return rc;
-    if (counters_out &&
-        (rc = cuda_check(ctx, cudaMemcpyAsync(counters_out, d_cnt, (size_t)n_sims * sizeof(nmpcmc_work_counters),
-                                              cudaMemcpyDeviceToHost, ctx->stream), "D2H counters")) != NMPCMC_OK)
-        return rc;
-    if ((rc = cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "kernel execution")) != NMPCMC_OK) return rc;
+    const size_t ncnt = (size_t)n_sims * sizeof(nmpcmc_work_counters);
+    if ((rc = ensure(ctx, rec_buf, rec_cap, nrec)) != NMPCMC_OK) return rc;
+    if (counters_out && (rc = ensure(ctx, cnt_buf, cnt_cap, ncnt)) != NMPCMC_OK) return rc;
+    auto* d_rec = static_cast<nmpcmc_sim_record*>(*rec_buf);
+    auto* d_cnt = counters_out ? static_cast<nmpcmc_work_counters*>(*cnt_buf) : nullptr;
+    rc = launch(ctx, tg, *sc, first_sim, n_sims, nbar, d_rec, d_cnt, nullptr, 0);
+    if (rc == NMPCMC_OK)
+        rc = cuda_check(ctx, cudaMemcpyAsync(records_out, d_rec, nrec, cudaMemcpyDeviceToHost, tg.stream),
+                        "D2H records");
+    if (rc == NMPCMC_OK && counters_out)
+        rc = cuda_check(ctx, cudaMemcpyAsync(counters_out, d_cnt, ncnt, cudaMemcpyDeviceToHost, tg.stream),
+                        "D2H counters");
+    if (l) lane_end(l);
+    return rc;
+}
+
+int nmpcmc_gpu_join(nmpcmc_gpu_ctx* ctx) {
+    if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    for (Lane& l : ctx->lane)
+        if (l.pending) {
+            cudaStreamWaitEvent(ctx->stream, l.done, 0);
+            l.pending = false;
+        }
+    return NMPCMC_OK;
+}
+
+int nmpcmc_gpu_wait(nmpcmc_gpu_ctx* ctx) {
+    if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    nmpcmc_gpu_join(ctx);
+    return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "kernel execution");
+}
+
+int nmpcmc_gpu_run(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
+                   int64_t n_sims, nmpcmc_sim_record* records_out,
+                   nmpcmc_work_counters* counters_out, nmpcmc_aggregate* agg_out) {
+    int rc = nmpcmc_gpu_run_async(ctx, sc, first_sim, n_sims, records_out, counters_out);
+    if (rc != NMPCMC_OK) return rc;
+    if ((rc = nmpcmc_gpu_wait(ctx)) != NMPCMC_OK) return rc;
     if (agg_out) return nmpcmc_gpu_aggregate(records_out, n_sims, agg_out);
     return NMPCMC_OK;
 }
@@ -231,7 +355,8 @@ int nmpcmc_gpu_run_traj(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t
     if ((rc = cuda_check(ctx, cudaMemsetAsync(ctx->d_traj, 0xff, ntraj, ctx->stream), "memset")) != NMPCMC_OK) return rc;
     auto* d_rec = static_cast<nmpcmc_sim_record*>(ctx->d_rec);
     auto* d_traj = static_cast<double*>(ctx->d_traj);
-    if ((rc = launch(ctx, *sc, first_sim, n_sims, nbar, d_rec, nullptr, d_traj, rows)) != NMPCMC_OK) return rc;
+    if ((rc = launch(ctx, main_target(ctx), *sc, first_sim, n_sims, nbar, d_rec, nullptr, d_traj, rows)) != NMPCMC_OK)
+        return rc;
     cudaMemcpyAsync(records_out, d_rec, nrec, cudaMemcpyDeviceToHost, ctx->stream);
     cudaMemcpyAsync(traj_out, d_traj, ntraj, cudaMemcpyDeviceToHost, ctx->stream);
     return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "kernel execution");

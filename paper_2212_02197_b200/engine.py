@@ -93,6 +93,9 @@ def library():
     lib.nmpcmc_gpu_set_option.argtypes = [P, C.c_int32, C.c_int64]
     lib.nmpcmc_gpu_run.argtypes = [P, S, C.c_uint64, C.c_int64, R, W, A]
     lib.nmpcmc_gpu_run_device.argtypes = [P, S, C.c_uint64, C.c_int64, P, P]
+    lib.nmpcmc_gpu_run_async.argtypes = [P, S, C.c_uint64, C.c_int64, P, P]
+    lib.nmpcmc_gpu_join.argtypes = [P]
+    lib.nmpcmc_gpu_wait.argtypes = [P]
     lib.nmpcmc_gpu_traj_rows.argtypes = [S]
     lib.nmpcmc_gpu_traj_rows.restype = C.c_int32
     lib.nmpcmc_gpu_run_traj.argtypes = [P, S, C.c_uint64, C.c_int64, R, C.POINTER(C.c_double)]
@@ -166,8 +169,28 @@ class Context:
             _ptr(cnt, abi.WorkCounters) if cnt is not None else None, None))
         return rec, cnt
 
+    def set_lanes(self, lanes: int):
+        """NMPCMC_OPT_LANES: 2 pipelines consecutive batches over two internal
+        streams (a batch's drain overlaps the next); 1 = context stream only."""
+        self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 3, lanes))
+
+    def run_async(self, sc, first_sim: int, n_sims: int, rec_ptr: int, cnt_ptr: int = 0):
+        """Enqueue a batch and the copy of its records (counters) into HOST
+        memory at rec_ptr (cnt_ptr); valid after wait(). Pinned memory lets
+        consecutive calls overlap."""
+        self._check(self.lib.nmpcmc_gpu_run_async(
+            self.handle, C.byref(sc), first_sim, n_sims, C.c_void_p(rec_ptr),
+            C.c_void_p(cnt_ptr) if cnt_ptr else None))
+
+    def join(self):
+        """Order the context stream after all lane work (no host wait)."""
+        self._check(self.lib.nmpcmc_gpu_join(self.handle))
+
+    def wait(self):
+        self._check(self.lib.nmpcmc_gpu_wait(self.handle))
+
     def run_device(self, sc, first_sim: int, n_sims: int, rec_ptr: int, cnt_ptr: int = 0):
-        """Enqueue on the context stream; outputs are device pointers."""
+        """Enqueue on the context stream (or a lane); outputs are device pointers."""
         self._check(self.lib.nmpcmc_gpu_run_device(
             self.handle, C.byref(sc), first_sim, n_sims, C.c_void_p(rec_ptr),
             C.c_void_p(cnt_ptr) if cnt_ptr else None))
