@@ -105,7 +105,11 @@ __device__ __forceinline__ bool mant_nonzero(double x) {
     return ((__double2hiint(x) & 0x000fffff) | __double2loint(x)) != 0;
 }
 
-/// l ~ sqrt(h) and y ~ 1/l for h > 0: Newton on the hardware rsqrt seed and
+#ifndef NMPCMC_SQRT_ONE_NEWTON
+#define NMPCMC_SQRT_ONE_NEWTON 1
+#endif
+/// l ~ sqrt(h) and y ~ 1/l for h > 0: one Newton step (default; two with
+/// NMPCMC_SQRT_ONE_NEWTON=0) on the hardware rsqrt seed and
 /// a Markstein correction. Not yet certified (see cert_sqrt).
 __device__ __forceinline__ void fast_sqrt(double h, double& l, double& y) {
     double y0;
@@ -113,8 +117,10 @@ __device__ __forceinline__ void fast_sqrt(double h, double& l, double& y) {
     const double hh = 0.5 * h;
     double e = __fma_rn(-hh, y0 * y0, 0.5);
     y0 = __fma_rn(y0, e, y0);
+#if !NMPCMC_SQRT_ONE_NEWTON
     e = __fma_rn(-hh, y0 * y0, 0.5);
     y0 = __fma_rn(y0, e, y0);
+#endif
     const double s = h * y0;
     const double d = __fma_rn(-s, s, h);
     l = __fma_rn(d, 0.5 * y0, s);
