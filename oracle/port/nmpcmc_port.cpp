@@ -21,7 +21,18 @@
 
 #include "nmpcmc_gpu.h"
 
-#ifdef PORT_XLIBM
+// Op-counting build (oracle/port/flopcount.cpp) supplies its own libm and
+// phase/unit markers; they are empty here.
+#ifndef PORT_PHASE
+#define PORT_PHASE(ph)
+#define PORT_UNIT(u, n)
+#define PORT_TO_DOUBLE(x) (x)
+#define PORT_REAL double
+#endif
+
+#if defined(PORT_CUSTOM_LIBM)
+#define PFX(name) nmpcmc_portc_##name
+#elif defined(PORT_XLIBM)
 extern "C" {
 double nmx_exp(double);
 double nmx_log(double);
@@ -304,6 +315,7 @@ struct Cstr {
 // ------------------------------------------------------------------ plant
 /// simulate_interval + euler_maruyama_step (model.cpp:13-37).
 static Vec simulate(const Cstr& m, double t0, double t1, Vec x, double u, int ns, Rng& rng) {
+    PORT_PHASE(PLANT);
     const double dt = (t1 - t0) / ns;
     const double sdt = std::sqrt(dt);
     Vec dw(m.nx);
@@ -321,6 +333,7 @@ static Vec simulate(const Cstr& m, double t0, double t1, Vec x, double u, int ns
 
 /// measure (model.cpp:39-48), n_y = 1.
 static double measure(const Cstr& m, bool hasR, double R, const Vec& x, Rng& rng) {
+    PORT_PHASE(PLANT);
     Vec y{m.out(x)};
     if (hasR) {
         Mat Rm(1, 1);
@@ -335,6 +348,7 @@ static double measure(const Cstr& m, bool hasR, double R, const Vec& x, Rng& rng
 // -------------------------------------------------------------------- EKF
 /// predict (ekf.cpp:12-57): RK4 on (x, P), symmetrised each step.
 static void ekf_predict(const Cstr& m, Vec& x, Mat& P, double u, double t, double tn, int np) {
+    PORT_PHASE(EKF);
     const double h = (tn - t) / np;
     auto rhs = [&](const Vec& xs, const Mat& Ps, Vec& dx, Mat& dP) {
         dx = m.drift(xs, u);
@@ -367,6 +381,7 @@ static void ekf_predict(const Cstr& m, Vec& x, Mat& P, double u, double t, doubl
 
 /// filter_update (ekf.cpp:59-96), Joseph form, n_y = 1.
 static void ekf_update(const Cstr& m, Vec& x, Mat& P, double y, double R) {
+    PORT_PHASE(EKF);
     const int n = m.nx;
     Mat C(1, n);
     C.at(0, n - 1) = 1.0 / m.p.V;
@@ -417,6 +432,8 @@ struct Shot {
 
 /// shoot (ocp.cpp:9-74): Nc RK4 steps with forward sensitivities.
 static Shot shoot(const Nlp& q, const Vec& x, double u) {
+    PORT_PHASE(SHOOT);
+    PORT_UNIT(SHOOT, 1);
     const Cstr& m = *q.m;
     const double h = q.Ts / q.Nc;
     Shot s{x, Mat::eye(q.nx), Mat(q.nx, 1)};
@@ -509,6 +526,7 @@ static Blocks constraints(const Nlp& q, const Vec& xi) {
 
 /// xi_from_inputs (ocp.cpp:137-154).
 static Vec xi_from_u(const Nlp& q, const Vec& us) {
+    PORT_PHASE(XI);
     Vec xi(q.size());
     Vec xk = q.x0;
     for (int k = 0; k < q.N; ++k) {
@@ -614,6 +632,7 @@ static void rsolve(const std::vector<Stage>& st, int N, int nx, const Factor& f,
 
 /// solve_qp (qp.cpp:173-423): Mehrotra predictor-corrector interior point.
 static QpOut solve_qp(const std::vector<Stage>& st, int N, int nx, double tol, int max_iter) {
+    PORT_PHASE(QP);
     const int w = 1 + nx;
     auto uo = [&](int k) { return k * w; };
     auto xo = [&](int k) { return (k - 1) * w + 1; };
@@ -764,6 +783,7 @@ static QpOut solve_qp(const std::vector<Stage>& st, int N, int nx, double tol, i
             if (fl[k]) sl[k] += a * dsl[k], nl[k] += a * dnl[k];
             if (fu[k]) su[k] += a * dsu[k], nu[k] += a * dnu[k];
         }
+        PORT_UNIT(IPM, N);
     }
     for (int k = 0; k < N; ++k) {
         double& v = o.dxi[uo(k)];
@@ -868,6 +888,7 @@ struct SqpRes {
 
 /// sqp_solve (sqp.cpp:182-411); opts per SqpOptions (sqp.hpp:50-58).
 static SqpRes sqp(const Nlp& q, Vec xi, Duals d, const nmpcmc_sqp_options& op) {
+    PORT_PHASE(SQP);
     const int nx = q.nx, N = q.N;
     const int m = N * nx + (std::isfinite(q.umin) ? N : 0) + (std::isfinite(q.umax) ? N : 0);
     SqpRes out;
@@ -892,6 +913,7 @@ static SqpRes sqp(const Nlp& q, Vec xi, Duals d, const nmpcmc_sqp_options& op) {
             break;
         }
         if (it >= op.max_iter) break;
+        PORT_UNIT(SQP, N);
         QpOut qp = solve_qp(stages(q, W, gf, cb, out.xi), N, nx, op.qp_tol, op.qp_max_iter);
         if (qp.status == 2) {
             identity_blocks(W, N, nx);
@@ -1051,7 +1073,7 @@ static double nmpc_step(Nmpc& s, const nmpcmc_scenario& sc, double t, double y, 
 }
 
 static double sp_at(const nmpcmc_scenario& sc, double t) {  // SetpointProfile::at, montecarlo.cpp:26-32
-    const double* e = std::upper_bound(sc.sp_times, sc.sp_times + sc.n_setpoints, t);
+    const PORT_REAL* e = std::upper_bound(sc.sp_times, sc.sp_times + sc.n_setpoints, t);
     return sc.sp_values[(e - sc.sp_times) - 1];
 }
 
@@ -1063,9 +1085,9 @@ static void closed_loop(const nmpcmc_scenario& sc, uint64_t idx, nmpcmc_sim_reco
     if (sc.perturb) {  // include/nmpcmc_gpu.h perturbation rule
         Rng pr(sc.base_seed, idx | 0x8000000000000000ULL);
         const double z0 = pr.normal(), z1 = pr.normal(), z2 = pr.normal();
-        tp.cA_in = tp.cA_in * (1.0 + sc.perturb_rel_std[0] * z0);
-        tp.cB_in = tp.cB_in * (1.0 + sc.perturb_rel_std[1] * z1);
-        tp.EaR = tp.EaR * (1.0 + sc.perturb_rel_std[2] * z2);
+        tp.cA_in = PORT_TO_DOUBLE(tp.cA_in * (1.0 + sc.perturb_rel_std[0] * z0));
+        tp.cB_in = PORT_TO_DOUBLE(tp.cB_in * (1.0 + sc.perturb_rel_std[1] * z1));
+        tp.EaR = PORT_TO_DOUBLE(tp.EaR * (1.0 + sc.perturb_rel_std[2] * z2));
     }
     const Cstr truth(tp, sc.truth_variant);
     const int nbar = static_cast<int>(std::llround((sc.tf - sc.t0) / sc.Ts));
@@ -1101,6 +1123,7 @@ static void closed_loop(const nmpcmc_scenario& sc, uint64_t idx, nmpcmc_sim_reco
                 for (int k = 1; k <= sc.N; ++k) sp[k - 1] = sp_at(sc, t + k * sc.Ts);
                 bool conv = false;
                 u = nmpc_step(ctl, sc, t, y, sp, &conv);
+                PORT_UNIT(STEP, 1);
                 ++solves;
                 if (!conv) ++fails;
             } else {  // pi_step (controllers.cpp:12-23)
@@ -1123,7 +1146,7 @@ static void closed_loop(const nmpcmc_scenario& sc, uint64_t idx, nmpcmc_sim_reco
             const double r = z - zb;
             acc += r * r;
         }
-        rec->phi = acc / static_cast<double>(nbar + 1);
+        rec->phi = PORT_TO_DOUBLE(acc / static_cast<double>(nbar + 1));
         rec->failed = 0;
         if (traj) {
             double* w = traj + row * 5;
@@ -1133,16 +1156,17 @@ static void closed_loop(const nmpcmc_scenario& sc, uint64_t idx, nmpcmc_sim_reco
         rec->ocp_failures = fails;
         rec->status = 0;
     } catch (const NonFinite&) {
-        *rec = {nan, 1, solves, fails, NMPCMC_NON_FINITE_STATE};
+        *rec = {PORT_TO_DOUBLE(nan), 1, solves, fails, NMPCMC_NON_FINITE_STATE};
     } catch (const Domain&) {
-        *rec = {nan, 1, solves, fails, NMPCMC_DOMAIN_ERROR};
+        *rec = {PORT_TO_DOUBLE(nan), 1, solves, fails, NMPCMC_DOMAIN_ERROR};
     } catch (const NotPD&) {  // escapes run_closed_loop; the worker's catch(...) zeroes the record
-        *rec = {nan, 1, 0, 0, NMPCMC_NOT_POSITIVE_DEFINITE};
+        *rec = {PORT_TO_DOUBLE(nan), 1, 0, 0, NMPCMC_NOT_POSITIVE_DEFINITE};
     }
 }
 
 }  // namespace port
 
+#ifndef PORT_NO_CAPI
 extern "C" {
 
 int PFX(run_closed_loop)(const nmpcmc_scenario* sc, uint64_t idx, nmpcmc_sim_record* out, double* traj, int rows) {
@@ -1172,3 +1196,4 @@ void PFX(normals)(uint64_t seed, uint64_t stream, int64_t n, double* out) {
 void PFX(philox_block)(const uint32_t* in, uint32_t* out) { port::Rng::block(in, in[4], in[5], out); }
 
 }  // extern "C"
+#endif  // PORT_NO_CAPI
