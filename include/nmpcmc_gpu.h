@@ -237,6 +237,36 @@ int nmpcmc_gpu_libm(nmpcmc_gpu_ctx* ctx, int32_t fn, const double* x, int64_t n,
  * for the FP64 closed-loop kernels (use_fma=1: DFMA, 2 flops each; 0: DADD). */
 int nmpcmc_gpu_fp64_peak(nmpcmc_gpu_ctx* ctx, int use_fma, double* tflops_out);
 
+/* ---- Batched standalone stagewise QP ----------
+ * solve_qp (qp.hpp:47-56, qp.cpp:173-423; mode 0) or riccati_factor_solve
+ * (qp.hpp:42-45, qp.cpp:157-171; mode 1) for `batch` independent QPs of the
+ * same dimensions, bitwise the reference's results. n_x <= 8, n_u <= 4.
+ * stages: HOST, batch * (N+1) * nmpcmc_qp_stage_doubles(n_x, n_u) doubles;
+ * per stage Q[nx*nx] M[nx*nu] R[nu*nu] q[nx] r[nu] Jx[nx*nx] Ju[nx*nu] b[nx]
+ * lb[nu] ub[nu] (QpStageData, qp.hpp:24-30; matrices column-major; members a
+ * stage does not use are ignored: stage 0 has no Q M q Jx, stage N only Q q).
+ * solutions: HOST, batch * nmpcmc_qp_solution_doubles(N, n_x, n_u):
+ * delta_xi[N(nu+nx)] mu[N nx] nu_l[N nu] nu_u[N nu] (QpSolution, qp.hpp:34-41).
+ * status[batch]: NMPCMC_QP_*; iterations[batch]: IPM iterations. Per-QP
+ * DomainError (lb > ub) and NotPositiveDefinite (mode 1) are statuses, not
+ * call failures; the call fails only on bad dimensions (DIMENSION_MISMATCH). */
+typedef struct nmpcmc_qp_dims {
+    int32_t N;        /* stages 0..N: N inputs, terminal state N */
+    int32_t n_x;
+    int32_t n_u;
+    int32_t max_iter; /* solve_qp max_iter (default 50) */
+    double tol;       /* solve_qp tol (default 1e-10) */
+    int32_t mode;     /* 0 solve_qp, 1 riccati_factor_solve */
+    int32_t _pad;
+} nmpcmc_qp_dims;
+enum { NMPCMC_QP_OPTIMAL = 0, NMPCMC_QP_MAXITER = 1, NMPCMC_QP_FAILED = 2, NMPCMC_QP_DOMAIN_ERROR = 3,
+       NMPCMC_QP_NOT_POSITIVE_DEFINITE = 4 };
+int64_t nmpcmc_qp_stage_doubles(int32_t n_x, int32_t n_u);
+int64_t nmpcmc_qp_solution_doubles(int32_t N, int32_t n_x, int32_t n_u);
+int nmpcmc_gpu_solve_qp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_qp_dims* dims, int64_t batch,
+                              const double* stages, double* solutions, int32_t* status,
+                              int32_t* iterations);
+
 #ifdef __cplusplus
 }
 #endif

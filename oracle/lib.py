@@ -103,3 +103,21 @@ def run_traj(lib, sc, idx, rows, prefix="nmpcmc_ref"):
     getattr(lib, f"{prefix}_run_closed_loop")(C.byref(sc), idx, C.byref(rec),
                                               traj.ctypes.data_as(C.POINTER(C.c_double)), rows)
     return rec, traj
+
+
+def solve_qp_batch(lib, packed, nx, nu, tol=1e-10, max_iter=50, riccati_only=False):
+    """The reference's solve_qp / riccati_factor_solve over a packed batch
+    (layout of nmpcmc_gpu_solve_qp_batch): (solutions, status, iterations)."""
+    from paper_2212_02197_b200 import qp as Q
+    packed = np.ascontiguousarray(packed, dtype=np.float64)
+    batch, N = packed.shape[0], packed.shape[1] - 1
+    d = Q.QpDims(N, nx, nu, max_iter, tol, 1 if riccati_only else 0, 0)
+    sol = np.zeros((batch, Q.solution_doubles(N, nx, nu)))
+    st = np.zeros(batch, dtype=np.int32)
+    it = np.zeros(batch, dtype=np.int32)
+    lib.nmpcmc_ref_solve_qp_batch(C.byref(d), C.c_int64(batch), packed.ctypes.data_as(C.POINTER(C.c_double)),
+                                  sol.ctypes.data_as(C.POINTER(C.c_double)),
+                                  st.ctypes.data_as(C.POINTER(C.c_int32)),
+                                  it.ctypes.data_as(C.POINTER(C.c_int32)))
+    return sol, st, it
+

@@ -9,6 +9,7 @@
 //   run_monte_carlo  (montecarlo.cpp:213-251)  -> nmpcmc_ref_run_batch
 //   aggregate_stats  (montecarlo.cpp:172-211)  -> nmpcmc_ref_aggregate
 //   phi_histogram    (montecarlo.cpp:268-304)  -> nmpcmc_ref_histogram
+//   solve_qp / riccati_factor_solve (qp.cpp:157-423) -> nmpcmc_ref_solve_qp_batch
 // and, for unit-level pins, CounterRng / pi_step / nmpc_step.
 // Only tests/, __graft_entry__.smoke() and bench.py's CPU arm load it.
 #include <algorithm>
@@ -22,7 +23,9 @@
 
 #include "nmpcmc/controllers.hpp"
 #include "nmpcmc/cstr.hpp"
+#include "nmpcmc/errors.hpp"
 #include "nmpcmc/montecarlo.hpp"
+#include "nmpcmc/qp.hpp"
 #include "nmpcmc/rng.hpp"
 #include "nmpcmc_gpu.h"
 
@@ -274,6 +277,75 @@ double nmpcmc_ref_reaction_rate(const nmpcmc_cstr_params* p, const double* c) {
     } catch (...) {
         return std::numeric_limits<double>::quiet_NaN();
     }
+}
+
+/// The reference's solve_qp (mode 0) / riccati_factor_solve (mode 1) over a
+/// batch in the packed layout of nmpcmc_gpu_solve_qp_batch (include/nmpcmc_gpu.h).
+int nmpcmc_ref_solve_qp_batch(const nmpcmc_qp_dims* d, std::int64_t batch, const double* stages,
+                              double* solutions, std::int32_t* status, std::int32_t* iterations) {
+    const int N = d->N, nx = d->n_x, nu = d->n_u;
+    const int SB = 2 * nx * nx + 2 * nx * nu + nu * nu + 2 * nx + 3 * nu;
+    const std::int64_t SO = (std::int64_t)N * (nu + nx) + (std::int64_t)N * nx + 2 * (std::int64_t)N * nu;
+    auto mat = [](const double* p, int r, int c) {
+        Matrix m(r, c);
+        for (int j = 0; j < c; ++j)
+            for (int i = 0; i < r; ++i) m(i, j) = p[j * r + i];
+        return m;
+    };
+    auto vec = [](const double* p, int n) { return Vec(p, p + n); };
+    for (std::int64_t b = 0; b < batch; ++b) {
+        std::vector<QpStageData> st(N + 1);
+        for (int k = 0; k <= N; ++k) {
+            const double* p = stages + (b * (N + 1) + k) * SB;
+            const int oM = nx * nx, oR = oM + nx * nu, oq = oR + nu * nu, orr = oq + nx, oJx = orr + nu,
+                      oJu = oJx + nx * nx, ob = oJu + nx * nu, olb = ob + nx, oub = olb + nu;
+            QpStageData& s = st[k];
+            if (k == N) {
+                s.Q = mat(p, nx, nx);
+                s.q = vec(p + oq, nx);
+                continue;
+            }
+            if (k >= 1) {
+                s.Q = mat(p, nx, nx);
+                s.M = mat(p + oM, nx, nu);
+                s.q = vec(p + oq, nx);
+                s.Jx = mat(p + oJx, nx, nx);
+            }
+            s.R = mat(p + oR, nu, nu);
+            s.r = vec(p + orr, nu);
+            s.Ju = mat(p + oJu, nx, nu);
+            s.b = vec(p + ob, nx);
+            s.lb = vec(p + olb, nu);
+            s.ub = vec(p + oub, nu);
+        }
+        double* o = solutions + b * SO;
+        std::fill(o, o + SO, 0.0);
+        const std::int64_t L = (std::int64_t)N * (nu + nx), NX = (std::int64_t)N * nx, NV = (std::int64_t)N * nu;
+        iterations[b] = 0;
+        try {
+            if (d->mode == 1) {
+                const auto [dxi, mu] = riccati_factor_solve(st);
+                std::copy(dxi.begin(), dxi.end(), o);
+                std::copy(mu.begin(), mu.end(), o + L);
+                status[b] = NMPCMC_QP_OPTIMAL;
+            } else {
+                const QpSolution sol = solve_qp(st, d->tol, d->max_iter);
+                std::copy(sol.delta_xi.begin(), sol.delta_xi.end(), o);
+                std::copy(sol.mu.begin(), sol.mu.end(), o + L);
+                std::copy(sol.nu_l.begin(), sol.nu_l.end(), o + L + NX);
+                std::copy(sol.nu_u.begin(), sol.nu_u.end(), o + L + NX + NV);
+                status[b] = sol.status == QpStatus::Optimal ? NMPCMC_QP_OPTIMAL
+                            : sol.status == QpStatus::MaxIter ? NMPCMC_QP_MAXITER
+                                                              : NMPCMC_QP_FAILED;
+                iterations[b] = sol.iterations;
+            }
+        } catch (const DomainError&) {
+            status[b] = NMPCMC_QP_DOMAIN_ERROR;
+        } catch (const NotPositiveDefinite&) {
+            status[b] = NMPCMC_QP_NOT_POSITIVE_DEFINITE;
+        }
+    }
+    return 0;
 }
 
 }  // extern "C"

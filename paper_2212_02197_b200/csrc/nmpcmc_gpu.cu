@@ -16,6 +16,7 @@
 #include "nmpc_gen_kernel.cuh"
 #include "nmpcmc_gpu.h"
 #include "pi_kernel.cuh"
+#include "qp_batch_kernel.cuh"
 
 /// Where one launch runs and the workspace it owns. The context's own target
 /// uses ctx->stream; with NMPCMC_OPT_LANES = 2, NMPC launches alternate
@@ -502,4 +503,51 @@ extern "C" int nmpcmc_gpu_fp64_peak(nmpcmc_gpu_ctx* ctx, int use_fma, double* tf
     cudaEventDestroy(e1);
     *tflops_out = best;
     return cuda_check(ctx, cudaGetLastError(), "fp64 peak");
+}
+
+// ------------------------------------------------------------ batched QP
+extern "C" int64_t nmpcmc_qp_stage_doubles(int32_t n_x, int32_t n_u) {
+    return nmpcmc_dev::qpb::stage_doubles(n_x, n_u);
+}
+extern "C" int64_t nmpcmc_qp_solution_doubles(int32_t N, int32_t n_x, int32_t n_u) {
+    return nmpcmc_dev::qpb::solution_doubles(N, n_x, n_u);
+}
+
+extern "C" int nmpcmc_gpu_solve_qp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_qp_dims* dims, int64_t batch,
+                                         const double* stages, double* solutions, int32_t* status,
+                                         int32_t* iterations) {
+    if (ctx == nullptr || dims == nullptr || batch < 0 || (batch > 0 && (!stages || !solutions || !status || !iterations)))
+        return NMPCMC_INVALID_ARGUMENT;
+    const nmpcmc_qp_dims d = *dims;
+    // QP validate (qp.cpp:21-58): at least one input stage and positive blocks
+    if (d.N < 1 || d.n_x < 1 || d.n_u < 1) return fail(ctx, NMPCMC_DIMENSION_MISMATCH, "QP dimensions");
+    if (d.n_x > nmpcmc_dev::qpb::QX || d.n_u > nmpcmc_dev::qpb::QU)
+        return fail(ctx, NMPCMC_UNSUPPORTED, "QP batch: n_x <= 8 and n_u <= 4 on device");
+    if (d.mode != 0 && d.mode != 1) return fail(ctx, NMPCMC_INVALID_ARGUMENT, "QP batch: mode");
+    if (batch == 0) return NMPCMC_OK;
+    cudaSetDevice(ctx->device);
+    const int64_t SB = nmpcmc_dev::qpb::stage_doubles(d.n_x, d.n_u);
+    const int64_t SO = nmpcmc_dev::qpb::solution_doubles(d.N, d.n_x, d.n_u);
+    const size_t in_b = (size_t)batch * (d.N + 1) * SB * sizeof(double);
+    const size_t out_b = (size_t)batch * SO * sizeof(double);
+    const size_t st_b = (size_t)batch * 2 * sizeof(int32_t);
+    const int64_t slots = nmpcmc_dev::qpb::qp_slots(ctx->sm_count, batch);
+    const size_t ws_b = (size_t)slots * (size_t)nmpcmc_dev::qpb::Lay(d.N, d.n_x, d.n_u).total * sizeof(double);
+    int rc = ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap, in_b + out_b + st_b + 256);
+    if (rc == NMPCMC_OK) rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, ws_b);
+    if (rc != NMPCMC_OK) return rc;
+    char* base = static_cast<char*>(ctx->d_scratch);
+    auto* d_in = reinterpret_cast<double*>(base);
+    auto* d_out = reinterpret_cast<double*>(base + in_b);
+    auto* d_st = reinterpret_cast<int32_t*>(base + in_b + out_b);
+    cudaMemcpyAsync(d_in, stages, in_b, cudaMemcpyHostToDevice, ctx->stream);
+    nmpcmc_dev::qpb::Dims kd{d.N, d.n_x, d.n_u, d.max_iter, d.mode, d.tol};
+    const unsigned grid = (unsigned)((slots + nmpcmc_dev::qpb::kBlock - 1) / nmpcmc_dev::qpb::kBlock);
+    nmpcmc_dev::qpb::qp_batch_kernel<<<grid, nmpcmc_dev::qpb::kBlock, 0, ctx->stream>>>(
+        kd, batch, d_in, d_out, d_st, d_st + batch, static_cast<double*>(ctx->d_ws), slots);
+    if ((rc = cuda_check(ctx, cudaGetLastError(), "qp_batch_kernel launch")) != NMPCMC_OK) return rc;
+    cudaMemcpyAsync(solutions, d_out, out_b, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(status, d_st, (size_t)batch * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(iterations, d_st + batch, (size_t)batch * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream);
+    return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "qp_batch_kernel");
 }

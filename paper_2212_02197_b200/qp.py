@@ -1,0 +1,161 @@
+"""Batched standalone stagewise QP service: the
+reference's solve_qp / riccati_factor_solve (qp.hpp:24-56) for a batch of
+independent QPs of equal dimensions, on the GPU kernel K5
+(csrc/qp_batch_kernel.cuh) through nmpcmc_gpu_solve_qp_batch.
+
+A QP is a list of N+1 stage dicts with the members of QpStageData
+(qp.hpp:24-30): Q, M, R, q, r, Jx, Ju, b, lb, ub (numpy arrays; M is n_x x
+n_u as in the reference). Stage 0 needs R r Ju b lb ub; stages 1..N-1 all
+members; stage N only Q q.
+"""
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import engine
+
+OPTIMAL, MAXITER, FAILED, DOMAIN_ERROR, NOT_POSITIVE_DEFINITE = range(5)
+STATUS_NAMES = {OPTIMAL: "Optimal", MAXITER: "MaxIter", FAILED: "Failed", DOMAIN_ERROR: "DomainError",
+                NOT_POSITIVE_DEFINITE: "NotPositiveDefinite"}
+
+
+class QpDims(C.Structure):
+    _fields_ = [("N", C.c_int32), ("n_x", C.c_int32), ("n_u", C.c_int32), ("max_iter", C.c_int32),
+                ("tol", C.c_double), ("mode", C.c_int32), ("_pad", C.c_int32)]
+
+
+def stage_doubles(nx: int, nu: int) -> int:
+    return 2 * nx * nx + 2 * nx * nu + nu * nu + 2 * nx + 3 * nu
+
+
+def solution_doubles(N: int, nx: int, nu: int) -> int:
+    return N * (nu + nx) + N * nx + 2 * N * nu
+
+
+def pack(qps, nx: int, nu: int) -> np.ndarray:
+    """Packed input (batch, N+1, stage_doubles) from a list of QPs."""
+    N = len(qps[0]) - 1
+    out = np.zeros((len(qps), N + 1, stage_doubles(nx, nu)))
+    z = {"Q": (nx, nx), "M": (nx, nu), "R": (nu, nu), "q": (nx,), "r": (nu,), "Jx": (nx, nx), "Ju": (nx, nu),
+         "b": (nx,), "lb": (nu,), "ub": (nu,)}
+    for bi, qp in enumerate(qps):
+        if len(qp) != N + 1:
+            raise ValueError("all QPs of a batch need the same number of stages")
+        for k, st in enumerate(qp):
+            parts = []
+            for name in ("Q", "M", "R", "q", "r", "Jx", "Ju", "b", "lb", "ub"):
+                v = st.get(name)
+                a = np.zeros(z[name]) if v is None else np.asarray(v, dtype=np.float64).reshape(z[name])
+                parts.append(a.reshape(-1, order="F"))
+            out[bi, k] = np.concatenate(parts)
+    return out
+
+
+@dataclass
+class QpSolution:
+    """QpSolution (qp.hpp:34-41) of one QP of a batch."""
+    delta_xi: np.ndarray
+    mu: np.ndarray
+    nu_l: np.ndarray
+    nu_u: np.ndarray
+    iterations: int
+    status: int
+
+
+def unpack(sol: np.ndarray, status, iterations, N: int, nx: int, nu: int):
+    L, NX, NV = N * (nu + nx), N * nx, N * nu
+    return [QpSolution(s[:L].copy(), s[L:L + NX].copy(), s[L + NX:L + NX + NV].copy(), s[L + NX + NV:].copy(),
+                       int(it), int(st)) for s, st, it in zip(sol, status, iterations)]
+
+
+def solve_qp_batch(qps_or_packed, nx: int = None, nu: int = None, tol: float = 1e-10, max_iter: int = 50,
+                   riccati_only: bool = False, ctx=None, raw: bool = False):
+    """solve_qp(stages, tol, max_iter) for every QP of the batch (or
+    riccati_factor_solve with riccati_only). Input: a list of QPs (stage-dict
+    lists) or a packed (batch, N+1, stage_doubles) array with nx, nu given.
+    Returns a list of QpSolution, or (solutions, status, iterations) arrays
+    with raw=True."""
+    if isinstance(qps_or_packed, np.ndarray):
+        packed = np.ascontiguousarray(qps_or_packed, dtype=np.float64)
+        if nx is None or nu is None:
+            raise ValueError("packed input needs nx, nu")
+    else:
+        qps = qps_or_packed
+        if nu is None:
+            nu = np.atleast_2d(np.asarray(qps[0][0]["R"], dtype=np.float64)).shape[0]
+        if nx is None:
+            nx = np.atleast_2d(np.asarray(qps[0][-1]["Q"], dtype=np.float64)).shape[0]
+        packed = pack(qps, nx, nu)
+    batch, N = packed.shape[0], packed.shape[1] - 1
+    d = QpDims(N, nx, nu, max_iter, tol, 1 if riccati_only else 0, 0)
+    sol = np.zeros((batch, solution_doubles(N, nx, nu)))
+    st = np.zeros(batch, dtype=np.int32)
+    it = np.zeros(batch, dtype=np.int32)
+    ctx = ctx or engine._context(0)
+    ctx._check(ctx.lib.nmpcmc_gpu_solve_qp_batch(
+        ctx.handle, C.byref(d), batch, packed.ctypes.data_as(C.POINTER(C.c_double)),
+        sol.ctypes.data_as(C.POINTER(C.c_double)), st.ctypes.data_as(C.POINTER(C.c_int32)),
+        it.ctypes.data_as(C.POINTER(C.c_int32))))
+    if raw:
+        return sol, st, it
+    return unpack(sol, st, it, N, nx, nu)
+
+
+# ---------------------------------------------------------- instance builders
+def random_instance(rng: np.random.Generator, N: int, nx: int, nu: int, bounded: bool = True,
+                    inf_frac: float = 0.15):
+    """A random convex stagewise QP: PD joint (x, u) Hessian blocks, near-
+    identity dynamics, tight-ish input boxes (some sides infinite) so bounds
+    are active in a good share of instances."""
+    qp = []
+    for k in range(N + 1):
+        st = {}
+        if k < N:
+            A = rng.uniform(-1, 1, (nx + nu, nx + nu))
+            W = A @ A.T + 0.5 * np.eye(nx + nu)
+            st["R"] = W[nx:, nx:]
+            st["r"] = rng.uniform(-1, 1, nu)
+            st["Ju"] = rng.uniform(-1, 1, (nx, nu))
+            st["b"] = 0.2 * rng.uniform(-1, 1, nx)
+            if bounded:
+                lb = -rng.uniform(0.05, 0.6, nu)
+                ub = rng.uniform(0.05, 0.6, nu)
+                lb[rng.uniform(size=nu) < inf_frac] = -np.inf
+                ub[rng.uniform(size=nu) < inf_frac] = np.inf
+            else:
+                lb, ub = np.full(nu, -np.inf), np.full(nu, np.inf)
+            st["lb"], st["ub"] = lb, ub
+            if k >= 1:
+                st["Q"], st["M"] = W[:nx, :nx], W[:nx, nx:]
+                st["q"] = rng.uniform(-1, 1, nx)
+                st["Jx"] = np.eye(nx) + 0.3 * rng.uniform(-1, 1, (nx, nx))
+        else:
+            A = rng.uniform(-1, 1, (nx, nx))
+            st["Q"] = A @ A.T + 0.5 * np.eye(nx)
+            st["q"] = rng.uniform(-1, 1, nx)
+        qp.append(st)
+    return qp
+
+
+def scalar_instance(r_hess, r_lin, p_term, p_lin, ju, b0, lb, ub):
+    """One input, one terminal state: min 1/2 R u^2 + r u + 1/2 P x1^2 + p x1,
+    x1 = ju u + b0, lb <= u <= ub."""
+    return [{"R": [[r_hess]], "r": [r_lin], "Ju": [[ju]], "b": [b0], "lb": [lb], "ub": [ub]},
+            {"Q": [[p_term]], "q": [p_lin]}]
+
+
+def double_integrator(rng: np.random.Generator, N: int, h: float):
+    """Discrete double integrator (x = position, velocity; u = acceleration)
+    with random linear terms and offsets, unconstrained."""
+    Jx = np.array([[1.0, h], [0.0, 1.0]])
+    Ju = np.array([[0.5 * h * h], [h]])
+    qp = []
+    for k in range(N):
+        st = {"R": [[0.1]], "r": [rng.uniform(-1, 1)], "Jx": Jx, "Ju": Ju, "b": 0.2 * rng.uniform(-1, 1, 2),
+              "lb": [-np.inf], "ub": [np.inf]}
+        if k >= 1:
+            st.update(Q=np.diag([1.0, 0.1]), M=np.zeros((2, 1)), q=rng.uniform(-1, 1, 2))
+        qp.append(st)
+    qp.append({"Q": np.diag([5.0, 1.0]), "q": rng.uniform(-1, 1, 2)})
+    return qp

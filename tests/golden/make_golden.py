@@ -71,6 +71,49 @@ def gen_rng():
     print("rng done")
 
 
+def gen_qp():
+    """Batched QP fixtures: the reference's solve_qp /
+    riccati_factor_solve on packed batches, mirroring the cases of the
+    reference's tests/test_qp.cpp. Groups of equal dimensions; each stores
+    the packed input, the dims and the reference's outputs."""
+    from paper_2212_02197_b200 import qp as Q
+    L = O.ref("glibc")  # no libm on this path: both link variants agree
+    inf = np.inf
+    rng = np.random.default_rng(20260101)
+    groups = {}
+
+    def add(name, qps, nx, nu, tol=1e-10, max_iter=50, riccati_only=False):
+        packed = Q.pack(qps, nx, nu)
+        sol, st, it = O.solve_qp_batch(L, packed, nx, nu, tol, max_iter, riccati_only)
+        groups[name] = dict(packed=packed, dims=np.array([len(qps[0]) - 1, nx, nu, max_iter, int(riccati_only)]),
+                            tol=np.array(tol), sol=sol, status=st, iters=it)
+        print(f"qp {name}: batch {len(qps)} status {np.bincount(st, minlength=5).tolist()} iters {it.min()}..{it.max()}")
+
+    add("rand_box", [Q.random_instance(rng, 4, 3, 2) for _ in range(60)], 3, 2)
+    unc = [Q.random_instance(rng, 4, 3, 2, bounded=False) for _ in range(10)]
+    add("rand_unc", unc, 3, 2)
+    add("rand_unc_riccati", unc, 3, 2, riccati_only=True)
+    dint = [Q.double_integrator(rng, 20, 0.1) for _ in range(5)]
+    add("dint", dint, 2, 1)
+    add("dint_riccati", dint, 2, 1, riccati_only=True)
+    add("big", [Q.random_instance(rng, 60, 6, 3) for _ in range(12)], 6, 3)
+    scal = [Q.scalar_instance(1.0, 2.0, 1.0, 0.0, 0.0, 0.0, -10.0, 10.0),   # slack bounds: u* = -2
+            Q.scalar_instance(1.0, 2.0, 1.0, 0.0, 0.0, 0.0, -1.0, 10.0),    # active lower bound
+            Q.scalar_instance(1.0, 2.0, 1.0, 0.0, 0.0, 0.0, 0.5, 0.5),      # pinned input
+            Q.scalar_instance(1.0, 0.0, 1.0, 0.0, 1.0, 0.0, -1.0, 1.0),     # all-zero linear data
+            Q.scalar_instance(-1.0, 2.0, 1.0, 0.0, 0.0, 0.0, -inf, inf),    # indefinite stage Hessian
+            Q.scalar_instance(1.0, 2.0, 1.0, 0.0, 0.0, 0.0, 1.0, -1.0),     # lb > ub
+            Q.scalar_instance(2.0, -1.0, 3.0, 0.5, 0.7, 0.2, -inf, 0.3)]    # one-sided box
+    add("scalar", scal, 1, 1)
+    add("scalar_riccati", scal, 1, 1, riccati_only=True)
+    add("maxiter", [Q.scalar_instance(1.0, 2.0, 1.0, 0.0, 0.0, 0.0, -0.5, 0.5)], 1, 1, tol=0.0, max_iter=5)
+    out = {}
+    for g, d in groups.items():
+        for k, v in d.items():
+            out[f"{g}__{k}"] = v
+    np.savez_compressed(os.path.join(OUT, "qp_batch.npz"), **out)
+
+
 def main(which):
     if which in ("rng", "all"):
         gen_rng()
@@ -87,6 +130,8 @@ def main(which):
         gen_case("nmpc_n30_short", dict(controller="nmpc", N=30, n_steps=120), 64, 2)
         gen_case("nmpc_n60_pert_short", dict(controller="nmpc", N=60, n_steps=120, perturb=True), 32, 1)
         gen_case("nmpc_n120_short", dict(controller="nmpc", N=120, n_steps=60), 16, 1)
+    if which in ("qp", "all"):
+        gen_qp()
     if which in ("nmpc3", "all"):
         # three-state controller model (config 2 read literally: CD-EKF and
         # OCP on the 3-state CSTR; ctrl_variant 0 = THREE_STATE) -> kernel K3g
