@@ -164,8 +164,10 @@ const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx);
  * one-state controller model with N <= 255:
  * WARP (default) = one warp per sample, workspace in shared memory (K3);
  * THREAD = one thread per sample, workspace in HBM (K3b);
- * GENERIC = one thread per sample, any controller state dimension (K3g).
- * A three-state controller model or N > 255 always runs K3g. Results are
+ * GENERIC = one thread per sample, any controller state dimension (K3g);
+ * GENERIC_WARP = one warp per sample, any controller state dimension (K3w).
+ * A three-state controller model or N > 255 always runs a generic kernel:
+ * K3w, or K3g when GENERIC is selected. Results are
  * bitwise identical; only speed differs. NMPCMC_OPT_TPS_WARPS_PER_SM = resident
  * warps per SM for K3b (default 8). */
 enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2, NMPCMC_OPT_LANES = 3 };
@@ -177,7 +179,8 @@ enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2, NMPCMC_OPT_L
  * on the context stream is ordered after the lanes only through
  * nmpcmc_gpu_join / nmpcmc_gpu_wait. 1 (default) = everything on the context
  * stream. */
-enum { NMPCMC_NMPC_KERNEL_WARP = 1, NMPCMC_NMPC_KERNEL_THREAD = 2, NMPCMC_NMPC_KERNEL_GENERIC = 3 };
+enum { NMPCMC_NMPC_KERNEL_WARP = 1, NMPCMC_NMPC_KERNEL_THREAD = 2, NMPCMC_NMPC_KERNEL_GENERIC = 3,
+       NMPCMC_NMPC_KERNEL_GENERIC_WARP = 4 };
 int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value);
 /* CUDA stream the context launches on (as void*; 0 = legacy default). */
 int nmpcmc_gpu_set_stream(nmpcmc_gpu_ctx* ctx, void* stream);

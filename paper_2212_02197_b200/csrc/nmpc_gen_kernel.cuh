@@ -1,5 +1,7 @@
-// nmpc_gen_kernel.cuh -- K3g: NMPC closed loop for a controller model of any
-// state dimension NX (compile time), one thread per sample.
+// nmpc_gen_kernel.cuh -- K3g / K3w: NMPC closed loop for a controller model
+// of any state dimension NX (compile time). W = lanes per sample: W = 1 is
+// K3g (one thread per sample), W = 32 is K3w (one warp per sample: stage
+// loops across lanes, Riccati sweeps and ordered sums serial on every lane).
 //
 // K3 (nmpc_kernel.cuh) is the one-state fast path. K3g covers the
 // three-state controller model: the literal "CD-EKF on the 3-state model"
@@ -17,10 +19,15 @@
 // records are bitwise those of the exact-libm reference (tests/test_gpu_gen.py).
 //
 // Layout: a per-sample workspace of ~9k doubles (N = 60, NX = 3) in global
-// memory, element e of slot t at ws[e * T + t] (T = resident slots), so the
-// 32 lanes of a warp touch 32 consecutive doubles. Small matrices (NX x NX)
-// live in registers. Reference exceptions become status codes returned to
-// exactly the callers that catch them.
+// memory. K3g: element e of slot t at ws[e * T + t] (T = resident slots), so
+// the 32 lanes of a warp touch 32 consecutive doubles. K3w: one contiguous
+// slab per warp (T = 1), lanes touching consecutive stages. Small matrices
+// (NX x NX) live in registers. Reference exceptions become status codes
+// returned to exactly the callers that catch them. In K3w every serial
+// section runs redundantly on all lanes and only ever stores (no
+// read-modify-write of a shared slot); order-independent reductions (inf
+// norms, step minima, counts) combine per-lane partials with std::max/min
+// semantics; ordered sums stay serial.
 #pragma once
 
 #include "device_common.cuh"
@@ -35,6 +42,40 @@ struct Ws {
     double* p;
     int64_t T;
     __device__ __forceinline__ double& operator[](int64_t e) const { return p[e * T]; }
+};
+
+/// Lane helpers: W = 1 (thread per sample) or 32 (warp per sample).
+constexpr unsigned kMask = 0xffffffffu;
+template <int W>
+struct Lanes {
+    __device__ static int lane() { return W == 1 ? 0 : (int)(threadIdx.x & 31); }
+    __device__ static void sync() {
+        if (W > 1) __syncwarp();
+    }
+    __device__ static bool any(bool p) { return W == 1 ? p : __any_sync(kMask, p); }
+    __device__ static int sum(int v) { return W == 1 ? v : __reduce_add_sync(kMask, v); }
+    __device__ static int imin(int v) { return W == 1 ? v : __reduce_min_sync(kMask, v); }
+    __device__ static int bcast(int v, int src) { return W == 1 ? v : __shfl_sync(kMask, v, src); }
+    /// std::max fold of per-lane partials (NaN-free, no -0).
+    __device__ static double max_fold(double m) {
+        if (W > 1)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double v = __shfl_xor_sync(kMask, m, o);
+                m = (m < v) ? v : m;
+            }
+        return m;
+    }
+    /// std::min fold of per-lane partials (NaN-free, no -0).
+    __device__ static double min_fold(double m) {
+        if (W > 1)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double v = __shfl_xor_sync(kMask, m, o);
+                m = (v < m) ? v : m;
+            }
+        return m;
+    }
 };
 
 /// Element offsets of the per-sample arrays for horizon N (NX compile time).
@@ -242,7 +283,7 @@ __device__ __noinline__ int shoot(const Model<NX>& m, const double* x, double u,
 }
 
 // -------------------------------------------------------------------- OCP
-template <int NX>
+template <int NX, int W>
 struct Ocp {
     Model<NX> m;
     Layout<NX> lay;
@@ -254,44 +295,53 @@ struct Ocp {
 };
 
 /// eval_objective (ocp.cpp:76-99) of xi set s; gradient into GF[s] if grad.
-template <int NX>
-__device__ __noinline__ double objective(const Ocp<NX>& o, int s, bool grad) {
+template <int NX, int W>
+__device__ __noinline__ double objective(const Ocp<NX, W>& o, int s, bool grad) {
+    // serial on every lane (phi is an ordered sum); the gradient is stored,
+    // not accumulated: each slot is 0.0 + 2 Ts g once (ocp.cpp:80-97)
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
     double phi = 0.0;
-    if (grad)
-        for (int i = 0; i < L.L; ++i) w[L.GF[s] + i] = 0.0;
 #pragma unroll 1
     for (int k = 1; k <= o.N; ++k) {
         const double res = w[L.XI[s] + L.xo(k) + NX - 1] / o.m.p.V - w[L.SP + k - 1];
         const double qres = 1.0 * (0.0 + o.Qz * res) + 0.0;
         phi += o.Ts * (0.0 + res * qres);
         if (grad) {
+            w[L.GF[s] + L.uo(k - 1)] = 0.0;
 #pragma unroll
             for (int i = 0; i < NX; ++i) {
                 const double hi = (i == NX - 1) ? o.invV : 0.0;
                 const double g = 1.0 * (0.0 + hi * qres) + 0.0;
-                w[L.GF[s] + L.xo(k) + i] += 2.0 * o.Ts * g;
+                w[L.GF[s] + L.xo(k) + i] = 0.0 + 2.0 * o.Ts * g;
             }
         }
     }
+    Lanes<W>::sync();
     return phi;
 }
 
 /// eval_constraints (ocp.cpp:101-135) of xi set s into G/FX/FU/BB[s].
-template <int NX>
-__device__ __noinline__ int constraints(const Ocp<NX>& o, int s) {
+template <int NX, int W>
+__device__ __noinline__ int constraints(const Ocp<NX, W>& o, int s) {
+    // stages are independent (multiple shooting): lane-parallel; the status
+    // is the one of the lowest failing stage, as the sequential loop returns
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
-    double xk[NX];
-#pragma unroll
-    for (int i = 0; i < NX; ++i) xk[i] = o.x0[i];
+    int bad_k = 0x7fffffff, bad_st = G_OK, shot = 0;
 #pragma unroll 1
-    for (int k = 0; k < o.N; ++k) {
+    for (int k = Lanes<W>::lane(); k < o.N; k += W) {
+        double xk[NX];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) xk[i] = k == 0 ? o.x0[i] : w[L.XI[s] + L.xo(k) + i];
         double F[NX], Fx[NX * NX], Fu[NX];
         const int st = shoot<NX, true>(o.m, xk, w[L.XI[s] + L.uo(k)], o.h, o.Nc, F, Fx, Fu);
-        o.cnt->shoot_full += 1;  // one stage interval (workmodel.SHOOT_FULL)
-        if (st) return st;
+        ++shot;  // one stage interval (workmodel.SHOOT_FULL)
+        if (st) {
+            bad_k = k;
+            bad_st = st;
+            break;
+        }
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
             const double nx = w[L.XI[s] + L.xo(k + 1) + i];
@@ -300,15 +350,18 @@ __device__ __noinline__ int constraints(const Ocp<NX>& o, int s) {
             w[L.FU[s] + k * NX + i] = Fu[i];
 #pragma unroll
             for (int j = 0; j < NX; ++j) w[L.FX[s] + (k * NX + j) * NX + i] = Fx[j * NX + i];
-            xk[i] = nx;
         }
     }
-    return G_OK;
+    o.cnt->shoot_full += Lanes<W>::sum(shot);
+    const int kmin = Lanes<W>::imin(bad_k);
+    Lanes<W>::sync();
+    if (kmin == 0x7fffffff) return G_OK;
+    return Lanes<W>::bcast(bad_st, kmin % W);
 }
 
 /// xi_from_inputs (ocp.cpp:137-154): u from US, result into XI[s].
-template <int NX>
-__device__ __noinline__ int xi_from_u(const Ocp<NX>& o, int s) {
+template <int NX, int W>
+__device__ __noinline__ int xi_from_u(const Ocp<NX, W>& o, int s) {
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
     double xk[NX];
@@ -321,13 +374,17 @@ __device__ __noinline__ int xi_from_u(const Ocp<NX>& o, int s) {
         double F[NX];
         const int st = shoot<NX, false>(o.m, xk, u, o.h, o.Nc, F, nullptr, nullptr);
         o.cnt->shoot_fonly += 1;
-        if (st) return st;
+        if (st) {
+            Lanes<W>::sync();
+            return st;
+        }
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
             w[L.XI[s] + L.xo(k + 1) + i] = F[i];
             xk[i] = F[i];
         }
     }
+    Lanes<W>::sync();
     return G_OK;
 }
 
@@ -336,17 +393,17 @@ __device__ __noinline__ int xi_from_u(const Ocp<NX>& o, int s) {
 // for k >= 1, Q = W_k[0:nx,0:nx], M = W_k[0:nx,nx], R = W_k[nx,nx],
 // q = gf(x_k); r = gf(u_k); Jx/Ju/b = the constraint blocks of set s;
 // terminal Q = W_N, q = gf(x_N); lb/ub = umin/umax - u_k.
-template <int NX>
+template <int NX, int W>
 struct QpView {
-    const Ocp<NX>* o;
+    const Ocp<NX, W>* o;
     int s;  // evaluation set of the current iterate
-    __device__ double W(int k, int i, int j) const {
+    __device__ double Wb(int k, int i, int j) const {
         const int ld = k == 0 ? 1 : (k < o->N ? NX + 1 : NX);
         return o->ws[o->lay.WB + (int64_t)k * Layout<NX>::B + j * ld + i];
     }
-    __device__ double R(int k) const { return k == 0 ? W(0, 0, 0) : W(k, NX, NX); }
-    __device__ double Q(int k, int i, int j) const { return W(k, i, j); }
-    __device__ double M(int k, int i) const { return W(k, i, NX); }
+    __device__ double R(int k) const { return k == 0 ? Wb(0, 0, 0) : Wb(k, NX, NX); }
+    __device__ double Q(int k, int i, int j) const { return Wb(k, i, j); }
+    __device__ double M(int k, int i) const { return Wb(k, i, NX); }
     __device__ double q(int k, int i) const { return o->ws[o->lay.GF[s] + o->lay.xo(k) + i]; }
     __device__ double r(int k) const { return o->ws[o->lay.GF[s] + o->lay.uo(k)]; }
     __device__ double Jx(int k, int i, int j) const { return o->ws[o->lay.FX[s] + ((int64_t)k * NX + j) * NX + i]; }
@@ -359,9 +416,9 @@ struct QpView {
 
 /// riccati_factor (qp.cpp:73-110) with barrier diagonal BAR. Returns true on
 /// NotPositiveDefinite.
-template <int NX>
-__device__ __noinline__ bool rfactor(const QpView<NX>& v) {
-    const Ocp<NX>& o = *v.o;
+template <int NX, int W>
+__device__ __noinline__ bool rfactor(const QpView<NX, W>& v) {
+    const Ocp<NX, W>& o = *v.o;
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
     const int N = o.N;
@@ -465,9 +522,9 @@ __device__ __noinline__ bool rfactor(const QpView<NX>& v) {
 
 /// riccati_solve_vectors (qp.cpp:116-155) for the condensed right-hand side
 /// rh = RH, qhat_k = rs(x_k), bhat_k = -rd_k; step into DXI, DMU.
-template <int NX>
-__device__ __noinline__ void rsolve(const QpView<NX>& v) {
-    const Ocp<NX>& o = *v.o;
+template <int NX, int W>
+__device__ __noinline__ void rsolve(const QpView<NX, W>& v) {
+    const Ocp<NX, W>& o = *v.o;
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
     const int N = o.N;
@@ -555,15 +612,15 @@ __device__ __noinline__ void rsolve(const QpView<NX>& v) {
 enum : int { QP_OPTIMAL = 0, QP_MAXITER = 1, QP_FAILED = 2, QP_DOMAIN = 3 };
 
 /// residuals (qp.cpp:237-284) into RS, RD, RL, RU.
-template <int NX>
-__device__ __noinline__ void qp_resid(const QpView<NX>& v) {
-    const Ocp<NX>& o = *v.o;
+template <int NX, int W>
+__device__ __noinline__ void qp_resid(const QpView<NX, W>& v) {
+    const Ocp<NX, W>& o = *v.o;
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
     const int N = o.N;
     auto dxi = [&](int e) -> double { return w[L.QDXI + e]; };
 #pragma unroll 1
-    for (int k = 0; k < N; ++k) {
+    for (int k = Lanes<W>::lane(); k < N; k += W) {
         const double vk = dxi(L.uo(k));
         double r = 1.0 * (0.0 + v.R(k) * vk) + 1.0 * v.r(k);
         if (k >= 1) {
@@ -596,7 +653,7 @@ __device__ __noinline__ void qp_resid(const QpView<NX>& v) {
         for (int i = 0; i < NX; ++i) w[L.RD + k * NX + i] = -1.0 * (0.0 + v.Ju(k, i) * vk) + 1.0 * d[i];
     }
 #pragma unroll 1
-    for (int k = 1; k <= N; ++k) {
+    for (int k = 1 + Lanes<W>::lane(); k <= N; k += W) {
         double x[NX];
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
@@ -621,37 +678,40 @@ __device__ __noinline__ void qp_resid(const QpView<NX>& v) {
         for (int i = 0; i < NX; ++i) w[L.RS + L.xo(k) + i] = x[i] + w[L.QMU + (k - 1) * NX + i];
     }
 #pragma unroll 1
-    for (int k = 0; k < N; ++k) {
+    for (int k = Lanes<W>::lane(); k < N; k += W) {
         const double vk = dxi(L.uo(k));
         const double lb = v.lb(k), ub = v.ub(k);
         w[L.RL + k] = dfinite(lb) ? vk - w[L.SL + k] - lb : 0.0;
         w[L.RU + k] = dfinite(ub) ? ub - vk - w[L.SU + k] : 0.0;
     }
+    Lanes<W>::sync();
 }
 
 /// Condensed right-hand side (qp.cpp:288-305) into RH, then the vector solve.
-template <int NX>
-__device__ __forceinline__ void qp_csolve(const QpView<NX>& v) {
-    const Ocp<NX>& o = *v.o;
+template <int NX, int W>
+__device__ __forceinline__ void qp_csolve(const QpView<NX, W>& v) {
+    const Ocp<NX, W>& o = *v.o;
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
 #pragma unroll 1
-    for (int k = 0; k < o.N; ++k) {
+    for (int k = Lanes<W>::lane(); k < o.N; k += W) {
         double x = w[L.RS + L.uo(k)];
         if (dfinite(v.lb(k))) x -= (w[L.CL + k] - w[L.QNL + k] * w[L.RL + k]) / w[L.SL + k];
         if (dfinite(v.ub(k))) x += (w[L.CU + k] - w[L.QNU + k] * w[L.RU + k]) / w[L.SU + k];
         w[L.RH + k] = x;
     }
-    rsolve<NX>(v);
+    Lanes<W>::sync();
+    rsolve<NX, W>(v);
+    Lanes<W>::sync();
 }
 /// expand (qp.cpp:308-317) of the step in DXI.
-template <int NX>
-__device__ __forceinline__ void qp_expand(const QpView<NX>& v) {
-    const Ocp<NX>& o = *v.o;
+template <int NX, int W>
+__device__ __forceinline__ void qp_expand(const QpView<NX, W>& v) {
+    const Ocp<NX, W>& o = *v.o;
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
 #pragma unroll 1
-    for (int k = 0; k < o.N; ++k) {
+    for (int k = Lanes<W>::lane(); k < o.N; k += W) {
         const double dv = w[L.DXI + L.uo(k)];
         const bool fl = dfinite(v.lb(k)), fu = dfinite(v.ub(k));
         const double dsl = fl ? dv + w[L.RL + k] : 0.0;
@@ -661,11 +721,12 @@ __device__ __forceinline__ void qp_expand(const QpView<NX>& v) {
         w[L.DNL + k] = fl ? (w[L.CL + k] - w[L.QNL + k] * dsl) / w[L.SL + k] : 0.0;
         w[L.DNU + k] = fu ? (w[L.CU + k] - w[L.QNU + k] * dsu) / w[L.SU + k] : 0.0;
     }
+    Lanes<W>::sync();
 }
 /// max_step (qp.cpp:321-337).
-template <int NX>
-__device__ __forceinline__ double qp_step(const QpView<NX>& v, double frac) {
-    const Ocp<NX>& o = *v.o;
+template <int NX, int W>
+__device__ __forceinline__ double qp_step(const QpView<NX, W>& v, double frac) {
+    const Ocp<NX, W>& o = *v.o;
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
     double a = 1.0;
@@ -673,29 +734,30 @@ __device__ __forceinline__ double qp_step(const QpView<NX>& v, double frac) {
         if (dir < 0.0) a = smin(a, -frac * val / dir);
     };
 #pragma unroll 1
-    for (int k = 0; k < o.N; ++k) {
+    for (int k = Lanes<W>::lane(); k < o.N; k += W) {
         if (dfinite(v.lb(k))) cap(w[L.SL + k], w[L.DSL + k]), cap(w[L.QNL + k], w[L.DNL + k]);
         if (dfinite(v.ub(k))) cap(w[L.SU + k], w[L.DSU + k]), cap(w[L.QNU + k], w[L.DNU + k]);
     }
-    return a;
+    return Lanes<W>::min_fold(a);
 }
 
 __device__ __forceinline__ double inf_fold(double m, double x) { return smax(m, fabs(x)); }
 
 /// solve_qp (qp.cpp:173-423): Mehrotra predictor-corrector interior point.
 /// Result in QDXI, QMU, QNL, QNU.
-template <int NX>
-__device__ __noinline__ int solve_qp(const QpView<NX>& v, double tol, int max_iter) {
-    const Ocp<NX>& o = *v.o;
+template <int NX, int W>
+__device__ __noinline__ int solve_qp(const QpView<NX, W>& v, double tol, int max_iter) {
+    const Ocp<NX, W>& o = *v.o;
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
-    const int N = o.N;
+    const int N = o.N, lane = Lanes<W>::lane();
     int m = 0;
-    double scale = 1.0;
+    double scale = 1.0;  // data_scale: an order-independent max (NaN ignored)
+    bool domain = false;
 #pragma unroll 1
-    for (int k = 0; k < N; ++k) {
+    for (int k = lane; k < N; k += W) {
         const double lb = v.lb(k), ub = v.ub(k);
-        if (lb > ub) return QP_DOMAIN;
+        if (lb > ub) domain = true;
         if (dfinite(lb)) ++m, scale = smax(scale, fabs(lb));
         if (dfinite(ub)) ++m, scale = smax(scale, fabs(ub));
         scale = smax(scale, inf_fold(0.0, v.r(k)));
@@ -704,18 +766,21 @@ __device__ __noinline__ int solve_qp(const QpView<NX>& v, double tol, int max_it
         for (int i = 0; i < NX; ++i) nb = inf_fold(nb, v.b(k, i));
         scale = smax(scale, nb);
     }
+    if (Lanes<W>::any(domain)) return QP_DOMAIN;
 #pragma unroll 1
-    for (int k = 1; k <= N; ++k) {
+    for (int k = 1 + lane; k <= N; k += W) {
         double nq = 0.0;
 #pragma unroll
         for (int i = 0; i < NX; ++i) nq = inf_fold(nq, v.q(k, i));
         scale = smax(scale, nq);
     }
+    m = Lanes<W>::sum(m);
+    scale = Lanes<W>::max_fold(scale);
     const double eps = tol * scale;
-    for (int e = 0; e < L.L; ++e) w[L.QDXI + e] = 0.0;
-    for (int e = 0; e < L.NN; ++e) w[L.QMU + e] = 0.0;
+    for (int e = lane; e < L.L; e += W) w[L.QDXI + e] = 0.0;
+    for (int e = lane; e < L.NN; e += W) w[L.QMU + e] = 0.0;
 #pragma unroll 1
-    for (int k = 0; k < N; ++k) {
+    for (int k = lane; k < N; k += W) {
         const double lb = v.lb(k), ub = v.ub(k);
         const bool fl = dfinite(lb), fu = dfinite(ub);
         w[L.SL + k] = fl ? smax(1.0, fabs(lb)) : 0.0;
@@ -725,12 +790,13 @@ __device__ __noinline__ int solve_qp(const QpView<NX>& v, double tol, int max_it
         w[L.CL + k] = 0.0;
         w[L.CU + k] = 0.0;
     }
+    Lanes<W>::sync();
     int status = QP_FAILED;
 #pragma unroll 1
     for (int it = 0;; ++it) {
-        qp_resid<NX>(v);
+        qp_resid<NX, W>(v);
         double gap = 0.0;
-        if (m > 0) {
+        if (m > 0) {  // ordered sums: serial on every lane
             double dl = 0.0, du = 0.0;
 #pragma unroll 1
             for (int k = 0; k < N; ++k) dl += w[L.SL + k] * w[L.QNL + k];
@@ -739,13 +805,17 @@ __device__ __noinline__ int solve_qp(const QpView<NX>& v, double tol, int max_it
             gap = (dl + du) / m;
         }
         double ns = 0.0, nd = 0.0, nl = 0.0, nu = 0.0;
-        for (int e = 0; e < L.L; ++e) ns = inf_fold(ns, w[L.RS + e]);
-        for (int e = 0; e < L.NN; ++e) nd = inf_fold(nd, w[L.RD + e]);
+        for (int e = lane; e < L.L; e += W) ns = inf_fold(ns, w[L.RS + e]);
+        for (int e = lane; e < L.NN; e += W) nd = inf_fold(nd, w[L.RD + e]);
 #pragma unroll 1
-        for (int k = 0; k < N; ++k) {
+        for (int k = lane; k < N; k += W) {
             nl = inf_fold(nl, w[L.RL + k]);
             nu = inf_fold(nu, w[L.RU + k]);
         }
+        ns = Lanes<W>::max_fold(ns);
+        nd = Lanes<W>::max_fold(nd);
+        nl = Lanes<W>::max_fold(nl);
+        nu = Lanes<W>::max_fold(nu);
         if (ns <= eps && nd <= eps && nl <= eps && nu <= eps && gap <= eps) {
             status = QP_OPTIMAL;
             break;
@@ -755,26 +825,29 @@ __device__ __noinline__ int solve_qp(const QpView<NX>& v, double tol, int max_it
             break;
         }
 #pragma unroll 1
-        for (int k = 0; k < N; ++k) {
+        for (int k = lane; k < N; k += W) {
             double b = 0.0;
             if (dfinite(v.lb(k))) b += w[L.QNL + k] / w[L.SL + k];
             if (dfinite(v.ub(k))) b += w[L.QNU + k] / w[L.SU + k];
             w[L.BAR + k] = b;
         }
-        if (rfactor<NX>(v)) {
+        Lanes<W>::sync();
+        const bool npd = rfactor<NX, W>(v);
+        Lanes<W>::sync();
+        if (npd) {
             status = QP_FAILED;
             break;
         }
 #pragma unroll 1
-        for (int k = 0; k < N; ++k) {
+        for (int k = lane; k < N; k += W) {
             w[L.CL + k] = dfinite(v.lb(k)) ? -w[L.SL + k] * w[L.QNL + k] : 0.0;
             w[L.CU + k] = dfinite(v.ub(k)) ? -w[L.SU + k] * w[L.QNU + k] : 0.0;
         }
-        qp_csolve<NX>(v);
-        qp_expand<NX>(v);
+        qp_csolve<NX, W>(v);
+        qp_expand<NX, W>(v);
         double sig = 0.0;
         if (m > 0 && gap > 0.0) {
-            const double aa = qp_step<NX>(v, 1.0);
+            const double aa = qp_step<NX, W>(v, 1.0);
             double ga = 0.0;
 #pragma unroll 1
             for (int k = 0; k < N; ++k) {
@@ -788,19 +861,19 @@ __device__ __noinline__ int solve_qp(const QpView<NX>& v, double tol, int max_it
             sig = smin(1.0, ratio * ratio * ratio);
         }
 #pragma unroll 1
-        for (int k = 0; k < N; ++k) {
+        for (int k = lane; k < N; k += W) {
             if (dfinite(v.lb(k)))
                 w[L.CL + k] = sig * gap - w[L.SL + k] * w[L.QNL + k] - w[L.DSL + k] * w[L.DNL + k];
             if (dfinite(v.ub(k)))
                 w[L.CU + k] = sig * gap - w[L.SU + k] * w[L.QNU + k] - w[L.DSU + k] * w[L.DNU + k];
         }
-        qp_csolve<NX>(v);
-        qp_expand<NX>(v);
-        const double a = qp_step<NX>(v, 0.995);
-        for (int e = 0; e < L.L; ++e) w[L.QDXI + e] += a * w[L.DXI + e];
-        for (int e = 0; e < L.NN; ++e) w[L.QMU + e] += a * w[L.DMU + e];
+        qp_csolve<NX, W>(v);
+        qp_expand<NX, W>(v);
+        const double a = qp_step<NX, W>(v, 0.995);
+        for (int e = lane; e < L.L; e += W) w[L.QDXI + e] += a * w[L.DXI + e];
+        for (int e = lane; e < L.NN; e += W) w[L.QMU + e] += a * w[L.DMU + e];
 #pragma unroll 1
-        for (int k = 0; k < N; ++k) {
+        for (int k = lane; k < N; k += W) {
             if (dfinite(v.lb(k))) {
                 w[L.SL + k] += a * w[L.DSL + k];
                 w[L.QNL + k] += a * w[L.DNL + k];
@@ -810,52 +883,63 @@ __device__ __noinline__ int solve_qp(const QpView<NX>& v, double tol, int max_it
                 w[L.QNU + k] += a * w[L.DNU + k];
             }
         }
+        Lanes<W>::sync();
         o.cnt->ipm_stage += N;
     }
 #pragma unroll 1
-    for (int k = 0; k < N; ++k) {
+    for (int k = lane; k < N; k += W) {
         double& x = w[L.QDXI + L.uo(k)];
         x = smin(smax(x, v.lb(k)), v.ub(k));
     }
+    Lanes<W>::sync();
     return status;
 }
 
 // -------------------------------------------------------------------- SQP
 /// h += J_g' lam (add_constraint_term, sqp.cpp:102-116) on the blocks of
 /// set s; h at element offset H.
-template <int NX>
-__device__ void add_jt(const Ocp<NX>& o, int s, int64_t LAMo, int64_t H) {
+template <int NX, int W>
+__device__ void add_jt(const Ocp<NX, W>& o, int s, int64_t LAMo, int64_t H) {
+    // lane-parallel by slot ownership: unit k owns u_k and x_{k+1}; per slot
+    // the reference's order is kept: x_{k+1} gets + lam_k (iteration k), then
+    // - Fx_{k+1}' lam_{k+1} term by term (iteration k+1)
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
 #pragma unroll 1
-    for (int k = 0; k < o.N; ++k) {
-#pragma unroll
-        for (int i = 0; i < NX; ++i) w[H + L.xo(k + 1) + i] += w[LAMo + k * NX + i];
+    for (int k = Lanes<W>::lane(); k < o.N; k += W) {
 #pragma unroll
         for (int j = 0; j < NX; ++j) w[H + L.uo(k)] -= w[L.FU[s] + k * NX + j] * w[LAMo + k * NX + j];
-        if (k >= 1) {
+        const int kn = k + 1;
 #pragma unroll
-            for (int i = 0; i < NX; ++i)
+        for (int i = 0; i < NX; ++i) {
+            double h = w[H + L.xo(kn) + i] + w[LAMo + k * NX + i];
+            if (kn < o.N) {
 #pragma unroll
                 for (int j = 0; j < NX; ++j)
-                    w[H + L.xo(k) + i] -= w[L.FX[s] + ((int64_t)k * NX + i) * NX + j] * w[LAMo + k * NX + j];
+                    h -= w[L.FX[s] + ((int64_t)kn * NX + i) * NX + j] * w[LAMo + kn * NX + j];
+            }
+            w[H + L.xo(kn) + i] = h;
         }
     }
+    Lanes<W>::sync();
 }
 
 /// lagrangian_gradient (sqp.cpp:118-128) into HO for duals (LAMo, PLo, PUo),
 /// then check_convergence (sqp.cpp:86-96).
-template <int NX>
-__device__ __noinline__ bool kkt_ok(const Ocp<NX>& o, int s, int64_t LAMo, int64_t PLo, int64_t PUo, int m,
+template <int NX, int W>
+__device__ __noinline__ bool kkt_ok(const Ocp<NX, W>& o, int s, int64_t LAMo, int64_t PLo, int64_t PUo, int m,
                                     double eps) {
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
-    for (int e = 0; e < L.L; ++e) w[L.HO + e] = w[L.GF[s] + e];
-    add_jt<NX>(o, s, LAMo, L.HO);
+    const int lane = Lanes<W>::lane();
+    for (int e = lane; e < L.L; e += W) w[L.HO + e] = w[L.GF[s] + e];
+    Lanes<W>::sync();
+    add_jt<NX, W>(o, s, LAMo, L.HO);
 #pragma unroll 1
-    for (int k = 0; k < o.N; ++k) w[L.HO + L.uo(k)] += w[PUo + k] - w[PLo + k];
+    for (int k = lane; k < o.N; k += W) w[L.HO + L.uo(k)] += w[PUo + k] - w[PLo + k];
+    Lanes<W>::sync();
     double sd = 1.0;
-    if (m > 0) {
+    if (m > 0) {  // ordered one-norm sums: serial on every lane
         double a = 0.0, b = 0.0, c = 0.0;
         for (int e = 0; e < L.NN; ++e) a += fabs(w[LAMo + e]);
 #pragma unroll 1
@@ -865,28 +949,31 @@ __device__ __noinline__ bool kkt_ok(const Ocp<NX>& o, int s, int64_t LAMo, int64
         sd = smax(100.0, (a + b + c) / m) / 100.0;
     }
     double gl = 0.0, gg = 0.0;
-    for (int e = 0; e < L.L; ++e) gl = inf_fold(gl, w[L.HO + e]);
-    for (int e = 0; e < L.NN; ++e) gg = inf_fold(gg, w[L.G[s] + e]);
+    for (int e = lane; e < L.L; e += W) gl = inf_fold(gl, w[L.HO + e]);
+    for (int e = lane; e < L.NN; e += W) gg = inf_fold(gg, w[L.G[s] + e]);
+    gl = Lanes<W>::max_fold(gl);
+    gg = Lanes<W>::max_fold(gg);
     return gl / sd <= eps && gg <= eps;
 }
 
 /// reset_blocks (sqp.cpp:173-178): identities of size 1, nx+1, ..., nx.
-template <int NX>
-__device__ void identity_blocks(const Ocp<NX>& o) {
+template <int NX, int W>
+__device__ void identity_blocks(const Ocp<NX, W>& o) {
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
 #pragma unroll 1
-    for (int k = 0; k <= o.N; ++k) {
+    for (int k = Lanes<W>::lane(); k <= o.N; k += W) {
         const int n = k == 0 ? 1 : (k < o.N ? NX + 1 : NX);
         for (int j = 0; j < n; ++j)
             for (int i = 0; i < n; ++i) w[L.WB + (int64_t)k * Layout<NX>::B + j * n + i] = (i == j) ? 1.0 : 0.0;
     }
+    Lanes<W>::sync();
 }
 
 /// bfgs_block_update (sqp.cpp:61-84) of block k with s, y of length n.
 /// Returns true on NotPositiveDefinite (the Cholesky audit).
-template <int NX>
-__device__ bool bfgs_block(const Ocp<NX>& o, int k, int n, const double* s, const double* y) {
+template <int NX, int W>
+__device__ bool bfgs_block(const Ocp<NX, W>& o, int k, int n, const double* s, const double* y) {
     const Ws& w = o.ws;
     const int64_t base = o.lay.WB + (int64_t)k * Layout<NX>::B;
     auto Wm = [&](int i, int j) -> double& { return w[base + j * n + i]; };
@@ -941,52 +1028,54 @@ struct SqpOut {
 
 /// sqp_solve (sqp.cpp:182-411) from the iterate in XI[0] and duals LAM/PL/PU.
 /// On return the iterate is in XI[*cur].
-template <int NX>
-__device__ __noinline__ SqpOut sqp_solve(const Ocp<NX>& o, const nmpcmc_sqp_options& op, int* cur) {
+template <int NX, int W>
+__device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_options& op, int* cur) {
     const Ws& w = o.ws;
     const Layout<NX>& L = o.lay;
-    const int N = o.N;
+    const int N = o.N, lane = Lanes<W>::lane();
     const int m = N * NX + (dfinite(o.umin) ? N : 0) + (dfinite(o.umax) ? N : 0);
     int s = 0;
     *cur = 0;
-    identity_blocks<NX>(o);
-    double f = objective<NX>(o, s, true);
+    identity_blocks<NX, W>(o);
+    double f = objective<NX, W>(o, s, true);
     {
-        const int st = constraints<NX>(o, s);
+        const int st = constraints<NX, W>(o, s);
         if (st == G_DOMAIN) return SqpOut{false, G_DOMAIN};
         if (st != G_OK) return SqpOut{false, G_OK};
     }
     bool first = true;
 #pragma unroll 1
     for (int it = 0;; ++it) {
-        if (kkt_ok<NX>(o, s, L.LAM, L.PL, L.PU, m, op.eps)) return SqpOut{true, G_OK};
+        if (kkt_ok<NX, W>(o, s, L.LAM, L.PL, L.PU, m, op.eps)) return SqpOut{true, G_OK};
         if (it >= op.max_iter) break;
         o.cnt->sqp_stage += N;
-        const QpView<NX> v{&o, s};
-        int qs = solve_qp<NX>(v, op.qp_tol, op.qp_max_iter);
+        const QpView<NX, W> v{&o, s};
+        int qs = solve_qp<NX, W>(v, op.qp_tol, op.qp_max_iter);
         o.cnt->qp += 1;
         if (qs == QP_DOMAIN) return SqpOut{false, G_DOMAIN};
         if (qs == QP_FAILED) {
-            identity_blocks<NX>(o);
-            qs = solve_qp<NX>(v, op.qp_tol, op.qp_max_iter);
+            identity_blocks<NX, W>(o);
+            qs = solve_qp<NX, W>(v, op.qp_tol, op.qp_max_iter);
             o.cnt->qp += 1;
             if (qs == QP_DOMAIN) return SqpOut{false, G_DOMAIN};
             if (qs == QP_FAILED) break;
         }
-        if (kkt_ok<NX>(o, s, L.QMU, L.QNL, L.QNU, m, op.eps)) {
-            for (int e = 0; e < L.NN; ++e) w[L.LAM + e] = w[L.QMU + e];
+        if (kkt_ok<NX, W>(o, s, L.QMU, L.QNL, L.QNU, m, op.eps)) {
+            for (int e = lane; e < L.NN; e += W) w[L.LAM + e] = w[L.QMU + e];
 #pragma unroll 1
-            for (int k = 0; k < N; ++k) {
+            for (int k = lane; k < N; k += W) {
                 w[L.PL + k] = w[L.QNL + k];
                 w[L.PU + k] = w[L.QNU + k];
             }
+            Lanes<W>::sync();
             return SqpOut{true, G_OK};
         }
         // merit_weights_update (sqp.cpp:12-20)
-        for (int e = 0; e < L.NN; ++e) {
+        for (int e = lane; e < L.NN; e += W) {
             const double am = fabs(w[L.QMU + e]);
             w[L.SIG + e] = first ? am : smax(am, 0.5 * (w[L.SIG + e] + am));
         }
+        Lanes<W>::sync();
         first = false;
         // line_search (sqp.cpp:22-59); the trial of the accepted step is the
         // new iterate (identical by construction, sqp.cpp:331-352)
@@ -1001,10 +1090,11 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX>& o, const nmpcmc_sqp_opti
         bool ok = false, tfin = false;
 #pragma unroll 1
         for (int bt = 0;; ++bt) {
-            for (int e = 0; e < L.L; ++e) w[L.XI[t] + e] = w[L.XI[s] + e] + a * w[L.QDXI + e];
+            for (int e = lane; e < L.L; e += W) w[L.XI[t] + e] = w[L.XI[s] + e] + a * w[L.QDXI + e];
+            Lanes<W>::sync();
             merit = __longlong_as_double(0x7ff0000000000000LL);
-            ft = objective<NX>(o, t, true);
-            const int st = constraints<NX>(o, t);
+            ft = objective<NX, W>(o, t, true);
+            const int st = constraints<NX, W>(o, t);
             if (st == G_DOMAIN) return SqpOut{false, G_DOMAIN};
             o.cnt->ls += 1;  // counted like K3: a trial that raises DomainError ends the solve uncounted
             tfin = st == G_OK;
@@ -1019,22 +1109,25 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX>& o, const nmpcmc_sqp_opti
         if (!ok && !dfinite(merit)) break;
         if (!tfin) break;  // the re-evaluation at xn would throw NonFiniteState
         // duals (sqp.cpp:355-364)
-        for (int e = 0; e < L.NN; ++e) w[L.LAM + e] += a * (w[L.QMU + e] - w[L.LAM + e]);
+        for (int e = lane; e < L.NN; e += W) w[L.LAM + e] += a * (w[L.QMU + e] - w[L.LAM + e]);
 #pragma unroll 1
-        for (int k = 0; k < N; ++k) {
+        for (int k = lane; k < N; k += W) {
             w[L.PL + k] += a * (w[L.QNL + k] - w[L.PL + k]);
             w[L.PU + k] += a * (w[L.QNU + k] - w[L.PU + k]);
         }
         // BFGS on the Lagrangian gradients with the new multipliers (sqp.cpp:366-396)
-        for (int e = 0; e < L.L; ++e) {
+        for (int e = lane; e < L.L; e += W) {
             w[L.HO + e] = w[L.GF[s] + e];
             w[L.HN + e] = w[L.GF[t] + e];
         }
-        add_jt<NX>(o, s, L.LAM, L.HO);
-        add_jt<NX>(o, t, L.LAM, L.HN);
+        Lanes<W>::sync();
+        add_jt<NX, W>(o, s, L.LAM, L.HO);
+        add_jt<NX, W>(o, t, L.LAM, L.HN);
+        // blocks are independent; a lost block resets all of them below, so
+        // updating the others in parallel changes nothing (sqp.cpp:377-396)
         bool lost = false;
 #pragma unroll 1
-        for (int blk = 0; blk <= N && !lost; ++blk) {
+        for (int blk = lane; blk <= N && !lost; blk += W) {
             const int off = blk == 0 ? 0 : (blk < N ? L.xo(blk) : L.xo(N));
             const int len = blk == 0 ? 1 : (blk < N ? NX + 1 : NX);
             double sv[NX + 1], yv[NX + 1];
@@ -1042,9 +1135,11 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX>& o, const nmpcmc_sqp_opti
                 sv[i] = a * w[L.QDXI + off + i];
                 yv[i] = w[L.HN + off + i] - w[L.HO + off + i];
             }
-            lost = bfgs_block<NX>(o, blk, len, sv, yv);
+            lost = bfgs_block<NX, W>(o, blk, len, sv, yv);
         }
-        if (lost) identity_blocks<NX>(o);
+        lost = Lanes<W>::any(lost);
+        Lanes<W>::sync();
+        if (lost) identity_blocks<NX, W>(o);
         f = ft;
         s = t;
         *cur = s;
@@ -1221,7 +1316,7 @@ __device__ __noinline__ bool ekf_update(const Model<NX>& m, double* x, double* P
 // ------------------------------------------------------------ closed loop
 /// The NMPC branch of run_closed_loop (montecarlo.cpp:80-157) for one sample
 /// with a controller model of NX states and a truth plant of TX states.
-template <int TX, int NX>
+template <int TX, int NX, int W>
 __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar, const Ws& ws,
                                          nmpcmc_sim_record* rec, nmpcmc_work_counters* cntp, double* traj) {
     const Cstr p = sample_truth(sc, sim_index);
@@ -1234,7 +1329,8 @@ __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim
     const double lR = has_R ? chol_semidef_1x1(sc.noise_R) : 0.0;
     const int stride = sc.record_stride < 1 ? 1 : sc.record_stride;
     Cnt cnt = {};
-    Ocp<NX> o{make_model<NX>(sc.ctrl), Layout<NX>(sc.N), ws, sc.N, sc.Nc, sc.horizon_Ts, sc.horizon_Ts / sc.Nc,
+    const int lane = Lanes<W>::lane();
+    Ocp<NX, W> o{make_model<NX>(sc.ctrl), Layout<NX>(sc.N), ws, sc.N, sc.Nc, sc.horizon_Ts, sc.horizon_Ts / sc.Nc,
               sc.u_min, sc.u_max, sc.Qz, 0.0, {}, &cnt};
     o.invV = 1.0 / o.m.p.V;
     const Layout<NX>& L = o.lay;
@@ -1266,7 +1362,8 @@ __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim
             break;
         }
 #pragma unroll 1
-        for (int k = 0; k < N; ++k) ws[L.SP + k] = setpoint_at(sc, t + (k + 1) * sc.Ts);
+        for (int k = lane; k < N; k += W) ws[L.SP + k] = setpoint_at(sc, t + (k + 1) * sc.Ts);
+        Lanes<W>::sync();
         double xf[NX], Pn[NX * NX];
 #pragma unroll
         for (int e = 0; e < NX; ++e) xf[e] = xhat[e];
@@ -1288,76 +1385,65 @@ __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim
         // warm / cold start (controllers.cpp:147-186)
         if (have_last) {
 #pragma unroll 1
-            for (int k = 0; k < N; ++k) ws[L.US + k] = clampu(ws[L.LXI + L.uo(k + 1 < N ? k + 1 : N - 1)]);
-            const int st = xi_from_u<NX>(o, 0);
+            for (int k = lane; k < N; k += W) ws[L.US + k] = clampu(ws[L.LXI + L.uo(k + 1 < N ? k + 1 : N - 1)]);
+            Lanes<W>::sync();
+            const int st = xi_from_u<NX, W>(o, 0);
             if (st == G_DOMAIN) {
                 status = G_DOMAIN;
                 break;
             }
-            if (st != G_OK) {  // shifted_warm_start (controllers.cpp:97-110)
+            if (st != G_OK) {  // shifted_warm_start (controllers.cpp:97-110), clamped inputs
                 const int w = Layout<NX>::W;
-                for (int e = 0; e < L.L; ++e) ws[L.XI[0] + e] = 0.0;
-                for (int e = w; e < L.L; ++e) ws[L.XI[0] + e - w] = ws[L.LXI + e];
-                for (int e = L.L - w; e < L.L; ++e) ws[L.XI[0] + e] = ws[L.LXI + e];
-#pragma unroll 1
-                for (int k = 0; k < N; ++k) ws[L.XI[0] + L.uo(k)] = clampu(ws[L.XI[0] + L.uo(k)]);
+                for (int e = lane; e < L.L; e += W) {
+                    double x = e < L.L - w ? ws[L.LXI + e + w] : ws[L.LXI + e];
+                    if (e % w == 0) x = clampu(x);
+                    ws[L.XI[0] + e] = x;
+                }
             }
             // shifted_multipliers (controllers.cpp:87-93), projected (sqp.cpp:219-222)
-            if (L.NN >= 2 * NX) {
-                for (int e = 0; e < L.NN - NX; ++e) ws[L.LAM + e] = ws[L.LLAM + e + NX];
-                for (int e = L.NN - NX; e < L.NN; ++e) ws[L.LAM + e] = ws[L.LLAM + e];
-            } else {
-                for (int e = 0; e < L.NN; ++e) ws[L.LAM + e] = ws[L.LLAM + e];
-            }
-            if (N >= 2) {
+            for (int e = lane; e < L.NN; e += W)
+                ws[L.LAM + e] = (L.NN >= 2 * NX && e < L.NN - NX) ? ws[L.LLAM + e + NX] : ws[L.LLAM + e];
 #pragma unroll 1
-                for (int k = 0; k < N - 1; ++k) {
-                    ws[L.PL + k] = ws[L.LPL + k + 1];
-                    ws[L.PU + k] = ws[L.LPU + k + 1];
-                }
-                ws[L.PL + N - 1] = ws[L.LPL + N - 1];
-                ws[L.PU + N - 1] = ws[L.LPU + N - 1];
-            } else {
-                ws[L.PL] = ws[L.LPL];
-                ws[L.PU] = ws[L.LPU];
-            }
-#pragma unroll 1
-            for (int k = 0; k < N; ++k) {
-                ws[L.PL + k] = smax(0.0, ws[L.PL + k]);
-                ws[L.PU + k] = smax(0.0, ws[L.PU + k]);
+            for (int k = lane; k < N; k += W) {
+                const int src = k < N - 1 ? k + 1 : k;
+                ws[L.PL + k] = smax(0.0, ws[L.LPL + src]);
+                ws[L.PU + k] = smax(0.0, ws[L.LPU + src]);
             }
         } else {
             const double un = fl && fh ? 0.5 * (o.umin + o.umax) : clampu(0.0);
 #pragma unroll 1
-            for (int k = 0; k < N; ++k) ws[L.US + k] = un;
-            const int st = xi_from_u<NX>(o, 0);
+            for (int k = lane; k < N; k += W) ws[L.US + k] = un;
+            Lanes<W>::sync();
+            const int st = xi_from_u<NX, W>(o, 0);
             if (st == G_DOMAIN) {
                 status = G_DOMAIN;
                 break;
             }
             if (st != G_OK) {
 #pragma unroll 1
-                for (int k = 0; k < N; ++k) {
+                for (int k = lane; k < N; k += W) {
                     ws[L.XI[0] + L.uo(k)] = un;
 #pragma unroll
                     for (int e = 0; e < NX; ++e) ws[L.XI[0] + L.xo(k + 1) + e] = xf[e];
                 }
             }
-            for (int e = 0; e < L.NN; ++e) ws[L.LAM + e] = 0.0;
+            for (int e = lane; e < L.NN; e += W) ws[L.LAM + e] = 0.0;
 #pragma unroll 1
-            for (int k = 0; k < N; ++k) ws[L.PL + k] = 0.0, ws[L.PU + k] = 0.0;
+            for (int k = lane; k < N; k += W) ws[L.PL + k] = 0.0, ws[L.PU + k] = 0.0;
         }
+        Lanes<W>::sync();
         int cur = 0;
-        const SqpOut so = sqp_solve<NX>(o, sc.sqp, &cur);
+        const SqpOut so = sqp_solve<NX, W>(o, sc.sqp, &cur);
         if (so.status != G_OK) {
             status = so.status;
             break;
         }
         const double u = clampu(ws[L.XI[cur] + L.uo(0)]);
-        for (int e = 0; e < L.L; ++e) ws[L.LXI + e] = ws[L.XI[cur] + e];
-        for (int e = 0; e < L.NN; ++e) ws[L.LLAM + e] = ws[L.LAM + e];
+        for (int e = lane; e < L.L; e += W) ws[L.LXI + e] = ws[L.XI[cur] + e];
+        for (int e = lane; e < L.NN; e += W) ws[L.LLAM + e] = ws[L.LAM + e];
 #pragma unroll 1
-        for (int k = 0; k < N; ++k) ws[L.LPL + k] = ws[L.PL + k], ws[L.LPU + k] = ws[L.PU + k];
+        for (int k = lane; k < N; k += W) ws[L.LPL + k] = ws[L.PL + k], ws[L.LPU + k] = ws[L.PU + k];
+        Lanes<W>::sync();
         have_last = true;
         {
             const int st = ekf_predict<NX>(o.m, xf, Pn, u, t, t + sc.horizon_Ts, sc.np);
@@ -1374,8 +1460,10 @@ __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim
         if (!so.converged) ++fails;
         cnt.steps += 1;
         if (traj != nullptr && i % stride == 0) {
-            double* rw = traj + (size_t)row * 5;
-            rw[0] = t, rw[1] = z, rw[2] = zbar, rw[3] = u, rw[4] = y;
+            if (lane == 0) {
+                double* rw = traj + (size_t)row * 5;
+                rw[0] = t, rw[1] = z, rw[2] = zbar, rw[3] = u, rw[4] = y;
+            }
             ++row;
         }
         status = simulate_interval<TX>(p, pl, t, t + sc.Ts, u, sc.Ns, rng);
@@ -1386,6 +1474,7 @@ __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim
         const double r = z - zbar;
         acc += r * r;
     }
+    if (lane != 0) return;
     if (status == G_OK) {
         rec->phi = acc / (double)(nbar + 1);
         rec->failed = 0;
@@ -1433,8 +1522,27 @@ __global__ void __launch_bounds__(kGenBlock) nmpc_gen_kernel(const __grid_consta
     for (;;) {
         const unsigned long long i = atomicAdd(next, 1ULL);
         if (i >= (unsigned long long)n_sims) break;
-        closed_loop<TX, NX>(sc, first_sim + i, nbar, ws, records + i, counters ? counters + i : nullptr,
-                            traj ? traj + (size_t)i * traj_rows * 5 : nullptr);
+        closed_loop<TX, NX, 1>(sc, first_sim + i, nbar, ws, records + i, counters ? counters + i : nullptr,
+                               traj ? traj + (size_t)i * traj_rows * 5 : nullptr);
+    }
+}
+
+/// K3w: one warp per sample, persistent one-warp blocks pulling samples from
+/// an atomic counter; workspace = one contiguous slab per block.
+template <int TX, int NX>
+__global__ void __launch_bounds__(32) nmpc_genw_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
+                                                       int64_t n_sims, int nbar, nmpcmc_sim_record* records,
+                                                       nmpcmc_work_counters* counters, double* traj, int traj_rows,
+                                                       double* ws_all, int64_t slab, unsigned long long* next) {
+    const Ws ws{ws_all + (int64_t)blockIdx.x * slab, 1};
+#pragma unroll 1
+    for (;;) {
+        unsigned long long i = 0;
+        if ((threadIdx.x & 31) == 0) i = atomicAdd(next, 1ULL);
+        i = __shfl_sync(kMask, i, 0);
+        if (i >= (unsigned long long)n_sims) break;
+        closed_loop<TX, NX, 32>(sc, first_sim + i, nbar, ws, records + i, counters ? counters + i : nullptr,
+                                traj ? traj + (size_t)i * traj_rows * 5 : nullptr);
     }
 }
 
@@ -1456,6 +1564,42 @@ inline int64_t gen_slots(const nmpcmc_scenario& sc, int sm_count, int64_t n) {
     const bool t3 = sc.truth_variant == NMPCMC_THREE_STATE, c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
     if (t3) return c3 ? gen_slots_t<3, 3>(sm_count, n) : gen_slots_t<3, 1>(sm_count, n);
     return c3 ? gen_slots_t<1, 3>(sm_count, n) : gen_slots_t<1, 1>(sm_count, n);
+}
+
+/// K3w resident blocks (one warp each): occupancy, capped so the per-warp
+/// slabs stay L2-resident (~72 KB each at N = 60, NX = 3).
+template <int TX, int NX>
+inline int64_t genw_blocks_t(int sm_count, int64_t n, int64_t slab_doubles) {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nmpc_genw_kernel<TX, NX>, 32, 0);
+    if (b < 1) b = 1;
+    int64_t blocks = (int64_t)sm_count * b;
+    const int64_t l2_cap = (int64_t)(96ull << 20) / (slab_doubles * 8);
+    if (blocks > l2_cap) blocks = l2_cap < sm_count ? sm_count : l2_cap;
+    return blocks < n ? blocks : n;
+}
+inline int64_t genw_blocks(const nmpcmc_scenario& sc, int sm_count, int64_t n) {
+    const bool t3 = sc.truth_variant == NMPCMC_THREE_STATE, c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
+    const int64_t slab = gen_ws_doubles(sc);
+    if (t3) return c3 ? genw_blocks_t<3, 3>(sm_count, n, slab) : genw_blocks_t<3, 1>(sm_count, n, slab);
+    return c3 ? genw_blocks_t<1, 3>(sm_count, n, slab) : genw_blocks_t<1, 1>(sm_count, n, slab);
+}
+inline int launch_genw(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
+                       nmpcmc_work_counters* d_cnt, double* d_traj, int rows, double* ws, int64_t blocks,
+                       unsigned long long* counter, cudaStream_t stream) {
+    if (blocks < 1) return NMPCMC_INVALID_ARGUMENT;
+    const int64_t slab = gen_ws_doubles(sc);
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    const bool t3 = sc.truth_variant == NMPCMC_THREE_STATE, c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
+#define NMPCMC_GENW_LAUNCH(T, C)                                                                              \
+    nmpc_genw_kernel<T, C><<<(unsigned)blocks, 32, 0, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ws, \
+                                                                slab, counter)
+    if (t3 && c3) NMPCMC_GENW_LAUNCH(3, 3);
+    else if (t3) NMPCMC_GENW_LAUNCH(3, 1);
+    else if (c3) NMPCMC_GENW_LAUNCH(1, 3);
+    else NMPCMC_GENW_LAUNCH(1, 1);
+#undef NMPCMC_GENW_LAUNCH
+    return NMPCMC_OK;
 }
 
 inline int launch_gen(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,

@@ -124,8 +124,17 @@ int launch(nmpcmc_gpu_ctx* ctx, const Target& tg, const nmpcmc_scenario& sc, uin
     }
     int rc;
     const bool generic = sc.ctrl_variant != NMPCMC_ONE_STATE || sc.N > 255 ||
-                         ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC;
-    if (generic) {
+                         ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC ||
+                         ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC_WARP;
+    if (generic && ctx->nmpc_kernel != NMPCMC_NMPC_KERNEL_GENERIC) {  // K3w unless K3g is asked for
+        const int64_t blocks = nmpcmc_dev::gen::genw_blocks(sc, ctx->sm_count, n);
+        const size_t need = (size_t)blocks * (size_t)nmpcmc_dev::gen::gen_ws_doubles(sc) * sizeof(double);
+        if ((rc = ensure(ctx, tg.d_ws, tg.ws_cap, need)) != NMPCMC_OK) return rc;
+        if ((rc = ensure(ctx, tg.d_counter, tg.counter_cap, 256)) != NMPCMC_OK) return rc;
+        rc = nmpcmc_dev::gen::launch_genw(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
+                                          static_cast<double*>(*tg.d_ws), blocks,
+                                          static_cast<unsigned long long*>(*tg.d_counter), tg.stream);
+    } else if (generic) {
         const int64_t slots = nmpcmc_dev::gen::gen_slots(sc, ctx->sm_count, n);
         const size_t need = (size_t)slots * (size_t)nmpcmc_dev::gen::gen_ws_doubles(sc) * sizeof(double);
         if ((rc = ensure(ctx, tg.d_ws, tg.ws_cap, need)) != NMPCMC_OK) return rc;
@@ -234,8 +243,7 @@ int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value) {
     if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
     switch (option) {
         case NMPCMC_OPT_NMPC_KERNEL:
-            if (value != NMPCMC_NMPC_KERNEL_WARP && value != NMPCMC_NMPC_KERNEL_THREAD &&
-                value != NMPCMC_NMPC_KERNEL_GENERIC)
+            if (value < NMPCMC_NMPC_KERNEL_WARP || value > NMPCMC_NMPC_KERNEL_GENERIC_WARP)
                 return NMPCMC_INVALID_ARGUMENT;
             ctx->nmpc_kernel = (int)value;
             return NMPCMC_OK;

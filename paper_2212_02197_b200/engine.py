@@ -146,12 +146,13 @@ class Context:
         if rc != 0:
             _raise(rc, self.lib.nmpcmc_gpu_last_error(self.handle).decode())
 
-    KERNELS = {"warp": 1, "thread": 2, "generic": 3}
+    KERNELS = {"warp": 1, "thread": 2, "generic": 3, "generic_warp": 4}
 
     def set_nmpc_kernel(self, kind: str):
-        """'warp' (K3, default), 'thread' (K3b) or 'generic' (K3g) for a
-        one-state controller model; bitwise-identical results. A three-state
-        controller model (or N > 255) always runs K3g."""
+        """'warp' (K3, default), 'thread' (K3b), 'generic' (K3g) or
+        'generic_warp' (K3w) for a one-state controller model; bitwise-
+        identical results. A three-state controller model (or N > 255) runs
+        K3w, or K3g when 'generic' is selected."""
         self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 1, self.KERNELS[kind]))
 
     def set_tps_warps_per_sm(self, w: int):

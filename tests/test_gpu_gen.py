@@ -12,43 +12,48 @@ from paper_2212_02197_b200 import configs
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(params=["generic", "generic_warp"])
+def gctx(request, gpu_ctx):
+    """K3g (thread per sample) or K3w (warp per sample) for the generic path."""
+    gpu_ctx.set_nmpc_kernel(request.param)
+    yield gpu_ctx
+    gpu_ctx.set_nmpc_kernel("warp")
+
 GEN_CASES = ["nmpc3_n30_short", "nmpc3_n60_pert_short", "nmpc3_cfg2", "nmpc_n256_short"]
 
 
 @pytest.mark.parametrize("name", GEN_CASES)
-def test_gen_records_bitwise_vs_exact_libm_reference(gpu_ctx, name):
+def test_gen_records_bitwise_vs_exact_libm_reference(gctx, name):
     d, _, sc = load_golden(name)
     want = d["rec_xlibm"]
-    got, _ = gpu_ctx.run(sc, int(d["first"]), len(want))
+    got, _ = gctx.run(sc, int(d["first"]), len(want))
     assert_records_equal(got, want)
 
 
 @pytest.mark.parametrize("name", GEN_CASES)
-def test_gen_trajectories_bitwise(gpu_ctx, name):
+def test_gen_trajectories_bitwise(gctx, name):
     d, kw, _ = load_golden(name)
     sct = configs.make_scenario(**kw, record=True)
     want = d["traj_xlibm"]
-    _, traj = gpu_ctx.run_traj(sct, int(d["first"]), want.shape[0])
+    _, traj = gctx.run_traj(sct, int(d["first"]), want.shape[0])
     np.testing.assert_array_equal(traj, want)
 
 
 @pytest.mark.parametrize("name", ["nmpc_n30_short", "nmpc_n60_pert_short"])
-def test_gen_one_state_matches_reference(gpu_ctx, name):
+def test_gen_one_state_matches_reference(gctx, name):
     d, _, sc = load_golden(name)
-    gpu_ctx.set_nmpc_kernel("generic")
-    try:
-        got, _ = gpu_ctx.run(sc, int(d["first"]), len(d["rec_xlibm"]))
-    finally:
-        gpu_ctx.set_nmpc_kernel("warp")
+    got, _ = gctx.run(sc, int(d["first"]), len(d["rec_xlibm"]))
     assert_records_equal(got, d["rec_xlibm"])
 
 
-def test_gen_matches_k3_at_scale(gpu_ctx):
-    """K3g and K3 on 512 perturbed one-state samples: identical records and
-    work counters."""
+@pytest.mark.parametrize("kind", ["generic", "generic_warp"])
+def test_gen_matches_k3_at_scale(gpu_ctx, kind):
+    """K3g / K3w and K3 on 512 perturbed one-state samples: identical records
+    and work counters."""
     sc = configs.make_scenario("nmpc", N=30, n_steps=40, perturb=True)
     a, ca = gpu_ctx.run(sc, 5000, 512, counters=True)
-    gpu_ctx.set_nmpc_kernel("generic")
+    gpu_ctx.set_nmpc_kernel(kind)
     try:
         b, cb = gpu_ctx.run(sc, 5000, 512, counters=True)
     finally:
@@ -58,9 +63,23 @@ def test_gen_matches_k3_at_scale(gpu_ctx):
         np.testing.assert_array_equal(ca[f], cb[f])
 
 
-def test_gen_three_state_sharding_invariance(gpu_ctx):
+def test_gen_three_state_sharding_invariance(gctx):
     sc = configs.make_scenario("nmpc", N=20, n_steps=15, perturb=True, ctrl_variant=configs.THREE_STATE)
-    full, _ = gpu_ctx.run(sc, 0, 200)
-    a, _ = gpu_ctx.run(sc, 0, 77)
-    b, _ = gpu_ctx.run(sc, 77, 123)
+    full, _ = gctx.run(sc, 0, 200)
+    a, _ = gctx.run(sc, 0, 77)
+    b, _ = gctx.run(sc, 77, 123)
     assert_records_equal(np.concatenate([a, b]), full)
+
+
+def test_k3w_matches_k3g_three_state_at_scale(gpu_ctx):
+    sc = configs.make_scenario("nmpc", N=40, n_steps=12, perturb=True, ctrl_variant=configs.THREE_STATE)
+    gpu_ctx.set_nmpc_kernel("generic")
+    try:
+        a, ca = gpu_ctx.run(sc, 100, 700, counters=True)
+        gpu_ctx.set_nmpc_kernel("generic_warp")
+        b, cb = gpu_ctx.run(sc, 100, 700, counters=True)
+    finally:
+        gpu_ctx.set_nmpc_kernel("warp")
+    assert_records_equal(a, b)
+    for f in ("control_steps", "ipm_stage_iters", "sqp_iterations", "qp_solves", "ls_evals"):
+        np.testing.assert_array_equal(ca[f], cb[f])
