@@ -423,19 +423,22 @@ __device__ __noinline__ bool rfactor(const QpView<NX, W>& v) {
     const Layout<NX>& L = o.lay;
     const int N = o.N;
     auto P = [&](int k, int i, int j) -> double& { return w[L.FP + ((int64_t)k * NX + j) * NX + i]; };
+    // P_{k+1} is carried in registers from one stage to the next: reloading
+    // what the previous stage just stored would put a store-to-load round trip
+    // through the cache hierarchy on the recursion's critical path
+    double Pn[NX * NX];
 #pragma unroll
     for (int j = 0; j < NX; ++j)
 #pragma unroll
-        for (int i = 0; i < NX; ++i) P(N, i, j) = v.Q(N, i, j);
+        for (int i = 0; i < NX; ++i) {
+            Pn[j * NX + i] = v.Q(N, i, j);
+            P(N, i, j) = Pn[j * NX + i];
+        }
 #pragma unroll 1
     for (int k = N - 1; k >= 0; --k) {
-        double Pn[NX * NX], ju[NX];
+        double ju[NX];
 #pragma unroll
-        for (int j = 0; j < NX; ++j) {
-            ju[j] = v.Ju(k, j);
-#pragma unroll
-            for (int i = 0; i < NX; ++i) Pn[j * NX + i] = P(k + 1, i, j);
-        }
+        for (int j = 0; j < NX; ++j) ju[j] = v.Ju(k, j);
         double PJu[NX];
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
@@ -513,7 +516,10 @@ __device__ __noinline__ bool rfactor(const QpView<NX, W>& v) {
                 w[L.FK + k * NX + j] = K[j];
                 w[L.FG + k * NX + j] = G[j];
 #pragma unroll
-                for (int i = 0; i < NX; ++i) P(k, i, j) = Pk[j * NX + i];
+                for (int i = 0; i < NX; ++i) {
+                    P(k, i, j) = Pk[j * NX + i];
+                    Pn[j * NX + i] = Pk[j * NX + i];
+                }
             }
         }
     }
@@ -530,8 +536,12 @@ __device__ __noinline__ void rsolve(const QpView<NX, W>& v) {
     const int N = o.N;
     auto P = [&](int k, int i, int j) -> double { return w[L.FP + ((int64_t)k * NX + j) * NX + i]; };
     auto bh = [&](int k, int i) -> double { return -w[L.RD + k * NX + i]; };
+    double pvn[NX];  // p_{k+1}, carried in registers (see rfactor)
 #pragma unroll
-    for (int i = 0; i < NX; ++i) w[L.PV + N * NX + i] = w[L.RS + L.xo(N) + i];
+    for (int i = 0; i < NX; ++i) {
+        pvn[i] = w[L.RS + L.xo(N) + i];
+        w[L.PV + N * NX + i] = pvn[i];
+    }
 #pragma unroll 1
     for (int k = N - 1; k >= 0; --k) {
         double t[NX];
@@ -540,7 +550,7 @@ __device__ __noinline__ void rsolve(const QpView<NX, W>& v) {
             double s = 0.0;
 #pragma unroll
             for (int j = 0; j < NX; ++j) s += P(k + 1, i, j) * bh(k, j);
-            t[i] = 1.0 * s + 1.0 * w[L.PV + (k + 1) * NX + i];
+            t[i] = 1.0 * s + 1.0 * pvn[i];
         }
         double hv;
         {
@@ -563,6 +573,7 @@ __device__ __noinline__ void rsolve(const QpView<NX, W>& v) {
                 double p = 1.0 * s + 1.0 * w[L.RS + L.xo(k) + i];
                 p = 1.0 * (0.0 + w[L.FG + k * NX + i] * dff) + 1.0 * p;
                 w[L.PV + k * NX + i] = p;
+                pvn[i] = p;
             }
         }
     }

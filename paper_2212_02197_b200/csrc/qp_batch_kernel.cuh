@@ -150,14 +150,19 @@ __device__ void chol_solve(const Ctx& c, int k, double* b) {
 /// riccati_factor (qp.cpp:73-110); barrier = nullptr-equivalent when !bar.
 __device__ bool rfactor(const Ctx& c, bool bar) {
     const int N = c.N, nx = c.nx, nu = c.nu;
+    // P_{k+1} carried from stage to stage (no store-to-load round trip)
+    double pn[QX * QX];
     for (int j = 0; j < nx; ++j)
-        for (int i = 0; i < nx; ++i) c.val(N, i, j) = c.in.Q(N, i, j);
+        for (int i = 0; i < nx; ++i) {
+            pn[j * nx + i] = c.in.Q(N, i, j);
+            c.val(N, i, j) = pn[j * nx + i];
+        }
     for (int k = N - 1; k >= 0; --k) {
         double pju[QX * QU], h[QU * QU];
         for (int j = 0; j < nu; ++j)  // pju = P_{k+1} Ju
             for (int i = 0; i < nx; ++i) {
                 double s = 0.0;
-                for (int l = 0; l < nx; ++l) s += c.val(k + 1, i, l) * c.in.Ju(k, l, j);
+                for (int l = 0; l < nx; ++l) s += pn[l * nx + i] * c.in.Ju(k, l, j);
                 pju[j * nx + i] = 1.0 * s + 0.0;
             }
         for (int j = 0; j < nu; ++j)  // h = Ju' pju
@@ -182,7 +187,7 @@ __device__ bool rfactor(const Ctx& c, bool bar) {
             for (int j = 0; j < nx; ++j)  // pjx = P_{k+1} Jx
                 for (int i = 0; i < nx; ++i) {
                     double s = 0.0;
-                    for (int l = 0; l < nx; ++l) s += c.val(k + 1, i, l) * c.in.Jx(k, l, j);
+                    for (int l = 0; l < nx; ++l) s += pn[l * nx + i] * c.in.Jx(k, l, j);
                     pjx[j * nx + i] = 1.0 * s + 0.0;
                 }
             for (int j = 0; j < nx; ++j)  // g = Ju' pjx + M'
@@ -220,7 +225,10 @@ __device__ bool rfactor(const Ctx& c, bool bar) {
                     p[r * nx + cc] = v;
                 }
             for (int j = 0; j < nx; ++j) {
-                for (int i = 0; i < nx; ++i) c.val(k, i, j) = p[j * nx + i];
+                for (int i = 0; i < nx; ++i) {
+                    c.val(k, i, j) = p[j * nx + i];
+                    pn[j * nx + i] = p[j * nx + i];
+                }
                 for (int i = 0; i < nu; ++i) c.gmat(k, i, j) = g[j * nu + i];
             }
         }
@@ -238,13 +246,17 @@ __device__ void rsolve(const Ctx& c, int64_t DX, int64_t DM) {
     auto qh = [&](int k, int i) -> double { return RHS_QP ? w[c.L.RS + c.xo(k) + i] : c.in.q(k, i); };
     auto bh = [&](int k, int i) -> double { return RHS_QP ? -w[c.L.RD + k * nx + i] : c.in.b(k, i); };
     auto rh = [&](int k, int i) -> double { return RHS_QP ? w[c.L.RH + k * nu + i] : c.in.r(k, i); };
-    for (int i = 0; i < nx; ++i) w[c.L.PV + N * nx + i] = qh(N, i);
+    double pvn[QX];  // p_{k+1} carried from stage to stage
+    for (int i = 0; i < nx; ++i) {
+        pvn[i] = qh(N, i);
+        w[c.L.PV + N * nx + i] = pvn[i];
+    }
     for (int k = N - 1; k >= 0; --k) {
         double tmp[QX], h[QU];
         for (int i = 0; i < nx; ++i) {
             double s = 0.0;
             for (int j = 0; j < nx; ++j) s += c.val(k + 1, i, j) * bh(k, j);
-            tmp[i] = 1.0 * s + 1.0 * w[c.L.PV + (k + 1) * nx + i];
+            tmp[i] = 1.0 * s + 1.0 * pvn[i];
         }
         for (int i = 0; i < nu; ++i) {
             double s = 0.0;
@@ -262,6 +274,7 @@ __device__ void rsolve(const Ctx& c, int64_t DX, int64_t DM) {
                 for (int j = 0; j < nu; ++j) s2 += c.gmat(k, j, i) * w[c.L.DFF + k * nu + j];
                 p = 1.0 * s2 + 1.0 * p;
                 w[c.L.PV + k * nx + i] = p;
+                pvn[i] = p;
             }
         }
     }
