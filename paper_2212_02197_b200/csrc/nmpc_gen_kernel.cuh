@@ -30,6 +30,7 @@
 // semantics; ordered sums stay serial.
 #pragma once
 
+#include "certified_math.cuh"
 #include "device_common.cuh"
 
 namespace nmpcmc_dev {
@@ -37,12 +38,20 @@ namespace gen {
 
 enum : int { G_OK = 0, G_NPD = ST_NPD, G_NONFINITE = ST_NONFINITE, G_DOMAIN = ST_DOMAIN };
 
-/// Per-thread view of the SoA workspace.
-struct Ws {
+/// View of one sample's workspace. K3g (W = 1): SoA across slots, element e
+/// at p[e * T]; K3w (W = 32): one contiguous slab, element e at p[e] -- the
+/// stride is a compile-time 1 and offsets are 32-bit, so an access is one
+/// integer add instead of a 64-bit multiply chain.
+template <int W>
+struct WsT {
     double* p;
     int64_t T;
-    __device__ __forceinline__ double& operator[](int64_t e) const { return p[e * T]; }
+    __device__ __forceinline__ double& operator[](int64_t e) const {
+        if (W == 1) return p[e * T];
+        return p[(int)e];
+    }
 };
+using Ws = WsT<1>;
 
 /// Lane helpers: W = 1 (thread per sample) or 32 (warp per sample).
 constexpr unsigned kMask = 0xffffffffu;
@@ -85,13 +94,13 @@ struct Layout {
     static constexpr int W = 1 + NX;  // stride of xi (n_u + n_x)
     static constexpr int B = (NX + 1) * (NX + 1);
     int N, L, NN;
-    int64_t XI[2], GF[2], G[2], FX[2], FU[2], BB[2];
-    int64_t LAM, PL, PU, QDXI, QMU, QNL, QNU, SL, SU, RS, RD, RL, RU, CL, CU, DSL, DSU, DNL, DNU, BAR, DXI,
-        DMU, RH, FP, FLL, FK, FG, PV, DFF, WB, SIG, HO, HN, LXI, LLAM, LPL, LPU, SP, US, total;
+    int XI[2], GF[2], G[2], FX[2], FU[2], BB[2];
+    int LAM, PL, PU, QDXI, QMU, QNL, QNU, SL, SU, RS, RD, RL, RU, CL, CU, DSL, DSU, DNL, DNU, BAR, DXI,
+        DMU, RH, FP, FLL, FLY, FK, FG, PV, DFF, WB, SIG, HO, HN, LXI, LLAM, LPL, LPU, SP, US, total;
     __host__ __device__ explicit Layout(int n) : N(n), L(n * W), NN(n * NX) {
-        int64_t o = 0;
-        auto take = [&](int64_t len) {
-            const int64_t at = o;
+        int o = 0;
+        auto take = [&](int len) {
+            const int at = o;
             o += len;
             return at;
         };
@@ -99,7 +108,7 @@ struct Layout {
             XI[s] = take(L);
             GF[s] = take(L);
             G[s] = take(NN);
-            FX[s] = take((int64_t)NN * NX);
+            FX[s] = take(NN * NX);
             FU[s] = take(NN);
             BB[s] = take(NN);
         }
@@ -108,9 +117,9 @@ struct Layout {
         SL = take(N), SU = take(N), RS = take(L), RD = take(NN), RL = take(N), RU = take(N);
         CL = take(N), CU = take(N), DSL = take(N), DSU = take(N), DNL = take(N), DNU = take(N);
         BAR = take(N), DXI = take(L), DMU = take(NN), RH = take(N);
-        FP = take((int64_t)(N + 1) * NX * NX), FLL = take(N), FK = take(NN), FG = take(NN);
-        PV = take((int64_t)(N + 1) * NX), DFF = take(N);
-        WB = take((int64_t)(N + 1) * B);
+        FP = take((N + 1) * NX * NX), FLL = take(N), FLY = take(N), FK = take(NN), FG = take(NN);
+        PV = take((N + 1) * NX), DFF = take(N);
+        WB = take((N + 1) * B);
         SIG = take(NN), HO = take(L), HN = take(L);
         LXI = take(L), LLAM = take(NN), LPL = take(N), LPU = take(N);
         SP = take(N), US = take(N);
@@ -287,7 +296,7 @@ template <int NX, int W>
 struct Ocp {
     Model<NX> m;
     Layout<NX> lay;
-    Ws ws;
+    WsT<W> ws;
     int N, Nc;
     double Ts, h, umin, umax, Qz, invV;
     double x0[NX];
@@ -299,7 +308,7 @@ template <int NX, int W>
 __device__ __noinline__ double objective(const Ocp<NX, W>& o, int s, bool grad) {
     // serial on every lane (phi is an ordered sum); the gradient is stored,
     // not accumulated: each slot is 0.0 + 2 Ts g once (ocp.cpp:80-97)
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
     double phi = 0.0;
 #pragma unroll 1
@@ -326,7 +335,7 @@ template <int NX, int W>
 __device__ __noinline__ int constraints(const Ocp<NX, W>& o, int s) {
     // stages are independent (multiple shooting): lane-parallel; the status
     // is the one of the lowest failing stage, as the sequential loop returns
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
     int bad_k = 0x7fffffff, bad_st = G_OK, shot = 0;
 #pragma unroll 1
@@ -362,7 +371,7 @@ __device__ __noinline__ int constraints(const Ocp<NX, W>& o, int s) {
 /// xi_from_inputs (ocp.cpp:137-154): u from US, result into XI[s].
 template <int NX, int W>
 __device__ __noinline__ int xi_from_u(const Ocp<NX, W>& o, int s) {
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
     double xk[NX];
 #pragma unroll
@@ -399,14 +408,14 @@ struct QpView {
     int s;  // evaluation set of the current iterate
     __device__ double Wb(int k, int i, int j) const {
         const int ld = k == 0 ? 1 : (k < o->N ? NX + 1 : NX);
-        return o->ws[o->lay.WB + (int64_t)k * Layout<NX>::B + j * ld + i];
+        return o->ws[o->lay.WB + k * Layout<NX>::B + j * ld + i];
     }
     __device__ double R(int k) const { return k == 0 ? Wb(0, 0, 0) : Wb(k, NX, NX); }
     __device__ double Q(int k, int i, int j) const { return Wb(k, i, j); }
     __device__ double M(int k, int i) const { return Wb(k, i, NX); }
     __device__ double q(int k, int i) const { return o->ws[o->lay.GF[s] + o->lay.xo(k) + i]; }
     __device__ double r(int k) const { return o->ws[o->lay.GF[s] + o->lay.uo(k)]; }
-    __device__ double Jx(int k, int i, int j) const { return o->ws[o->lay.FX[s] + ((int64_t)k * NX + j) * NX + i]; }
+    __device__ double Jx(int k, int i, int j) const { return o->ws[o->lay.FX[s] + (k * NX + j) * NX + i]; }
     __device__ double Ju(int k, int i) const { return o->ws[o->lay.FU[s] + k * NX + i]; }
     __device__ double b(int k, int i) const { return o->ws[o->lay.BB[s] + k * NX + i]; }
     __device__ double u(int k) const { return o->ws[o->lay.XI[s] + o->lay.uo(k)]; }
@@ -416,13 +425,13 @@ struct QpView {
 
 /// riccati_factor (qp.cpp:73-110) with barrier diagonal BAR. Returns true on
 /// NotPositiveDefinite.
-template <int NX, int W>
-__device__ __noinline__ bool rfactor(const QpView<NX, W>& v) {
+template <int NX, int W, bool FAST>
+__device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
     const Ocp<NX, W>& o = *v.o;
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
     const int N = o.N;
-    auto P = [&](int k, int i, int j) -> double& { return w[L.FP + ((int64_t)k * NX + j) * NX + i]; };
+    auto P = [&](int k, int i, int j) -> double& { return w[L.FP + (k * NX + j) * NX + i]; };
     // P_{k+1} is carried in registers from one stage to the next: reloading
     // what the previous stage just stored would put a store-to-load round trip
     // through the cache hierarchy on the recursion's critical path
@@ -457,8 +466,16 @@ __device__ __noinline__ bool rfactor(const QpView<NX, W>& v) {
         H += v.R(k);
         H += w[L.BAR + k];
         if (H <= 0.0 || !dfinite(H)) return true;  // cholesky_factor (linalg.cpp:69-103)
-        const double l = sqrt(H);
+        double l, y;
+        if (FAST) {
+            fast_sqrt(H, l, y);
+            *cert &= cert_sqrt_bf(H, l);
+        } else {
+            l = sqrt(H);
+            y = 1.0 / l;  // seed of rsolve's certified division
+        }
         w[L.FLL + k] = l;
+        w[L.FLY + k] = y;
         if (k >= 1) {
             double PJx[NX * NX], G[NX], K[NX];
 #pragma unroll
@@ -481,8 +498,14 @@ __device__ __noinline__ bool rfactor(const QpView<NX, W>& v) {
             for (int j = 0; j < NX; ++j) G[j] += v.M(k, j);
 #pragma unroll
             for (int j = 0; j < NX; ++j) {  // cholesky_solve of the 1x1 factor, then negate
-                double t = G[j] / l;
-                t = t / l;
+                double t;
+                if (FAST) {
+                    t = cdiv_seed(G[j], l, y, *cert);
+                    t = cdiv_seed(t, l, y, *cert);
+                } else {
+                    t = G[j] / l;
+                    t = t / l;
+                }
                 K[j] = -t;
             }
             double Pk[NX * NX];
@@ -525,16 +548,26 @@ __device__ __noinline__ bool rfactor(const QpView<NX, W>& v) {
     }
     return false;
 }
+/// riccati_factor with the certified fast sqrt/division; any uncertified
+/// stage (or a fast NotPositiveDefinite) replays the sweep with IEEE ops.
+template <int NX, int W>
+__device__ __forceinline__ bool rfactor(const QpView<NX, W>& v) {
+    bool cert = true;
+    bool npd = rfactor_t<NX, W, true>(v, &cert);
+    if (npd || !cert) npd = rfactor_t<NX, W, false>(v, nullptr);
+    return npd;
+}
 
 /// riccati_solve_vectors (qp.cpp:116-155) for the condensed right-hand side
 /// rh = RH, qhat_k = rs(x_k), bhat_k = -rd_k; step into DXI, DMU.
-template <int NX, int W>
-__device__ __noinline__ void rsolve(const QpView<NX, W>& v) {
+template <int NX, int W, bool FAST>
+__device__ __noinline__ bool rsolve_t(const QpView<NX, W>& v) {
+    bool cert = true;
     const Ocp<NX, W>& o = *v.o;
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
     const int N = o.N;
-    auto P = [&](int k, int i, int j) -> double { return w[L.FP + ((int64_t)k * NX + j) * NX + i]; };
+    auto P = [&](int k, int i, int j) -> double { return w[L.FP + (k * NX + j) * NX + i]; };
     auto bh = [&](int k, int i) -> double { return -w[L.RD + k * NX + i]; };
     double pvn[NX];  // p_{k+1}, carried in registers (see rfactor)
 #pragma unroll
@@ -560,8 +593,14 @@ __device__ __noinline__ void rsolve(const QpView<NX, W>& v) {
             hv = 1.0 * s + 1.0 * w[L.RH + k];
         }
         const double l = w[L.FLL + k];
-        hv = hv / l;
-        hv = hv / l;
+        if (FAST) {
+            const double y = w[L.FLY + k];
+            hv = cdiv_seed(hv, l, y, cert);
+            hv = cdiv_seed(hv, l, y, cert);
+        } else {
+            hv = hv / l;
+            hv = hv / l;
+        }
         const double dff = -hv;
         w[L.DFF + k] = dff;
         if (k >= 1) {
@@ -618,6 +657,13 @@ __device__ __noinline__ void rsolve(const QpView<NX, W>& v) {
             w[L.DMU + k * NX + i] = -mv;
         }
     }
+    return cert;
+}
+/// riccati_solve_vectors with the certified fast division (replayed with
+/// IEEE ops if any quotient is not certified).
+template <int NX, int W>
+__device__ __forceinline__ void rsolve(const QpView<NX, W>& v) {
+    if (!rsolve_t<NX, W, true>(v)) rsolve_t<NX, W, false>(v);
 }
 
 enum : int { QP_OPTIMAL = 0, QP_MAXITER = 1, QP_FAILED = 2, QP_DOMAIN = 3 };
@@ -626,7 +672,7 @@ enum : int { QP_OPTIMAL = 0, QP_MAXITER = 1, QP_FAILED = 2, QP_DOMAIN = 3 };
 template <int NX, int W>
 __device__ __noinline__ void qp_resid(const QpView<NX, W>& v) {
     const Ocp<NX, W>& o = *v.o;
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
     const int N = o.N;
     auto dxi = [&](int e) -> double { return w[L.QDXI + e]; };
@@ -702,7 +748,7 @@ __device__ __noinline__ void qp_resid(const QpView<NX, W>& v) {
 template <int NX, int W>
 __device__ __forceinline__ void qp_csolve(const QpView<NX, W>& v) {
     const Ocp<NX, W>& o = *v.o;
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k < o.N; k += W) {
@@ -719,7 +765,7 @@ __device__ __forceinline__ void qp_csolve(const QpView<NX, W>& v) {
 template <int NX, int W>
 __device__ __forceinline__ void qp_expand(const QpView<NX, W>& v) {
     const Ocp<NX, W>& o = *v.o;
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k < o.N; k += W) {
@@ -738,7 +784,7 @@ __device__ __forceinline__ void qp_expand(const QpView<NX, W>& v) {
 template <int NX, int W>
 __device__ __forceinline__ double qp_step(const QpView<NX, W>& v, double frac) {
     const Ocp<NX, W>& o = *v.o;
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
     double a = 1.0;
     auto cap = [&](double val, double dir) {
@@ -759,7 +805,7 @@ __device__ __forceinline__ double inf_fold(double m, double x) { return smax(m, 
 template <int NX, int W>
 __device__ __noinline__ int solve_qp(const QpView<NX, W>& v, double tol, int max_iter) {
     const Ocp<NX, W>& o = *v.o;
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
     const int N = o.N, lane = Lanes<W>::lane();
     int m = 0;
@@ -910,11 +956,11 @@ __device__ __noinline__ int solve_qp(const QpView<NX, W>& v, double tol, int max
 /// h += J_g' lam (add_constraint_term, sqp.cpp:102-116) on the blocks of
 /// set s; h at element offset H.
 template <int NX, int W>
-__device__ void add_jt(const Ocp<NX, W>& o, int s, int64_t LAMo, int64_t H) {
+__device__ void add_jt(const Ocp<NX, W>& o, int s, int LAMo, int H) {
     // lane-parallel by slot ownership: unit k owns u_k and x_{k+1}; per slot
     // the reference's order is kept: x_{k+1} gets + lam_k (iteration k), then
     // - Fx_{k+1}' lam_{k+1} term by term (iteration k+1)
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k < o.N; k += W) {
@@ -927,7 +973,7 @@ __device__ void add_jt(const Ocp<NX, W>& o, int s, int64_t LAMo, int64_t H) {
             if (kn < o.N) {
 #pragma unroll
                 for (int j = 0; j < NX; ++j)
-                    h -= w[L.FX[s] + ((int64_t)kn * NX + i) * NX + j] * w[LAMo + kn * NX + j];
+                    h -= w[L.FX[s] + (kn * NX + i) * NX + j] * w[LAMo + kn * NX + j];
             }
             w[H + L.xo(kn) + i] = h;
         }
@@ -938,9 +984,9 @@ __device__ void add_jt(const Ocp<NX, W>& o, int s, int64_t LAMo, int64_t H) {
 /// lagrangian_gradient (sqp.cpp:118-128) into HO for duals (LAMo, PLo, PUo),
 /// then check_convergence (sqp.cpp:86-96).
 template <int NX, int W>
-__device__ __noinline__ bool kkt_ok(const Ocp<NX, W>& o, int s, int64_t LAMo, int64_t PLo, int64_t PUo, int m,
+__device__ __noinline__ bool kkt_ok(const Ocp<NX, W>& o, int s, int LAMo, int PLo, int PUo, int m,
                                     double eps) {
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
     const int lane = Lanes<W>::lane();
     for (int e = lane; e < L.L; e += W) w[L.HO + e] = w[L.GF[s] + e];
@@ -970,13 +1016,13 @@ __device__ __noinline__ bool kkt_ok(const Ocp<NX, W>& o, int s, int64_t LAMo, in
 /// reset_blocks (sqp.cpp:173-178): identities of size 1, nx+1, ..., nx.
 template <int NX, int W>
 __device__ void identity_blocks(const Ocp<NX, W>& o) {
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k <= o.N; k += W) {
         const int n = k == 0 ? 1 : (k < o.N ? NX + 1 : NX);
         for (int j = 0; j < n; ++j)
-            for (int i = 0; i < n; ++i) w[L.WB + (int64_t)k * Layout<NX>::B + j * n + i] = (i == j) ? 1.0 : 0.0;
+            for (int i = 0; i < n; ++i) w[L.WB + k * Layout<NX>::B + j * n + i] = (i == j) ? 1.0 : 0.0;
     }
     Lanes<W>::sync();
 }
@@ -985,8 +1031,8 @@ __device__ void identity_blocks(const Ocp<NX, W>& o) {
 /// Returns true on NotPositiveDefinite (the Cholesky audit).
 template <int NX, int W>
 __device__ bool bfgs_block(const Ocp<NX, W>& o, int k, int n, const double* s, const double* y) {
-    const Ws& w = o.ws;
-    const int64_t base = o.lay.WB + (int64_t)k * Layout<NX>::B;
+    const WsT<W>& w = o.ws;
+    const int base = o.lay.WB + k * Layout<NX>::B;
     auto Wm = [&](int i, int j) -> double& { return w[base + j * n + i]; };
     double Ws_[NX + 1];
     for (int i = 0; i < n; ++i) {
@@ -1041,7 +1087,7 @@ struct SqpOut {
 /// On return the iterate is in XI[*cur].
 template <int NX, int W>
 __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_options& op, int* cur) {
-    const Ws& w = o.ws;
+    const WsT<W>& w = o.ws;
     const Layout<NX>& L = o.lay;
     const int N = o.N, lane = Lanes<W>::lane();
     const int m = N * NX + (dfinite(o.umin) ? N : 0) + (dfinite(o.umax) ? N : 0);
@@ -1328,7 +1374,7 @@ __device__ __noinline__ bool ekf_update(const Model<NX>& m, double* x, double* P
 /// The NMPC branch of run_closed_loop (montecarlo.cpp:80-157) for one sample
 /// with a controller model of NX states and a truth plant of TX states.
 template <int TX, int NX, int W>
-__device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar, const Ws& ws,
+__device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar, const WsT<W>& ws,
                                          nmpcmc_sim_record* rec, nmpcmc_work_counters* cntp, double* traj) {
     const Cstr p = sample_truth(sc, sim_index);
     NormalStream rng;
@@ -1545,7 +1591,7 @@ __global__ void __launch_bounds__(32) nmpc_genw_kernel(const __grid_constant__ n
                                                        int64_t n_sims, int nbar, nmpcmc_sim_record* records,
                                                        nmpcmc_work_counters* counters, double* traj, int traj_rows,
                                                        double* ws_all, int64_t slab, unsigned long long* next) {
-    const Ws ws{ws_all + (int64_t)blockIdx.x * slab, 1};
+    const WsT<32> ws{ws_all + (int64_t)blockIdx.x * slab, 1};
 #pragma unroll 1
     for (;;) {
         unsigned long long i = 0;
