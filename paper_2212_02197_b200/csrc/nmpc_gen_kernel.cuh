@@ -428,10 +428,24 @@ struct QpView {
 template <int NX, int W, bool FAST>
 __device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
     const Ocp<NX, W>& o = *v.o;
-    const WsT<W>& w = o.ws;
+    const WsT<W> w = o.ws;  // by value: base/stride and the offsets below live in registers
     const Layout<NX>& L = o.lay;
+    const int oBAR = L.BAR, oFG = L.FG, oFK = L.FK, oFLL = L.FLL, oFLY = L.FLY, oFP = L.FP;
+    const int oFXs = L.FX[v.s], oFUs = L.FU[v.s], oWB = L.WB, oXIs = L.XI[v.s], oGFs = L.GF[v.s];
+    auto Jx_ = [&](int k, int i, int j) -> double { return w[oFXs + (k * NX + j) * NX + i]; };
+    auto Ju_ = [&](int k, int i) -> double { return w[oFUs + k * NX + i]; };
+    const int nN = o.N;
+    auto Wb_ = [&](int k, int i, int j) -> double {
+        const int ld = k == 0 ? 1 : (k < nN ? NX + 1 : NX);
+        return w[oWB + k * Layout<NX>::B + j * ld + i];
+    };
+    auto R_ = [&](int k) -> double { return k == 0 ? Wb_(0, 0, 0) : Wb_(k, NX, NX); };
+    auto Q_ = [&](int k, int i, int j) -> double { return Wb_(k, i, j); };
+    auto M_ = [&](int k, int i) -> double { return Wb_(k, i, NX); };
+    (void)oXIs, (void)oGFs;
+
     const int N = o.N;
-    auto P = [&](int k, int i, int j) -> double& { return w[L.FP + (k * NX + j) * NX + i]; };
+    auto P = [&](int k, int i, int j) -> double& { return w[oFP + (k * NX + j) * NX + i]; };
     // P_{k+1} is carried in registers from one stage to the next: reloading
     // what the previous stage just stored would put a store-to-load round trip
     // through the cache hierarchy on the recursion's critical path
@@ -440,14 +454,14 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
     for (int j = 0; j < NX; ++j)
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
-            Pn[j * NX + i] = v.Q(N, i, j);
+            Pn[j * NX + i] = Q_(N, i, j);
             P(N, i, j) = Pn[j * NX + i];
         }
 #pragma unroll 1
     for (int k = N - 1; k >= 0; --k) {
         double ju[NX];
 #pragma unroll
-        for (int j = 0; j < NX; ++j) ju[j] = v.Ju(k, j);
+        for (int j = 0; j < NX; ++j) ju[j] = Ju_(k, j);
         double PJu[NX];
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
@@ -463,8 +477,8 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
             for (int l = 0; l < NX; ++l) s += ju[l] * PJu[l];
             H = 1.0 * s + 0.0;
         }
-        H += v.R(k);
-        H += w[L.BAR + k];
+        H += R_(k);
+        H += w[oBAR + k];
         if (H <= 0.0 || !dfinite(H)) return true;  // cholesky_factor (linalg.cpp:69-103)
         double l, y;
         if (FAST) {
@@ -474,8 +488,8 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
             l = sqrt(H);
             y = 1.0 / l;  // seed of rsolve's certified division
         }
-        w[L.FLL + k] = l;
-        w[L.FLY + k] = y;
+        w[oFLL + k] = l;
+        w[oFLY + k] = y;
         if (k >= 1) {
             double PJx[NX * NX], G[NX], K[NX];
 #pragma unroll
@@ -484,7 +498,7 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
                 for (int i = 0; i < NX; ++i) {
                     double s = 0.0;
 #pragma unroll
-                    for (int m = 0; m < NX; ++m) s += Pn[m * NX + i] * v.Jx(k, m, j);
+                    for (int m = 0; m < NX; ++m) s += Pn[m * NX + i] * Jx_(k, m, j);
                     PJx[j * NX + i] = 1.0 * s + 0.0;
                 }
 #pragma unroll
@@ -495,7 +509,7 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
                 G[j] = 1.0 * s + 0.0;
             }
 #pragma unroll
-            for (int j = 0; j < NX; ++j) G[j] += v.M(k, j);
+            for (int j = 0; j < NX; ++j) G[j] += M_(k, j);
 #pragma unroll
             for (int j = 0; j < NX; ++j) {  // cholesky_solve of the 1x1 factor, then negate
                 double t;
@@ -515,13 +529,13 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
                 for (int i = 0; i < NX; ++i) {
                     double s = 0.0;
 #pragma unroll
-                    for (int m = 0; m < NX; ++m) s += v.Jx(k, m, i) * PJx[j * NX + m];
+                    for (int m = 0; m < NX; ++m) s += Jx_(k, m, i) * PJx[j * NX + m];
                     Pk[j * NX + i] = 1.0 * s + 0.0;
                 }
 #pragma unroll
             for (int j = 0; j < NX; ++j)
 #pragma unroll
-                for (int i = 0; i < NX; ++i) Pk[j * NX + i] += v.Q(k, i, j);
+                for (int i = 0; i < NX; ++i) Pk[j * NX + i] += Q_(k, i, j);
 #pragma unroll
             for (int j = 0; j < NX; ++j)
 #pragma unroll
@@ -536,8 +550,8 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
                 }
 #pragma unroll
             for (int j = 0; j < NX; ++j) {
-                w[L.FK + k * NX + j] = K[j];
-                w[L.FG + k * NX + j] = G[j];
+                w[oFK + k * NX + j] = K[j];
+                w[oFG + k * NX + j] = G[j];
 #pragma unroll
                 for (int i = 0; i < NX; ++i) {
                     P(k, i, j) = Pk[j * NX + i];
@@ -564,16 +578,30 @@ template <int NX, int W, bool FAST>
 __device__ __noinline__ bool rsolve_t(const QpView<NX, W>& v) {
     bool cert = true;
     const Ocp<NX, W>& o = *v.o;
-    const WsT<W>& w = o.ws;
+    const WsT<W> w = o.ws;  // by value: base/stride and the offsets below live in registers
     const Layout<NX>& L = o.lay;
+    const int oDFF = L.DFF, oDMU = L.DMU, oDXI = L.DXI, oFG = L.FG, oFK = L.FK, oFLL = L.FLL, oFLY = L.FLY, oFP = L.FP, oPV = L.PV, oRD = L.RD, oRH = L.RH, oRS = L.RS;
+    const int oFXs = L.FX[v.s], oFUs = L.FU[v.s], oWB = L.WB, oXIs = L.XI[v.s], oGFs = L.GF[v.s];
+    auto Jx_ = [&](int k, int i, int j) -> double { return w[oFXs + (k * NX + j) * NX + i]; };
+    auto Ju_ = [&](int k, int i) -> double { return w[oFUs + k * NX + i]; };
+    const int nN = o.N;
+    auto Wb_ = [&](int k, int i, int j) -> double {
+        const int ld = k == 0 ? 1 : (k < nN ? NX + 1 : NX);
+        return w[oWB + k * Layout<NX>::B + j * ld + i];
+    };
+    auto R_ = [&](int k) -> double { return k == 0 ? Wb_(0, 0, 0) : Wb_(k, NX, NX); };
+    auto Q_ = [&](int k, int i, int j) -> double { return Wb_(k, i, j); };
+    auto M_ = [&](int k, int i) -> double { return Wb_(k, i, NX); };
+    (void)oXIs, (void)oGFs;
+
     const int N = o.N;
-    auto P = [&](int k, int i, int j) -> double { return w[L.FP + (k * NX + j) * NX + i]; };
-    auto bh = [&](int k, int i) -> double { return -w[L.RD + k * NX + i]; };
+    auto P = [&](int k, int i, int j) -> double { return w[oFP + (k * NX + j) * NX + i]; };
+    auto bh = [&](int k, int i) -> double { return -w[oRD + k * NX + i]; };
     double pvn[NX];  // p_{k+1}, carried in registers (see rfactor)
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
-        pvn[i] = w[L.RS + L.xo(N) + i];
-        w[L.PV + N * NX + i] = pvn[i];
+        pvn[i] = w[oRS + L.xo(N) + i];
+        w[oPV + N * NX + i] = pvn[i];
     }
 #pragma unroll 1
     for (int k = N - 1; k >= 0; --k) {
@@ -589,12 +617,12 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W>& v) {
         {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < NX; ++j) s += v.Ju(k, j) * t[j];
-            hv = 1.0 * s + 1.0 * w[L.RH + k];
+            for (int j = 0; j < NX; ++j) s += Ju_(k, j) * t[j];
+            hv = 1.0 * s + 1.0 * w[oRH + k];
         }
-        const double l = w[L.FLL + k];
+        const double l = w[oFLL + k];
         if (FAST) {
-            const double y = w[L.FLY + k];
+            const double y = w[oFLY + k];
             hv = cdiv_seed(hv, l, y, cert);
             hv = cdiv_seed(hv, l, y, cert);
         } else {
@@ -602,16 +630,16 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W>& v) {
             hv = hv / l;
         }
         const double dff = -hv;
-        w[L.DFF + k] = dff;
+        w[oDFF + k] = dff;
         if (k >= 1) {
 #pragma unroll
             for (int i = 0; i < NX; ++i) {
                 double s = 0.0;
 #pragma unroll
-                for (int j = 0; j < NX; ++j) s += v.Jx(k, j, i) * t[j];
-                double p = 1.0 * s + 1.0 * w[L.RS + L.xo(k) + i];
-                p = 1.0 * (0.0 + w[L.FG + k * NX + i] * dff) + 1.0 * p;
-                w[L.PV + k * NX + i] = p;
+                for (int j = 0; j < NX; ++j) s += Jx_(k, j, i) * t[j];
+                double p = 1.0 * s + 1.0 * w[oRS + L.xo(k) + i];
+                p = 1.0 * (0.0 + w[oFG + k * NX + i] * dff) + 1.0 * p;
+                w[oPV + k * NX + i] = p;
                 pvn[i] = p;
             }
         }
@@ -621,14 +649,14 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W>& v) {
     for (int i = 0; i < NX; ++i) dx[i] = 0.0;
 #pragma unroll 1
     for (int k = 0; k < N; ++k) {
-        double du = w[L.DFF + k];
+        double du = w[oDFF + k];
         if (k >= 1) {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < NX; ++j) s += w[L.FK + k * NX + j] * dx[j];
+            for (int j = 0; j < NX; ++j) s += w[oFK + k * NX + j] * dx[j];
             du = 1.0 * s + 1.0 * du;
         }
-        w[L.DXI + L.uo(k)] = du;
+        w[oDXI + L.uo(k)] = du;
         double dn[NX];
 #pragma unroll
         for (int i = 0; i < NX; ++i) dn[i] = bh(k, i);
@@ -637,24 +665,24 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W>& v) {
             for (int i = 0; i < NX; ++i) {
                 double s = 0.0;
 #pragma unroll
-                for (int j = 0; j < NX; ++j) s += v.Jx(k, i, j) * dx[j];
+                for (int j = 0; j < NX; ++j) s += Jx_(k, i, j) * dx[j];
                 dn[i] = 1.0 * s + 1.0 * dn[i];
             }
         }
 #pragma unroll
-        for (int i = 0; i < NX; ++i) dn[i] = 1.0 * (0.0 + v.Ju(k, i) * du) + 1.0 * dn[i];
+        for (int i = 0; i < NX; ++i) dn[i] = 1.0 * (0.0 + Ju_(k, i) * du) + 1.0 * dn[i];
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
             dx[i] = dn[i];
-            w[L.DXI + L.uo(k) + 1 + i] = dx[i];
+            w[oDXI + L.uo(k) + 1 + i] = dx[i];
         }
 #pragma unroll
         for (int i = 0; i < NX; ++i) {
             double s = 0.0;
 #pragma unroll
             for (int j = 0; j < NX; ++j) s += P(k + 1, i, j) * dx[j];
-            const double mv = 1.0 * s + 1.0 * w[L.PV + (k + 1) * NX + i];
-            w[L.DMU + k * NX + i] = -mv;
+            const double mv = 1.0 * s + 1.0 * w[oPV + (k + 1) * NX + i];
+            w[oDMU + k * NX + i] = -mv;
         }
     }
     return cert;
