@@ -308,8 +308,8 @@ template <int NX, int W>
 __device__ __noinline__ double objective(const Ocp<NX, W>& o, int s, bool grad) {
     // serial on every lane (phi is an ordered sum); the gradient is stored,
     // not accumulated: each slot is 0.0 + 2 Ts g once (ocp.cpp:80-97)
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
     double phi = 0.0;
 #pragma unroll 1
     for (int k = 1; k <= o.N; ++k) {
@@ -335,8 +335,8 @@ template <int NX, int W>
 __device__ __noinline__ int constraints(const Ocp<NX, W>& o, int s) {
     // stages are independent (multiple shooting): lane-parallel; the status
     // is the one of the lowest failing stage, as the sequential loop returns
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
     int bad_k = 0x7fffffff, bad_st = G_OK, shot = 0;
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k < o.N; k += W) {
@@ -371,8 +371,8 @@ __device__ __noinline__ int constraints(const Ocp<NX, W>& o, int s) {
 /// xi_from_inputs (ocp.cpp:137-154): u from US, result into XI[s].
 template <int NX, int W>
 __device__ __noinline__ int xi_from_u(const Ocp<NX, W>& o, int s) {
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
     double xk[NX];
 #pragma unroll
     for (int i = 0; i < NX; ++i) xk[i] = o.x0[i];
@@ -406,30 +406,37 @@ template <int NX, int W>
 struct QpView {
     const Ocp<NX, W>* o;
     int s;  // evaluation set of the current iterate
+    // cached by value, so the accessors need no reload through *o after stores
+    WsT<W> w;
+    int N, WB, GFs, FXs, FUs, BBs, XIs;
+    double umin, umax;
+    __device__ QpView(const Ocp<NX, W>* op, int set)
+        : o(op), s(set), w(op->ws), N(op->N), WB(op->lay.WB), GFs(op->lay.GF[set]), FXs(op->lay.FX[set]),
+          FUs(op->lay.FU[set]), BBs(op->lay.BB[set]), XIs(op->lay.XI[set]), umin(op->umin), umax(op->umax) {}
     __device__ double Wb(int k, int i, int j) const {
-        const int ld = k == 0 ? 1 : (k < o->N ? NX + 1 : NX);
-        return o->ws[o->lay.WB + k * Layout<NX>::B + j * ld + i];
+        const int ld = k == 0 ? 1 : (k < N ? NX + 1 : NX);
+        return w[WB + k * Layout<NX>::B + j * ld + i];
     }
     __device__ double R(int k) const { return k == 0 ? Wb(0, 0, 0) : Wb(k, NX, NX); }
     __device__ double Q(int k, int i, int j) const { return Wb(k, i, j); }
     __device__ double M(int k, int i) const { return Wb(k, i, NX); }
-    __device__ double q(int k, int i) const { return o->ws[o->lay.GF[s] + o->lay.xo(k) + i]; }
-    __device__ double r(int k) const { return o->ws[o->lay.GF[s] + o->lay.uo(k)]; }
-    __device__ double Jx(int k, int i, int j) const { return o->ws[o->lay.FX[s] + (k * NX + j) * NX + i]; }
-    __device__ double Ju(int k, int i) const { return o->ws[o->lay.FU[s] + k * NX + i]; }
-    __device__ double b(int k, int i) const { return o->ws[o->lay.BB[s] + k * NX + i]; }
-    __device__ double u(int k) const { return o->ws[o->lay.XI[s] + o->lay.uo(k)]; }
-    __device__ double lb(int k) const { return o->umin - u(k); }
-    __device__ double ub(int k) const { return o->umax - u(k); }
+    __device__ double q(int k, int i) const { return w[GFs + Layout<NX>::W * (k - 1) + 1 + i]; }
+    __device__ double r(int k) const { return w[GFs + Layout<NX>::W * k]; }
+    __device__ double Jx(int k, int i, int j) const { return w[FXs + (k * NX + j) * NX + i]; }
+    __device__ double Ju(int k, int i) const { return w[FUs + k * NX + i]; }
+    __device__ double b(int k, int i) const { return w[BBs + k * NX + i]; }
+    __device__ double u(int k) const { return w[XIs + Layout<NX>::W * k]; }
+    __device__ double lb(int k) const { return umin - u(k); }
+    __device__ double ub(int k) const { return umax - u(k); }
 };
 
 /// riccati_factor (qp.cpp:73-110) with barrier diagonal BAR. Returns true on
 /// NotPositiveDefinite.
 template <int NX, int W, bool FAST>
-__device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
+__device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
     const Ocp<NX, W>& o = *v.o;
     const WsT<W> w = o.ws;  // by value: base/stride and the offsets below live in registers
-    const Layout<NX>& L = o.lay;
+    const Layout<NX> L = o.lay;
     const int oBAR = L.BAR, oFG = L.FG, oFK = L.FK, oFLL = L.FLL, oFLY = L.FLY, oFP = L.FP;
     const int oFXs = L.FX[v.s], oFUs = L.FU[v.s], oWB = L.WB, oXIs = L.XI[v.s], oGFs = L.GF[v.s];
     auto Jx_ = [&](int k, int i, int j) -> double { return w[oFXs + (k * NX + j) * NX + i]; };
@@ -565,7 +572,7 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W>& v, bool* cert) {
 /// riccati_factor with the certified fast sqrt/division; any uncertified
 /// stage (or a fast NotPositiveDefinite) replays the sweep with IEEE ops.
 template <int NX, int W>
-__device__ __forceinline__ bool rfactor(const QpView<NX, W>& v) {
+__device__ __forceinline__ bool rfactor(const QpView<NX, W> v) {
     bool cert = true;
     bool npd = rfactor_t<NX, W, true>(v, &cert);
     if (npd || !cert) npd = rfactor_t<NX, W, false>(v, nullptr);
@@ -575,11 +582,11 @@ __device__ __forceinline__ bool rfactor(const QpView<NX, W>& v) {
 /// riccati_solve_vectors (qp.cpp:116-155) for the condensed right-hand side
 /// rh = RH, qhat_k = rs(x_k), bhat_k = -rd_k; step into DXI, DMU.
 template <int NX, int W, bool FAST>
-__device__ __noinline__ bool rsolve_t(const QpView<NX, W>& v) {
+__device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
     bool cert = true;
     const Ocp<NX, W>& o = *v.o;
     const WsT<W> w = o.ws;  // by value: base/stride and the offsets below live in registers
-    const Layout<NX>& L = o.lay;
+    const Layout<NX> L = o.lay;
     const int oDFF = L.DFF, oDMU = L.DMU, oDXI = L.DXI, oFG = L.FG, oFK = L.FK, oFLL = L.FLL, oFLY = L.FLY, oFP = L.FP, oPV = L.PV, oRD = L.RD, oRH = L.RH, oRS = L.RS;
     const int oFXs = L.FX[v.s], oFUs = L.FU[v.s], oWB = L.WB, oXIs = L.XI[v.s], oGFs = L.GF[v.s];
     auto Jx_ = [&](int k, int i, int j) -> double { return w[oFXs + (k * NX + j) * NX + i]; };
@@ -690,7 +697,7 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W>& v) {
 /// riccati_solve_vectors with the certified fast division (replayed with
 /// IEEE ops if any quotient is not certified).
 template <int NX, int W>
-__device__ __forceinline__ void rsolve(const QpView<NX, W>& v) {
+__device__ __forceinline__ void rsolve(const QpView<NX, W> v) {
     if (!rsolve_t<NX, W, true>(v)) rsolve_t<NX, W, false>(v);
 }
 
@@ -698,10 +705,10 @@ enum : int { QP_OPTIMAL = 0, QP_MAXITER = 1, QP_FAILED = 2, QP_DOMAIN = 3 };
 
 /// residuals (qp.cpp:237-284) into RS, RD, RL, RU.
 template <int NX, int W>
-__device__ __noinline__ void qp_resid(const QpView<NX, W>& v) {
+__device__ __noinline__ void qp_resid(const QpView<NX, W> v) {
     const Ocp<NX, W>& o = *v.o;
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
     const int N = o.N;
     auto dxi = [&](int e) -> double { return w[L.QDXI + e]; };
 #pragma unroll 1
@@ -774,10 +781,10 @@ __device__ __noinline__ void qp_resid(const QpView<NX, W>& v) {
 
 /// Condensed right-hand side (qp.cpp:288-305) into RH, then the vector solve.
 template <int NX, int W>
-__device__ __forceinline__ void qp_csolve(const QpView<NX, W>& v) {
+__device__ __forceinline__ void qp_csolve(const QpView<NX, W> v) {
     const Ocp<NX, W>& o = *v.o;
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k < o.N; k += W) {
         double x = w[L.RS + L.uo(k)];
@@ -791,10 +798,10 @@ __device__ __forceinline__ void qp_csolve(const QpView<NX, W>& v) {
 }
 /// expand (qp.cpp:308-317) of the step in DXI.
 template <int NX, int W>
-__device__ __forceinline__ void qp_expand(const QpView<NX, W>& v) {
+__device__ __forceinline__ void qp_expand(const QpView<NX, W> v) {
     const Ocp<NX, W>& o = *v.o;
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k < o.N; k += W) {
         const double dv = w[L.DXI + L.uo(k)];
@@ -810,10 +817,10 @@ __device__ __forceinline__ void qp_expand(const QpView<NX, W>& v) {
 }
 /// max_step (qp.cpp:321-337).
 template <int NX, int W>
-__device__ __forceinline__ double qp_step(const QpView<NX, W>& v, double frac) {
+__device__ __forceinline__ double qp_step(const QpView<NX, W> v, double frac) {
     const Ocp<NX, W>& o = *v.o;
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
     double a = 1.0;
     auto cap = [&](double val, double dir) {
         if (dir < 0.0) a = smin(a, -frac * val / dir);
@@ -831,10 +838,10 @@ __device__ __forceinline__ double inf_fold(double m, double x) { return smax(m, 
 /// solve_qp (qp.cpp:173-423): Mehrotra predictor-corrector interior point.
 /// Result in QDXI, QMU, QNL, QNU.
 template <int NX, int W>
-__device__ __noinline__ int solve_qp(const QpView<NX, W>& v, double tol, int max_iter) {
+__device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_iter) {
     const Ocp<NX, W>& o = *v.o;
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
     const int N = o.N, lane = Lanes<W>::lane();
     int m = 0;
     double scale = 1.0;  // data_scale: an order-independent max (NaN ignored)
@@ -988,8 +995,8 @@ __device__ void add_jt(const Ocp<NX, W>& o, int s, int LAMo, int H) {
     // lane-parallel by slot ownership: unit k owns u_k and x_{k+1}; per slot
     // the reference's order is kept: x_{k+1} gets + lam_k (iteration k), then
     // - Fx_{k+1}' lam_{k+1} term by term (iteration k+1)
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k < o.N; k += W) {
 #pragma unroll
@@ -1014,8 +1021,8 @@ __device__ void add_jt(const Ocp<NX, W>& o, int s, int LAMo, int H) {
 template <int NX, int W>
 __device__ __noinline__ bool kkt_ok(const Ocp<NX, W>& o, int s, int LAMo, int PLo, int PUo, int m,
                                     double eps) {
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
     const int lane = Lanes<W>::lane();
     for (int e = lane; e < L.L; e += W) w[L.HO + e] = w[L.GF[s] + e];
     Lanes<W>::sync();
@@ -1044,8 +1051,8 @@ __device__ __noinline__ bool kkt_ok(const Ocp<NX, W>& o, int s, int LAMo, int PL
 /// reset_blocks (sqp.cpp:173-178): identities of size 1, nx+1, ..., nx.
 template <int NX, int W>
 __device__ void identity_blocks(const Ocp<NX, W>& o) {
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k <= o.N; k += W) {
         const int n = k == 0 ? 1 : (k < o.N ? NX + 1 : NX);
@@ -1059,7 +1066,7 @@ __device__ void identity_blocks(const Ocp<NX, W>& o) {
 /// Returns true on NotPositiveDefinite (the Cholesky audit).
 template <int NX, int W>
 __device__ bool bfgs_block(const Ocp<NX, W>& o, int k, int n, const double* s, const double* y) {
-    const WsT<W>& w = o.ws;
+    const WsT<W> w = o.ws;
     const int base = o.lay.WB + k * Layout<NX>::B;
     auto Wm = [&](int i, int j) -> double& { return w[base + j * n + i]; };
     double Ws_[NX + 1];
@@ -1115,8 +1122,8 @@ struct SqpOut {
 /// On return the iterate is in XI[*cur].
 template <int NX, int W>
 __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_options& op, int* cur) {
-    const WsT<W>& w = o.ws;
-    const Layout<NX>& L = o.lay;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
     const int N = o.N, lane = Lanes<W>::lane();
     const int m = N * NX + (dfinite(o.umin) ? N : 0) + (dfinite(o.umax) ? N : 0);
     int s = 0;
@@ -1134,7 +1141,7 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_o
         if (kkt_ok<NX, W>(o, s, L.LAM, L.PL, L.PU, m, op.eps)) return SqpOut{true, G_OK};
         if (it >= op.max_iter) break;
         o.cnt->sqp_stage += N;
-        const QpView<NX, W> v{&o, s};
+        const QpView<NX, W> v(&o, s);
         int qs = solve_qp<NX, W>(v, op.qp_tol, op.qp_max_iter);
         o.cnt->qp += 1;
         if (qs == QP_DOMAIN) return SqpOut{false, G_DOMAIN};
@@ -1418,7 +1425,7 @@ __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim
     Ocp<NX, W> o{make_model<NX>(sc.ctrl), Layout<NX>(sc.N), ws, sc.N, sc.Nc, sc.horizon_Ts, sc.horizon_Ts / sc.Nc,
               sc.u_min, sc.u_max, sc.Qz, 0.0, {}, &cnt};
     o.invV = 1.0 / o.m.p.V;
-    const Layout<NX>& L = o.lay;
+    const Layout<NX> L = o.lay;
     const int N = o.N;
     // make_nmpc_state (controllers.cpp:25-48)
     double xhat[NX], Pf[NX * NX];
