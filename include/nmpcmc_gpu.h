@@ -240,6 +240,22 @@ int nmpcmc_gpu_libm(nmpcmc_gpu_ctx* ctx, int32_t fn, const double* x, int64_t n,
  * for the FP64 closed-loop kernels (use_fma=1: DFMA, 2 flops each; 0: DADD). */
 int nmpcmc_gpu_fp64_peak(nmpcmc_gpu_ctx* ctx, int use_fma, double* tflops_out);
 
+/* ---- Batched OCP service ---------------------
+ * sqp_solve (sqp.hpp:148-151, sqp.cpp:182-411) on the regulator OcpProblem
+ * (sqp.hpp:27-50) of the scenario's controller model (ctrl, ctrl_variant),
+ * horizon {N, horizon_Ts, Nc}, Qz, u_min/u_max, setpoint profile and
+ * SqpOptions, for `batch` instances: instance b starts at state x0[b*nx ..]
+ * (nx = 1 or 3 by ctrl_variant) at time t0[b] (setpoints at t0 + k Ts,
+ * k = 1..N). xi0 == NULL: cold start exactly as nmpc_step
+ * (controllers.cpp:166-185); else xi0[b*L ..] with zero duals. HOST buffers;
+ * L = N (1 + nx). Outputs per instance: xi[L], lambda[N nx], pi_l[N], pi_u[N]
+ * (SqpReport, sqp.hpp:79-90), converged, status (0, or NMPCMC_DOMAIN_ERROR if
+ * a DomainError escaped the solve). Bitwise the reference's results. */
+int nmpcmc_gpu_solve_ocp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, int64_t batch,
+                               const double* x0, const double* t0, const double* xi0, double* xi,
+                               double* lambda, double* pi_l, double* pi_u, int32_t* converged,
+                               int32_t* status);
+
 /* ---- Batched standalone stagewise QP ----------
  * solve_qp (qp.hpp:47-56, qp.cpp:173-423; mode 0) or riccati_factor_solve
  * (qp.hpp:42-45, qp.cpp:157-171; mode 1) for `batch` independent QPs of the

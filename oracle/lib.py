@@ -121,3 +121,21 @@ def solve_qp_batch(lib, packed, nx, nu, tol=1e-10, max_iter=50, riccati_only=Fal
                                   it.ctypes.data_as(C.POINTER(C.c_int32)))
     return sol, st, it
 
+
+def solve_ocp_batch(lib, sc, x0, t0, xi0=None):
+    """The reference's sqp_solve on the regulator OcpProblem per instance
+    (layout of nmpcmc_gpu_solve_ocp_batch): dict of arrays."""
+    x0 = np.ascontiguousarray(np.atleast_2d(x0), dtype=np.float64)
+    t0 = np.ascontiguousarray(t0, dtype=np.float64).reshape(-1)
+    B, nx, N = x0.shape[0], x0.shape[1], sc.N
+    L = N * (1 + nx)
+    out = dict(xi=np.zeros((B, L)), **{"lambda": np.zeros((B, N * nx))}, pi_l=np.zeros((B, N)),
+               pi_u=np.zeros((B, N)), converged=np.zeros(B, dtype=np.int32), status=np.zeros(B, dtype=np.int32))
+    P = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    xi0p = None if xi0 is None else P(np.ascontiguousarray(xi0, dtype=np.float64))
+    lib.nmpcmc_ref_solve_ocp_batch(C.byref(sc), C.c_int64(B), P(x0), P(t0), xi0p, P(out["xi"]), P(out["lambda"]),
+                                   P(out["pi_l"]), P(out["pi_u"]),
+                                   out["converged"].ctypes.data_as(C.POINTER(C.c_int32)),
+                                   out["status"].ctypes.data_as(C.POINTER(C.c_int32)))
+    return out
+

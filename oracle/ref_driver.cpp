@@ -10,6 +10,7 @@
 //   aggregate_stats  (montecarlo.cpp:172-211)  -> nmpcmc_ref_aggregate
 //   phi_histogram    (montecarlo.cpp:268-304)  -> nmpcmc_ref_histogram
 //   solve_qp / riccati_factor_solve (qp.cpp:157-423) -> nmpcmc_ref_solve_qp_batch
+//   sqp_solve on the regulator OcpProblem (sqp.cpp:182-411)  -> nmpcmc_ref_solve_ocp_batch
 // and, for unit-level pins, CounterRng / pi_step / nmpc_step.
 // Only tests/, __graft_entry__.smoke() and bench.py's CPU arm load it.
 #include <algorithm>
@@ -25,7 +26,9 @@
 #include "nmpcmc/cstr.hpp"
 #include "nmpcmc/errors.hpp"
 #include "nmpcmc/montecarlo.hpp"
+#include "nmpcmc/ocp.hpp"
 #include "nmpcmc/qp.hpp"
+#include "nmpcmc/sqp.hpp"
 #include "nmpcmc/rng.hpp"
 #include "nmpcmc_gpu.h"
 
@@ -343,6 +346,78 @@ int nmpcmc_ref_solve_qp_batch(const nmpcmc_qp_dims* d, std::int64_t batch, const
             status[b] = NMPCMC_QP_DOMAIN_ERROR;
         } catch (const NotPositiveDefinite&) {
             status[b] = NMPCMC_QP_NOT_POSITIVE_DEFINITE;
+        }
+    }
+    return 0;
+}
+
+/// The reference's sqp_solve on the regulator OcpProblem of the scenario's
+/// controller model for each (x0[b], t0[b]): NlpInstance as nmpc_step builds it
+/// (controllers.cpp:134-145) and its cold start (controllers.cpp:166-185) when
+/// xi0 is NULL, else the given iterate with zero duals. status[b]: 0, or
+/// NMPCMC_DOMAIN_ERROR if a DomainError escaped.
+int nmpcmc_ref_solve_ocp_batch(const nmpcmc_scenario* s, std::int64_t batch, const double* x0, const double* t0,
+                               const double* xi0_in, double* xi_out, double* lam_out, double* pil_out,
+                               double* piu_out, std::int32_t* converged, std::int32_t* status) {
+    const int nx = nx_of(s->ctrl_variant), N = s->N, L = N * (1 + nx);
+    SqpOptions opts;
+    opts.eps = s->sqp.eps;
+    opts.max_iter = s->sqp.max_iter;
+    opts.max_backtracks = s->sqp.max_backtracks;
+    opts.c1 = s->sqp.c1;
+    opts.backtrack_factor = s->sqp.backtrack_factor;
+    opts.qp_tol = s->sqp.qp_tol;
+    opts.qp_max_iter = s->sqp.qp_max_iter;
+    SetpointProfile prof;
+    for (int i = 0; i < s->n_setpoints; ++i) {
+        prof.times.push_back(s->sp_times[i]);
+        prof.values.push_back(Vec{s->sp_values[i]});
+    }
+    for (std::int64_t b = 0; b < batch; ++b) {
+        NlpInstance nlp;
+        nlp.horizon = Horizon{N, s->horizon_Ts, s->Nc};
+        nlp.model = make_cstr_model(to_params(s->ctrl), to_variant(s->ctrl_variant));
+        nlp.t0 = t0[b];
+        nlp.x0.assign(x0 + b * nx, x0 + (b + 1) * nx);
+        nlp.u_min = {s->u_min};
+        nlp.u_max = {s->u_max};
+        for (int k = 1; k <= N; ++k) nlp.setpoints.push_back(prof.at(t0[b] + k * s->Ts));
+        nlp.Qz = Matrix::from_rows({{s->Qz}});
+        double* xo = xi_out + b * L;
+        std::fill(xo, xo + L, 0.0);
+        std::fill(lam_out + b * N * nx, lam_out + (b + 1) * N * nx, 0.0);
+        std::fill(pil_out + b * N, pil_out + (b + 1) * N, 0.0);
+        std::fill(piu_out + b * N, piu_out + (b + 1) * N, 0.0);
+        converged[b] = 0;
+        try {
+            const OcpProblem problem(std::move(nlp));
+            Vec xi0;
+            if (xi0_in != nullptr) {
+                xi0.assign(xi0_in + b * L, xi0_in + (b + 1) * L);
+            } else {  // cold start (controllers.cpp:166-185), nominal_input (:58-66)
+                const bool fl = std::isfinite(s->u_min), fh = std::isfinite(s->u_max);
+                const double un = fl && fh ? 0.5 * (s->u_min + s->u_max) : std::max(s->u_min, std::min(s->u_max, 0.0));
+                try {
+                    xi0 = xi_from_inputs(problem.nlp(), std::vector<Vec>(N, Vec{un}));
+                } catch (const NonFiniteState&) {
+                    xi0.assign(L, 0.0);
+                    for (int k = 0; k < N; ++k) {
+                        xi0[k * (1 + nx)] = un;
+                        for (int i = 0; i < nx; ++i) xi0[k * (1 + nx) + 1 + i] = problem.nlp().x0[i];
+                    }
+                }
+            }
+            const SqpReport rep = sqp_solve(problem, xi0, opts, SqpWarmStart{});
+            std::copy(rep.xi.begin(), rep.xi.end(), xo);
+            std::copy(rep.lambda.begin(), rep.lambda.end(), lam_out + b * N * nx);
+            std::copy(rep.pi_l.begin(), rep.pi_l.end(), pil_out + b * N);
+            std::copy(rep.pi_u.begin(), rep.pi_u.end(), piu_out + b * N);
+            converged[b] = rep.converged ? 1 : 0;
+            status[b] = 0;
+        } catch (const DomainError&) {
+            status[b] = NMPCMC_DOMAIN_ERROR;
+        } catch (const NonFiniteState&) {
+            status[b] = NMPCMC_NON_FINITE_STATE;
         }
     }
     return 0;

@@ -1638,6 +1638,88 @@ __global__ void __launch_bounds__(32) nmpc_genw_kernel(const __grid_constant__ n
     }
 }
 
+/// Batched OCP service (nmpcmc_gpu_solve_ocp_batch): sqp_solve on the
+/// regulator OcpProblem of the controller model for each (x0[b], t0[b]), cold
+/// start as nmpc_step (controllers.cpp:166-185) or the given xi0 with zero
+/// duals. One warp per instance (K3w's code path).
+template <int NX>
+__global__ void __launch_bounds__(32) ocp_batch_kernel(const __grid_constant__ nmpcmc_scenario sc, int64_t batch,
+                                                       const double* x0, const double* t0, const double* xi0,
+                                                       double* xi_out, double* lam_out, double* pil_out,
+                                                       double* piu_out, int32_t* converged, int32_t* status,
+                                                       double* ws_all, int64_t slab, unsigned long long* next) {
+    const WsT<32> ws{ws_all + (int64_t)blockIdx.x * slab, 1};
+    const int lane = Lanes<32>::lane();
+#pragma unroll 1
+    for (;;) {
+        unsigned long long bi = 0;
+        if (lane == 0) bi = atomicAdd(next, 1ULL);
+        bi = __shfl_sync(kMask, bi, 0);
+        if (bi >= (unsigned long long)batch) break;
+        const int64_t b = (int64_t)bi;
+        Cnt cnt = {};
+        Ocp<NX, 32> o{make_model<NX>(sc.ctrl), Layout<NX>(sc.N), ws, sc.N, sc.Nc, sc.horizon_Ts,
+                      sc.horizon_Ts / sc.Nc, sc.u_min, sc.u_max, sc.Qz, 0.0, {}, &cnt};
+        o.invV = 1.0 / o.m.p.V;
+        const Layout<NX> L = o.lay;
+        const int N = o.N;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) o.x0[i] = x0[b * NX + i];
+        for (int k = lane; k < N; k += 32) ws[L.SP + k] = setpoint_at(sc, t0[b] + (k + 1) * sc.Ts);
+        int st = G_OK;
+        if (xi0 != nullptr) {
+            for (int e = lane; e < L.L; e += 32) ws[L.XI[0] + e] = xi0[b * L.L + e];
+        } else {
+            const bool fl = dfinite(o.umin), fh = dfinite(o.umax);
+            const double un = fl && fh ? 0.5 * (o.umin + o.umax) : smax(o.umin, smin(o.umax, 0.0));
+            for (int k = lane; k < N; k += 32) ws[L.US + k] = un;
+            Lanes<32>::sync();
+            st = xi_from_u<NX, 32>(o, 0);
+            if (st != G_OK && st != G_DOMAIN) {  // NonFiniteState: flat guess
+                for (int k = lane; k < N; k += 32) {
+                    ws[L.XI[0] + L.uo(k)] = un;
+#pragma unroll
+                    for (int e = 0; e < NX; ++e) ws[L.XI[0] + L.xo(k + 1) + e] = o.x0[e];
+                }
+                st = G_OK;
+            }
+        }
+        for (int e = lane; e < L.NN; e += 32) ws[L.LAM + e] = 0.0;
+        for (int k = lane; k < N; k += 32) ws[L.PL + k] = 0.0, ws[L.PU + k] = 0.0;
+        Lanes<32>::sync();
+        int cur = 0;
+        SqpOut so{false, st};
+        if (st == G_OK) so = sqp_solve<NX, 32>(o, sc.sqp, &cur);
+        const bool ok = so.status == G_OK;
+        for (int e = lane; e < L.L; e += 32) xi_out[b * L.L + e] = ok ? (double)ws[L.XI[cur] + e] : 0.0;
+        for (int e = lane; e < L.NN; e += 32) lam_out[b * L.NN + e] = ok ? (double)ws[L.LAM + e] : 0.0;
+        for (int k = lane; k < N; k += 32) {
+            pil_out[b * N + k] = ok ? (double)ws[L.PL + k] : 0.0;
+            piu_out[b * N + k] = ok ? (double)ws[L.PU + k] : 0.0;
+        }
+        if (lane == 0) {
+            converged[b] = ok && so.converged ? 1 : 0;
+            status[b] = ok ? 0 : so.status;
+        }
+        Lanes<32>::sync();
+    }
+}
+
+inline int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const double* x0, const double* t0,
+                            const double* xi0, double* xi, double* lam, double* pil, double* piu, int32_t* conv,
+                            int32_t* status, double* ws, int64_t blocks, unsigned long long* counter,
+                            cudaStream_t stream) {
+    const int64_t slab = sc.ctrl_variant == NMPCMC_THREE_STATE ? Layout<3>(sc.N).total : Layout<1>(sc.N).total;
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    if (sc.ctrl_variant == NMPCMC_THREE_STATE)
+        ocp_batch_kernel<3><<<(unsigned)blocks, 32, 0, stream>>>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv,
+                                                                 status, ws, slab, counter);
+    else
+        ocp_batch_kernel<1><<<(unsigned)blocks, 32, 0, stream>>>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv,
+                                                                 status, ws, slab, counter);
+    return NMPCMC_OK;
+}
+
 /// Doubles of workspace per slot.
 inline int64_t gen_ws_doubles(const nmpcmc_scenario& sc) {
     return sc.ctrl_variant == NMPCMC_THREE_STATE ? Layout<3>(sc.N).total : Layout<1>(sc.N).total;

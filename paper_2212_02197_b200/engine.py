@@ -95,6 +95,8 @@ def library():
     lib.nmpcmc_gpu_run_device.argtypes = [P, S, C.c_uint64, C.c_int64, P, P]
     lib.nmpcmc_gpu_run_async.argtypes = [P, S, C.c_uint64, C.c_int64, P, P]
     lib.nmpcmc_gpu_join.argtypes = [P]
+    lib.nmpcmc_gpu_solve_ocp_batch.argtypes = [P, S, C.c_int64] + [C.c_void_p] * 9
+    lib.nmpcmc_gpu_solve_qp_batch.argtypes = [P, C.c_void_p, C.c_int64] + [C.c_void_p] * 4
     lib.nmpcmc_gpu_wait.argtypes = [P]
     lib.nmpcmc_gpu_traj_rows.argtypes = [S]
     lib.nmpcmc_gpu_traj_rows.restype = C.c_int32

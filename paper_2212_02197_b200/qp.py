@@ -1,7 +1,10 @@
-"""Batched standalone stagewise QP service: the
-reference's solve_qp / riccati_factor_solve (qp.hpp:24-56) for a batch of
-independent QPs of equal dimensions, on the GPU kernel K5
-(csrc/qp_batch_kernel.cuh) through nmpcmc_gpu_solve_qp_batch.
+"""Batched standalone QP and OCP services:
+- solve_qp_batch: the reference's solve_qp / riccati_factor_solve
+  (qp.hpp:24-56) for a batch of independent QPs of equal dimensions, on the
+  GPU kernel K5 (csrc/qp_batch_kernel.cuh), nmpcmc_gpu_solve_qp_batch;
+- solve_ocp_batch: the reference's sqp_solve on the regulator OcpProblem
+  (sqp.hpp:27-50, :148-151) for a batch of initial states, one warp per
+  instance (K3w's code path), nmpcmc_gpu_solve_ocp_batch.
 
 A QP is a list of N+1 stage dicts with the members of QpStageData
 (qp.hpp:24-30): Q, M, R, q, r, Jx, Ju, b, lb, ub (numpy arrays; M is n_x x
@@ -159,3 +162,30 @@ def double_integrator(rng: np.random.Generator, N: int, h: float):
         qp.append(st)
     qp.append({"Q": np.diag([5.0, 1.0]), "q": rng.uniform(-1, 1, 2)})
     return qp
+
+
+# ----------------------------------------------------------- OCP service
+def solve_ocp_batch(sc, x0, t0, xi0=None, ctx=None):
+    """sqp_solve on the CSTR regulator OCP of scenario sc (its controller
+    model, horizon, Qz, bounds, setpoints and SqpOptions) for each initial
+    state x0[b] (shape (B, nx)) at time t0[b]; cold start as nmpc_step unless
+    xi0 (B, L) is given. Returns a dict of numpy arrays: xi (B, L), lambda
+    (B, N nx), pi_l, pi_u (B, N), converged, status (B,)."""
+    x0 = np.ascontiguousarray(np.atleast_2d(x0), dtype=np.float64)
+    t0 = np.ascontiguousarray(t0, dtype=np.float64).reshape(-1)
+    B, nx, N = x0.shape[0], x0.shape[1], sc.N
+    L = N * (1 + nx)
+    out = dict(xi=np.zeros((B, L)), **{"lambda": np.zeros((B, N * nx))}, pi_l=np.zeros((B, N)),
+               pi_u=np.zeros((B, N)), converged=np.zeros(B, dtype=np.int32), status=np.zeros(B, dtype=np.int32))
+    xi0p = None
+    if xi0 is not None:
+        xi0 = np.ascontiguousarray(xi0, dtype=np.float64)
+        xi0p = xi0.ctypes.data_as(C.POINTER(C.c_double))
+    P = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    ctx = ctx or engine._context(0)
+    ctx._check(ctx.lib.nmpcmc_gpu_solve_ocp_batch(
+        ctx.handle, C.byref(sc), B, P(x0), P(t0), xi0p, P(out["xi"]), P(out["lambda"]), P(out["pi_l"]),
+        P(out["pi_u"]), out["converged"].ctypes.data_as(C.POINTER(C.c_int32)),
+        out["status"].ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
+

@@ -114,6 +114,35 @@ def gen_qp():
     np.savez_compressed(os.path.join(OUT, "qp_batch.npz"), **out)
 
 
+def gen_ocp():
+    """Batched OCP fixtures: the reference's sqp_solve on the regulator
+    OcpProblem (one-state config 2 at N=60; three-state at N=30), cold starts
+    from random states/times, and one warm group from a given iterate."""
+    rng = np.random.default_rng(424242)
+    out = {}
+    for tag, kw, B in (("one", dict(controller="nmpc", N=60), 48),
+                       ("three", dict(controller="nmpc", N=30, ctrl_variant=0), 16)):
+        sc = configs.make_scenario(**kw)
+        nx = 3 if kw.get("ctrl_variant", 1) == 0 else 1
+        T = rng.uniform(322.0, 348.0, B)
+        p = configs.study_params()
+        x0 = np.array([configs.manifold_state(p, t)[3 - nx:] for t in T])
+        x0 *= 1.0 + 0.01 * rng.standard_normal(x0.shape)
+        t0 = rng.uniform(0.0, 7000.0, B)
+        ref = O.solve_ocp_batch(O.ref("xlibm"), sc, x0, t0)
+        xi_warm = np.roll(ref["xi"], 1, axis=0)  # another instance's solution as the start
+        warm = O.solve_ocp_batch(O.ref("xlibm"), sc, x0, t0, xi0=xi_warm)
+        out[f"{tag}__kwargs"] = np.array(json.dumps(kw))
+        out[f"{tag}__x0"], out[f"{tag}__t0"], out[f"{tag}__xi0"] = x0, t0, xi_warm
+        for k, v in ref.items():
+            out[f"{tag}__cold_{k}"] = v
+        for k, v in warm.items():
+            out[f"{tag}__warm_{k}"] = v
+        print(f"ocp {tag}: {B} instances, converged cold {ref['converged'].sum()} warm {warm['converged'].sum()}, "
+              f"status {np.bincount(ref['status']).tolist()}")
+    np.savez_compressed(os.path.join(OUT, "ocp_batch.npz"), **out)
+
+
 def main(which):
     if which in ("rng", "all"):
         gen_rng()
@@ -132,6 +161,8 @@ def main(which):
         gen_case("nmpc_n120_short", dict(controller="nmpc", N=120, n_steps=60), 16, 1)
     if which in ("qp", "all"):
         gen_qp()
+    if which in ("ocp", "all"):
+        gen_ocp()
     if which in ("nmpc3", "all"):
         # three-state controller model (config 2 read literally: CD-EKF and
         # OCP on the 3-state CSTR; ctrl_variant 0 = THREE_STATE) -> kernel K3g
