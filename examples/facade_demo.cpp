@@ -47,5 +47,21 @@ int main(int argc, char** argv) {
     nmpcmc::gpu::Context ctx(0);
     const auto r = nmpcmc::gpu::run_monte_carlo(ctx, sc, 1000);
     std::printf("mean phi %.6f, failed %d\n", r.aggregate.mean, r.aggregate.n_failed);
+    // standalone QP service: min 1/2 u^2 + 2u + 1/2 x1^2, x1 = 0.5 u, u in [-1, 10]
+    nmpcmc::gpu::QpStage s0, s1;
+    s0.R = {1.0};
+    s0.r = {2.0};
+    s0.Ju = {0.5};
+    s0.b = {0.0};
+    s0.lb = {-1.0};
+    s0.ub = {10.0};
+    s1.Q = {1.0};
+    s1.q = {0.0};
+    const auto qp = nmpcmc::gpu::solve_qp_batch(ctx, {{s0, s1}}, 1, 1);
+    std::printf("qp status %d u %.9f iterations %d\n", qp[0].status, qp[0].delta_xi[0], qp[0].iterations);
+    // OCP service on the NMPC variant of the scenario, cold start at T = 335 K
+    sc.controller = NMPCMC_CTRL_NMPC;
+    const auto ocp = nmpcmc::gpu::solve_ocp_batch(ctx, sc, {T0 * p.V}, {0.0});
+    std::printf("ocp converged %d u0 %.6f\n", ocp[0].converged ? 1 : 0, ocp[0].xi[0]);
     return 0;
 }

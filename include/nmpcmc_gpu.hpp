@@ -138,6 +138,104 @@ inline SimResult run_closed_loop(Context& ctx, const Scenario& sc, std::uint64_t
     return run_monte_carlo(ctx, sc, 1, sim_index).sims.front();
 }
 
+/// QpStageData (qp.hpp:24-30), matrices column-major (M is n_x x n_u). The
+/// members a stage does not use may stay empty (stage 0: Q M q Jx; stage N:
+/// all but Q q).
+struct QpStage {
+    std::vector<double> Q, M, R, q, r, Jx, Ju, b, lb, ub;
+};
+/// QpSolution (qp.hpp:34-41); status: NMPCMC_QP_OPTIMAL / MAXITER / FAILED, or
+/// NMPCMC_QP_DOMAIN_ERROR / NMPCMC_QP_NOT_POSITIVE_DEFINITE where the
+/// reference throws.
+struct QpSolution {
+    std::vector<double> delta_xi, mu, nu_l, nu_u;
+    int iterations = 0;
+    int status = NMPCMC_QP_FAILED;
+};
+
+/// solve_qp (qp.hpp:52-56) -- or riccati_factor_solve (qp.hpp:42-45) with
+/// riccati_only -- for a batch of stagewise QPs of equal dimensions.
+inline std::vector<QpSolution> solve_qp_batch(Context& ctx, const std::vector<std::vector<QpStage>>& qps, int n_x,
+                                              int n_u, double tol = 1e-10, int max_iter = 50,
+                                              bool riccati_only = false) {
+    if (qps.empty()) return {};
+    const int N = static_cast<int>(qps.front().size()) - 1;
+    const int64_t SB = nmpcmc_qp_stage_doubles(n_x, n_u), SO = nmpcmc_qp_solution_doubles(N, n_x, n_u);
+    std::vector<double> packed(qps.size() * static_cast<std::size_t>((N + 1) * SB), 0.0);
+    const int sizes[10] = {n_x * n_x, n_x * n_u, n_u * n_u, n_x, n_u, n_x * n_x, n_x * n_u, n_x, n_u, n_u};
+    for (std::size_t bi = 0; bi < qps.size(); ++bi) {
+        if (static_cast<int>(qps[bi].size()) != N + 1)
+            throw DimensionMismatch(NMPCMC_DIMENSION_MISMATCH, "solve_qp_batch: unequal stage counts");
+        for (int k = 0; k <= N; ++k) {
+            const QpStage& st = qps[bi][k];
+            const std::vector<double>* parts[10] = {&st.Q, &st.M, &st.R, &st.q, &st.r,
+                                                    &st.Jx, &st.Ju, &st.b, &st.lb, &st.ub};
+            double* dst = packed.data() + (bi * (N + 1) + k) * SB;
+            for (int m = 0; m < 10; ++m) {
+                if (!parts[m]->empty()) {
+                    if (static_cast<int>(parts[m]->size()) != sizes[m])
+                        throw DimensionMismatch(NMPCMC_DIMENSION_MISMATCH, "solve_qp_batch: block size");
+                    std::copy(parts[m]->begin(), parts[m]->end(), dst);
+                }
+                dst += sizes[m];
+            }
+        }
+    }
+    const nmpcmc_qp_dims d{N, n_x, n_u, max_iter, tol, riccati_only ? 1 : 0, 0};
+    std::vector<double> sol(qps.size() * static_cast<std::size_t>(SO));
+    std::vector<int32_t> status(qps.size()), iters(qps.size());
+    check(nmpcmc_gpu_solve_qp_batch(ctx.get(), &d, static_cast<int64_t>(qps.size()), packed.data(), sol.data(),
+                                    status.data(), iters.data()),
+          "solve_qp_batch", ctx.get());
+    std::vector<QpSolution> out(qps.size());
+    const int L = N * (n_u + n_x), NX = N * n_x, NV = N * n_u;
+    for (std::size_t bi = 0; bi < qps.size(); ++bi) {
+        const double* s = sol.data() + bi * SO;
+        out[bi].delta_xi.assign(s, s + L);
+        out[bi].mu.assign(s + L, s + L + NX);
+        out[bi].nu_l.assign(s + L + NX, s + L + NX + NV);
+        out[bi].nu_u.assign(s + L + NX + NV, s + L + NX + 2 * NV);
+        out[bi].iterations = iters[bi];
+        out[bi].status = status[bi];
+    }
+    return out;
+}
+
+/// SqpReport (sqp.hpp:79-90) of one OCP instance.
+struct OcpSolution {
+    std::vector<double> xi, lambda, pi_l, pi_u;
+    bool converged = false;
+    int status = 0;  // NMPCMC_DOMAIN_ERROR if a DomainError escaped
+};
+
+/// sqp_solve (sqp.hpp:148-151) on the regulator OcpProblem of sc's controller
+/// model for each (x0[b], t0[b]); x0 holds n_x entries per instance. Cold
+/// start as nmpc_step unless xi0 (L entries per instance) is given.
+inline std::vector<OcpSolution> solve_ocp_batch(Context& ctx, const Scenario& sc, const std::vector<double>& x0,
+                                                const std::vector<double>& t0,
+                                                const std::vector<double>* xi0 = nullptr) {
+    const int nx = sc.ctrl_variant == NMPCMC_THREE_STATE ? 3 : 1, N = sc.N, L = N * (1 + nx);
+    const std::size_t B = t0.size();
+    if (x0.size() != B * nx || (xi0 && xi0->size() != B * L))
+        throw LengthMismatch(NMPCMC_LENGTH_MISMATCH, "solve_ocp_batch: input lengths");
+    std::vector<double> xi(B * L), lam(B * N * nx), pil(B * N), piu(B * N);
+    std::vector<int32_t> conv(B), st(B);
+    check(nmpcmc_gpu_solve_ocp_batch(ctx.get(), &sc, static_cast<int64_t>(B), x0.data(), t0.data(),
+                                     xi0 ? xi0->data() : nullptr, xi.data(), lam.data(), pil.data(), piu.data(),
+                                     conv.data(), st.data()),
+          "solve_ocp_batch", ctx.get());
+    std::vector<OcpSolution> out(B);
+    for (std::size_t b = 0; b < B; ++b) {
+        out[b].xi.assign(xi.begin() + b * L, xi.begin() + (b + 1) * L);
+        out[b].lambda.assign(lam.begin() + b * N * nx, lam.begin() + (b + 1) * N * nx);
+        out[b].pi_l.assign(pil.begin() + b * N, pil.begin() + (b + 1) * N);
+        out[b].pi_u.assign(piu.begin() + b * N, piu.begin() + (b + 1) * N);
+        out[b].converged = conv[b] != 0;
+        out[b].status = st[b];
+    }
+    return out;
+}
+
 /// phi_histogram (montecarlo.cpp:268-304).
 inline Histogram phi_histogram(const std::vector<double>& phi, int bins = 0) {
     std::vector<double> edges(201);
