@@ -362,12 +362,17 @@ int nmpcmc_gpu_run_traj(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t
     if ((rc = ensure(ctx, &ctx->d_traj, &ctx->traj_cap, ntraj)) != NMPCMC_OK) return rc;
     // rows a failed run never reaches stay NaN (0xff.. bytes are a NaN pattern)
     if ((rc = cuda_check(ctx, cudaMemsetAsync(ctx->d_traj, 0xff, ntraj, ctx->stream), "memset")) != NMPCMC_OK) return rc;
+    cudaError_t cerr = cudaSuccess;
+    auto cp = [&](void* dst, const void* src, size_t n, cudaMemcpyKind kind) {
+        if (cerr == cudaSuccess && n > 0) cerr = cudaMemcpyAsync(dst, src, n, kind, ctx->stream);
+    };
     auto* d_rec = static_cast<nmpcmc_sim_record*>(ctx->d_rec);
     auto* d_traj = static_cast<double*>(ctx->d_traj);
     if ((rc = launch(ctx, main_target(ctx), *sc, first_sim, n_sims, nbar, d_rec, nullptr, d_traj, rows)) != NMPCMC_OK)
         return rc;
-    cudaMemcpyAsync(records_out, d_rec, nrec, cudaMemcpyDeviceToHost, ctx->stream);
-    cudaMemcpyAsync(traj_out, d_traj, ntraj, cudaMemcpyDeviceToHost, ctx->stream);
+    cp(records_out, d_rec, nrec, cudaMemcpyDeviceToHost);
+    cp(traj_out, d_traj, ntraj, cudaMemcpyDeviceToHost);
+    if (cerr != cudaSuccess) return cuda_check(ctx, cerr, "cudaMemcpyAsync");
     return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "kernel execution");
 }
 
@@ -416,10 +421,15 @@ int scratch_roundtrip(nmpcmc_gpu_ctx* ctx, const void* in, size_t in_bytes, size
     if (rc != NMPCMC_OK) return rc;
     char* base = static_cast<char*>(ctx->d_scratch);
     char* d_out = base + ((in_bytes + 255) / 256) * 256;
-    if (in_bytes) cudaMemcpyAsync(base, in, in_bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (in_bytes &&
+        (rc = cuda_check(ctx, cudaMemcpyAsync(base, in, in_bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D")) !=
+            NMPCMC_OK)
+        return rc;
     kernel_launch(base, d_out);
     if ((rc = cuda_check(ctx, cudaGetLastError(), "unit kernel launch")) != NMPCMC_OK) return rc;
-    cudaMemcpyAsync(out, d_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream);
+    if ((rc = cuda_check(ctx, cudaMemcpyAsync(out, d_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H")) !=
+        NMPCMC_OK)
+        return rc;
     return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "unit kernel");
 }
 
@@ -548,15 +558,20 @@ extern "C" int nmpcmc_gpu_solve_qp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_qp_di
     auto* d_in = reinterpret_cast<double*>(base);
     auto* d_out = reinterpret_cast<double*>(base + in_b);
     auto* d_st = reinterpret_cast<int32_t*>(base + in_b + out_b);
-    cudaMemcpyAsync(d_in, stages, in_b, cudaMemcpyHostToDevice, ctx->stream);
+    cudaError_t cerr = cudaSuccess;
+    auto cp = [&](void* dst, const void* src, size_t n, cudaMemcpyKind kind) {
+        if (cerr == cudaSuccess && n > 0) cerr = cudaMemcpyAsync(dst, src, n, kind, ctx->stream);
+    };
+    cp(d_in, stages, in_b, cudaMemcpyHostToDevice);
     nmpcmc_dev::qpb::Dims kd{d.N, d.n_x, d.n_u, d.max_iter, d.mode, d.tol};
     const unsigned grid = (unsigned)((slots + nmpcmc_dev::qpb::kBlock - 1) / nmpcmc_dev::qpb::kBlock);
     nmpcmc_dev::qpb::qp_batch_kernel<<<grid, nmpcmc_dev::qpb::kBlock, 0, ctx->stream>>>(
         kd, batch, d_in, d_out, d_st, d_st + batch, static_cast<double*>(ctx->d_ws), slots);
     if ((rc = cuda_check(ctx, cudaGetLastError(), "qp_batch_kernel launch")) != NMPCMC_OK) return rc;
-    cudaMemcpyAsync(solutions, d_out, out_b, cudaMemcpyDeviceToHost, ctx->stream);
-    cudaMemcpyAsync(status, d_st, (size_t)batch * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream);
-    cudaMemcpyAsync(iterations, d_st + batch, (size_t)batch * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream);
+    cp(solutions, d_out, out_b, cudaMemcpyDeviceToHost);
+    cp(status, d_st, (size_t)batch * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    cp(iterations, d_st + batch, (size_t)batch * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    if (cerr != cudaSuccess) return cuda_check(ctx, cerr, "cudaMemcpyAsync");
     return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "qp_batch_kernel");
 }
 
@@ -601,18 +616,23 @@ extern "C" int nmpcmc_gpu_solve_ocp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scen
     const size_t ws_b = (size_t)blocks * (size_t)nmpcmc_dev::gen::gen_ws_doubles(*sc) * sizeof(double);
     if ((rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, ws_b)) != NMPCMC_OK) return rc;
     if ((rc = ensure(ctx, &ctx->d_counter, &ctx->counter_cap, 256)) != NMPCMC_OK) return rc;
-    cudaMemcpyAsync(d_x0, x0, b_x0, cudaMemcpyHostToDevice, ctx->stream);
-    cudaMemcpyAsync(d_t0, t0, b_t0, cudaMemcpyHostToDevice, ctx->stream);
-    if (xi0) cudaMemcpyAsync(d_xi0, xi0, b_xi, cudaMemcpyHostToDevice, ctx->stream);
+    cudaError_t cerr = cudaSuccess;
+    auto cp = [&](void* dst, const void* src, size_t n, cudaMemcpyKind kind) {
+        if (cerr == cudaSuccess && n > 0) cerr = cudaMemcpyAsync(dst, src, n, kind, ctx->stream);
+    };
+    cp(d_x0, x0, b_x0, cudaMemcpyHostToDevice);
+    cp(d_t0, t0, b_t0, cudaMemcpyHostToDevice);
+    if (xi0) cp(d_xi0, xi0, b_xi, cudaMemcpyHostToDevice);
     nmpcmc_dev::gen::launch_ocp_batch(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv, d_st,
                                       static_cast<double*>(ctx->d_ws), blocks,
                                       static_cast<unsigned long long*>(ctx->d_counter), ctx->stream);
     if ((rc = cuda_check(ctx, cudaGetLastError(), "ocp_batch_kernel launch")) != NMPCMC_OK) return rc;
-    cudaMemcpyAsync(xi, d_xi, b_xi, cudaMemcpyDeviceToHost, ctx->stream);
-    cudaMemcpyAsync(lambda, d_lam, b_lam, cudaMemcpyDeviceToHost, ctx->stream);
-    cudaMemcpyAsync(pi_l, d_pil, b_pi, cudaMemcpyDeviceToHost, ctx->stream);
-    cudaMemcpyAsync(pi_u, d_piu, b_pi, cudaMemcpyDeviceToHost, ctx->stream);
-    cudaMemcpyAsync(converged, d_conv, b_i, cudaMemcpyDeviceToHost, ctx->stream);
-    cudaMemcpyAsync(status, d_st, b_i, cudaMemcpyDeviceToHost, ctx->stream);
+    cp(xi, d_xi, b_xi, cudaMemcpyDeviceToHost);
+    cp(lambda, d_lam, b_lam, cudaMemcpyDeviceToHost);
+    cp(pi_l, d_pil, b_pi, cudaMemcpyDeviceToHost);
+    cp(pi_u, d_piu, b_pi, cudaMemcpyDeviceToHost);
+    cp(converged, d_conv, b_i, cudaMemcpyDeviceToHost);
+    cp(status, d_st, b_i, cudaMemcpyDeviceToHost);
+    if (cerr != cudaSuccess) return cuda_check(ctx, cerr, "cudaMemcpyAsync");
     return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "ocp_batch_kernel");
 }
