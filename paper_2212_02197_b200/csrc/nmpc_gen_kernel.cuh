@@ -53,6 +53,48 @@ struct WsT {
 };
 using Ws = WsT<1>;
 
+/// The Riccati sweep arrays (value matrices, pivots and their reciprocal
+/// seeds, gains, G, value gradients, feedforward steps) are private to
+/// rfactor_t / rsolve_t. K3w keeps them in the block's shared memory (one warp
+/// per block): 32-bit LDS/STS addressing and LDS latency on the serial
+/// recursions. K3g keeps them in its global slab.
+extern __shared__ __align__(16) double gen_smem[];
+template <int NX>
+struct SweepLay {
+    int FP, FLL, FLY, FK, FG, PV, DFF, total;
+    __host__ __device__ explicit SweepLay(int N) {
+        FP = 0;
+        FLL = FP + (N + 1) * NX * NX;
+        FLY = FLL + N;
+        FK = FLY + N;
+        FG = FK + N * NX;
+        PV = FG + N * NX;
+        DFF = PV + (N + 1) * NX;
+        total = DFF + N;
+    }
+};
+/// Bytes of shared memory K3w needs per block; K3w runs only if it fits.
+template <int NX>
+__host__ __device__ inline size_t sweep_smem_bytes(int N) {
+    return (size_t)SweepLay<NX>(N).total * sizeof(double);
+}
+constexpr size_t kSweepSmemMax = 200u << 10;
+/// Pointer view of one sweep array (pre-offset; K3g strided by T).
+template <int W>
+struct ArrT {
+    double* p;
+    int64_t T;
+    __device__ __forceinline__ double& operator[](int i) const {
+        if (W == 1) return p[(int64_t)i * T];
+        return p[i];
+    }
+};
+template <int W>
+__device__ __forceinline__ ArrT<W> sweep_arr(const WsT<W>& w, int goff, int soff) {
+    if (W == 1) return ArrT<W>{w.p + (int64_t)goff * w.T, w.T};
+    return ArrT<W>{gen_smem + soff, 1};
+}
+
 /// Lane helpers: W = 1 (thread per sample) or 32 (warp per sample).
 constexpr unsigned kMask = 0xffffffffu;
 template <int W>
@@ -438,6 +480,12 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
     const WsT<W> w = o.ws;  // by value: base/stride and the offsets below live in registers
     const Layout<NX> L = o.lay;
     const int oBAR = L.BAR, oFG = L.FG, oFK = L.FK, oFLL = L.FLL, oFLY = L.FLY, oFP = L.FP;
+    const SweepLay<NX> SL(o.N);
+    const ArrT<W> aFP = sweep_arr<W>(w, oFP, SL.FP);
+    const ArrT<W> aFLL = sweep_arr<W>(w, oFLL, SL.FLL);
+    const ArrT<W> aFLY = sweep_arr<W>(w, oFLY, SL.FLY);
+    const ArrT<W> aFK = sweep_arr<W>(w, oFK, SL.FK);
+    const ArrT<W> aFG = sweep_arr<W>(w, oFG, SL.FG);
     const int oFXs = L.FX[v.s], oFUs = L.FU[v.s], oWB = L.WB, oXIs = L.XI[v.s], oGFs = L.GF[v.s];
     auto Jx_ = [&](int k, int i, int j) -> double { return w[oFXs + (k * NX + j) * NX + i]; };
     auto Ju_ = [&](int k, int i) -> double { return w[oFUs + k * NX + i]; };
@@ -452,7 +500,7 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
     (void)oXIs, (void)oGFs;
 
     const int N = o.N;
-    auto P = [&](int k, int i, int j) -> double& { return w[oFP + (k * NX + j) * NX + i]; };
+    auto P = [&](int k, int i, int j) -> double& { return aFP[(k * NX + j) * NX + i]; };
     // P_{k+1} is carried in registers from one stage to the next: reloading
     // what the previous stage just stored would put a store-to-load round trip
     // through the cache hierarchy on the recursion's critical path
@@ -495,8 +543,8 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
             l = sqrt(H);
             y = 1.0 / l;  // seed of rsolve's certified division
         }
-        w[oFLL + k] = l;
-        w[oFLY + k] = y;
+        aFLL[k] = l;
+        aFLY[k] = y;
         if (k >= 1) {
             double PJx[NX * NX], G[NX], K[NX];
 #pragma unroll
@@ -557,8 +605,8 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
                 }
 #pragma unroll
             for (int j = 0; j < NX; ++j) {
-                w[oFK + k * NX + j] = K[j];
-                w[oFG + k * NX + j] = G[j];
+                aFK[k * NX + j] = K[j];
+                aFG[k * NX + j] = G[j];
 #pragma unroll
                 for (int i = 0; i < NX; ++i) {
                     P(k, i, j) = Pk[j * NX + i];
@@ -588,6 +636,14 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
     const WsT<W> w = o.ws;  // by value: base/stride and the offsets below live in registers
     const Layout<NX> L = o.lay;
     const int oDFF = L.DFF, oDMU = L.DMU, oDXI = L.DXI, oFG = L.FG, oFK = L.FK, oFLL = L.FLL, oFLY = L.FLY, oFP = L.FP, oPV = L.PV, oRD = L.RD, oRH = L.RH, oRS = L.RS;
+    const SweepLay<NX> SL(o.N);
+    const ArrT<W> aFP = sweep_arr<W>(w, oFP, SL.FP);
+    const ArrT<W> aFLL = sweep_arr<W>(w, oFLL, SL.FLL);
+    const ArrT<W> aFLY = sweep_arr<W>(w, oFLY, SL.FLY);
+    const ArrT<W> aFK = sweep_arr<W>(w, oFK, SL.FK);
+    const ArrT<W> aFG = sweep_arr<W>(w, oFG, SL.FG);
+    const ArrT<W> aPV = sweep_arr<W>(w, oPV, SL.PV);
+    const ArrT<W> aDFF = sweep_arr<W>(w, oDFF, SL.DFF);
     const int oFXs = L.FX[v.s], oFUs = L.FU[v.s], oWB = L.WB, oXIs = L.XI[v.s], oGFs = L.GF[v.s];
     auto Jx_ = [&](int k, int i, int j) -> double { return w[oFXs + (k * NX + j) * NX + i]; };
     auto Ju_ = [&](int k, int i) -> double { return w[oFUs + k * NX + i]; };
@@ -602,13 +658,13 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
     (void)oXIs, (void)oGFs;
 
     const int N = o.N;
-    auto P = [&](int k, int i, int j) -> double { return w[oFP + (k * NX + j) * NX + i]; };
+    auto P = [&](int k, int i, int j) -> double { return aFP[(k * NX + j) * NX + i]; };
     auto bh = [&](int k, int i) -> double { return -w[oRD + k * NX + i]; };
     double pvn[NX];  // p_{k+1}, carried in registers (see rfactor)
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
         pvn[i] = w[oRS + L.xo(N) + i];
-        w[oPV + N * NX + i] = pvn[i];
+        aPV[N * NX + i] = pvn[i];
     }
 #pragma unroll 1
     for (int k = N - 1; k >= 0; --k) {
@@ -627,9 +683,9 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
             for (int j = 0; j < NX; ++j) s += Ju_(k, j) * t[j];
             hv = 1.0 * s + 1.0 * w[oRH + k];
         }
-        const double l = w[oFLL + k];
+        const double l = aFLL[k];
         if (FAST) {
-            const double y = w[oFLY + k];
+            const double y = aFLY[k];
             hv = cdiv_seed(hv, l, y, cert);
             hv = cdiv_seed(hv, l, y, cert);
         } else {
@@ -637,7 +693,7 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
             hv = hv / l;
         }
         const double dff = -hv;
-        w[oDFF + k] = dff;
+        aDFF[k] = dff;
         if (k >= 1) {
 #pragma unroll
             for (int i = 0; i < NX; ++i) {
@@ -645,8 +701,8 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
 #pragma unroll
                 for (int j = 0; j < NX; ++j) s += Jx_(k, j, i) * t[j];
                 double p = 1.0 * s + 1.0 * w[oRS + L.xo(k) + i];
-                p = 1.0 * (0.0 + w[oFG + k * NX + i] * dff) + 1.0 * p;
-                w[oPV + k * NX + i] = p;
+                p = 1.0 * (0.0 + aFG[k * NX + i] * dff) + 1.0 * p;
+                aPV[k * NX + i] = p;
                 pvn[i] = p;
             }
         }
@@ -656,11 +712,11 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
     for (int i = 0; i < NX; ++i) dx[i] = 0.0;
 #pragma unroll 1
     for (int k = 0; k < N; ++k) {
-        double du = w[oDFF + k];
+        double du = aDFF[k];
         if (k >= 1) {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < NX; ++j) s += w[oFK + k * NX + j] * dx[j];
+            for (int j = 0; j < NX; ++j) s += aFK[k * NX + j] * dx[j];
             du = 1.0 * s + 1.0 * du;
         }
         w[oDXI + L.uo(k)] = du;
@@ -688,7 +744,7 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
             double s = 0.0;
 #pragma unroll
             for (int j = 0; j < NX; ++j) s += P(k + 1, i, j) * dx[j];
-            const double mv = 1.0 * s + 1.0 * w[oPV + (k + 1) * NX + i];
+            const double mv = 1.0 * s + 1.0 * aPV[(k + 1) * NX + i];
             w[oDMU + k * NX + i] = -mv;
         }
     }
@@ -1709,14 +1765,17 @@ inline int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const doub
                             const double* xi0, double* xi, double* lam, double* pil, double* piu, int32_t* conv,
                             int32_t* status, double* ws, int64_t blocks, unsigned long long* counter,
                             cudaStream_t stream) {
-    const int64_t slab = sc.ctrl_variant == NMPCMC_THREE_STATE ? Layout<3>(sc.N).total : Layout<1>(sc.N).total;
+    const bool c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
+    const int64_t slab = c3 ? Layout<3>(sc.N).total : Layout<1>(sc.N).total;
+    const size_t smem = c3 ? sweep_smem_bytes<3>(sc.N) : sweep_smem_bytes<1>(sc.N);
+    if (smem > kSweepSmemMax) return NMPCMC_UNSUPPORTED;
     cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
-    if (sc.ctrl_variant == NMPCMC_THREE_STATE)
-        ocp_batch_kernel<3><<<(unsigned)blocks, 32, 0, stream>>>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv,
-                                                                 status, ws, slab, counter);
+    if (c3)
+        ocp_batch_kernel<3><<<(unsigned)blocks, 32, smem, stream>>>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv,
+                                                                    status, ws, slab, counter);
     else
-        ocp_batch_kernel<1><<<(unsigned)blocks, 32, 0, stream>>>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv,
-                                                                 status, ws, slab, counter);
+        ocp_batch_kernel<1><<<(unsigned)blocks, 32, smem, stream>>>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv,
+                                                                    status, ws, slab, counter);
     return NMPCMC_OK;
 }
 
@@ -1743,9 +1802,12 @@ inline int64_t gen_slots(const nmpcmc_scenario& sc, int sm_count, int64_t n) {
 /// K3w resident blocks (one warp each): occupancy, capped so the per-warp
 /// slabs stay L2-resident (~72 KB each at N = 60, NX = 3).
 template <int TX, int NX>
-inline int64_t genw_blocks_t(int sm_count, int64_t n, int64_t slab_doubles) {
+inline int64_t genw_blocks_t(int sm_count, int64_t n, int64_t slab_doubles, int N) {
+    const size_t smem = sweep_smem_bytes<NX>(N);
+    cudaFuncSetAttribute(nmpc_genw_kernel<TX, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(ocp_batch_kernel<NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nmpc_genw_kernel<TX, NX>, 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nmpc_genw_kernel<TX, NX>, 32, smem);
     if (b < 1) b = 1;
     int64_t blocks = (int64_t)sm_count * b;
     const int64_t l2_cap = (int64_t)(96ull << 20) / (slab_doubles * 8);
@@ -1755,18 +1817,24 @@ inline int64_t genw_blocks_t(int sm_count, int64_t n, int64_t slab_doubles) {
 inline int64_t genw_blocks(const nmpcmc_scenario& sc, int sm_count, int64_t n) {
     const bool t3 = sc.truth_variant == NMPCMC_THREE_STATE, c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
     const int64_t slab = gen_ws_doubles(sc);
-    if (t3) return c3 ? genw_blocks_t<3, 3>(sm_count, n, slab) : genw_blocks_t<3, 1>(sm_count, n, slab);
-    return c3 ? genw_blocks_t<1, 3>(sm_count, n, slab) : genw_blocks_t<1, 1>(sm_count, n, slab);
+    if (t3) return c3 ? genw_blocks_t<3, 3>(sm_count, n, slab, sc.N) : genw_blocks_t<3, 1>(sm_count, n, slab, sc.N);
+    return c3 ? genw_blocks_t<1, 3>(sm_count, n, slab, sc.N) : genw_blocks_t<1, 1>(sm_count, n, slab, sc.N);
 }
+/// K3w needs its sweep arrays in shared memory (N up to ~1,000 stages at NX = 3).
+inline size_t genw_smem(const nmpcmc_scenario& sc) {
+    return sc.ctrl_variant == NMPCMC_THREE_STATE ? sweep_smem_bytes<3>(sc.N) : sweep_smem_bytes<1>(sc.N);
+}
+inline bool genw_fits(const nmpcmc_scenario& sc) { return genw_smem(sc) <= kSweepSmemMax; }
 inline int launch_genw(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
                        nmpcmc_work_counters* d_cnt, double* d_traj, int rows, double* ws, int64_t blocks,
                        unsigned long long* counter, cudaStream_t stream) {
-    if (blocks < 1) return NMPCMC_INVALID_ARGUMENT;
+    if (blocks < 1 || !genw_fits(sc)) return NMPCMC_INVALID_ARGUMENT;
     const int64_t slab = gen_ws_doubles(sc);
+    const size_t smem = genw_smem(sc);
     cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
     const bool t3 = sc.truth_variant == NMPCMC_THREE_STATE, c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
 #define NMPCMC_GENW_LAUNCH(T, C)                                                                              \
-    nmpc_genw_kernel<T, C><<<(unsigned)blocks, 32, 0, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ws, \
+    nmpc_genw_kernel<T, C><<<(unsigned)blocks, 32, smem, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ws, \
                                                                 slab, counter)
     if (t3 && c3) NMPCMC_GENW_LAUNCH(3, 3);
     else if (t3) NMPCMC_GENW_LAUNCH(3, 1);

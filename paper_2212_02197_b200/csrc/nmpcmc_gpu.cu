@@ -126,7 +126,7 @@ int launch(nmpcmc_gpu_ctx* ctx, const Target& tg, const nmpcmc_scenario& sc, uin
     const bool generic = sc.ctrl_variant != NMPCMC_ONE_STATE || sc.N > 255 ||
                          ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC ||
                          ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC_WARP;
-    if (generic && ctx->nmpc_kernel != NMPCMC_NMPC_KERNEL_GENERIC) {  // K3w unless K3g is asked for
+    if (generic && ctx->nmpc_kernel != NMPCMC_NMPC_KERNEL_GENERIC && nmpcmc_dev::gen::genw_fits(sc)) {  // K3w unless K3g is asked for (or N too long)
         const int64_t blocks = nmpcmc_dev::gen::genw_blocks(sc, ctx->sm_count, n);
         const size_t need = (size_t)blocks * (size_t)nmpcmc_dev::gen::gen_ws_doubles(sc) * sizeof(double);
         if ((rc = ensure(ctx, tg.d_ws, tg.ws_cap, need)) != NMPCMC_OK) return rc;
@@ -623,9 +623,11 @@ extern "C" int nmpcmc_gpu_solve_ocp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scen
     cp(d_x0, x0, b_x0, cudaMemcpyHostToDevice);
     cp(d_t0, t0, b_t0, cudaMemcpyHostToDevice);
     if (xi0) cp(d_xi0, xi0, b_xi, cudaMemcpyHostToDevice);
-    nmpcmc_dev::gen::launch_ocp_batch(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv, d_st,
-                                      static_cast<double*>(ctx->d_ws), blocks,
-                                      static_cast<unsigned long long*>(ctx->d_counter), ctx->stream);
+    if ((rc = nmpcmc_dev::gen::launch_ocp_batch(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv,
+                                                d_st, static_cast<double*>(ctx->d_ws), blocks,
+                                                static_cast<unsigned long long*>(ctx->d_counter), ctx->stream)) !=
+        NMPCMC_OK)
+        return fail(ctx, rc, "OCP batch: horizon too long for the shared-memory sweep arrays");
     if ((rc = cuda_check(ctx, cudaGetLastError(), "ocp_batch_kernel launch")) != NMPCMC_OK) return rc;
     cp(xi, d_xi, b_xi, cudaMemcpyDeviceToHost);
     cp(lambda, d_lam, b_lam, cudaMemcpyDeviceToHost);
