@@ -6,7 +6,9 @@ models, parameter perturbation, bounds). Scenarios the reference's own
 validation rejects are skipped. Raw scenario bytes are stored (these are not
 configs.make_scenario outputs).
 
-  python tests/golden/make_fuzz.py [n_scenarios] [seed]
+  python tests/golden/make_fuzz.py [n_scenarios] [seed] [--long]
+
+--long: NMPC only, 20-60 control steps, horizons 10-80 -> fuzz_long.npz.
 """
 import ctypes as C
 import os
@@ -24,12 +26,12 @@ from paper_2212_02197_b200 import abi, configs  # noqa: E402
 OUT = os.path.dirname(os.path.abspath(__file__))
 
 
-def random_scenario(rng):
-    nmpc = rng.uniform() < 0.8
-    steps = int(rng.integers(4, 21))
+def random_scenario(rng, long=False):
+    nmpc = long or rng.uniform() < 0.8
+    steps = int(rng.integers(20, 61)) if long else int(rng.integers(4, 21))
     Ts = float(rng.choice([2.0, 5.0, 10.0, 20.0]))
     kw = dict(controller="nmpc" if nmpc else "pi", n_steps=steps, Ts=Ts, Ns=int(rng.integers(1, 13)),
-              N=int(rng.integers(3, 41)), Nc=int(rng.integers(1, 7)), np_=int(rng.integers(1, 7)),
+              N=int(rng.integers(10, 81)) if long else int(rng.integers(3, 41)), Nc=int(rng.integers(1, 7)), np_=int(rng.integers(1, 7)),
               max_iter=int(rng.integers(1, 21)), eps=float(rng.choice([1e-4, 1e-6, 1e-8])),
               perturb=bool(rng.uniform() < 0.5), rel_std=tuple(float(x) for x in rng.uniform(0.0, 0.2, 3)),
               base_seed=int(rng.integers(0, 2**62)),
@@ -58,14 +60,16 @@ def random_scenario(rng):
 
 
 def main():
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 60
-    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 20261020
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    long = "--long" in sys.argv
+    n = int(args[0]) if len(args) > 0 else 60
+    seed = int(args[1]) if len(args) > 1 else 20261020
     rng = np.random.default_rng(seed)
     Lx, Lg = O.ref("xlibm"), O.ref("glibc")
     scen, rec_x, rec_g, firsts = [], [], [], []
     t0 = time.time()
     while len(scen) < n:
-        sc = random_scenario(rng)
+        sc = random_scenario(rng, long)
         nbar = C.c_int(0)
         if Lx.nmpcmc_ref_validate(C.byref(sc), C.byref(nbar)) != 0:
             continue
@@ -76,7 +80,7 @@ def main():
         rec_x.append(rx)
         rec_g.append(rg)
         firsts.append(first)
-    np.savez_compressed(os.path.join(OUT, "fuzz.npz"), scenarios=np.array(scen), rec_xlibm=np.array(rec_x),
+    np.savez_compressed(os.path.join(OUT, "fuzz_long.npz" if long else "fuzz.npz"), scenarios=np.array(scen), rec_xlibm=np.array(rec_x),
                         rec_glibc=np.array(rec_g), first=np.array(firsts), seed=np.array(seed))
     fails = int(sum(int(r["failed"].sum()) for r in rec_x))
     print(f"fuzz: {n} scenarios x 6 samples in {time.time() - t0:.1f}s, {fails} failed samples")
