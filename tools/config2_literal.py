@@ -33,7 +33,7 @@ line = {"config": "BASELINE config 2, three-state controller model (CD-EKF + OCP
         "n_failed": int(rec["failed"].sum()), "phi_mean": mc.aggregate["mean"]}
 try:
     from oracle import lib as O
-    m = 8
+    m = os.cpu_count() or 8  # one sample per host thread
     ref, wall = O.run_batch(O.ref("xlibm"), sc, 0, m, os.cpu_count())
     same = all(np.array_equal(rec[f][:m], ref[f], equal_nan=(f == "phi")) for f in ("phi", "failed", "ocp_solves",
                                                                                   "ocp_failures"))
