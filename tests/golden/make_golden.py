@@ -107,6 +107,11 @@ def gen_qp():
     add("scalar", scal, 1, 1)
     add("scalar_riccati", scal, 1, 1, riccati_only=True)
     add("maxiter", [Q.scalar_instance(1.0, 2.0, 1.0, 0.0, 0.0, 0.0, -0.5, 0.5)], 1, 1, tol=0.0, max_iter=5)
+    # dimension limits of the device kernel (n_x <= 8, n_u <= 4) and the minimal horizon
+    add("limits", [Q.random_instance(rng, 8, 8, 4) for _ in range(8)], 8, 4)
+    add("minimal", [Q.random_instance(rng, 1, 2, 2) for _ in range(8)], 2, 2)
+    add("minimal_riccati", [Q.random_instance(rng, 1, 2, 2, bounded=False) for _ in range(4)], 2, 2,
+        riccati_only=True)
     out = {}
     for g, d in groups.items():
         for k, v in d.items():

@@ -75,7 +75,7 @@ def _kkt_residual(packed_qp, s, N, nx, nu):
     return g
 
 
-@pytest.mark.parametrize("name", ["rand_box", "big"])
+@pytest.mark.parametrize("name", ["rand_box", "big", "limits", "minimal"])
 def test_box_qp_solutions_are_kkt_points(name):
     g = G[name]
     sols, N, nx, nu = _sols(g)
@@ -93,7 +93,8 @@ def test_box_qp_solutions_are_kkt_points(name):
             assert np.all(np.abs(nl[fl] * (u[fl] - st["lb"][fl])) <= 1e-6)
             assert np.all(np.abs(nuu[fu] * (st["ub"][fu] - u[fu])) <= 1e-6)
             active += int(np.sum(nl > 1e-6) + np.sum(nuu > 1e-6))
-    assert active > 30  # the bounds matter in this population
+    if name in ("rand_box", "big"):
+        assert active > 30  # the bounds matter in this population
 
 
 @pytest.mark.parametrize("name", ["rand_unc", "dint"])
