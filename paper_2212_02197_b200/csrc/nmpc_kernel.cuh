@@ -1647,6 +1647,109 @@ inline int launch_nmpc(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int
     return NMPCMC_UNSUPPORTED;
 }
 
+/// Batched OCP service on K3's phases (one-state controller model, N <= 255):
+/// for instance b, sqp_solve on the regulator OCP from x0[b] at t0[b], cold
+/// start as nmpc_step (start_iterate) or the given xi0 with zero duals. The
+/// iterate is scattered back to the interleaved xi layout (u_k, x_{k+1}).
+template <int ST>
+__global__ void __launch_bounds__(32, NMPCMC_MIN_BLOCKS)
+    ocp1_kernel(const __grid_constant__ nmpcmc_scenario sc, int64_t batch, const double* x0, const double* t0,
+                const double* xi0, double* xi_out, double* lam_out, double* pil_out, double* piu_out,
+                int32_t* conv_out, int32_t* status_out, double* gws_all, unsigned long long* next) {
+    double* gws = gws_all + (size_t)blockIdx.x * kGlobArrays * ST;
+    const int lane = threadIdx.x & 31;
+#pragma unroll 1
+    for (;;) {
+        unsigned long long bi = 0;
+        if (lane == 0) bi = atomicAdd(next, 1ULL);
+        bi = __shfl_sync(FULLMASK, bi, 0);
+        if (bi >= (unsigned long long)batch) break;
+        const int64_t b = (int64_t)bi;
+        Ocp o;
+        o.p = load_cstr(sc.ctrl);
+        o.N = sc.N;
+        o.Nc = sc.Nc;
+        o.Ts = sc.horizon_Ts;
+        o.h = sc.horizon_Ts / sc.Nc;
+        o.umin = sc.u_min;
+        o.umax = sc.u_max;
+        o.Qz = sc.Qz;
+        o.inv_V = 1.0 / o.p.V;
+        o.x0 = x0[b];
+        o.gws = gws;
+        const int N = o.N;
+        Cnt cnt = {};
+#pragma unroll 1
+        for (int k = lane; k < N; k += 32) GA(G_SP)[k] = setpoint_at(sc, t0[b] + (k + 1) * sc.Ts);
+        __syncwarp();
+        int st = ST_OK;
+        if (xi0 != nullptr) {
+#pragma unroll 1
+            for (int k = lane; k < N; k += 32) {
+                GA(G_U)[k] = xi0[b * 2 * N + 2 * k];
+                GA(G_X)[k] = xi0[b * 2 * N + 2 * k + 1];
+                GA(G_LAM)[k] = 0.0;
+                GA(G_PIL)[k] = 0.0;
+                GA(G_PIU)[k] = 0.0;
+            }
+            __syncwarp();
+        } else {
+            st = start_iterate<ST>(o, false, &cnt);
+        }
+        SqpOut so{false, st};
+        if (st == ST_OK) so = sqp_solve<ST>(o, sc.sqp, &cnt);
+        const bool ok = so.status == ST_OK;
+#pragma unroll 1
+        for (int k = lane; k < N; k += 32) {
+            xi_out[b * 2 * N + 2 * k] = ok ? GA(G_U)[k] : 0.0;
+            xi_out[b * 2 * N + 2 * k + 1] = ok ? GA(G_X)[k] : 0.0;
+            lam_out[b * N + k] = ok ? GA(G_LAM)[k] : 0.0;
+            pil_out[b * N + k] = ok ? GA(G_PIL)[k] : 0.0;
+            piu_out[b * N + k] = ok ? GA(G_PIU)[k] : 0.0;
+        }
+        if (lane == 0) {
+            conv_out[b] = ok && so.converged ? 1 : 0;
+            status_out[b] = ok ? 0 : so.status;
+        }
+        __syncwarp();
+    }
+}
+
+template <int ST>
+inline int launch_ocp1_t(const nmpcmc_scenario& sc, int64_t batch, const double* x0, const double* t0,
+                         const double* xi0, double* xi, double* lam, double* pil, double* piu, int32_t* conv,
+                         int32_t* status, int sm_count, double* gws, int64_t gws_blocks, unsigned long long* counter,
+                         cudaStream_t stream) {
+    const size_t smem = ws_bytes_for(ST);
+    cudaFuncSetAttribute(ocp1_kernel<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ocp1_kernel<ST>, 32, smem);
+    int64_t grid = (int64_t)sm_count * (per < 1 ? 1 : per);
+    if (grid > batch) grid = batch;
+    if (grid > gws_blocks) grid = gws_blocks;
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    ocp1_kernel<ST><<<(unsigned)grid, 32, smem, stream>>>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv, status,
+                                                          gws, counter);
+    return NMPCMC_OK;
+}
+/// One-state OCP batches on K3's phases; returns NMPCMC_UNSUPPORTED otherwise.
+inline int launch_ocp1(const nmpcmc_scenario& sc, int64_t batch, const double* x0, const double* t0,
+                       const double* xi0, double* xi, double* lam, double* pil, double* piu, int32_t* conv,
+                       int32_t* status, int sm_count, double* gws, int64_t gws_blocks, unsigned long long* counter,
+                       cudaStream_t stream) {
+    if (sc.ctrl_variant != NMPCMC_ONE_STATE || sc.N < 1 || sc.N > 255) return NMPCMC_UNSUPPORTED;
+    switch (ws_stride_for(sc.N)) {
+        case 32: return launch_ocp1_t<32>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv, status, sm_count, gws,
+                                          gws_blocks, counter, stream);
+        case 64: return launch_ocp1_t<64>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv, status, sm_count, gws,
+                                          gws_blocks, counter, stream);
+        case 128: return launch_ocp1_t<128>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv, status, sm_count, gws,
+                                            gws_blocks, counter, stream);
+        default: return launch_ocp1_t<256>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv, status, sm_count, gws,
+                                           gws_blocks, counter, stream);
+    }
+}
+
 #undef SA
 #undef GA
 #undef IA

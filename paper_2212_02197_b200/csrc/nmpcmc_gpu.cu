@@ -612,9 +612,19 @@ extern "C" int nmpcmc_gpu_solve_ocp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scen
     auto* d_piu = reinterpret_cast<double*>(take(b_pi));
     auto* d_conv = reinterpret_cast<int32_t*>(take(b_i));
     auto* d_st = reinterpret_cast<int32_t*>(take(b_i));
-    const int64_t blocks = nmpcmc_dev::gen::genw_blocks(*sc, ctx->sm_count, batch);
-    const size_t ws_b = (size_t)blocks * (size_t)nmpcmc_dev::gen::gen_ws_doubles(*sc) * sizeof(double);
-    if ((rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, ws_b)) != NMPCMC_OK) return rc;
+    // one-state OCPs with N <= 255 run on K3's phases (shared-memory Riccati
+    // sweeps, certified sqrt/division); the rest on K3w's generic path
+    const bool k3 = sc->ctrl_variant == NMPCMC_ONE_STATE && sc->N <= 255;
+    int64_t blocks = 0;
+    if (k3) {
+        size_t gbytes = 0;
+        nmpcmc_dev::nmpc_gws_need(*sc, ctx->sm_count, batch, &gbytes, &blocks);
+        if ((rc = ensure(ctx, &ctx->d_gws, &ctx->gws_cap, gbytes)) != NMPCMC_OK) return rc;
+    } else {
+        blocks = nmpcmc_dev::gen::genw_blocks(*sc, ctx->sm_count, batch);
+        const size_t ws_b = (size_t)blocks * (size_t)nmpcmc_dev::gen::gen_ws_doubles(*sc) * sizeof(double);
+        if ((rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, ws_b)) != NMPCMC_OK) return rc;
+    }
     if ((rc = ensure(ctx, &ctx->d_counter, &ctx->counter_cap, 256)) != NMPCMC_OK) return rc;
     cudaError_t cerr = cudaSuccess;
     auto cp = [&](void* dst, const void* src, size_t n, cudaMemcpyKind kind) {
@@ -623,10 +633,13 @@ extern "C" int nmpcmc_gpu_solve_ocp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scen
     cp(d_x0, x0, b_x0, cudaMemcpyHostToDevice);
     cp(d_t0, t0, b_t0, cudaMemcpyHostToDevice);
     if (xi0) cp(d_xi0, xi0, b_xi, cudaMemcpyHostToDevice);
-    if ((rc = nmpcmc_dev::gen::launch_ocp_batch(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv,
+    rc = k3 ? nmpcmc_dev::launch_ocp1(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv, d_st,
+                                      ctx->sm_count, static_cast<double*>(ctx->d_gws), blocks,
+                                      static_cast<unsigned long long*>(ctx->d_counter), ctx->stream)
+            : nmpcmc_dev::gen::launch_ocp_batch(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv,
                                                 d_st, static_cast<double*>(ctx->d_ws), blocks,
-                                                static_cast<unsigned long long*>(ctx->d_counter), ctx->stream)) !=
-        NMPCMC_OK)
+                                                static_cast<unsigned long long*>(ctx->d_counter), ctx->stream);
+    if (rc != NMPCMC_OK)
         return fail(ctx, rc, "OCP batch: horizon too long for the shared-memory sweep arrays");
     if ((rc = cuda_check(ctx, cudaGetLastError(), "ocp_batch_kernel launch")) != NMPCMC_OK) return rc;
     cp(xi, d_xi, b_xi, cudaMemcpyDeviceToHost);
