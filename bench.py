@@ -289,6 +289,19 @@ def run_ours(args):
     e2e_value = world * S * Ke / e2e_s
     ctx.set_lanes(1)
 
+    # PI at BASELINE config 1's own size (30,000 perturbed samples, one launch):
+    # the step's PI batch above is launch-bound at S samples
+    n_pi = TOTAL_SIMS
+    rec_pi = torch.empty(n_pi * rec_sz, dtype=torch.uint8, device="cuda")
+    ctx.run_device(sc_p, 0, n_pi, rec_pi.data_ptr())
+    pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    torch.cuda.synchronize()
+    pe[0].record(stream)
+    ctx.run_device(sc_p, 0, n_pi, rec_pi.data_ptr())
+    pe[1].record(stream)
+    torch.cuda.synchronize()
+    pi_cfg1_s = pe[0].elapsed_time(pe[1]) / 1e3
+
     # final statistics: gather the last timed step's records from every rank (NCCL)
     last_n, last_p = rec_n[W + K - 1], rec_p[W + K - 1]
     if world > 1:
@@ -352,6 +365,10 @@ def run_ours(args):
                                  "is the FP64 issue rate (peak_nonfma_issue)"},
             "pi": {"kernel_ms_per_step": 1e3 * pi_kernel_s / K, "sims_per_s_kernel": S * K / pi_kernel_s,
                    "achieved_tflops": pi_flops / pi_kernel_s / 1e12},
+            "pi_config1": {"n_sims": n_pi, "ms": 1e3 * pi_cfg1_s, "sims_per_s": n_pi / pi_cfg1_s,
+                           "achieved_tflops": workmodel.pi_flops(n_pi * 720) / pi_cfg1_s / 1e12,
+                           "note": "BASELINE config 1 (PI, 30k samples, per-sim parameters) as one launch, "
+                                   "device-timed; reference PI rate: cpu_baseline.pi_only_sims_per_s"},
             "work_per_nmpc_sample": {k: float(cn[k].sum()) / (S * K) for k in cn.dtype.names},
             "clocks": clocks,
             "stats_last_step": stats,
