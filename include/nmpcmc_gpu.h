@@ -182,7 +182,9 @@ enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2, NMPCMC_OPT_L
 enum { NMPCMC_NMPC_KERNEL_WARP = 1, NMPCMC_NMPC_KERNEL_THREAD = 2, NMPCMC_NMPC_KERNEL_GENERIC = 3,
        NMPCMC_NMPC_KERNEL_GENERIC_WARP = 4 };
 int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value);
-/* CUDA stream the context launches on (as void*; 0 = legacy default). */
+/* CUDA stream the context launches on (as void*; 0 = legacy default). The
+ * new stream is ordered after all work already enqueued on the old stream and
+ * its lanes (join + event), because launches share the context's workspace. */
 int nmpcmc_gpu_set_stream(nmpcmc_gpu_ctx* ctx, void* stream);
 
 /* run_monte_carlo over the global sample range [first_sim, first_sim+n_sims)
@@ -226,6 +228,69 @@ int nmpcmc_gpu_aggregate(const nmpcmc_sim_record* records, int64_t n, nmpcmc_agg
 /* phi_histogram (montecarlo.cpp:268-304), host. edges_out[201], counts_out[200]. */
 int nmpcmc_gpu_histogram(const double* phi, int64_t n, int32_t bins, double* edges_out,
                          int32_t* counts_out, int32_t* nbins_out);
+
+/* ---- Statistics on the device (K4; north_star "final block reduction") --
+ * aggregate_stats (montecarlo.cpp:172-211) and, when counts_out != NULL,
+ * phi_histogram (montecarlo.cpp:268-304; bins <= 0: Freedman-Diaconis,
+ * edges_out[201], counts_out[200]) of DEVICE-resident records, bitwise the
+ * reference's host results: exact integer totals, the serial index-order sums
+ * of the mean and the two-pass variance, a device sort for min / max /
+ * deciles. agg_out may be NULL. nmpcmc_gpu_run computes its agg_out this way. */
+int nmpcmc_gpu_aggregate_device(nmpcmc_gpu_ctx* ctx, const nmpcmc_sim_record* records_dev, int64_t n,
+                                nmpcmc_aggregate* agg_out, int32_t bins, double* edges_out,
+                                int32_t* counts_out, int32_t* nbins_out);
+/* The records of the last nmpcmc_gpu_run / nmpcmc_gpu_run_sharded stay on the
+ * device (all of them, gathered, on device_ids[0] for a multi-device context)
+ * until the next call: their device pointer, count and device id. */
+int nmpcmc_gpu_last_records(nmpcmc_gpu_ctx* ctx, const nmpcmc_sim_record** records_dev, int64_t* n,
+                            int* device);
+/* phi_histogram of the last run's records, on the device (see above). */
+int nmpcmc_gpu_histogram_last(nmpcmc_gpu_ctx* ctx, int32_t bins, double* edges_out, int32_t* counts_out,
+                              int32_t* nbins_out);
+/* Work counters of the last run summed over all samples, devices and ranks
+ * (an NCCL int64 all-reduce when several GPUs took part). */
+int nmpcmc_gpu_last_totals(const nmpcmc_gpu_ctx* ctx, nmpcmc_work_counters* out);
+
+/* ---- Multi-GPU --------------------------------
+ * run_monte_carlo's worker pool (montecarlo.cpp:213-251) across the GPUs of
+ * one process: a context over n_devices devices, one sub-context (stream,
+ * workspace) per id. On it nmpcmc_gpu_run shards [first, first + n) into
+ * contiguous blocks (nmpcmc_gpu_shard_range), one host thread per device
+ * launches its block and copies its records into records_out at the block's
+ * offset; the records are then all-gathered over NCCL onto device_ids[0]
+ * (ncclCommInitAll; the only exchange) where K4 computes agg_out, and the
+ * work counters are all-reduced. Records are bitwise independent of the
+ * device count (every stream is keyed by the global sample index).
+ * nmpcmc_gpu_run_async / _join / _wait / _run_traj / _set_option work per
+ * device the same way; _run_device and _set_stream are single-device only.
+ * Repeated ids are allowed (several blocks share a GPU; peer copies replace
+ * NCCL); with distinct ids NCCL is required (loaded with dlopen). On failure
+ * nmpcmc_gpu_last_error(NULL) says why. */
+int nmpcmc_gpu_ctx_create_multi(const int* device_ids, int n_devices, nmpcmc_gpu_ctx** out);
+int nmpcmc_gpu_ctx_num_devices(const nmpcmc_gpu_ctx* ctx);
+/* 1 when records are exchanged over NCCL (distinct devices or ranks). */
+int nmpcmc_gpu_ctx_uses_nccl(const nmpcmc_gpu_ctx* ctx);
+/* Block g of G of [0, n): [g*ceil(n/G), min(n, (g+1)*ceil(n/G))). Host only. */
+void nmpcmc_gpu_shard_range(int64_t n, int g, int G, int64_t* begin, int64_t* count);
+
+/* One process per GPU (torchrun-style launch): rank 0 creates an NCCL id and
+ * ships it to the others out of band; every rank joins with its own
+ * single-device context. nmpcmc_gpu_run_sharded then runs this rank's block
+ * of [first, first + n), all-gathers the records (NCCL) so that
+ * records_out[n] (HOST, may be NULL) holds all of them in index order on every
+ * rank, all-reduces the work counters (nmpcmc_gpu_last_totals) and computes
+ * agg_out (may be NULL) with K4. Without nmpcmc_gpu_comm_init it is
+ * nmpcmc_gpu_run on one GPU. */
+int nmpcmc_gpu_nccl_unique_id(uint8_t id_out[128]);
+int nmpcmc_gpu_comm_init(nmpcmc_gpu_ctx* ctx, const uint8_t id[128], int rank, int nranks);
+int nmpcmc_gpu_run_sharded(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim, int64_t n_sims,
+                           nmpcmc_sim_record* records_out, nmpcmc_aggregate* agg_out);
+/* The exchange alone, for callers that run their blocks themselves (e.g.
+ * with nmpcmc_gpu_run_device): all-gather `chunk` DEVICE records from every
+ * rank into all_dev[nranks * chunk] (rank r's at r * chunk), enqueued on the
+ * context stream (NCCL; a device copy with one rank). */
+int nmpcmc_gpu_allgather_records(nmpcmc_gpu_ctx* ctx, const nmpcmc_sim_record* local_dev, int64_t chunk,
+                                 nmpcmc_sim_record* all_dev);
 
 /* Unit-level device entry points (parity tests of rng.cpp and the libm). */
 /* CounterRng::philox_block (rng.cpp:31-43): in[6*n] = counter[4], key[2]; out[4*n]. */

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libnmpcmc_gpu.so")
-SOURCES = ["nmpcmc_gpu.cu", "host_api.cpp"]
+SOURCES = ["nmpcmc_gpu.cu", "nmpcmc_multi.cu", "host_api.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [
@@ -42,7 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
     cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", out]
+           *[os.path.join(CSRC, s) for s in SOURCES], "-ldl", "-o", out]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(LIBDIR, "build.log") if out == LIB else out + ".build.log"
     with open(log, "w") as fh:

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "nmpc_kernel.cuh"
 #include "nmpc_tps_kernel.cuh"
@@ -17,77 +19,13 @@
 #include "nmpcmc_gpu.h"
 #include "pi_kernel.cuh"
 #include "qp_batch_kernel.cuh"
-
-/// Where one launch runs and the workspace it owns. The context's own target
-/// uses ctx->stream; with NMPCMC_OPT_LANES = 2, NMPC launches alternate
-/// between two lanes and PI launches use a third, each lane with its own
-/// stream and workspace, so a batch's drain overlaps the next batch.
-struct Lane {
-    cudaStream_t stream = nullptr;
-    cudaEvent_t done = nullptr;
-    bool pending = false;
-    void* d_gws = nullptr;
-    size_t gws_cap = 0;
-    void* d_counter = nullptr;
-    size_t counter_cap = 0;
-    void* d_ws = nullptr;
-    size_t ws_cap = 0;
-    void* d_rec = nullptr;
-    size_t rec_cap = 0;
-    void* d_cnt = nullptr;
-    size_t cnt_cap = 0;
-};
-
-struct nmpcmc_gpu_ctx {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    std::string err;
-    void* d_rec = nullptr;
-    size_t rec_cap = 0;
-    void* d_cnt = nullptr;
-    size_t cnt_cap = 0;
-    void* d_traj = nullptr;
-    size_t traj_cap = 0;
-    void* d_scratch = nullptr;
-    size_t scratch_cap = 0;
-    void* d_ws = nullptr;  // K3b structure-of-arrays workspace
-    size_t ws_cap = 0;
-    void* d_gws = nullptr;  // K3 per-block global workspace
-    size_t gws_cap = 0;
-    void* d_counter = nullptr;  // K3 work counter
-    size_t counter_cap = 0;
-    int sm_count = 0;
-    int nmpc_kernel = NMPCMC_NMPC_KERNEL_WARP;    // which NMPC kernel to launch
-    int tps_warps_per_sm = 8;                     // K3b resident warps per SM
-    cudaStream_t own = nullptr;                   // the stream ctx_create made (set_stream may replace ctx->stream)
-    int lanes = 1;                                // NMPCMC_OPT_LANES
-    int next_nmpc_lane = 0;
-    Lane lane[3];
-    cudaEvent_t fork = nullptr;
-};
+#include "ctx_internal.h"
 
 namespace {
 
-int fail(nmpcmc_gpu_ctx* ctx, int code, const std::string& msg) {
-    if (ctx) ctx->err = msg;
-    return code;
-}
-
-int cuda_check(nmpcmc_gpu_ctx* ctx, cudaError_t e, const char* what) {
-    if (e == cudaSuccess) return NMPCMC_OK;
-    return fail(ctx, NMPCMC_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-int ensure(nmpcmc_gpu_ctx* ctx, void** buf, size_t* cap, size_t need) {
-    if (need <= *cap) return NMPCMC_OK;
-    if (*buf) cudaFree(*buf);
-    *buf = nullptr;
-    *cap = 0;
-    cudaError_t e = cudaMalloc(buf, need);
-    if (e != cudaSuccess) return cuda_check(ctx, e, "cudaMalloc");
-    *cap = need;
-    return NMPCMC_OK;
-}
+using nmpcmc_host::cuda_check;
+using nmpcmc_host::ensure;
+using nmpcmc_host::fail;
 
 /// Launch target: a stream and the workspace buffers the launch may use.
 struct Target {
@@ -218,6 +156,10 @@ int nmpcmc_gpu_ctx_create(int device, nmpcmc_gpu_ctx** out) {
 
 void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx) {
     if (ctx == nullptr) return;
+    for (size_t g = 0; g < ctx->comms.size(); ++g)
+        if (ctx->comms[g]) nmpcmc_host::nccl().CommDestroy(ctx->comms[g]);
+    for (nmpcmc_gpu_ctx* s : ctx->subs) nmpcmc_gpu_ctx_destroy(s);
+    if (ctx->comm) nmpcmc_host::nccl().CommDestroy(ctx->comm);
     cudaSetDevice(ctx->device);
     for (Lane& l : ctx->lane) {
         if (l.stream) {
@@ -230,17 +172,22 @@ void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx) {
     }
     if (ctx->fork) cudaEventDestroy(ctx->fork);
     if (ctx->own) cudaStreamDestroy(ctx->own);
-    for (void* p : {ctx->d_rec, ctx->d_cnt, ctx->d_traj, ctx->d_scratch, ctx->d_ws, ctx->d_gws, ctx->d_counter})
+    for (void* p : {ctx->d_rec, ctx->d_cnt, ctx->d_traj, ctx->d_scratch, ctx->d_ws, ctx->d_gws, ctx->d_counter,
+                    ctx->d_k4, ctx->d_all, ctx->d_state, ctx->d_tot})
         if (p) cudaFree(p);
     delete ctx;
 }
 
 const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx) {
-    return ctx ? ctx->err.c_str() : "null context";
+    return ctx ? ctx->err.c_str() : nmpcmc_host::create_error().c_str();
 }
 
 int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value) {
     if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    for (nmpcmc_gpu_ctx* s : ctx->subs) {
+        const int rc = nmpcmc_gpu_set_option(s, option, value);
+        if (rc != NMPCMC_OK) return rc;
+    }
     switch (option) {
         case NMPCMC_OPT_NMPC_KERNEL:
             if (value < NMPCMC_NMPC_KERNEL_WARP || value > NMPCMC_NMPC_KERNEL_GENERIC_WARP)
@@ -263,8 +210,21 @@ int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value) {
 
 int nmpcmc_gpu_set_stream(nmpcmc_gpu_ctx* ctx, void* stream) {
     if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    if (!ctx->subs.empty()) return fail(ctx, NMPCMC_UNSUPPORTED, "set_stream: one stream per device on a multi-device context");
+    cudaStream_t next = static_cast<cudaStream_t>(stream);
+    if (next == ctx->stream) return NMPCMC_OK;
+    cudaSetDevice(ctx->device);
     nmpcmc_gpu_join(ctx);  // lanes stay ordered before later work on the old stream
-    ctx->stream = static_cast<cudaStream_t>(stream);
+    // every launch shares the context's workspace and work counter, so work
+    // on the new stream must start after everything on the old one: an event
+    // on the old stream after the join, waited on by the new stream
+    int rc;
+    if (ctx->fork == nullptr &&
+        (rc = cuda_check(ctx, cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming), "event")) != NMPCMC_OK)
+        return rc;
+    if ((rc = cuda_check(ctx, cudaEventRecord(ctx->fork, ctx->stream), "event record")) != NMPCMC_OK) return rc;
+    if ((rc = cuda_check(ctx, cudaStreamWaitEvent(next, ctx->fork, 0), "stream wait")) != NMPCMC_OK) return rc;
+    ctx->stream = next;
     return NMPCMC_OK;
 }
 
@@ -273,6 +233,8 @@ int nmpcmc_gpu_run_device(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64
                           nmpcmc_work_counters* counters_dev) {
     if (ctx == nullptr || sc == nullptr || (records_dev == nullptr && n_sims > 0) || n_sims < 0)
         return NMPCMC_INVALID_ARGUMENT;
+    if (!ctx->subs.empty())
+        return fail(ctx, NMPCMC_UNSUPPORTED, "run_device: device buffers are per device; use run / run_async");
     int32_t nbar = 0;
     int rc = nmpcmc_gpu_validate(sc, &nbar);
     if (rc != NMPCMC_OK) return fail(ctx, rc, "scenario validation failed");
@@ -292,6 +254,7 @@ int nmpcmc_gpu_run_async(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_
                          nmpcmc_work_counters* counters_out) {
     if (ctx == nullptr || sc == nullptr || records_out == nullptr || n_sims < 1)
         return NMPCMC_INVALID_ARGUMENT;
+    if (!ctx->subs.empty()) return nmpcmc_host::multi_run_async(ctx, sc, first_sim, n_sims, records_out, counters_out);
     int32_t nbar = 0;
     int rc = nmpcmc_gpu_validate(sc, &nbar);
     if (rc != NMPCMC_OK) return fail(ctx, rc, "scenario validation failed");
@@ -322,6 +285,7 @@ int nmpcmc_gpu_run_async(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_
 
 int nmpcmc_gpu_join(nmpcmc_gpu_ctx* ctx) {
     if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    for (nmpcmc_gpu_ctx* s : ctx->subs) nmpcmc_gpu_join(s);
     for (Lane& l : ctx->lane)
         if (l.pending) {
             cudaStreamWaitEvent(ctx->stream, l.done, 0);
@@ -332,6 +296,10 @@ int nmpcmc_gpu_join(nmpcmc_gpu_ctx* ctx) {
 
 int nmpcmc_gpu_wait(nmpcmc_gpu_ctx* ctx) {
     if (ctx == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    for (nmpcmc_gpu_ctx* s : ctx->subs) {
+        const int rc = nmpcmc_gpu_wait(s);
+        if (rc != NMPCMC_OK) return fail(ctx, rc, s->err);
+    }
     cudaSetDevice(ctx->device);
     nmpcmc_gpu_join(ctx);
     return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "kernel execution");
@@ -340,10 +308,34 @@ int nmpcmc_gpu_wait(nmpcmc_gpu_ctx* ctx) {
 int nmpcmc_gpu_run(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t first_sim,
                    int64_t n_sims, nmpcmc_sim_record* records_out,
                    nmpcmc_work_counters* counters_out, nmpcmc_aggregate* agg_out) {
-    int rc = nmpcmc_gpu_run_async(ctx, sc, first_sim, n_sims, records_out, counters_out);
+    if (ctx == nullptr || sc == nullptr || records_out == nullptr || n_sims < 1)
+        return NMPCMC_INVALID_ARGUMENT;
+    if (!ctx->subs.empty())
+        return nmpcmc_host::multi_run(ctx, sc, first_sim, n_sims, records_out, counters_out, agg_out);
+    // one device: launch, statistics on the device (K4) while the records and
+    // counters stream back, one host wait
+    nmpcmc_sim_record* dr = nullptr;
+    nmpcmc_work_counters* dc = nullptr;
+    int rc = nmpcmc_host::run_to_device(ctx, *sc, first_sim, n_sims, n_sims, true, &dr, &dc);
     if (rc != NMPCMC_OK) return rc;
-    if ((rc = nmpcmc_gpu_wait(ctx)) != NMPCMC_OK) return rc;
-    if (agg_out) return nmpcmc_gpu_aggregate(records_out, n_sims, agg_out);
+    if ((rc = ensure(ctx, &ctx->d_tot, &ctx->tot_cap, 64)) != NMPCMC_OK) return rc;
+    if ((rc = nmpcmc_host::counters_sum(ctx, ctx->stream, dc, n_sims, static_cast<long long*>(ctx->d_tot))) !=
+        NMPCMC_OK)
+        return rc;
+    long long tot[8];
+    cudaError_t e = cudaMemcpyAsync(tot, ctx->d_tot, sizeof tot, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(records_out, dr, (size_t)n_sims * sizeof(nmpcmc_sim_record), cudaMemcpyDeviceToHost,
+                            ctx->stream);
+    if (e == cudaSuccess && counters_out)
+        e = cudaMemcpyAsync(counters_out, dc, (size_t)n_sims * sizeof(nmpcmc_work_counters), cudaMemcpyDeviceToHost,
+                            ctx->stream);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "cudaMemcpyAsync");
+    if ((rc = cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "kernel execution")) != NMPCMC_OK) return rc;
+    ctx->last_totals = nmpcmc_work_counters{tot[0], tot[1], tot[2], tot[3], tot[4], tot[5], tot[6], tot[7]};
+    ctx->last_rec = dr;
+    ctx->last_n = n_sims;
+    if (agg_out) return nmpcmc_host::k4_run(ctx, ctx->stream, dr, n_sims, agg_out, 0, nullptr, nullptr, nullptr);
     return NMPCMC_OK;
 }
 
@@ -351,6 +343,26 @@ int nmpcmc_gpu_run_traj(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t
                         int64_t n_sims, nmpcmc_sim_record* records_out, double* traj_out) {
     if (ctx == nullptr || sc == nullptr || records_out == nullptr || traj_out == nullptr || n_sims < 1)
         return NMPCMC_INVALID_ARGUMENT;
+    if (!ctx->subs.empty()) {
+        // one host thread per device, each on its contiguous block
+        const int G = (int)ctx->subs.size();
+        const int64_t rows = nmpcmc_gpu_traj_rows(sc);
+        std::vector<int> rcs(G, NMPCMC_OK);
+        std::vector<std::thread> pool;
+        for (int g = 0; g < G; ++g) {
+            int64_t b = 0, cnt = 0;
+            nmpcmc_gpu_shard_range(n_sims, g, G, &b, &cnt);
+            if (cnt == 0) continue;
+            pool.emplace_back([&, g, b, cnt] {
+                rcs[g] = nmpcmc_gpu_run_traj(ctx->subs[g], sc, first_sim + (uint64_t)b, cnt, records_out + b,
+                                             traj_out + (size_t)b * rows * 5);
+            });
+        }
+        for (std::thread& t : pool) t.join();
+        for (int g = 0; g < G; ++g)
+            if (rcs[g] != NMPCMC_OK) return fail(ctx, rcs[g], ctx->subs[g]->err);
+        return NMPCMC_OK;
+    }
     int32_t nbar = 0;
     int rc = nmpcmc_gpu_validate(sc, &nbar);
     if (rc != NMPCMC_OK) return fail(ctx, rc, "scenario validation failed");
@@ -377,6 +389,31 @@ int nmpcmc_gpu_run_traj(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, uint64_t
 }
 
 }  // extern "C"
+
+namespace nmpcmc_host {
+
+/// Launch [first, first + n) on the context's own stream into its device
+/// record / counter buffers, sized for at least `cap` samples (a sharded run
+/// sizes every block's buffer for the largest block, so an empty block still
+/// owns a buffer the all-gather can read). Enqueued only.
+int run_to_device(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario& sc, uint64_t first, int64_t n, int64_t cap,
+                  bool want_counters, nmpcmc_sim_record** d_rec, nmpcmc_work_counters** d_cnt) {
+    int32_t nbar = 0;
+    int rc = nmpcmc_gpu_validate(&sc, &nbar);
+    if (rc != NMPCMC_OK) return fail(ctx, rc, "scenario validation failed");
+    cudaSetDevice(ctx->device);
+    nmpcmc_gpu_join(ctx);
+    const int64_t c = std::max<int64_t>(std::max(cap, n), 1);
+    if ((rc = ensure(ctx, &ctx->d_rec, &ctx->rec_cap, (size_t)c * sizeof(nmpcmc_sim_record))) != NMPCMC_OK) return rc;
+    if (want_counters &&
+        (rc = ensure(ctx, &ctx->d_cnt, &ctx->cnt_cap, (size_t)c * sizeof(nmpcmc_work_counters))) != NMPCMC_OK)
+        return rc;
+    *d_rec = static_cast<nmpcmc_sim_record*>(ctx->d_rec);
+    *d_cnt = want_counters ? static_cast<nmpcmc_work_counters*>(ctx->d_cnt) : nullptr;
+    return launch(ctx, main_target(ctx), sc, first, n, nbar, *d_rec, *d_cnt, nullptr, 0);
+}
+
+}  // namespace nmpcmc_host
 
 // ------------------------------------------------------- unit entry points
 namespace {

@@ -42,7 +42,9 @@ __device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, in
     }
     int status = ST_OK;
     int row = 0;
+    int steps = 0;  // control steps entered (a failing step counts: its work ran)
     for (int i = 0; i < nbar; ++i) {
+        ++steps;
         const double y = measure<NX>(p, pl, has_R, lR, rng);
         // pi_step (controllers.cpp:12-23), evaluated in the documented order
         const double ybar = setpoint_at(sc, t);
@@ -90,7 +92,7 @@ __device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, in
     rec->status = status;
     if (cnt != nullptr) {
         nmpcmc_work_counters c = {};
-        c.control_steps = nbar;
+        c.control_steps = steps;
         *cnt = c;
     }
     (void)traj_rows;

@@ -5,9 +5,11 @@ The reference's only parallelism is a std::thread pool over sample indices
 GLOBAL sample indices -- [g*ceil(n/G), min(n, (g+1)*ceil(n/G)))
 -- and every random stream is keyed by the global index, so records are
 bitwise independent of the number of GPUs. The data path has no collective;
-the single exchange is the final gather of the 24-byte per-sample records
-(all_gather over NCCL on GPUs, gloo in the CPU tests), after which rank 0
-computes aggregate_stats in index order exactly like the single-process call.
+the single exchange is the final gather of the 24-byte per-sample records,
+done by the library itself over NCCL (nmpcmc_gpu_run_sharded), after which
+K4 computes aggregate_stats in index order exactly like the single-process
+call. shard() and gather_records() restate the sharding / gather contract
+in Python for the multi-process CPU tests (gloo).
 """
 from typing import Optional, Tuple
 
@@ -46,9 +48,14 @@ def gather_records(local: np.ndarray, n_sims: int, rank: int, world: int, device
 
 
 def run_monte_carlo_distributed(sc, n_sims: int, local_rank: Optional[int] = None, counters: bool = False):
-    """run_monte_carlo over all ranks of the default process group: each rank
-    runs its shard on its GPU, records are gathered (NCCL), and every rank
-    returns the same McResult (aggregate computed from the gathered records)."""
+    """run_monte_carlo over all ranks of the default process group, one GPU
+    per rank. The data path and the exchange are the library's own C++
+    (nmpcmc_gpu_comm_init + nmpcmc_gpu_run_sharded): each rank runs its
+    contiguous block, the 24 B records are all-gathered and the work counters
+    all-reduced over NCCL inside the library, and K4 computes the aggregate on
+    the device. torch.distributed only ships the 128-byte NCCL id from rank 0
+    (out of band, as NCCL expects). Every rank returns the same McResult;
+    `counters` returns the all-reduced totals dict instead of per-sample rows."""
     import time
 
     import torch
@@ -58,14 +65,13 @@ def run_monte_carlo_distributed(sc, n_sims: int, local_rank: Optional[int] = Non
 
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = local_rank if local_rank is not None else torch.cuda.current_device()
-    first, count = shard(n_sims, rank, world)
-    ctx = engine._context(dev)
-    t0 = time.perf_counter()
-    rec = np.zeros(0, dtype=abi.RECORD_DTYPE)
-    cnt = None
-    if count:
-        rec, cnt = ctx.run(sc, first, count, counters=counters)
+    ctx = engine.Context(dev)
+    box = [engine.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    ctx.comm_init(box[0], rank, world)
     dist.barrier()
+    t0 = time.perf_counter()
+    allrec, agg = ctx.run_sharded(sc, 0, n_sims)
     wall = time.perf_counter() - t0
-    allrec = gather_records(rec, n_sims, rank, world, device=torch.device("cuda", dev))
-    return engine.McResult(allrec, engine.aggregate_stats(allrec), wall, cnt, 0)
+    totals = ctx.last_totals() if counters else None
+    return engine.McResult(allrec, agg, wall, totals, 0)

@@ -108,6 +108,23 @@ def library():
     lib.nmpcmc_gpu_normals.argtypes = [P, C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(C.c_double)]
     lib.nmpcmc_gpu_libm.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double)]
     lib.nmpcmc_gpu_fp64_peak.argtypes = [P, C.c_int, C.POINTER(C.c_double)]
+    # K4 (device statistics) and the multi-GPU forms
+    lib.nmpcmc_gpu_aggregate_device.argtypes = [P, P, C.c_int64, A, C.c_int32, C.POINTER(C.c_double),
+                                                C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    lib.nmpcmc_gpu_last_records.argtypes = [P, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int)]
+    lib.nmpcmc_gpu_histogram_last.argtypes = [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int32),
+                                              C.POINTER(C.c_int32)]
+    lib.nmpcmc_gpu_last_totals.argtypes = [P, W]
+    lib.nmpcmc_gpu_ctx_create_multi.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(P)]
+    lib.nmpcmc_gpu_ctx_num_devices.argtypes = [P]
+    lib.nmpcmc_gpu_ctx_uses_nccl.argtypes = [P]
+    lib.nmpcmc_gpu_shard_range.argtypes = [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_int64)]
+    lib.nmpcmc_gpu_shard_range.restype = None
+    lib.nmpcmc_gpu_nccl_unique_id.argtypes = [C.c_void_p]
+    lib.nmpcmc_gpu_comm_init.argtypes = [P, C.c_void_p, C.c_int, C.c_int]
+    lib.nmpcmc_gpu_run_sharded.argtypes = [P, S, C.c_uint64, C.c_int64, R, A]
+    lib.nmpcmc_gpu_allgather_records.argtypes = [P, P, C.c_int64, P]
     _lib = lib
     return lib
 
@@ -123,15 +140,47 @@ def _ptr(a: np.ndarray, ctype):
     return a.ctypes.data_as(C.POINTER(ctype))
 
 
-class Context:
-    """One device + one CUDA stream (C ABI nmpcmc_gpu_ctx)."""
+def shard_range(n: int, g: int, G: int):
+    """(begin, count) of block g of G of [0, n) (nmpcmc_gpu_shard_range, host)."""
+    b, c = C.c_int64(0), C.c_int64(0)
+    library().nmpcmc_gpu_shard_range(n, g, G, C.byref(b), C.byref(c))
+    return b.value, c.value
 
-    def __init__(self, device: int = 0):
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id for nmpcmc_gpu_comm_init (create on rank 0, ship to the others)."""
+    buf = (C.c_uint8 * 128)()
+    _raise(library().nmpcmc_gpu_nccl_unique_id(buf), "NCCL unique id")
+    return bytes(buf)
+
+
+class Context:
+    """One device + one CUDA stream (C ABI nmpcmc_gpu_ctx); or, with
+    devices=[...], one sub-context per GPU of this process
+    (nmpcmc_gpu_ctx_create_multi: runs shard by global index, records are
+    gathered over NCCL)."""
+
+    def __init__(self, device: int = 0, devices=None):
         self.lib = library()
         h = C.c_void_p()
-        _raise(self.lib.nmpcmc_gpu_ctx_create(device, C.byref(h)), f"device {device}")
+        if devices is None:
+            _raise(self.lib.nmpcmc_gpu_ctx_create(device, C.byref(h)), f"device {device}")
+            self.device = device
+        else:
+            ids = (C.c_int * len(devices))(*devices)
+            rc = self.lib.nmpcmc_gpu_ctx_create_multi(ids, len(devices), C.byref(h))
+            if rc != 0:
+                _raise(rc, self.lib.nmpcmc_gpu_last_error(None).decode())
+            self.device = devices[0]
         self.handle = h
-        self.device = device
+
+    @property
+    def num_devices(self) -> int:
+        return self.lib.nmpcmc_gpu_ctx_num_devices(self.handle)
+
+    @property
+    def uses_nccl(self) -> bool:
+        return self.lib.nmpcmc_gpu_ctx_uses_nccl(self.handle) == 1
 
     def close(self):
         if self.handle:
@@ -163,14 +212,71 @@ class Context:
     def set_stream(self, stream_ptr: int):
         self._check(self.lib.nmpcmc_gpu_set_stream(self.handle, C.c_void_p(stream_ptr)))
 
-    def run(self, sc, first_sim: int, n_sims: int, counters: bool = False):
-        """Records (numpy, index order) and optional work counters; host buffers."""
+    def run(self, sc, first_sim: int, n_sims: int, counters: bool = False, aggregate: bool = False):
+        """Records (numpy, index order) and optional work counters; host
+        buffers. aggregate=True also returns the device-computed (K4)
+        aggregate_stats dict as a third value."""
         rec = np.zeros(n_sims, dtype=abi.RECORD_DTYPE)
         cnt = np.zeros(n_sims, dtype=abi.COUNTERS_DTYPE) if counters else None
+        agg = abi.Aggregate() if aggregate else None
         self._check(self.lib.nmpcmc_gpu_run(
             self.handle, C.byref(sc), first_sim, n_sims, _ptr(rec, abi.SimRecord),
-            _ptr(cnt, abi.WorkCounters) if cnt is not None else None, None))
+            _ptr(cnt, abi.WorkCounters) if cnt is not None else None, C.byref(agg) if agg is not None else None))
+        if aggregate:
+            return rec, cnt, abi.aggregate_to_dict(agg)
         return rec, cnt
+
+    # ---- K4 statistics on the device
+    def aggregate_device(self, records_dev_ptr: int, n: int, bins: Optional[int] = None):
+        """aggregate_stats (and phi_histogram when bins is not None) of n
+        DEVICE-resident records at records_dev_ptr, on the device."""
+        agg = abi.Aggregate()
+        edges = np.zeros(201)
+        counts = np.zeros(200, dtype=np.int32)
+        nb = C.c_int32(0)
+        want_h = bins is not None
+        self._check(self.lib.nmpcmc_gpu_aggregate_device(
+            self.handle, C.c_void_p(records_dev_ptr), n, C.byref(agg), bins or 0,
+            _ptr(edges, C.c_double) if want_h else None, _ptr(counts, C.c_int32) if want_h else None,
+            C.byref(nb) if want_h else None))
+        h = Histogram(edges[: nb.value + 1].copy(), counts[: nb.value].copy()) if want_h else None
+        return abi.aggregate_to_dict(agg), h
+
+    def histogram_last(self, bins: int = 0) -> "Histogram":
+        """phi_histogram of the last run's records, computed on the device."""
+        edges = np.zeros(201)
+        counts = np.zeros(200, dtype=np.int32)
+        nb = C.c_int32(0)
+        self._check(self.lib.nmpcmc_gpu_histogram_last(self.handle, bins, _ptr(edges, C.c_double),
+                                                       _ptr(counts, C.c_int32), C.byref(nb)))
+        return Histogram(edges[: nb.value + 1].copy(), counts[: nb.value].copy())
+
+    def last_totals(self) -> dict:
+        """Work counters of the last run summed over samples, devices, ranks."""
+        w = abi.WorkCounters()
+        self._check(self.lib.nmpcmc_gpu_last_totals(self.handle, C.byref(w)))
+        return {k: int(getattr(w, k)) for k, _ in abi.WorkCounters._fields_}
+
+    # ---- one process per GPU
+    def comm_init(self, uid: bytes, rank: int, nranks: int):
+        """Join the NCCL communicator of nranks processes (nmpcmc_gpu_comm_init)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self._check(self.lib.nmpcmc_gpu_comm_init(self.handle, buf, rank, nranks))
+
+    def allgather_records(self, local_dev_ptr: int, chunk: int, all_dev_ptr: int):
+        """NCCL all-gather of `chunk` device records per rank (enqueued on the context stream)."""
+        self._check(self.lib.nmpcmc_gpu_allgather_records(self.handle, C.c_void_p(local_dev_ptr), chunk,
+                                                          C.c_void_p(all_dev_ptr)))
+
+    def run_sharded(self, sc, first_sim: int, n_sims: int, records: bool = True, aggregate: bool = True):
+        """This rank's block of [first, first + n), records all-gathered over
+        NCCL (every rank gets all n, index order), K4 aggregate."""
+        rec = np.zeros(n_sims, dtype=abi.RECORD_DTYPE) if records else None
+        agg = abi.Aggregate() if aggregate else None
+        self._check(self.lib.nmpcmc_gpu_run_sharded(
+            self.handle, C.byref(sc), first_sim, n_sims, _ptr(rec, abi.SimRecord) if rec is not None else None,
+            C.byref(agg) if agg is not None else None))
+        return rec, (abi.aggregate_to_dict(agg) if agg is not None else None)
 
     def set_lanes(self, lanes: int):
         """NMPCMC_OPT_LANES: 2 pipelines consecutive batches over two internal

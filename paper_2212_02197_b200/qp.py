@@ -16,7 +16,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import engine
+from . import abi, engine
 
 OPTIMAL, MAXITER, FAILED, DOMAIN_ERROR, NOT_POSITIVE_DEFINITE = range(5)
 STATUS_NAMES = {OPTIMAL: "Optimal", MAXITER: "MaxIter", FAILED: "Failed", DOMAIN_ERROR: "DomainError",
@@ -83,6 +83,9 @@ def solve_qp_batch(qps_or_packed, nx: int = None, nu: int = None, tol: float = 1
         packed = np.ascontiguousarray(qps_or_packed, dtype=np.float64)
         if nx is None or nu is None:
             raise ValueError("packed input needs nx, nu")
+        if packed.ndim != 3 or packed.shape[2] != stage_doubles(nx, nu) or packed.shape[1] < 2:
+            raise engine.DimensionMismatch(
+                f"packed QP batch must have shape (batch, N+1 >= 2, {stage_doubles(nx, nu)}), got {packed.shape}")
     else:
         qps = qps_or_packed
         if nu is None:
@@ -171,15 +174,28 @@ def solve_ocp_batch(sc, x0, t0, xi0=None, ctx=None):
     state x0[b] (shape (B, nx)) at time t0[b]; cold start as nmpc_step unless
     xi0 (B, L) is given. Returns a dict of numpy arrays: xi (B, L), lambda
     (B, N nx), pi_l, pi_u (B, N), converged, status (B,)."""
-    x0 = np.ascontiguousarray(np.atleast_2d(x0), dtype=np.float64)
-    t0 = np.ascontiguousarray(t0, dtype=np.float64).reshape(-1)
-    B, nx, N = x0.shape[0], x0.shape[1], sc.N
+    # the controller model fixes the state width (the C ABI reads nx from
+    # sc.ctrl_variant and copies B*nx / B*L doubles): check every buffer
+    # against it before anything crosses the boundary (nmpcmc_gpu.hpp)
+    nx, N = (3 if sc.ctrl_variant == abi.THREE_STATE else 1), sc.N
     L = N * (1 + nx)
+    x0 = np.asarray(x0, dtype=np.float64)
+    if x0.ndim == 1 and nx == 1:
+        x0 = x0.reshape(-1, 1)
+    if x0.ndim != 2 or x0.shape[1] != nx:
+        raise engine.LengthMismatch(f"solve_ocp_batch: x0 must have shape (B, {nx}), got {x0.shape}")
+    x0 = np.ascontiguousarray(x0)
+    B = x0.shape[0]
+    t0 = np.ascontiguousarray(t0, dtype=np.float64).reshape(-1)
+    if t0.size != B:
+        raise engine.LengthMismatch(f"solve_ocp_batch: t0 needs {B} entries, got {t0.size}")
     out = dict(xi=np.zeros((B, L)), **{"lambda": np.zeros((B, N * nx))}, pi_l=np.zeros((B, N)),
                pi_u=np.zeros((B, N)), converged=np.zeros(B, dtype=np.int32), status=np.zeros(B, dtype=np.int32))
     xi0p = None
     if xi0 is not None:
         xi0 = np.ascontiguousarray(xi0, dtype=np.float64)
+        if xi0.shape != (B, L):
+            raise engine.LengthMismatch(f"solve_ocp_batch: xi0 must have shape ({B}, {L}), got {xi0.shape}")
         xi0p = xi0.ctypes.data_as(C.POINTER(C.c_double))
     P = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
     ctx = ctx or engine._context(0)

@@ -8,7 +8,7 @@ tools/src/main.cpp:3-6). The keys and columns here are stable, and every file
 embeds the effective scenario and base seed, so any result can be re-derived
 from its own header (SPEC.md cli "Invariants & Properties"). Floats are written
 with Python's shortest round-trip repr, so files reload bit for bit. NaN and
-infinities become JSON null.
+infinities become the strings "nan", "inf", "-inf".
 """
 import csv
 import ctypes as C
@@ -25,9 +25,20 @@ FORMAT_VERSION = 1
 
 
 def _plain(x):
-    if isinstance(x, float):
-        return x if math.isfinite(x) else None
+    """Non-finite floats become the strings "inf", "-inf", "nan" (JSON has
+    no literal for them), so unbounded inputs round-trip bit for bit."""
+    if isinstance(x, float) and not math.isfinite(x):
+        return "nan" if math.isnan(x) else ("inf" if x > 0 else "-inf")
     return x
+
+
+def _num(v):
+    """Inverse of _plain (None from version-1 files reads as NaN)."""
+    if v is None:
+        return float("nan")
+    if isinstance(v, str):
+        return float(v)
+    return v
 
 
 def _struct_to_dict(s) -> dict:
@@ -69,9 +80,9 @@ def _fill(s, d: dict):
             _fill(cur, v)
         elif isinstance(cur, C.Array):
             for i, e in enumerate(v):
-                cur[i] = float("nan") if e is None else e
+                cur[i] = _num(e)
         else:
-            setattr(s, name, float("nan") if v is None else v)
+            setattr(s, name, _num(v))
 
 
 def scenario_from_dict(d: dict) -> abi.Scenario:

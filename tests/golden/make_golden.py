@@ -148,6 +148,25 @@ def gen_ocp():
     np.savez_compressed(os.path.join(OUT, "ocp_batch.npz"), **out)
 
 
+def gen_full():
+    """Round 2: full-length (720-step) pins of the configs that carry the
+    claims: the bench's config 3 (N=60, perturbed) at
+    indices 0.. and inside the bench's own index range (9,472..), config 4 at
+    N=30 and N=120, config 3 with the three-state controller model, and 1,000
+    samples of config 2 (both libm variants) for the distribution test."""
+    gen_case("nmpc_cfg3_full", dict(controller="nmpc", N=60, perturb=True), 64, 1)
+    gen_case("nmpc_cfg3_full_b", dict(controller="nmpc", N=60, perturb=True), 32, 0, first=9472)
+    gen_case("nmpc_cfg4_n30_full", dict(controller="nmpc", N=30, perturb=True), 32, 0)
+    gen_case("nmpc_cfg4_n120_full", dict(controller="nmpc", N=120, perturb=True), 32, 0)
+    gen_case("nmpc3_cfg3_full", dict(controller="nmpc", N=60, perturb=True, ctrl_variant=0), 16, 0)
+
+
+def gen_dist():
+    """1,000 samples of BASELINE config 2 (N=60, unperturbed, 720 steps) in
+    both libm variants: the Φ-distribution test's reference sample."""
+    gen_case("nmpc_cfg2_1000", dict(controller="nmpc", N=60), 1000, 0)
+
+
 def main(which):
     if which in ("rng", "all"):
         gen_rng()
@@ -168,6 +187,10 @@ def main(which):
         gen_qp()
     if which in ("ocp", "all"):
         gen_ocp()
+    if which in ("full", "all"):
+        gen_full()
+    if which in ("dist", "all"):
+        gen_dist()
     if which in ("nmpc3", "all"):
         # three-state controller model (config 2 read literally: CD-EKF and
         # OCP on the 3-state CSTR; ctrl_variant 0 = THREE_STATE) -> kernel K3g

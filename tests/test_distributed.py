@@ -71,3 +71,21 @@ def test_gloo_two_ranks_gather_equals_single_process(tmp_path):
         assert_records_equal(got, want)
         a = np.load(tmp_path / f"agg{r}.npy")
         assert a[0] == agg["mean"] and a[1] == agg["variance"] and a[2] == agg["n_failed"]
+
+
+@pytest.mark.parametrize("n,world", [(10, 2), (11, 2), (7, 3), (1, 4), (0, 2), (30000, 8), (1000003, 7)])
+def test_c_abi_shard_range_matches_python(n, world):
+    """nmpcmc_gpu_shard_range (the C++ multi-device / multi-rank split) is
+    the same contiguous split as distributed.shard."""
+    from paper_2212_02197_b200 import engine
+    for r in range(world):
+        assert engine.shard_range(n, r, world) == distributed.shard(n, r, world)
+
+
+def test_multi_device_context_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2212_02197_b200 import engine
+    with pytest.raises(engine.CudaError):
+        engine.Context(devices=[0, 1])

@@ -59,3 +59,16 @@ def test_trajectory_csv(tmp_path):
     np.testing.assert_array_equal(back, want)
     assert meta["rows"] == len(want) and meta["sim_index"] == 0
     assert open(p).read().splitlines()[1] == "t,z,zbar,u,y"
+
+
+def test_unbounded_inputs_round_trip():
+    """Non-finite scenario fields (unbounded inputs) survive the JSON echo
+    bit for bit (they used to come back as NaN)."""
+    sc = configs.make_scenario("nmpc", N=30)
+    sc.u_min, sc.u_max = float("-inf"), float("inf")
+    sc.ctrl.u_max = float("inf")
+    import json
+    d = json.loads(json.dumps(results.scenario_to_dict(sc), allow_nan=False))
+    back = results.scenario_from_dict(d)
+    assert bytes(back) == bytes(sc)
+    assert back.u_min == float("-inf") and back.u_max == float("inf")
