@@ -162,14 +162,14 @@ void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx);
 const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx);
 /* Context options. NMPCMC_OPT_NMPC_KERNEL selects the NMPC kernel for a
  * one-state controller model with N <= 255:
- * WARP (default) = one warp per sample, workspace in shared memory (K3);
- * THREAD = one thread per sample, workspace in HBM (K3b);
+ * WARP (default) = one warp per sample, sweep arrays in shared memory (K3);
  * GENERIC = one thread per sample, any controller state dimension (K3g);
+ * THREAD = alias of GENERIC (the one-thread-per-sample K3b was retired);
  * GENERIC_WARP = one warp per sample, any controller state dimension (K3w).
  * A three-state controller model or N > 255 always runs a generic kernel:
- * K3w, or K3g when GENERIC is selected. Results are
- * bitwise identical; only speed differs. NMPCMC_OPT_TPS_WARPS_PER_SM = resident
- * warps per SM for K3b (default 8). */
+ * K3w, or K3g when GENERIC / THREAD is selected. Results are bitwise
+ * identical; only speed differs. NMPCMC_OPT_TPS_WARPS_PER_SM is accepted and
+ * ignored (it tuned K3b). */
 enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2, NMPCMC_OPT_LANES = 3 };
 /* NMPCMC_OPT_LANES = 2 pipelines back-to-back batches: NMPC launches alternate
  * between two internal streams with their own workspace (PI launches use a

@@ -103,6 +103,76 @@ struct NormalStream {
     }
 };
 
+/// Box-Muller pair p of stream (seed, stream) -- the two normals
+/// NormalStream::normal() returns from Philox block p (rng.cpp:78-91):
+/// c = r cos a (returned first), s = r sin a (the cached spare).
+__device__ __forceinline__ void normal_pair(uint64_t seed, uint64_t stream, uint64_t p, double& c, double& s) {
+    const uint4 ctr = make_uint4((uint32_t)p, (uint32_t)(p >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
+    const uint4 b = philox4x32_10(ctr, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint64_t w0 = ((uint64_t)b.x << 32) | b.y;
+    const uint64_t w1 = ((uint64_t)b.z << 32) | b.w;
+    const double u1 = 1.0 - (double)(w0 >> 11) * 0x1.0p-53;
+    const double u2 = (double)(w1 >> 11) * 0x1.0p-53;
+    const double radius = sqrt(-2.0 * xlibm_log(u1));
+    const double angle = 0x1.921fb54442d18p+2 * u2;
+    double sn, cs;
+    xlibm_sincos(angle, &sn, &cs);
+    s = radius * sn;
+    c = radius * cs;
+}
+
+/// W consecutive pairs from pair0 into buf (element j at buf[j * stride]):
+/// W independent Philox / log / sincos chains, so they overlap (ILP).
+template <int W>
+__device__ __noinline__ void fill_normal_pairs(double* buf, int stride, uint64_t seed, uint64_t stream,
+                                               uint64_t pair0) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        double c, s;
+        normal_pair(seed, stream, pair0 + j, c, s);
+        buf[(2 * j) * stride] = c;
+        buf[(2 * j + 1) * stride] = s;
+    }
+}
+
+/// The normal stream of NormalStream, consumed through a window of W pairs
+/// generated ahead (fill_normal_pairs) instead of one pair per call: the same
+/// sequence bit for bit (normal k is component k & 1 of pair k >> 1), but
+/// the generation leaves the plant's serial Euler-Maruyama chain.
+template <int W>
+struct NormalWindow {
+    double* buf;
+    int stride;
+    uint64_t seed, stream;
+    uint64_t base;  // normal index of buf[0] (even)
+    uint64_t k;     // next normal index
+    __device__ void init(double* b, int st, uint64_t seed_, uint64_t stream_) {
+        buf = b;
+        stride = st;
+        seed = seed_;
+        stream = stream_;
+        k = 0;
+        base = 0;
+        fill_normal_pairs<W>(buf, stride, seed, stream, 0);
+    }
+    /// make normals k .. k+m-1 resident (m <= 2W - 1) with at most one refill
+    __device__ __forceinline__ void reserve(int m) {
+        if (k + (uint64_t)m > base + 2 * W) {
+            base = k & ~1ULL;
+            fill_normal_pairs<W>(buf, stride, seed, stream, base >> 1);
+        }
+    }
+    __device__ __forceinline__ double normal() {
+        if (k >= base + 2 * W) {
+            base = k & ~1ULL;
+            fill_normal_pairs<W>(buf, stride, seed, stream, base >> 1);
+        }
+        const double z = buf[(int)(k - base) * stride];
+        ++k;
+        return z;
+    }
+};
+
 // ------------------------------------------------------------ CSTR model
 constexpr double kMlMinToLs = 1e-3 / 60.0;  // cstr.hpp:46
 
@@ -190,9 +260,8 @@ struct Plant {
 
 /// measure (model.cpp:39-48): y = g(x) + L_R zeta, one normal per call when R
 /// has rows; g = x_T / V (cstr.cpp:86-89).
-template <int NX>
-__device__ __forceinline__ double measure(const Cstr& p, const Plant<NX>& pl, bool has_R, double lR,
-                                          NormalStream& rng) {
+template <int NX, class Rng>
+__device__ __forceinline__ double measure(const Cstr& p, const Plant<NX>& pl, bool has_R, double lR, Rng& rng) {
     double y = pl.x[NX - 1] / p.V;
     if (has_R) {
         const double zeta = rng.normal();
@@ -203,9 +272,9 @@ __device__ __forceinline__ double measure(const Cstr& p, const Plant<NX>& pl, bo
 
 /// simulate_interval (model.cpp:26-37) + euler_maruyama_step (model.cpp:13-24)
 /// for the CSTR (diffusion diag(F sigma_bar), cstr.cpp:55-65). Returns a status.
-template <int NX>
+template <int NX, class Rng>
 __device__ __forceinline__ int simulate_interval(const Cstr& p, Plant<NX>& pl, double t0, double t1,
-                                                 double u, int ns, NormalStream& rng) {
+                                                 double u, int ns, Rng& rng) {
     const double dt = (t1 - t0) / ns;
     const double sqrt_dt = sqrt(dt);
     const double f = u * kMlMinToLs;

@@ -1,0 +1,37 @@
+// k_gen.cu -- K3w / K3g (any controller state dimension) and their OCP batch
+// form; host launchers declared in launchers.h.
+#include "launchers.h"
+#include "nmpc_kernel.cuh"  // shared warp helpers and certified math used by the generic kernels
+#include "nmpc_gen_kernel.cuh"
+
+namespace nmpcmc_launch {
+
+bool genw_fits(const nmpcmc_scenario& sc) { return nmpcmc_dev::gen::genw_fits(sc); }
+int64_t genw_blocks(const nmpcmc_scenario& sc, int sm_count, int64_t n) {
+    return nmpcmc_dev::gen::genw_blocks(sc, sm_count, n);
+}
+int64_t gen_ws_doubles(const nmpcmc_scenario& sc) { return nmpcmc_dev::gen::gen_ws_doubles(sc); }
+int64_t gen_slots(const nmpcmc_scenario& sc, int sm_count, int64_t n) {
+    return nmpcmc_dev::gen::gen_slots(sc, sm_count, n);
+}
+
+int launch_genw(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
+                nmpcmc_work_counters* d_cnt, double* d_traj, int rows, double* ws, int64_t blocks,
+                unsigned long long* counter, cudaStream_t stream) {
+    return nmpcmc_dev::gen::launch_genw(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ws, blocks, counter, stream);
+}
+
+int launch_gen(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
+               nmpcmc_work_counters* d_cnt, double* d_traj, int rows, double* ws, int64_t slots,
+               unsigned long long* counter, cudaStream_t stream) {
+    return nmpcmc_dev::gen::launch_gen(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ws, slots, counter, stream);
+}
+
+int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const double* x0, const double* t0, const double* xi0,
+                     double* xi, double* lam, double* pil, double* piu, int32_t* conv, int32_t* status, double* ws,
+                     int64_t blocks, unsigned long long* counter, cudaStream_t stream) {
+    return nmpcmc_dev::gen::launch_ocp_batch(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv, status, ws, blocks,
+                                             counter, stream);
+}
+
+}  // namespace nmpcmc_launch

@@ -209,7 +209,7 @@ __device__ __forceinline__ int joint_rhs1(const Cstr& p, double x, double P, dou
 }
 
 // ----------------------------------------------------------- workspace
-/// Full per-sample array set; K3b (nmpc_tps_kernel.cuh) lays all of them out
+/// Full per-sample array set (the retired one-thread-per-sample K3b laid all of them out)
 /// in global memory. Stage arrays are indexed by k; for the interleaved
 /// decision vector xi = (u_0, x_1, ..., u_{N-1}, x_N) (ocp.hpp:37-43)
 /// U[k] = u_k and X[k] = x_{k+1}. W blocks: Wr[0] = block 0 (u_0),
@@ -274,7 +274,7 @@ enum IpmId { I_DU, I_DX, I_MU, I_NL, I_NU, I_SL, I_SU, I_RSU, I_RCL, I_RCU, I_DS
 /// Out-of-line IEEE division for the lane-parallel loops: one call site per
 /// use instead of an inlined ~25-instruction sequence keeps the hot code small
 /// (the kernel is instruction-cache bound; see profiles/).
-__device__ __noinline__ double qdiv(double a, double b) { return a / b; }
+static __device__ __noinline__ double qdiv(double a, double b) { return a / b; }
 
 #define SA(id) (smem_nmpc + (id) * ST)
 #define GA(id) (o.gws + (id) * ST)
@@ -1017,7 +1017,7 @@ __device__ __forceinline__ void reset_blocks(int N) {
     __syncwarp();
 }
 
-__device__ __noinline__ double qdiv(double a, double b);
+static __device__ __noinline__ double qdiv(double a, double b);
 
 /// bfgs_block_update (sqp.cpp:61-84) for a block of size n (1 or 2) stored as
 /// (q, m, r) = (w00, w01 = w10, w11). Returns -1 on NotPositiveDefinite,

@@ -13,13 +13,9 @@
 #include <thread>
 #include <vector>
 
-#include "nmpc_kernel.cuh"
-#include "nmpc_tps_kernel.cuh"
-#include "nmpc_gen_kernel.cuh"
-#include "nmpcmc_gpu.h"
-#include "pi_kernel.cuh"
-#include "qp_batch_kernel.cuh"
 #include "ctx_internal.h"
+#include "launchers.h"
+#include "nmpcmc_gpu.h"
 
 namespace {
 
@@ -50,52 +46,42 @@ int launch(nmpcmc_gpu_ctx* ctx, const Target& tg, const nmpcmc_scenario& sc, uin
            nmpcmc_sim_record* d_rec, nmpcmc_work_counters* d_cnt, double* d_traj, int rows) {
     if (n == 0) return NMPCMC_OK;
     if (sc.controller == NMPCMC_CTRL_PI) {
-        const int block = 128;
-        const int64_t grid = (n + block - 1) / block;
-        if (sc.truth_variant == NMPCMC_THREE_STATE)
-            nmpcmc_dev::pi_kernel<3><<<(unsigned)grid, block, 0, tg.stream>>>(
-                sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
-        else
-            nmpcmc_dev::pi_kernel<1><<<(unsigned)grid, block, 0, tg.stream>>>(
-                sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+        nmpcmc_launch::launch_pi(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, tg.stream);
         return cuda_check(ctx, cudaGetLastError(), "pi_kernel launch");
     }
     int rc;
-    const bool generic = sc.ctrl_variant != NMPCMC_ONE_STATE || sc.N > 255 ||
-                         ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC ||
+    // K3 for the one-state model (N <= 255) unless a generic kernel is asked
+    // for; THREAD (the retired one-thread-per-sample K3b) selects K3g, the
+    // generic one-thread-per-sample kernel
+    const bool thread = ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC ||
+                        ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_THREAD;
+    const bool generic = sc.ctrl_variant != NMPCMC_ONE_STATE || sc.N > 255 || thread ||
                          ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC_WARP;
-    if (generic && ctx->nmpc_kernel != NMPCMC_NMPC_KERNEL_GENERIC && nmpcmc_dev::gen::genw_fits(sc)) {  // K3w unless K3g is asked for (or N too long)
-        const int64_t blocks = nmpcmc_dev::gen::genw_blocks(sc, ctx->sm_count, n);
-        const size_t need = (size_t)blocks * (size_t)nmpcmc_dev::gen::gen_ws_doubles(sc) * sizeof(double);
+    if (generic && !thread && nmpcmc_launch::genw_fits(sc)) {  // K3w (or K3g when N is too long for it)
+        const int64_t blocks = nmpcmc_launch::genw_blocks(sc, ctx->sm_count, n);
+        const size_t need = (size_t)blocks * (size_t)nmpcmc_launch::gen_ws_doubles(sc) * sizeof(double);
         if ((rc = ensure(ctx, tg.d_ws, tg.ws_cap, need)) != NMPCMC_OK) return rc;
         if ((rc = ensure(ctx, tg.d_counter, tg.counter_cap, 256)) != NMPCMC_OK) return rc;
-        rc = nmpcmc_dev::gen::launch_genw(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
-                                          static_cast<double*>(*tg.d_ws), blocks,
-                                          static_cast<unsigned long long*>(*tg.d_counter), tg.stream);
+        rc = nmpcmc_launch::launch_genw(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
+                                        static_cast<double*>(*tg.d_ws), blocks,
+                                        static_cast<unsigned long long*>(*tg.d_counter), tg.stream);
     } else if (generic) {
-        const int64_t slots = nmpcmc_dev::gen::gen_slots(sc, ctx->sm_count, n);
-        const size_t need = (size_t)slots * (size_t)nmpcmc_dev::gen::gen_ws_doubles(sc) * sizeof(double);
+        const int64_t slots = nmpcmc_launch::gen_slots(sc, ctx->sm_count, n);
+        const size_t need = (size_t)slots * (size_t)nmpcmc_launch::gen_ws_doubles(sc) * sizeof(double);
         if ((rc = ensure(ctx, tg.d_ws, tg.ws_cap, need)) != NMPCMC_OK) return rc;
         if ((rc = ensure(ctx, tg.d_counter, tg.counter_cap, 256)) != NMPCMC_OK) return rc;
-        rc = nmpcmc_dev::gen::launch_gen(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
-                                         static_cast<double*>(*tg.d_ws), slots,
-                                         static_cast<unsigned long long*>(*tg.d_counter), tg.stream);
-    } else if (ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_WARP) {
+        rc = nmpcmc_launch::launch_gen(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
+                                       static_cast<double*>(*tg.d_ws), slots,
+                                       static_cast<unsigned long long*>(*tg.d_counter), tg.stream);
+    } else {
         size_t bytes = 0;
         int64_t blocks = 0;
-        nmpcmc_dev::nmpc_gws_need(sc, ctx->sm_count, n, &bytes, &blocks);
+        nmpcmc_launch::nmpc_gws_need(sc, ctx->sm_count, n, &bytes, &blocks);
         if ((rc = ensure(ctx, tg.d_gws, tg.gws_cap, bytes)) != NMPCMC_OK) return rc;
         if ((rc = ensure(ctx, tg.d_counter, tg.counter_cap, 256)) != NMPCMC_OK) return rc;
-        rc = nmpcmc_dev::launch_nmpc(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ctx->sm_count,
-                                     static_cast<double*>(*tg.d_gws), blocks,
-                                     static_cast<unsigned long long*>(*tg.d_counter), tg.stream);
-    } else {
-        int64_t slots = (int64_t)ctx->sm_count * ctx->tps_warps_per_sm * 32;
-        if (slots > n) slots = ((n + 31) / 32) * 32;
-        const size_t need = nmpcmc_dev::tps_ws_bytes(sc.N, slots);
-        if ((rc = ensure(ctx, tg.d_ws, tg.ws_cap, need)) != NMPCMC_OK) return rc;
-        rc = nmpcmc_dev::launch_nmpc_tps(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
-                                         static_cast<double*>(*tg.d_ws), slots, tg.stream);
+        rc = nmpcmc_launch::launch_nmpc(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ctx->sm_count,
+                                        static_cast<double*>(*tg.d_gws), blocks,
+                                        static_cast<unsigned long long*>(*tg.d_counter), tg.stream);
     }
     if (rc != NMPCMC_OK) return fail(ctx, rc, "nmpc launch: unsupported configuration");
     return cuda_check(ctx, cudaGetLastError(), "nmpc_kernel launch");
@@ -418,39 +404,6 @@ int run_to_device(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario& sc, uint64_t first
 // ------------------------------------------------------- unit entry points
 namespace {
 
-__global__ void philox_kernel(const uint32_t* in, int64_t n, uint32_t* out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t* c = in + 6 * i;
-    const uint4 r = nmpcmc_dev::philox4x32_10(make_uint4(c[0], c[1], c[2], c[3]), c[4], c[5]);
-    out[4 * i + 0] = r.x;
-    out[4 * i + 1] = r.y;
-    out[4 * i + 2] = r.z;
-    out[4 * i + 3] = r.w;
-}
-
-__global__ void normals_kernel(uint64_t seed, uint64_t stream, int64_t n, double* out) {
-    // one thread replays the stream serially: exactly the host call pattern
-    if (blockIdx.x != 0 || threadIdx.x != 0) return;
-    nmpcmc_dev::NormalStream rng;
-    rng.init(seed, stream);
-    for (int64_t i = 0; i < n; ++i) out[i] = rng.normal();
-}
-
-__global__ void libm_kernel(int fn, const double* x, int64_t n, double* out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double v = x[i];
-    double r;
-    switch (fn) {
-        case 0: r = xlibm_exp(v); break;
-        case 1: r = xlibm_log(v); break;
-        case 2: r = xlibm_sin(v); break;
-        default: r = xlibm_cos(v); break;
-    }
-    out[i] = r;
-}
-
 template <typename T>
 int scratch_roundtrip(nmpcmc_gpu_ctx* ctx, const void* in, size_t in_bytes, size_t out_bytes,
                       void* out, T&& kernel_launch) {
@@ -479,8 +432,8 @@ int nmpcmc_gpu_philox_blocks(nmpcmc_gpu_ctx* ctx, const uint32_t* in, int64_t n,
     cudaSetDevice(ctx->device);
     return scratch_roundtrip(ctx, in, n * 6 * sizeof(uint32_t), n * 4 * sizeof(uint32_t), out,
                              [&](char* din, char* dout) {
-                                 philox_kernel<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(
-                                     reinterpret_cast<uint32_t*>(din), n, reinterpret_cast<uint32_t*>(dout));
+                                 nmpcmc_launch::launch_philox(reinterpret_cast<uint32_t*>(din), n,
+                                                              reinterpret_cast<uint32_t*>(dout), ctx->stream);
                              });
 }
 
@@ -488,7 +441,7 @@ int nmpcmc_gpu_normals(nmpcmc_gpu_ctx* ctx, uint64_t seed, uint64_t stream, int6
     if (ctx == nullptr || out == nullptr || n < 1) return NMPCMC_INVALID_ARGUMENT;
     cudaSetDevice(ctx->device);
     return scratch_roundtrip(ctx, nullptr, 0, n * sizeof(double), out, [&](char*, char* dout) {
-        normals_kernel<<<1, 32, 0, ctx->stream>>>(seed, stream, n, reinterpret_cast<double*>(dout));
+        nmpcmc_launch::launch_normals(seed, stream, n, reinterpret_cast<double*>(dout), ctx->stream);
     });
 }
 
@@ -497,8 +450,8 @@ int nmpcmc_gpu_libm(nmpcmc_gpu_ctx* ctx, int32_t fn, const double* x, int64_t n,
         return NMPCMC_INVALID_ARGUMENT;
     cudaSetDevice(ctx->device);
     return scratch_roundtrip(ctx, x, n * sizeof(double), n * sizeof(double), out, [&](char* din, char* dout) {
-        libm_kernel<<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(
-            fn, reinterpret_cast<double*>(din), n, reinterpret_cast<double*>(dout));
+        nmpcmc_launch::launch_libm(fn, reinterpret_cast<double*>(din), n, reinterpret_cast<double*>(dout),
+                                   ctx->stream);
     });
 }
 
@@ -507,33 +460,7 @@ int nmpcmc_gpu_libm(nmpcmc_gpu_ctx* ctx, int32_t fn, const double* x, int64_t n,
 // --------------------------------------------- FP64 peak (roofline denominator)
 // MEASURED_PEAKS.json carries HBM and bf16 only; the closed loop runs on the
 // FP64 CUDA cores, so its roofline denominator is measured here: independent
-// DFMA chains, grid = 8 x SMs x 256 threads, 2 flops per DFMA.
-namespace {
-__global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, int use_fma) {
-    double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
-           a7 = a0 + 7;
-    const double b = 0.999999, c = 1e-7;
-    if (use_fma) {
-        for (int i = 0; i < iters; ++i) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                a0 = __fma_rn(a0, b, c); a1 = __fma_rn(a1, b, c); a2 = __fma_rn(a2, b, c); a3 = __fma_rn(a3, b, c);
-                a4 = __fma_rn(a4, b, c); a5 = __fma_rn(a5, b, c); a6 = __fma_rn(a6, b, c); a7 = __fma_rn(a7, b, c);
-            }
-        }
-    } else {
-        for (int i = 0; i < iters; ++i) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                a0 = __dadd_rn(a0, c); a1 = __dadd_rn(a1, c); a2 = __dadd_rn(a2, c); a3 = __dadd_rn(a3, c);
-                a4 = __dadd_rn(a4, c); a5 = __dadd_rn(a5, c); a6 = __dadd_rn(a6, c); a7 = __dadd_rn(a7, c);
-            }
-        }
-    }
-    out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
-}
-}  // namespace
-
+// DFMA chains, grid = 8 x SMs x 256 threads, 2 flops per DFMA (k_misc.cu).
 extern "C" int nmpcmc_gpu_fp64_peak(nmpcmc_gpu_ctx* ctx, int use_fma, double* tflops_out) {
     if (ctx == nullptr || tflops_out == nullptr) return NMPCMC_INVALID_ARGUMENT;
     cudaSetDevice(ctx->device);
@@ -546,7 +473,8 @@ extern "C" int nmpcmc_gpu_fp64_peak(nmpcmc_gpu_ctx* ctx, int use_fma, double* tf
     double best = 0.0;
     for (int rep = 0; rep < 4; ++rep) {
         cudaEventRecord(e0, ctx->stream);
-        fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(static_cast<double*>(ctx->d_scratch), iters, use_fma);
+        nmpcmc_launch::launch_fp64_peak(blocks, threads, static_cast<double*>(ctx->d_scratch), iters, use_fma,
+                                        ctx->stream);
         cudaEventRecord(e1, ctx->stream);
         cudaEventSynchronize(e1);
         float ms = 0.f;
@@ -562,10 +490,10 @@ extern "C" int nmpcmc_gpu_fp64_peak(nmpcmc_gpu_ctx* ctx, int use_fma, double* tf
 
 // ------------------------------------------------------------ batched QP
 extern "C" int64_t nmpcmc_qp_stage_doubles(int32_t n_x, int32_t n_u) {
-    return nmpcmc_dev::qpb::stage_doubles(n_x, n_u);
+    return nmpcmc_launch::qp_stage_doubles(n_x, n_u);
 }
 extern "C" int64_t nmpcmc_qp_solution_doubles(int32_t N, int32_t n_x, int32_t n_u) {
-    return nmpcmc_dev::qpb::solution_doubles(N, n_x, n_u);
+    return nmpcmc_launch::qp_solution_doubles(N, n_x, n_u);
 }
 
 extern "C" int nmpcmc_gpu_solve_qp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_qp_dims* dims, int64_t batch,
@@ -576,18 +504,18 @@ extern "C" int nmpcmc_gpu_solve_qp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_qp_di
     const nmpcmc_qp_dims d = *dims;
     // QP validate (qp.cpp:21-58): at least one input stage and positive blocks
     if (d.N < 1 || d.n_x < 1 || d.n_u < 1) return fail(ctx, NMPCMC_DIMENSION_MISMATCH, "QP dimensions");
-    if (d.n_x > nmpcmc_dev::qpb::QX || d.n_u > nmpcmc_dev::qpb::QU)
+    if (d.n_x > nmpcmc_launch::qp_max_nx() || d.n_u > nmpcmc_launch::qp_max_nu())
         return fail(ctx, NMPCMC_UNSUPPORTED, "QP batch: n_x <= 8 and n_u <= 4 on device");
     if (d.mode != 0 && d.mode != 1) return fail(ctx, NMPCMC_INVALID_ARGUMENT, "QP batch: mode");
     if (batch == 0) return NMPCMC_OK;
     cudaSetDevice(ctx->device);
-    const int64_t SB = nmpcmc_dev::qpb::stage_doubles(d.n_x, d.n_u);
-    const int64_t SO = nmpcmc_dev::qpb::solution_doubles(d.N, d.n_x, d.n_u);
+    const int64_t SB = nmpcmc_launch::qp_stage_doubles(d.n_x, d.n_u);
+    const int64_t SO = nmpcmc_launch::qp_solution_doubles(d.N, d.n_x, d.n_u);
     const size_t in_b = (size_t)batch * (d.N + 1) * SB * sizeof(double);
     const size_t out_b = (size_t)batch * SO * sizeof(double);
     const size_t st_b = (size_t)batch * 2 * sizeof(int32_t);
-    const int64_t slots = nmpcmc_dev::qpb::qp_slots(ctx->sm_count, batch);
-    const size_t ws_b = (size_t)slots * (size_t)nmpcmc_dev::qpb::Lay(d.N, d.n_x, d.n_u).total * sizeof(double);
+    const int64_t slots = nmpcmc_launch::qp_slots(ctx->sm_count, batch);
+    const size_t ws_b = (size_t)slots * (size_t)nmpcmc_launch::qp_ws_doubles(d.N, d.n_x, d.n_u) * sizeof(double);
     int rc = ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap, in_b + out_b + st_b + 256);
     if (rc == NMPCMC_OK) rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, ws_b);
     if (rc != NMPCMC_OK) return rc;
@@ -600,10 +528,8 @@ extern "C" int nmpcmc_gpu_solve_qp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_qp_di
         if (cerr == cudaSuccess && n > 0) cerr = cudaMemcpyAsync(dst, src, n, kind, ctx->stream);
     };
     cp(d_in, stages, in_b, cudaMemcpyHostToDevice);
-    nmpcmc_dev::qpb::Dims kd{d.N, d.n_x, d.n_u, d.max_iter, d.mode, d.tol};
-    const unsigned grid = (unsigned)((slots + nmpcmc_dev::qpb::kBlock - 1) / nmpcmc_dev::qpb::kBlock);
-    nmpcmc_dev::qpb::qp_batch_kernel<<<grid, nmpcmc_dev::qpb::kBlock, 0, ctx->stream>>>(
-        kd, batch, d_in, d_out, d_st, d_st + batch, static_cast<double*>(ctx->d_ws), slots);
+    nmpcmc_launch::launch_qp_batch(d, batch, d_in, d_out, d_st, d_st + batch, static_cast<double*>(ctx->d_ws), slots,
+                                   ctx->stream);
     if ((rc = cuda_check(ctx, cudaGetLastError(), "qp_batch_kernel launch")) != NMPCMC_OK) return rc;
     cp(solutions, d_out, out_b, cudaMemcpyDeviceToHost);
     cp(status, d_st, (size_t)batch * sizeof(int32_t), cudaMemcpyDeviceToHost);
@@ -655,11 +581,11 @@ extern "C" int nmpcmc_gpu_solve_ocp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scen
     int64_t blocks = 0;
     if (k3) {
         size_t gbytes = 0;
-        nmpcmc_dev::nmpc_gws_need(*sc, ctx->sm_count, batch, &gbytes, &blocks);
+        nmpcmc_launch::nmpc_gws_need(*sc, ctx->sm_count, batch, &gbytes, &blocks);
         if ((rc = ensure(ctx, &ctx->d_gws, &ctx->gws_cap, gbytes)) != NMPCMC_OK) return rc;
     } else {
-        blocks = nmpcmc_dev::gen::genw_blocks(*sc, ctx->sm_count, batch);
-        const size_t ws_b = (size_t)blocks * (size_t)nmpcmc_dev::gen::gen_ws_doubles(*sc) * sizeof(double);
+        blocks = nmpcmc_launch::genw_blocks(*sc, ctx->sm_count, batch);
+        const size_t ws_b = (size_t)blocks * (size_t)nmpcmc_launch::gen_ws_doubles(*sc) * sizeof(double);
         if ((rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, ws_b)) != NMPCMC_OK) return rc;
     }
     if ((rc = ensure(ctx, &ctx->d_counter, &ctx->counter_cap, 256)) != NMPCMC_OK) return rc;
@@ -670,10 +596,10 @@ extern "C" int nmpcmc_gpu_solve_ocp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scen
     cp(d_x0, x0, b_x0, cudaMemcpyHostToDevice);
     cp(d_t0, t0, b_t0, cudaMemcpyHostToDevice);
     if (xi0) cp(d_xi0, xi0, b_xi, cudaMemcpyHostToDevice);
-    rc = k3 ? nmpcmc_dev::launch_ocp1(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv, d_st,
+    rc = k3 ? nmpcmc_launch::launch_ocp1(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv, d_st,
                                       ctx->sm_count, static_cast<double*>(ctx->d_gws), blocks,
                                       static_cast<unsigned long long*>(ctx->d_counter), ctx->stream)
-            : nmpcmc_dev::gen::launch_ocp_batch(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv,
+            : nmpcmc_launch::launch_ocp_batch(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv,
                                                 d_st, static_cast<double*>(ctx->d_ws), blocks,
                                                 static_cast<unsigned long long*>(ctx->d_counter), ctx->stream);
     if (rc != NMPCMC_OK)

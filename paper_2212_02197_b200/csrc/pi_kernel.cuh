@@ -5,20 +5,30 @@
 // phi_metric (montecarlo.cpp:65-78; accumulated on the fly in the same index
 // order). The whole 720-step loop lives in registers; per-sample I/O is one
 // 24-byte record. Parallelism is across samples only: each sample is a serial
-// recursion in time.
+// recursion in time. The state-independent normals (31 per
+// control step: Philox + log + sincos, the bulk of the arithmetic) are
+// generated a window of 16 Box-Muller pairs at a time into shared memory --
+// 16 independent chains the scheduler overlaps -- so only the Euler-Maruyama
+// recursion itself stays serial.
 #pragma once
 
 #include "device_common.cuh"
 
 namespace nmpcmc_dev {
 
+/// Pairs of normals generated ahead per window refill (one control step
+/// consumes 1 + Ns * NX normals: 31 in every BASELINE config, one refill).
+constexpr int kPiPairs = 16;
+constexpr int kPiBlock = 128;
+
 template <int NX>
 __device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar,
                                nmpcmc_sim_record* rec, nmpcmc_work_counters* cnt, double* traj,
-                               int traj_rows) {
+                               int traj_rows, double* win_buf, int win_stride) {
     const Cstr p = sample_truth(sc, sim_index);
-    NormalStream rng;
-    rng.init(sc.base_seed, sim_index);
+    NormalWindow<kPiPairs> rng;
+    rng.init(win_buf, win_stride, sc.base_seed, sim_index);
+    const int per_step = (sc.has_noise_R != 0 ? 1 : 0) + sc.Ns * NX;
     Plant<NX> pl;
 #pragma unroll
     for (int i = 0; i < NX; ++i) pl.x[i] = sc.x0[i];
@@ -45,6 +55,7 @@ __device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, in
     int steps = 0;  // control steps entered (a failing step counts: its work ran)
     for (int i = 0; i < nbar; ++i) {
         ++steps;
+        if (per_step < 2 * kPiPairs) rng.reserve(per_step);  // this step's normals in one refill
         const double y = measure<NX>(p, pl, has_R, lR, rng);
         // pi_step (controllers.cpp:12-23), evaluated in the documented order
         const double ybar = setpoint_at(sc, t);
@@ -98,17 +109,20 @@ __device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, in
     (void)traj_rows;
 }
 
+/// One thread per sample; each thread's normal window lives in shared memory,
+/// element j of thread t at win[j * kPiBlock + t] (conflict-free).
 template <int NX>
-__global__ void __launch_bounds__(128) pi_kernel(const __grid_constant__ nmpcmc_scenario sc,
-                                                 uint64_t first_sim, int64_t n_sims, int nbar,
-                                                 nmpcmc_sim_record* records,
-                                                 nmpcmc_work_counters* counters, double* traj,
-                                                 int traj_rows) {
+__global__ void __launch_bounds__(kPiBlock) pi_kernel(const __grid_constant__ nmpcmc_scenario sc,
+                                                      uint64_t first_sim, int64_t n_sims, int nbar,
+                                                      nmpcmc_sim_record* records,
+                                                      nmpcmc_work_counters* counters, double* traj,
+                                                      int traj_rows) {
+    __shared__ double win[2 * kPiPairs * kPiBlock];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_sims) return;
     pi_closed_loop<NX>(sc, first_sim + (uint64_t)i, nbar, records + i,
                        counters ? counters + i : nullptr,
-                       traj ? traj + (size_t)i * traj_rows * 5 : nullptr, traj_rows);
+                       traj ? traj + (size_t)i * traj_rows * 5 : nullptr, traj_rows, win + threadIdx.x, kPiBlock);
 }
 
 }  // namespace nmpcmc_dev

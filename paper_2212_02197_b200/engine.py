@@ -200,14 +200,12 @@ class Context:
     KERNELS = {"warp": 1, "thread": 2, "generic": 3, "generic_warp": 4}
 
     def set_nmpc_kernel(self, kind: str):
-        """'warp' (K3, default), 'thread' (K3b), 'generic' (K3g) or
+        """'warp' (K3, default), 'generic' (K3g; 'thread' is its alias since
+        the one-thread-per-sample K3b was retired) or
         'generic_warp' (K3w) for a one-state controller model; bitwise-
         identical results. A three-state controller model (or N > 255) runs
         K3w, or K3g when 'generic' is selected."""
         self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 1, self.KERNELS[kind]))
-
-    def set_tps_warps_per_sm(self, w: int):
-        self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 2, w))
 
     def set_stream(self, stream_ptr: int):
         self._check(self.lib.nmpcmc_gpu_set_stream(self.handle, C.c_void_p(stream_ptr)))

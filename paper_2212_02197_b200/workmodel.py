@@ -55,7 +55,7 @@ def pi_flops(control_steps: int) -> float:
 def nmpc_flops(counters, nx: int = 1) -> float:
     """Total algorithmic flops of an NMPC launch from the per-sample device
     counters (numpy structured array, abi.COUNTERS_DTYPE); nx = controller
-    model state dimension (1: K3/K3b, 3: K3g three-state)."""
+    model state dimension (1: K3 / K3w / K3g one-state, 3: K3w / K3g three-state)."""
     m = _MEASURED[nx]
     c = {k: float(counters[k].sum()) for k in counters.dtype.names}
     return (c["control_steps"] * (m["plant_step"] + m["ekf_step"])

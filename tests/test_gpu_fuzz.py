@@ -1,5 +1,5 @@
 """Every closed-loop kernel against the reference on randomised scenarios
-(tests/golden/fuzz.npz, fuzz_long.npz; make_fuzz.py): PI on K2; one-state NMPC on K3, K3b,
+(tests/golden/fuzz.npz, fuzz_long.npz; make_fuzz.py): PI on K2; one-state NMPC on K3,
 K3g and K3w; three-state NMPC on K3w and K3g. Records bitwise equal to the
 exact-libm reference."""
 import numpy as np
@@ -19,7 +19,7 @@ def _kernels(sc):
         return ["warp"]
     if sc.ctrl_variant == abi.THREE_STATE:
         return ["generic_warp", "generic"]
-    return ["warp", "thread", "generic", "generic_warp"]
+    return ["warp", "generic", "generic_warp"]
 
 
 @pytest.mark.parametrize("fname", FUZZ_FILES)

@@ -13,9 +13,9 @@ from paper_2212_02197_b200 import configs, engine
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["thread", "warp"])
+@pytest.fixture(params=["generic_warp", "warp"])
 def nctx(request, gpu_ctx):
-    """The context with one of the two NMPC kernels selected (K3b / K3):
+    """The context with one of the two warp-per-sample NMPC kernels selected (K3w / K3):
     both must reproduce the reference bitwise."""
     gpu_ctx.set_nmpc_kernel(request.param)
     yield gpu_ctx
@@ -78,12 +78,12 @@ def test_nmpc_counters_consistent(nctx):
 
 
 def test_nmpc_kernels_agree_at_scale(gpu_ctx):
-    """K3 (warp per sample) and K3b (thread per sample) on 600 perturbed
+    """K3 (warp per sample) and K3g (generic, thread per sample) on 600 perturbed
     config-3 samples, 60 control steps: identical records."""
     sc = configs.make_scenario("nmpc", N=60, n_steps=60, perturb=True)
     gpu_ctx.set_nmpc_kernel("warp")
     a, ca = gpu_ctx.run(sc, 1000, 600, counters=True)
-    gpu_ctx.set_nmpc_kernel("thread")
+    gpu_ctx.set_nmpc_kernel("generic")
     b, cb = gpu_ctx.run(sc, 1000, 600, counters=True)
     gpu_ctx.set_nmpc_kernel("warp")
     assert_records_equal(a, b)
