@@ -47,6 +47,18 @@ int main(int argc, char** argv) {
     nmpcmc::gpu::Context ctx(0);
     const auto r = nmpcmc::gpu::run_monte_carlo(ctx, sc, 1000);
     std::printf("mean phi %.6f, failed %d\n", r.aggregate.mean, r.aggregate.n_failed);
+    // the reference's run_monte_carlo(sc, n_sims, workers) shape: a GPU count
+    // (every visible device here), records bitwise independent of it
+    const auto rm = nmpcmc::gpu::run_monte_carlo(sc, 1000, 0);
+    bool same = rm.sims.size() == r.sims.size() && rm.aggregate.mean == r.aggregate.mean;
+    for (std::size_t i = 0; same && i < r.sims.size(); ++i)
+        same = std::memcmp(&rm.sims[i].phi, &r.sims[i].phi, sizeof(double)) == 0;
+    // two blocks on the same device through the multi-device context
+    nmpcmc::gpu::Context two({0, 0});
+    const auto r2 = nmpcmc::gpu::run_monte_carlo(two, sc, 1000);
+    for (std::size_t i = 0; same && i < r.sims.size(); ++i)
+        same = std::memcmp(&r2.sims[i].phi, &r.sims[i].phi, sizeof(double)) == 0;
+    std::printf("multi-device records identical %d (devices %d)\n", same ? 1 : 0, two.num_devices());
     // standalone QP service: min 1/2 u^2 + 2u + 1/2 x1^2, x1 = 0.5 u, u in [-1, 10]
     nmpcmc::gpu::QpStage s0, s1;
     s0.R = {1.0};

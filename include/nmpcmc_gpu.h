@@ -158,6 +158,8 @@ int nmpcmc_gpu_validate(const nmpcmc_scenario* sc, int32_t* nbar_out);
 /* Context = one device + one stream + scratch. Replaces the std::thread pool
  * of run_monte_carlo (montecarlo.cpp:218-245). */
 int nmpcmc_gpu_ctx_create(int device, nmpcmc_gpu_ctx** out);
+/* Number of visible CUDA devices (0 and NMPCMC_NO_DEVICE without a driver). */
+int nmpcmc_gpu_device_count(int* count_out);
 void nmpcmc_gpu_ctx_destroy(nmpcmc_gpu_ctx* ctx);
 const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx);
 /* Context options. NMPCMC_OPT_NMPC_KERNEL selects the NMPC kernel for a

@@ -10,6 +10,7 @@
 // Field-by-field mapping: INTEGRATION.md.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -77,10 +78,19 @@ struct Histogram {
     std::vector<int> counts;
 };
 
-/// RAII device context (one GPU, one stream).
+/// RAII device context: one GPU and one stream, or -- from a list of device
+/// ids -- one sub-context per GPU with NCCL between them
+/// (nmpcmc_gpu_ctx_create_multi). The multi-device form replaces the worker
+/// pool of run_monte_carlo (montecarlo.cpp:218-245).
 class Context {
 public:
     explicit Context(int device = 0) { check(nmpcmc_gpu_ctx_create(device, &ctx_), "ctx_create"); }
+    explicit Context(const std::vector<int>& device_ids) {
+        if (device_ids.empty()) throw DomainError(NMPCMC_DOMAIN_ERROR, "Context: no device ids");
+        check(nmpcmc_gpu_ctx_create_multi(device_ids.data(), static_cast<int>(device_ids.size()), &ctx_),
+              "ctx_create_multi");
+    }
+    int num_devices() const { return nmpcmc_gpu_ctx_num_devices(ctx_); }
     ~Context() { nmpcmc_gpu_ctx_destroy(ctx_); }
     Context(const Context&) = delete;
     Context& operator=(const Context&) = delete;
@@ -97,9 +107,7 @@ inline int validate_scenario(const Scenario& sc) {
     return nbar;
 }
 
-inline McAggregate aggregate_stats(const std::vector<nmpcmc_sim_record>& rec) {
-    nmpcmc_aggregate a{};
-    check(nmpcmc_gpu_aggregate(rec.data(), static_cast<int64_t>(rec.size()), &a), "aggregate_stats");
+inline McAggregate to_aggregate(const nmpcmc_aggregate& a) {
     McAggregate out;
     out.n_sims = a.n_sims;
     out.n_failed = a.n_failed;
@@ -114,13 +122,24 @@ inline McAggregate aggregate_stats(const std::vector<nmpcmc_sim_record>& rec) {
     return out;
 }
 
+inline McAggregate aggregate_stats(const std::vector<nmpcmc_sim_record>& rec) {
+    nmpcmc_aggregate a{};
+    check(nmpcmc_gpu_aggregate(rec.data(), static_cast<int64_t>(rec.size()), &a), "aggregate_stats");
+    return to_aggregate(a);
+}
+
 /// run_monte_carlo (montecarlo.cpp:213-251) for samples [first, first + n).
+/// On a multi-device context the samples are sharded by global index over
+/// the GPUs and the aggregate is computed on device_ids[0] after the NCCL
+/// gather (K4); records are bitwise independent of the device count.
 inline McResult run_monte_carlo(Context& ctx, const Scenario& sc, int n_sims, std::uint64_t first = 0) {
     if (n_sims < 1) throw DomainError(NMPCMC_DOMAIN_ERROR, "run_monte_carlo: n_sims must be at least 1");
     std::vector<nmpcmc_sim_record> rec(static_cast<std::size_t>(n_sims));
-    check(nmpcmc_gpu_run(ctx.get(), &sc, first, n_sims, rec.data(), nullptr, nullptr), "run_monte_carlo",
-          ctx.get());
+    nmpcmc_aggregate a{};
+    const auto t0 = std::chrono::steady_clock::now();
+    check(nmpcmc_gpu_run(ctx.get(), &sc, first, n_sims, rec.data(), nullptr, &a), "run_monte_carlo", ctx.get());
     McResult r;
+    r.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     r.sims.resize(rec.size());
     for (std::size_t i = 0; i < rec.size(); ++i) {
         r.sims[i].sim_index = first + i;
@@ -129,8 +148,20 @@ inline McResult run_monte_carlo(Context& ctx, const Scenario& sc, int n_sims, st
         r.sims[i].ocp_solves = rec[i].ocp_solves;
         r.sims[i].ocp_failures = rec[i].ocp_failures;
     }
-    r.aggregate = aggregate_stats(rec);
+    r.aggregate = to_aggregate(a);
     return r;
+}
+
+/// The reference's signature run_monte_carlo(sc, n_sims, workers)
+/// (montecarlo.hpp:121) with the worker count read as a GPU count: devices
+/// 0 .. n_devices-1 of this process (0 = every visible device).
+inline McResult run_monte_carlo(const Scenario& sc, int n_sims, int n_devices = 0) {
+    if (n_devices <= 0) check(nmpcmc_gpu_device_count(&n_devices), "device_count");
+    if (n_devices <= 0) throw Error(NMPCMC_CUDA_ERROR, "run_monte_carlo: no CUDA device");
+    std::vector<int> ids(static_cast<std::size_t>(n_devices));
+    for (int i = 0; i < n_devices; ++i) ids[static_cast<std::size_t>(i)] = i;
+    Context ctx(ids);
+    return run_monte_carlo(ctx, sc, n_sims);
 }
 
 /// run_closed_loop (montecarlo.cpp:80-157) for one global sample index.

@@ -1353,6 +1353,80 @@ __device__ __noinline__ int start_iterate(const Ocp& o, bool warm, Cnt* cnt) {
     return ST_OK;
 }
 
+/// filter_update (ekf.cpp:59-96), one-state, with nmpc_step's jitter retry
+/// (controllers.cpp:123-132): posterior (xf, Pn) from the prediction (xhat,
+/// Pf) and y; innov = y - c xhat. ST_NPD when the jittered innovation
+/// covariance is still not positive definite.
+__device__ __forceinline__ int filter_update1(const Ocp& o, double R_filter, double y, double xhat, double Pf,
+                                              double& xf, double& Pn, double* innov = nullptr) {
+    const double c = o.inv_V;
+    const double e = y - xhat / o.p.V;
+    if (innov) *innov = e;
+    const double pc = epi0(dot1(Pf, c));
+    double Rr = R_filter;
+    double Re = epi1(dot1(c, pc), Rr);
+    if (Re <= 0.0 || !dfinite(Re)) {
+        Rr = Rr + 1e-10;
+        Re = epi1(dot1(c, pc), Rr);
+        if (Re <= 0.0 || !dfinite(Re)) return ST_NPD;
+    }
+    const double l = sqrt(Re);
+    double K = pc / l;
+    K = K / l;
+    xf = epi1(dot1(K, e), xhat);
+    const double ikc = epim1(dot1(K, c), 1.0);
+    const double ikc_p = epi0(dot1(ikc, Pf));
+    Pn = epi0(dot1(ikc_p, ikc));
+    const double kr = epi0(dot1(K, Rr));
+    Pn = epi1(dot1(kr, K), Pn);
+    return ST_OK;
+}
+
+/// predict (ekf.cpp:26-57), one-state: np RK4 steps on (x, P) over
+/// [t, t + Ts] under input u, in place.
+__device__ __forceinline__ int predict1(const Ocp& o, double t, int np, double u, double& x, double& P) {
+    const double t_next = t + o.Ts;
+    const double h = (t_next - t) / np;
+    int st = ST_OK;
+#pragma unroll 1
+    for (int s = 0; s < np && st == ST_OK; ++s) {
+        // RK4 stages at (x, P) + c h k_{j-1}, c = 0, 1/2, 1/2, 1, with
+        // 0.5 * h * k formed as (0.5 * h) * k (ekf.cpp:38-44); the
+        // weighted sum accumulates left to right (ekf.cpp:46-50)
+        double pkx = 0.0, pkp = 0.0, ax = 0.0, ap = 0.0;
+#pragma unroll 1
+        for (int j = 0; j < 4 && st == ST_OK; ++j) {
+            double xs = x, ps = P;
+            if (j == 1 || j == 2) {
+                xs = x + 0.5 * h * pkx;
+                ps = P + 0.5 * h * pkp;
+            } else if (j == 3) {
+                xs = x + h * pkx;
+                ps = P + h * pkp;
+            }
+            double kx, kp;
+            st = joint_rhs1(o.p, xs, ps, u, kx, kp);
+            if (j == 0) {
+                ax = kx;
+                ap = kp;
+            } else if (j < 3) {
+                ax = ax + 2.0 * kx;
+                ap = ap + 2.0 * kp;
+            } else {
+                ax = ax + kx;
+                ap = ap + kp;
+            }
+            pkx = kx;
+            pkp = kp;
+        }
+        if (st != ST_OK) break;
+        x += (h / 6.0) * ax;
+        P += (h / 6.0) * ap;
+        if (!dfinite(x) || !dfinite(P)) st = ST_NONFINITE;
+    }
+    return st;
+}
+
 /// The NMPC branch of run_closed_loop (montecarlo.cpp:80-157) for one sample.
 template <int NX, int ST>
 __device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar, double* gws,
@@ -1413,30 +1487,10 @@ __device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_
         for (int k = lane; k < N; k += 32) GA(G_SP)[k] = setpoint_at(sc, t + (k + 1) * sc.Ts);
         // filter_update (ekf.cpp:59-96) with the jitter retry (controllers.cpp:123-132)
         double xf, Pn;
-        {
-            const double c = o.inv_V;
-            const double e = y - xhat / o.p.V;
-            const double pc = epi0(dot1(Pf, c));
-            double Rr = sc.R_filter;
-            double Re = epi1(dot1(c, pc), Rr);
-            if (Re <= 0.0 || !dfinite(Re)) {
-                Rr = Rr + 1e-10;
-                Re = epi1(dot1(c, pc), Rr);
-                if (Re <= 0.0 || !dfinite(Re)) {
-                    status = ST_NPD;
-                    counts_lost = true;
-                    break;
-                }
-            }
-            const double l = sqrt(Re);
-            double K = pc / l;
-            K = K / l;
-            xf = epi1(dot1(K, e), xhat);
-            const double ikc = epim1(dot1(K, c), 1.0);
-            const double ikc_p = epi0(dot1(ikc, Pf));
-            Pn = epi0(dot1(ikc_p, ikc));
-            const double kr = epi0(dot1(K, Rr));
-            Pn = epi1(dot1(kr, K), Pn);
+        if (filter_update1(o, sc.R_filter, y, xhat, Pf, xf, Pn) != ST_OK) {
+            status = ST_NPD;
+            counts_lost = true;
+            break;
         }
         o.x0 = xf;
         __syncwarp();
@@ -1453,46 +1507,8 @@ __device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_
         have_last = true;
         // predict (ekf.cpp:26-57), np RK4 steps on (x, P)
         {
-            const double t_next = t + o.Ts;
-            const double h = (t_next - t) / sc.np;
             double x = xf, P = Pn;
-            int st = ST_OK;
-#pragma unroll 1
-            for (int s = 0; s < sc.np && st == ST_OK; ++s) {
-                // RK4 stages at (x, P) + c h k_{j-1}, c = 0, 1/2, 1/2, 1, with
-                // 0.5 * h * k formed as (0.5 * h) * k (ekf.cpp:38-44); the
-                // weighted sum accumulates left to right (ekf.cpp:46-50)
-                double pkx = 0.0, pkp = 0.0, ax = 0.0, ap = 0.0;
-#pragma unroll 1
-                for (int j = 0; j < 4 && st == ST_OK; ++j) {
-                    double xs = x, ps = P;
-                    if (j == 1 || j == 2) {
-                        xs = x + 0.5 * h * pkx;
-                        ps = P + 0.5 * h * pkp;
-                    } else if (j == 3) {
-                        xs = x + h * pkx;
-                        ps = P + h * pkp;
-                    }
-                    double kx, kp;
-                    st = joint_rhs1(o.p, xs, ps, u, kx, kp);
-                    if (j == 0) {
-                        ax = kx;
-                        ap = kp;
-                    } else if (j < 3) {
-                        ax = ax + 2.0 * kx;
-                        ap = ap + 2.0 * kp;
-                    } else {
-                        ax = ax + kx;
-                        ap = ap + kp;
-                    }
-                    pkx = kx;
-                    pkp = kp;
-                }
-                if (st != ST_OK) break;
-                x += (h / 6.0) * ax;
-                P += (h / 6.0) * ap;
-                if (!dfinite(x) || !dfinite(P)) st = ST_NONFINITE;
-            }
+            const int st = predict1(o, t, sc.np, u, x, P);
             if (st != ST_OK) {
                 status = st;
                 break;

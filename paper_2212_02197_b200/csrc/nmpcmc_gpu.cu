@@ -118,6 +118,15 @@ void lane_end(Lane* l) {
 
 extern "C" {
 
+int nmpcmc_gpu_device_count(int* count_out) {
+    if (count_out == nullptr) return NMPCMC_INVALID_ARGUMENT;
+    *count_out = 0;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) return NMPCMC_NO_DEVICE;
+    *count_out = count;
+    return NMPCMC_OK;
+}
+
 int nmpcmc_gpu_ctx_create(int device, nmpcmc_gpu_ctx** out) {
     if (out == nullptr) return NMPCMC_INVALID_ARGUMENT;
     *out = nullptr;

@@ -27,5 +27,6 @@ def test_facade_client_runs_on_gpu(tmp_path):
                     f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
     assert "mean phi" in out
+    assert "multi-device records identical 1 (devices 2)" in out
     assert "qp status 0 u -1.000000000" in out  # active lower bound (u* = -1.6 unconstrained)
     assert "ocp converged 1" in out
