@@ -75,5 +75,11 @@ int main(int argc, char** argv) {
     sc.controller = NMPCMC_CTRL_NMPC;
     const auto ocp = nmpcmc::gpu::solve_ocp_batch(ctx, sc, {T0 * p.V}, {0.0});
     std::printf("ocp converged %d u0 %.6f\n", ocp[0].converged ? 1 : 0, ocp[0].xi[0]);
+    // controller-level API: four NMPC controllers stepping on measurements
+    nmpcmc::gpu::NmpcBatch ctl(ctx, sc, 4);
+    std::vector<nmpcmc_nmpc_diag> dg;
+    std::vector<double> u;
+    for (int j = 0; j < 3; ++j) u = ctl.step({10.0 * j, 10.0 * j, 10.0 * j, 10.0 * j}, {335.0, 336.0, 334.0, 335.5}, &dg);
+    std::printf("nmpc_step warm %d status %d u finite %d\n", dg[0].warm_started, dg[0].status, u[0] == u[0] ? 1 : 0);
     return 0;
 }

@@ -353,6 +353,66 @@ int nmpcmc_gpu_solve_qp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_qp_dims* dims, i
                               const double* stages, double* solutions, int32_t* status,
                               int32_t* iterations);
 
+/* ---- Controller-level API (controllers.hpp:16-93) ----------------------
+ * PiState (controllers.hpp:16-25) and PiStepResult (:29-37); next_I_hat is
+ * result.next.I_hat (the rest of result.next equals the input state). */
+typedef struct nmpcmc_pi_state {
+    double kP, kI, kaw, Ts, u_bar, u_min, u_max, I_hat;
+} nmpcmc_pi_state;
+typedef struct nmpcmc_pi_step_result {
+    double e, P, I, u_hat, u, I_aw, next_I_hat;
+} nmpcmc_pi_step_result;
+/* pi_step (controllers.hpp:49, controllers.cpp:12-23) for n independent
+ * controllers: states[i] advances to result.next in place; results may be
+ * NULL. _batch takes HOST buffers (synchronous); _device takes DEVICE
+ * buffers and is enqueued on the context stream. */
+int nmpcmc_gpu_pi_step_batch(nmpcmc_gpu_ctx* ctx, nmpcmc_pi_state* states, const double* y, const double* y_bar,
+                             int64_t n, nmpcmc_pi_step_result* results);
+int nmpcmc_gpu_pi_step_device(nmpcmc_gpu_ctx* ctx, nmpcmc_pi_state* states_dev, const double* y_dev,
+                              const double* y_bar_dev, int64_t n, nmpcmc_pi_step_result* results_dev);
+
+/* A batch of B device-resident NmpcStates (controllers.hpp:54-65) for the
+ * scenario's controller model (ctrl, ctrl_variant; n_x = 1 or 3), horizon,
+ * Qz, R_filter, np, u_min / u_max and SqpOptions -- make_nmpc_state
+ * (controllers.cpp:25-48) per instance with prior x0_hat[b*n_x ..] and
+ * P0[b*n_x*n_x ..] (column-major; NULL = the scenario's x0_hat / P0 for
+ * every instance). HOST inputs; the states stay on the context's device. */
+typedef struct nmpcmc_nmpc_batch nmpcmc_nmpc_batch;
+int nmpcmc_gpu_nmpc_batch_create(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, int64_t batch,
+                                 const double* x0_hat, const double* P0, nmpcmc_nmpc_batch** out);
+void nmpcmc_gpu_nmpc_batch_destroy(nmpcmc_nmpc_batch* st);
+/* NmpcDiagnostics (controllers.hpp:68-73) of one step: the posterior
+ * estimate (FilterState) and innovation, SqpReport.converged / .iterations,
+ * warm_started, and status = the nmpcmc_status of the exception nmpc_step
+ * threw (0 if none). Entries beyond n_x are 0; NaN where the step threw
+ * before producing them. */
+typedef struct nmpcmc_nmpc_diag {
+    double x_filtered[3];
+    double P_filtered[9];
+    double innovation;
+    int32_t converged;
+    int32_t sqp_iterations;
+    int32_t warm_started;
+    int32_t status;
+} nmpcmc_nmpc_diag;
+/* nmpc_step (controllers.hpp:92-93, controllers.cpp:114-212) on every
+ * instance: measurement y[b] at time t[b]; setpoints[b*N + k] = zbar at
+ * stage k+1 (NULL: the scenario's SetpointProfile at t[b] + (k+1) Ts, as
+ * run_closed_loop passes them); no disturbance. u_out[b] = the applied
+ * input, NaN when the step threw (diag status). The states advance exactly
+ * as the reference's NmpcState does, including under exceptions. HOST
+ * buffers, synchronous; diag may be NULL. One warp per instance on K3w's
+ * code path; bitwise the reference's results. */
+int nmpcmc_gpu_nmpc_step_batch(nmpcmc_gpu_ctx* ctx, nmpcmc_nmpc_batch* st, const double* t, const double* y,
+                               const double* setpoints, double* u_out, nmpcmc_nmpc_diag* diag);
+/* Read the states back: x_hat[B*n_x], P[B*n_x*n_x] (the filter prediction
+ * valid at the next sample), last_xi[B*N*(1+n_x)], last_lambda[B*N*n_x],
+ * last_pi_l[B*N], last_pi_u[B*N] (meaningful where warm[b] = 1), warm[B].
+ * Any pointer may be NULL. */
+int nmpcmc_gpu_nmpc_batch_get(nmpcmc_nmpc_batch* st, double* x_hat, double* P, double* last_xi,
+                              double* last_lambda, double* last_pi_l, double* last_pi_u, int32_t* warm);
+int64_t nmpcmc_gpu_nmpc_batch_size(const nmpcmc_nmpc_batch* st);
+
 #ifdef __cplusplus
 }
 #endif

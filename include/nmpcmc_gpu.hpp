@@ -267,6 +267,58 @@ inline std::vector<OcpSolution> solve_ocp_batch(Context& ctx, const Scenario& sc
     return out;
 }
 
+/// pi_step (controllers.hpp:49) for a batch of PI controllers; states advance
+/// to result.next in place.
+inline std::vector<nmpcmc_pi_step_result> pi_step_batch(Context& ctx, std::vector<nmpcmc_pi_state>& states,
+                                                        const std::vector<double>& y,
+                                                        const std::vector<double>& y_bar) {
+    if (y.size() != states.size() || y_bar.size() != states.size())
+        throw LengthMismatch(NMPCMC_LENGTH_MISMATCH, "pi_step_batch: input lengths");
+    std::vector<nmpcmc_pi_step_result> r(states.size());
+    check(nmpcmc_gpu_pi_step_batch(ctx.get(), states.data(), y.data(), y_bar.data(),
+                                   static_cast<int64_t>(states.size()), r.data()),
+          "pi_step_batch", ctx.get());
+    return r;
+}
+
+/// B device-resident NmpcStates (make_nmpc_state, controllers.hpp:84-86) of
+/// the scenario's controller configuration; step() is nmpc_step
+/// (controllers.hpp:92-93) on every instance.
+class NmpcBatch {
+public:
+    NmpcBatch(Context& ctx, const Scenario& sc, int64_t batch, const std::vector<double>* x0_hat = nullptr,
+              const std::vector<double>* P0 = nullptr)
+        : ctx_(ctx), batch_(batch), N_(sc.N) {
+        check(nmpcmc_gpu_nmpc_batch_create(ctx.get(), &sc, batch, x0_hat ? x0_hat->data() : nullptr,
+                                           P0 ? P0->data() : nullptr, &st_),
+              "make_nmpc_state", ctx.get());
+    }
+    ~NmpcBatch() { nmpcmc_gpu_nmpc_batch_destroy(st_); }
+    NmpcBatch(const NmpcBatch&) = delete;
+    NmpcBatch& operator=(const NmpcBatch&) = delete;
+    /// Applied inputs (NaN where nmpc_step threw; diag[b].status says which).
+    std::vector<double> step(const std::vector<double>& t, const std::vector<double>& y,
+                             std::vector<nmpcmc_nmpc_diag>* diag = nullptr,
+                             const std::vector<double>* setpoints = nullptr) {
+        if (static_cast<int64_t>(t.size()) != batch_ || static_cast<int64_t>(y.size()) != batch_ ||
+            (setpoints && static_cast<int64_t>(setpoints->size()) != batch_ * N_))
+            throw LengthMismatch(NMPCMC_LENGTH_MISMATCH, "nmpc_step: input lengths");
+        std::vector<double> u(static_cast<std::size_t>(batch_));
+        if (diag) diag->resize(static_cast<std::size_t>(batch_));
+        check(nmpcmc_gpu_nmpc_step_batch(ctx_.get(), st_, t.data(), y.data(), setpoints ? setpoints->data() : nullptr,
+                                         u.data(), diag ? diag->data() : nullptr),
+              "nmpc_step", ctx_.get());
+        return u;
+    }
+    nmpcmc_nmpc_batch* get() const { return st_; }
+
+private:
+    Context& ctx_;
+    int64_t batch_;
+    int N_;
+    nmpcmc_nmpc_batch* st_ = nullptr;
+};
+
 /// phi_histogram (montecarlo.cpp:268-304).
 inline Histogram phi_histogram(const std::vector<double>& phi, int bins = 0) {
     std::vector<double> edges(201);

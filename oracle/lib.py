@@ -139,3 +139,32 @@ def solve_ocp_batch(lib, sc, x0, t0, xi0=None):
                                    out["status"].ctypes.data_as(C.POINTER(C.c_int32)))
     return out
 
+
+
+def nmpc_steps(lib, sc, x0_hat, P0, t, y, sp=None):
+    """The reference's make_nmpc_state + nmpc_step over T steps for B
+    controllers (nmpcmc_ref_nmpc_steps): u (B, T), diag (B, T) records in the
+    layout of nmpcmc_nmpc_diag, and the final NmpcStates."""
+    from paper_2212_02197_b200 import controllers as K
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    B, T = y.shape
+    nx = 3 if sc.ctrl_variant == abi.THREE_STATE else 1
+    N = sc.N
+    L = N * (1 + nx)
+    u = np.zeros((B, T))
+    diag = np.zeros((B, T), dtype=K.DIAG_DTYPE)
+    fin = dict(x_hat=np.zeros((B, nx)), P=np.zeros((B, nx * nx)), last_xi=np.zeros((B, L)),
+               last_lambda=np.zeros((B, N * nx)), last_pi_l=np.zeros((B, N)), last_pi_u=np.zeros((B, N)),
+               warm=np.zeros(B, dtype=np.int32))
+    V = C.c_void_p
+    f = lib.nmpcmc_ref_nmpc_steps
+    f.argtypes = [C.POINTER(abi.Scenario), C.c_int64, C.c_int] + [V] * 14
+    keep = [None if x0_hat is None else np.ascontiguousarray(x0_hat, dtype=np.float64),
+            None if P0 is None else np.ascontiguousarray(P0, dtype=np.float64),
+            None if sp is None else np.ascontiguousarray(sp, dtype=np.float64)]
+    f(C.byref(sc), B, T, None if keep[0] is None else keep[0].ctypes.data,
+      None if keep[1] is None else keep[1].ctypes.data, t.ctypes.data, y.ctypes.data,
+      None if keep[2] is None else keep[2].ctypes.data, u.ctypes.data, diag.ctypes.data,
+      *(fin[k].ctypes.data for k in ("x_hat", "P", "last_xi", "last_lambda", "last_pi_l", "last_pi_u", "warm")))
+    return u, diag, fin

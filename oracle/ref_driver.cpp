@@ -272,6 +272,86 @@ void nmpcmc_ref_pi_step(const double* st, double y, double ybar, double* out) {
     out[6] = r.next.I_hat;
 }
 
+/// The reference's make_nmpc_state (controllers.cpp:25-48) + nmpc_step
+/// (controllers.cpp:114-212) for B independent controllers over T steps:
+/// instance b steps with (t[b*T + j], y[b*T + j]) and setpoints
+/// sp[(b*T + j)*N + k] (NULL: the scenario's profile at t + (k+1) Ts). An
+/// exception fails only that step (status, NaN input); the NmpcState keeps
+/// whatever the reference left in it and the next step continues from there.
+/// Outputs per step: u, and the diagnostics in the layout of nmpcmc_nmpc_diag;
+/// per instance the final state (x_hat, P, last_xi, last duals, warm).
+int nmpcmc_ref_nmpc_steps(const nmpcmc_scenario* s, std::int64_t B, int T, const double* x0_hat, const double* P0,
+                          const double* t, const double* y, const double* sp, double* u_out, nmpcmc_nmpc_diag* diag,
+                          double* xhat_out, double* P_out, double* xi_out, double* lam_out, double* pil_out,
+                          double* piu_out, std::int32_t* warm_out) {
+    const int nx = nx_of(s->ctrl_variant), N = s->N, L = N * (1 + nx);
+    SqpOptions opts;
+    opts.eps = s->sqp.eps;
+    opts.max_iter = s->sqp.max_iter;
+    opts.max_backtracks = s->sqp.max_backtracks;
+    opts.c1 = s->sqp.c1;
+    opts.backtrack_factor = s->sqp.backtrack_factor;
+    opts.qp_tol = s->sqp.qp_tol;
+    opts.qp_max_iter = s->sqp.qp_max_iter;
+    SetpointProfile prof;
+    for (int i = 0; i < s->n_setpoints; ++i) {
+        prof.times.push_back(s->sp_times[i]);
+        prof.values.push_back(Vec{s->sp_values[i]});
+    }
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    for (std::int64_t b = 0; b < B; ++b) {
+        Vec xh(nx);
+        Matrix p0(nx, nx);
+        for (int i = 0; i < nx; ++i) xh[i] = x0_hat ? x0_hat[b * nx + i] : s->x0_hat[i];
+        for (int c = 0; c < nx; ++c)
+            for (int r = 0; r < nx; ++r) p0(r, c) = P0 ? P0[b * nx * nx + c * nx + r] : s->P0[c * nx + r];
+        NmpcState st = make_nmpc_state(make_cstr_model(to_params(s->ctrl), to_variant(s->ctrl_variant)),
+                                       Horizon{N, s->horizon_Ts, s->Nc}, Vec{s->u_min}, Vec{s->u_max},
+                                       Matrix::from_rows({{s->Qz}}), Matrix::from_rows({{s->R_filter}}), xh, p0,
+                                       s->np, opts);
+        for (int j = 0; j < T; ++j) {
+            const std::int64_t q = b * T + j;
+            std::vector<Vec> spv;
+            for (int k = 0; k < N; ++k)
+                spv.push_back(sp ? Vec{sp[q * N + k]} : prof.at(t[q] + (k + 1) * s->Ts));
+            NmpcDiagnostics dg;
+            nmpcmc_nmpc_diag& d = diag[q];
+            std::memset(&d, 0, sizeof d);
+            for (int i = 0; i < nx; ++i) d.x_filtered[i] = nan;
+            for (int i = 0; i < nx * nx; ++i) d.P_filtered[i] = nan;
+            d.innovation = std::isfinite(y[q]) ? y[q] - st.filter.x_hat[nx - 1] / s->ctrl.V : nan;
+            d.warm_started = static_cast<int>(st.last_xi.size()) == L ? 1 : 0;
+            try {
+                const Vec u = nmpc_step(st, t[q], Vec{y[q]}, spv, Vec{}, &dg);
+                u_out[q] = u[0];
+                for (int i = 0; i < nx; ++i) d.x_filtered[i] = dg.filtered.x_hat[i];
+                for (int c = 0; c < nx; ++c)
+                    for (int r = 0; r < nx; ++r) d.P_filtered[c * nx + r] = dg.filtered.P(r, c);
+                d.innovation = dg.innovation[0];
+                d.converged = dg.sqp.converged ? 1 : 0;
+                d.sqp_iterations = dg.sqp.iterations;
+                d.status = 0;
+            } catch (const NotPositiveDefinite&) {
+                u_out[q] = nan, d.status = NMPCMC_NOT_POSITIVE_DEFINITE;
+            } catch (const NonFiniteState&) {
+                u_out[q] = nan, d.status = NMPCMC_NON_FINITE_STATE;
+            } catch (const DomainError&) {
+                u_out[q] = nan, d.status = NMPCMC_DOMAIN_ERROR;
+            }
+        }
+        for (int i = 0; i < nx; ++i) xhat_out[b * nx + i] = st.filter.x_hat[i];
+        for (int c = 0; c < nx; ++c)
+            for (int r = 0; r < nx; ++r) P_out[b * nx * nx + c * nx + r] = st.filter.P(r, c);
+        const bool w = static_cast<int>(st.last_xi.size()) == L;
+        warm_out[b] = w ? 1 : 0;
+        for (int i = 0; i < L; ++i) xi_out[b * L + i] = w ? st.last_xi[i] : 0.0;
+        for (int i = 0; i < N * nx; ++i) lam_out[b * N * nx + i] = w ? st.last_duals.lambda[i] : 0.0;
+        for (int i = 0; i < N; ++i) pil_out[b * N + i] = w ? st.last_duals.pi_l[i] : 0.0;
+        for (int i = 0; i < N; ++i) piu_out[b * N + i] = w ? st.last_duals.pi_u[i] : 0.0;
+    }
+    return 0;
+}
+
 /// reaction_rate (cstr.cpp:36-40) on the three-state variant; NaN on DomainError.
 double nmpcmc_ref_reaction_rate(const nmpcmc_cstr_params* p, const double* c) {
     const CstrParams q = to_params(*p);

@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libnmpcmc_gpu.so")
 # largest first: the NMPC kernel units dominate the build
-SOURCES = ["k_gen.cu", "k_nmpc.cu", "k_misc.cu", "nmpcmc_multi.cu", "nmpcmc_gpu.cu", "host_api.cpp"]
+SOURCES = ["k_gen.cu", "k_nmpc.cu", "k_misc.cu", "nmpcmc_multi.cu", "nmpcmc_gpu.cu", "controllers_api.cu", "host_api.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

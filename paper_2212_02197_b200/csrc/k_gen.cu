@@ -34,4 +34,12 @@ int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const double* x0,
                                              counter, stream);
 }
 
+int64_t nmpc_state_doubles(const nmpcmc_scenario& sc) { return nmpcmc_dev::gen::nmpc_state_doubles(sc); }
+
+int launch_nmpc_step(const nmpcmc_scenario& sc, int64_t batch, double* states, const double* t, const double* y,
+                     const double* sp, double* u, nmpcmc_nmpc_diag* diag, double* ws, int64_t blocks,
+                     unsigned long long* counter, cudaStream_t stream) {
+    return nmpcmc_dev::gen::launch_nmpc_step(sc, batch, states, t, y, sp, u, diag, ws, blocks, counter, stream);
+}
+
 }  // namespace nmpcmc_launch

@@ -83,6 +83,15 @@ int launch_pi(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nm
     return NMPCMC_OK;
 }
 
+void launch_pi_step(nmpcmc_pi_state* states, const double* y, const double* ybar, int64_t n,
+                    nmpcmc_pi_step_result* results, int sm_count, cudaStream_t stream) {
+    int64_t grid = (n + 255) / 256;
+    const int64_t cap = (int64_t)sm_count * 8;
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    nmpcmc_dev::pi_step_kernel<<<(unsigned)grid, 256, 0, stream>>>(states, y, ybar, n, results);
+}
+
 void launch_philox(const uint32_t* in, int64_t n, uint32_t* out, cudaStream_t stream) {
     philox_kernel<<<(unsigned)((n + 127) / 128), 128, 0, stream>>>(in, n, out);
 }

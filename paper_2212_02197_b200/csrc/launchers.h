@@ -38,9 +38,17 @@ int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const double* x0,
                      double* xi, double* lam, double* pil, double* piu, int32_t* conv, int32_t* status, double* ws,
                      int64_t blocks, unsigned long long* counter, cudaStream_t stream);
 
+// ---- controller-level API: batched nmpc_step on K3w's path (k_gen.cu)
+int64_t nmpc_state_doubles(const nmpcmc_scenario& sc);
+int launch_nmpc_step(const nmpcmc_scenario& sc, int64_t batch, double* states, const double* t, const double* y,
+                     const double* sp, double* u, nmpcmc_nmpc_diag* diag, double* ws, int64_t blocks,
+                     unsigned long long* counter, cudaStream_t stream);
+
 // ---- K2 PI, unit kernels, FP64 peak, K5 batched QP (k_misc.cu)
 int launch_pi(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
               nmpcmc_work_counters* d_cnt, double* d_traj, int rows, cudaStream_t stream);
+void launch_pi_step(nmpcmc_pi_state* states, const double* y, const double* ybar, int64_t n,
+                    nmpcmc_pi_step_result* results, int sm_count, cudaStream_t stream);
 void launch_philox(const uint32_t* in, int64_t n, uint32_t* out, cudaStream_t stream);
 void launch_normals(uint64_t seed, uint64_t stream_id, int64_t n, double* out, cudaStream_t stream);
 void launch_libm(int fn, const double* x, int64_t n, double* out, cudaStream_t stream);

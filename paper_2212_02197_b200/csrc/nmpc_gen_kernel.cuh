@@ -1461,6 +1461,136 @@ __device__ __noinline__ bool ekf_update(const Model<NX>& m, double* x, double* P
     return false;
 }
 
+/// Result of one nmpc_step (nmpc_step_ws).
+struct StepRes {
+    int status;       // G_OK or the status of the exception that escaped
+    bool filter_npd;  // NotPositiveDefinite from filter_update after the jitter retry
+    bool converged;
+    bool adopted;     // last_xi / last_duals replaced by this step's solution
+    double u;
+};
+
+/// nmpc_step (controllers.cpp:114-212) on the carried NmpcState: the filter
+/// prediction (xhat, Pf), the previous solution in LXI / LLAM / LPL / LPU when
+/// have_last, the stage setpoints already in SP. Returns the clamped first
+/// input; xf / Pn receive the posterior (NmpcDiagnostics::filtered). State
+/// transitions follow the reference under exceptions: a throw before
+/// sqp_solve returns leaves the state untouched; once it has returned,
+/// last_xi / last_duals are adopted, and a throw from predict leaves only the
+/// filter at its old value.
+template <int NX, int W>
+__device__ __forceinline__ StepRes nmpc_step_ws(Ocp<NX, W>& o, const nmpcmc_scenario& sc, double t, double y,
+                                                double* xhat, double* Pf, bool& have_last, double* xf, double* Pn) {
+    StepRes r{G_OK, false, false, false, 0.0};
+    const WsT<W> ws = o.ws;
+    const Layout<NX> L = o.lay;
+    const int N = o.N;
+    const int lane = Lanes<W>::lane();
+    const bool fl = dfinite(o.umin), fh = dfinite(o.umax);
+    auto clampu = [&](double u) { return smax(o.umin, smin(o.umax, u)); };
+#pragma unroll
+    for (int e = 0; e < NX; ++e) xf[e] = xhat[e];
+#pragma unroll
+    for (int e = 0; e < NX * NX; ++e) Pn[e] = Pf[e];
+    if (ekf_update<NX>(o.m, xf, Pn, y, sc.R_filter)) {  // jitter retry (controllers.cpp:123-132)
+#pragma unroll
+        for (int e = 0; e < NX; ++e) xf[e] = xhat[e];
+#pragma unroll
+        for (int e = 0; e < NX * NX; ++e) Pn[e] = Pf[e];
+        if (ekf_update<NX>(o.m, xf, Pn, y, sc.R_filter + 1e-10)) {
+            r.status = G_NPD;
+            r.filter_npd = true;
+            return r;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < NX; ++e) o.x0[e] = xf[e];
+    // warm / cold start (controllers.cpp:147-186)
+    if (have_last) {
+#pragma unroll 1
+        for (int k = lane; k < N; k += W) ws[L.US + k] = clampu(ws[L.LXI + L.uo(k + 1 < N ? k + 1 : N - 1)]);
+        Lanes<W>::sync();
+        const int st = xi_from_u<NX, W>(o, 0);
+        if (st == G_DOMAIN) {
+            r.status = G_DOMAIN;
+            return r;
+        }
+        if (st != G_OK) {  // shifted_warm_start (controllers.cpp:97-110), clamped inputs
+            const int w = Layout<NX>::W;
+            for (int e = lane; e < L.L; e += W) {
+                double x = e < L.L - w ? ws[L.LXI + e + w] : ws[L.LXI + e];
+                if (e % w == 0) x = clampu(x);
+                ws[L.XI[0] + e] = x;
+            }
+        }
+        // shifted_multipliers (controllers.cpp:87-93), projected (sqp.cpp:219-222)
+        for (int e = lane; e < L.NN; e += W)
+            ws[L.LAM + e] = (L.NN >= 2 * NX && e < L.NN - NX) ? ws[L.LLAM + e + NX] : ws[L.LLAM + e];
+#pragma unroll 1
+        for (int k = lane; k < N; k += W) {
+            const int src = k < N - 1 ? k + 1 : k;
+            ws[L.PL + k] = smax(0.0, ws[L.LPL + src]);
+            ws[L.PU + k] = smax(0.0, ws[L.LPU + src]);
+        }
+    } else {
+        const double un = fl && fh ? 0.5 * (o.umin + o.umax) : clampu(0.0);
+#pragma unroll 1
+        for (int k = lane; k < N; k += W) ws[L.US + k] = un;
+        Lanes<W>::sync();
+        const int st = xi_from_u<NX, W>(o, 0);
+        if (st == G_DOMAIN) {
+            r.status = G_DOMAIN;
+            return r;
+        }
+        if (st != G_OK) {
+#pragma unroll 1
+            for (int k = lane; k < N; k += W) {
+                ws[L.XI[0] + L.uo(k)] = un;
+#pragma unroll
+                for (int e = 0; e < NX; ++e) ws[L.XI[0] + L.xo(k + 1) + e] = xf[e];
+            }
+        }
+        for (int e = lane; e < L.NN; e += W) ws[L.LAM + e] = 0.0;
+#pragma unroll 1
+        for (int k = lane; k < N; k += W) ws[L.PL + k] = 0.0, ws[L.PU + k] = 0.0;
+    }
+    Lanes<W>::sync();
+    int cur = 0;
+    const SqpOut so = sqp_solve<NX, W>(o, sc.sqp, &cur);
+    if (so.status != G_OK) {
+        r.status = so.status;
+        return r;
+    }
+    const double u = clampu(ws[L.XI[cur] + L.uo(0)]);
+    for (int e = lane; e < L.L; e += W) ws[L.LXI + e] = ws[L.XI[cur] + e];
+    for (int e = lane; e < L.NN; e += W) ws[L.LLAM + e] = ws[L.LAM + e];
+#pragma unroll 1
+    for (int k = lane; k < N; k += W) ws[L.LPL + k] = ws[L.PL + k], ws[L.LPU + k] = ws[L.PU + k];
+    Lanes<W>::sync();
+    have_last = true;
+    r.adopted = true;
+    r.converged = so.converged;
+    double xp[NX], Pp[NX * NX];
+#pragma unroll
+    for (int e = 0; e < NX; ++e) xp[e] = xf[e];
+#pragma unroll
+    for (int e = 0; e < NX * NX; ++e) Pp[e] = Pn[e];
+    {
+        const int st = ekf_predict<NX>(o.m, xp, Pp, u, t, t + sc.horizon_Ts, sc.np);
+        if (st != G_OK) {
+            r.status = st;
+            return r;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < NX; ++e) xhat[e] = xp[e];
+#pragma unroll
+    for (int e = 0; e < NX * NX; ++e) Pf[e] = Pp[e];
+    r.u = u;
+    r.converged = so.converged;
+    return r;
+}
+
 // ------------------------------------------------------------ closed loop
 /// The NMPC branch of run_closed_loop (montecarlo.cpp:80-157) for one sample
 /// with a controller model of NX states and a truth plant of TX states.
@@ -1499,8 +1629,6 @@ __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim
     }
     int status = G_OK, solves = 0, fails = 0, row = 0;
     bool counts_lost = false;
-    const bool fl = dfinite(o.umin), fh = dfinite(o.umax);
-    auto clampu = [&](double u) { return smax(o.umin, smin(o.umax, u)); };
 #pragma unroll 1
     for (int i = 0; i < nbar; ++i) {
         const double y = measure<TX>(p, pl, has_R, lR, rng);
@@ -1513,99 +1641,15 @@ __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim
         for (int k = lane; k < N; k += W) ws[L.SP + k] = setpoint_at(sc, t + (k + 1) * sc.Ts);
         Lanes<W>::sync();
         double xf[NX], Pn[NX * NX];
-#pragma unroll
-        for (int e = 0; e < NX; ++e) xf[e] = xhat[e];
-#pragma unroll
-        for (int e = 0; e < NX * NX; ++e) Pn[e] = Pf[e];
-        if (ekf_update<NX>(o.m, xf, Pn, y, sc.R_filter)) {  // jitter retry (controllers.cpp:123-132)
-#pragma unroll
-            for (int e = 0; e < NX; ++e) xf[e] = xhat[e];
-#pragma unroll
-            for (int e = 0; e < NX * NX; ++e) Pn[e] = Pf[e];
-            if (ekf_update<NX>(o.m, xf, Pn, y, sc.R_filter + 1e-10)) {
-                status = G_NPD;
-                counts_lost = true;
-                break;
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < NX; ++e) o.x0[e] = xf[e];
-        // warm / cold start (controllers.cpp:147-186)
-        if (have_last) {
-#pragma unroll 1
-            for (int k = lane; k < N; k += W) ws[L.US + k] = clampu(ws[L.LXI + L.uo(k + 1 < N ? k + 1 : N - 1)]);
-            Lanes<W>::sync();
-            const int st = xi_from_u<NX, W>(o, 0);
-            if (st == G_DOMAIN) {
-                status = G_DOMAIN;
-                break;
-            }
-            if (st != G_OK) {  // shifted_warm_start (controllers.cpp:97-110), clamped inputs
-                const int w = Layout<NX>::W;
-                for (int e = lane; e < L.L; e += W) {
-                    double x = e < L.L - w ? ws[L.LXI + e + w] : ws[L.LXI + e];
-                    if (e % w == 0) x = clampu(x);
-                    ws[L.XI[0] + e] = x;
-                }
-            }
-            // shifted_multipliers (controllers.cpp:87-93), projected (sqp.cpp:219-222)
-            for (int e = lane; e < L.NN; e += W)
-                ws[L.LAM + e] = (L.NN >= 2 * NX && e < L.NN - NX) ? ws[L.LLAM + e + NX] : ws[L.LLAM + e];
-#pragma unroll 1
-            for (int k = lane; k < N; k += W) {
-                const int src = k < N - 1 ? k + 1 : k;
-                ws[L.PL + k] = smax(0.0, ws[L.LPL + src]);
-                ws[L.PU + k] = smax(0.0, ws[L.LPU + src]);
-            }
-        } else {
-            const double un = fl && fh ? 0.5 * (o.umin + o.umax) : clampu(0.0);
-#pragma unroll 1
-            for (int k = lane; k < N; k += W) ws[L.US + k] = un;
-            Lanes<W>::sync();
-            const int st = xi_from_u<NX, W>(o, 0);
-            if (st == G_DOMAIN) {
-                status = G_DOMAIN;
-                break;
-            }
-            if (st != G_OK) {
-#pragma unroll 1
-                for (int k = lane; k < N; k += W) {
-                    ws[L.XI[0] + L.uo(k)] = un;
-#pragma unroll
-                    for (int e = 0; e < NX; ++e) ws[L.XI[0] + L.xo(k + 1) + e] = xf[e];
-                }
-            }
-            for (int e = lane; e < L.NN; e += W) ws[L.LAM + e] = 0.0;
-#pragma unroll 1
-            for (int k = lane; k < N; k += W) ws[L.PL + k] = 0.0, ws[L.PU + k] = 0.0;
-        }
-        Lanes<W>::sync();
-        int cur = 0;
-        const SqpOut so = sqp_solve<NX, W>(o, sc.sqp, &cur);
-        if (so.status != G_OK) {
-            status = so.status;
+        const StepRes sr = nmpc_step_ws<NX, W>(o, sc, t, y, xhat, Pf, have_last, xf, Pn);
+        if (sr.status != G_OK) {
+            status = sr.status;
+            counts_lost = sr.filter_npd;
             break;
         }
-        const double u = clampu(ws[L.XI[cur] + L.uo(0)]);
-        for (int e = lane; e < L.L; e += W) ws[L.LXI + e] = ws[L.XI[cur] + e];
-        for (int e = lane; e < L.NN; e += W) ws[L.LLAM + e] = ws[L.LAM + e];
-#pragma unroll 1
-        for (int k = lane; k < N; k += W) ws[L.LPL + k] = ws[L.PL + k], ws[L.LPU + k] = ws[L.PU + k];
-        Lanes<W>::sync();
-        have_last = true;
-        {
-            const int st = ekf_predict<NX>(o.m, xf, Pn, u, t, t + sc.horizon_Ts, sc.np);
-            if (st != G_OK) {
-                status = st;
-                break;
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < NX; ++e) xhat[e] = xf[e];
-#pragma unroll
-        for (int e = 0; e < NX * NX; ++e) Pf[e] = Pn[e];
+        const double u = sr.u;
         ++solves;
-        if (!so.converged) ++fails;
+        if (!sr.converged) ++fails;
         cnt.steps += 1;
         if (traj != nullptr && i % stride == 0) {
             if (lane == 0) {
@@ -1776,6 +1820,126 @@ inline int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const doub
     else
         ocp_batch_kernel<1><<<(unsigned)blocks, 32, smem, stream>>>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv,
                                                                     status, ws, slab, counter);
+    return NMPCMC_OK;
+}
+
+
+/// Layout of one device-resident NmpcState (controllers.hpp:54-65) of the
+/// batched controller API (nmpcmc_gpu_nmpc_step_batch): the filter
+/// prediction (x_hat, P), the warm flag (last_xi non-empty) and the previous
+/// solution in the reference's orders: xi = (u_0, x_1, ..., u_{N-1}, x_N),
+/// lambda stage-ordered, pi_l, pi_u.
+template <int NX>
+struct StateLay {
+    int XH, P, WARM, XI, LAM, PL, PU, total;
+    __host__ __device__ explicit StateLay(int N)
+        : XH(0), P(NX), WARM(NX + NX * NX), XI(WARM + 1), LAM(XI + N * (1 + NX)), PL(LAM + N * NX), PU(PL + N),
+          total(PU + N) {}
+};
+
+/// Batched nmpc_step (controllers.cpp:114-212): one warp per controller
+/// instance b, on K3w's code path. The instance's NmpcState lives in
+/// states[b * stride ..] (StateLay) and is updated in place with the
+/// reference's transitions under exceptions (nmpc_step_ws). setpoints:
+/// sp[b * N + k] for stage k+1, or the scenario's profile at t + (k+1) Ts
+/// when sp is null (as run_closed_loop passes them).
+template <int NX>
+__global__ void __launch_bounds__(32) nmpc_step_kernel(const __grid_constant__ nmpcmc_scenario sc, int64_t batch,
+                                                       double* states, const double* t, const double* y,
+                                                       const double* sp, double* u_out, nmpcmc_nmpc_diag* diag,
+                                                       double* ws_all, int64_t slab, unsigned long long* next) {
+    const WsT<32> ws{ws_all + (int64_t)blockIdx.x * slab, 1};
+    const int lane = Lanes<32>::lane();
+    const StateLay<NX> SL(sc.N);
+#pragma unroll 1
+    for (;;) {
+        unsigned long long bi = 0;
+        if (lane == 0) bi = atomicAdd(next, 1ULL);
+        bi = __shfl_sync(kMask, bi, 0);
+        if (bi >= (unsigned long long)batch) break;
+        const int64_t b = (int64_t)bi;
+        Cnt cnt = {};
+        Ocp<NX, 32> o{make_model<NX>(sc.ctrl), Layout<NX>(sc.N), ws, sc.N, sc.Nc, sc.horizon_Ts,
+                      sc.horizon_Ts / sc.Nc, sc.u_min, sc.u_max, sc.Qz, 0.0, {}, &cnt};
+        o.invV = 1.0 / o.m.p.V;
+        const Layout<NX> L = o.lay;
+        const int N = o.N;
+        double* S = states + b * SL.total;
+        double xhat[NX], Pf[NX * NX], xf[NX], Pn[NX * NX];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) xhat[i] = S[SL.XH + i], xf[i] = kNaN;
+#pragma unroll
+        for (int e = 0; e < NX * NX; ++e) Pf[e] = S[SL.P + e], Pn[e] = kNaN;
+        const bool warm = S[SL.WARM] != 0.0;
+        bool have_last = warm;
+        const double tb = t[b], yb = y[b];
+        const double innov = yb - xhat[NX - 1] / o.m.p.V;  // filter_update's e (ekf.cpp:66)
+        StepRes sr{G_OK, false, false, false, kNaN};
+        if (!dfinite(yb)) {
+            sr.status = G_NONFINITE;  // nmpc_step: measurement is not finite
+        } else {
+            if (warm) {
+                for (int e = lane; e < L.L; e += 32) ws[L.LXI + e] = S[SL.XI + e];
+                for (int e = lane; e < L.NN; e += 32) ws[L.LLAM + e] = S[SL.LAM + e];
+                for (int k = lane; k < N; k += 32) ws[L.LPL + k] = S[SL.PL + k], ws[L.LPU + k] = S[SL.PU + k];
+            }
+            for (int k = lane; k < N; k += 32)
+                ws[L.SP + k] = sp != nullptr ? sp[b * N + k] : setpoint_at(sc, tb + (k + 1) * sc.Ts);
+            Lanes<32>::sync();
+            sr = nmpc_step_ws<NX, 32>(o, sc, tb, yb, xhat, Pf, have_last, xf, Pn);
+        }
+        if (sr.adopted) {
+            for (int e = lane; e < L.L; e += 32) S[SL.XI + e] = ws[L.LXI + e];
+            for (int e = lane; e < L.NN; e += 32) S[SL.LAM + e] = ws[L.LLAM + e];
+            for (int k = lane; k < N; k += 32) S[SL.PL + k] = ws[L.LPL + k], S[SL.PU + k] = ws[L.LPU + k];
+        }
+        if (lane == 0) {
+            if (sr.adopted) S[SL.WARM] = 1.0;
+            if (sr.status == G_OK) {
+#pragma unroll
+                for (int i = 0; i < NX; ++i) S[SL.XH + i] = xhat[i];
+#pragma unroll
+                for (int e = 0; e < NX * NX; ++e) S[SL.P + e] = Pf[e];
+            }
+            u_out[b] = sr.status == G_OK ? sr.u : kNaN;
+            if (diag != nullptr) {
+                nmpcmc_nmpc_diag d;
+                for (int i = 0; i < 3; ++i) d.x_filtered[i] = i < NX ? xf[i] : 0.0;
+                for (int e = 0; e < 9; ++e) d.P_filtered[e] = e < NX * NX ? Pn[e] : 0.0;
+                d.innovation = dfinite(yb) ? innov : kNaN;
+                d.converged = sr.converged ? 1 : 0;
+                d.sqp_iterations = (int32_t)cnt.sqp;
+                d.warm_started = warm ? 1 : 0;
+                d.status = sr.status;
+                diag[b] = d;
+            }
+        }
+        Lanes<32>::sync();
+    }
+}
+
+/// Doubles of one device-resident NmpcState (StateLay) for this scenario.
+inline int64_t nmpc_state_doubles(const nmpcmc_scenario& sc) {
+    return sc.ctrl_variant == NMPCMC_THREE_STATE ? StateLay<3>(sc.N).total : StateLay<1>(sc.N).total;
+}
+
+inline int launch_nmpc_step(const nmpcmc_scenario& sc, int64_t batch, double* states, const double* t,
+                            const double* y, const double* sp, double* u, nmpcmc_nmpc_diag* diag, double* ws,
+                            int64_t blocks, unsigned long long* counter, cudaStream_t stream) {
+    const bool c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
+    const int64_t slab = c3 ? Layout<3>(sc.N).total : Layout<1>(sc.N).total;
+    const size_t smem = c3 ? sweep_smem_bytes<3>(sc.N) : sweep_smem_bytes<1>(sc.N);
+    if (smem > kSweepSmemMax || blocks < 1) return NMPCMC_UNSUPPORTED;
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    if (c3) {
+        cudaFuncSetAttribute(nmpc_step_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        nmpc_step_kernel<3><<<(unsigned)blocks, 32, smem, stream>>>(sc, batch, states, t, y, sp, u, diag, ws, slab,
+                                                                    counter);
+    } else {
+        cudaFuncSetAttribute(nmpc_step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        nmpc_step_kernel<1><<<(unsigned)blocks, 32, smem, stream>>>(sc, batch, states, t, y, sp, u, diag, ws, slab,
+                                                                    counter);
+    }
     return NMPCMC_OK;
 }
 

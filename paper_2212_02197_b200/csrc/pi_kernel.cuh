@@ -16,6 +16,35 @@
 
 namespace nmpcmc_dev {
 
+/// pi_step (controllers.cpp:12-23) in the documented order:
+///   e = ybar - y, P = kP e, I = I_hat + Ts kI e, u_hat = u_bar + P + I,
+///   u = max(u_min, min(u_max, u_hat)), I_aw = Ts kaw (u_hat - u),
+///   next.I_hat = I + I_aw.
+__device__ __forceinline__ nmpcmc_pi_step_result pi_law(const nmpcmc_pi_state& s, double y, double ybar) {
+    nmpcmc_pi_step_result r;
+    r.e = ybar - y;
+    r.P = s.kP * r.e;
+    r.I = s.I_hat + s.Ts * s.kI * r.e;
+    r.u_hat = s.u_bar + r.P + r.I;
+    r.u = smax(s.u_min, smin(s.u_max, r.u_hat));
+    r.I_aw = s.Ts * s.kaw * (r.u_hat - r.u);
+    r.next_I_hat = r.I + r.I_aw;
+    return r;
+}
+
+/// Batched pi_step: instance i maps (states[i], y[i], ybar[i]) to
+/// results[i] (may be null) and adopts result.next into states[i].
+__global__ void pi_step_kernel(nmpcmc_pi_state* states, const double* y, const double* ybar, int64_t n,
+                               nmpcmc_pi_step_result* results) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        nmpcmc_pi_state s = states[i];
+        const nmpcmc_pi_step_result r = pi_law(s, y[i], ybar[i]);
+        if (results != nullptr) results[i] = r;
+        s.I_hat = r.next_I_hat;
+        states[i] = s;
+    }
+}
+
 /// Pairs of normals generated ahead per window refill (one control step
 /// consumes 1 + Ns * NX normals: 31 in every BASELINE config, one refill).
 constexpr int kPiPairs = 16;
@@ -59,13 +88,10 @@ __device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, in
         const double y = measure<NX>(p, pl, has_R, lR, rng);
         // pi_step (controllers.cpp:12-23), evaluated in the documented order
         const double ybar = setpoint_at(sc, t);
-        const double e = ybar - y;
-        const double P = kP * e;
-        const double I = I_hat + Ts * kI * e;
-        const double u_hat = u_bar + P + I;
-        const double u = smax(u_min, smin(u_max, u_hat));
-        const double I_aw = Ts * kaw * (u_hat - u);
-        I_hat = I + I_aw;
+        const nmpcmc_pi_state ps{kP, kI, kaw, Ts, u_bar, u_min, u_max, I_hat};
+        const nmpcmc_pi_step_result pr = pi_law(ps, y, ybar);
+        const double u = pr.u;
+        I_hat = pr.next_I_hat;
         if (record && i % stride == 0) {
             double* rw = traj + (size_t)row * 5;
             rw[0] = t;

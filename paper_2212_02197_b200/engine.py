@@ -85,6 +85,7 @@ def library():
     lib.nmpcmc_gpu_abi_version.restype = C.c_int
     lib.nmpcmc_gpu_validate.argtypes = [S, C.POINTER(C.c_int32)]
     lib.nmpcmc_gpu_ctx_create.argtypes = [C.c_int, C.POINTER(P)]
+    lib.nmpcmc_gpu_device_count.argtypes = [C.POINTER(C.c_int)]
     lib.nmpcmc_gpu_ctx_destroy.argtypes = [P]
     lib.nmpcmc_gpu_ctx_destroy.restype = None
     lib.nmpcmc_gpu_last_error.argtypes = [P]
@@ -127,6 +128,13 @@ def library():
     lib.nmpcmc_gpu_allgather_records.argtypes = [P, P, C.c_int64, P]
     _lib = lib
     return lib
+
+
+def device_count() -> int:
+    """Visible CUDA devices (0 without a driver)."""
+    n = C.c_int(0)
+    library().nmpcmc_gpu_device_count(C.byref(n))
+    return n.value
 
 
 def validate_scenario(sc: abi.Scenario) -> int:

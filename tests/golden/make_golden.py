@@ -167,6 +167,68 @@ def gen_dist():
     gen_case("nmpc_cfg2_1000", dict(controller="nmpc", N=60), 1000, 0)
 
 
+def gen_steps():
+    """Controller-level fixtures (round 2): the reference's make_nmpc_state +
+    nmpc_step (controllers.cpp:25-48, :114-212) over T steps for B
+    controllers with measurement sequences around a closed-loop trajectory,
+    per-instance priors, a non-finite measurement and a measurement far
+    outside the model's domain (exceptions mid-sequence), with the
+    scenario's setpoint profile and with explicit setpoints; and pi_step
+    (controllers.cpp:12-23) on random states including saturation."""
+    rng = np.random.default_rng(777)
+    out = {}
+    for tag, kw, B, T, explicit in (("one", dict(controller="nmpc", N=30), 24, 12, False),
+                                    ("one_sp", dict(controller="nmpc", N=20), 12, 8, True),
+                                    ("three", dict(controller="nmpc", N=20, ctrl_variant=0), 8, 6, False)):
+        sc = configs.make_scenario(**kw)
+        nx = 3 if kw.get("ctrl_variant", 1) == 0 else 1
+        p = configs.study_params()
+        T0 = rng.uniform(330.0, 340.0, B)
+        x0_hat = np.array([configs.manifold_state(p, t)[3 - nx:] for t in T0])
+        P0 = np.zeros((B, nx * nx))
+        for i in range(nx):
+            P0[:, i * nx + i] = 10.0 ** rng.uniform(-7, -4, B)
+        t = np.tile(np.arange(T) * sc.Ts, (B, 1)) + rng.uniform(0, 3000, (B, 1)).round()
+        y = T0[:, None] + np.cumsum(rng.normal(0.0, 0.8, (B, T)), axis=1)
+        y[1, T // 2] = np.nan          # nmpc_step throws NonFiniteState, state untouched
+        y[2, T // 3] = -500.0          # estimate leaves the model's domain
+        y[3, 1] = 1e6                  # absurd measurement
+        sp = rng.uniform(325.0, 345.0, (B, T, sc.N)) if explicit else None
+        u, diag, fin = O.nmpc_steps(O.ref("xlibm"), sc, x0_hat, P0, t, y, sp)
+        out[f"{tag}__kwargs"] = np.array(json.dumps(kw))
+        out[f"{tag}__x0_hat"], out[f"{tag}__P0"], out[f"{tag}__t"], out[f"{tag}__y"] = x0_hat, P0, t, y
+        if explicit:
+            out[f"{tag}__sp"] = sp
+        out[f"{tag}__u"], out[f"{tag}__diag"] = u, diag
+        for k, v in fin.items():
+            out[f"{tag}__fin_{k}"] = v
+        print(f"steps {tag}: {B}x{T}, status {np.bincount(diag['status'].ravel()).tolist()}, "
+              f"converged {diag['converged'].mean():.2f}")
+    from paper_2212_02197_b200 import controllers as K
+    n = 4096
+    st = np.zeros(n, dtype=K.PI_STATE_DTYPE)
+    st["kP"], st["kI"], st["kaw"] = rng.uniform(-20, 0, n), rng.uniform(-0.5, 0, n), rng.uniform(-0.5, 0.5, n)
+    st["Ts"], st["u_bar"] = rng.uniform(0.5, 20, n), rng.uniform(0, 1000, n)
+    st["u_min"], st["u_max"] = rng.uniform(0, 200, n), rng.uniform(300, 1000, n)
+    st["I_hat"] = rng.normal(0, 300, n)
+    y = rng.normal(335, 10, n)
+    ybar = rng.normal(335, 5, n)
+    L = O.ref("xlibm")
+    res = np.zeros(n, dtype=K.PI_RESULT_DTYPE)
+    import ctypes as C
+    L.nmpcmc_ref_pi_step.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_void_p]
+    L.nmpcmc_ref_pi_step.restype = None
+    for i in range(n):
+        s = np.array([st[i][f] for f in K.PI_STATE_DTYPE.names])
+        o = np.zeros(7)
+        L.nmpcmc_ref_pi_step(s.ctypes.data, float(y[i]), float(ybar[i]), o.ctypes.data)
+        res[i] = tuple(o)
+    sat = np.mean((res["u"] == st["u_min"]) | (res["u"] == st["u_max"]))
+    print(f"pi_step: {n} states, saturated {sat:.2f}")
+    out["pi__states"], out["pi__y"], out["pi__ybar"], out["pi__results"] = st, y, ybar, res
+    np.savez_compressed(os.path.join(OUT, "controller_steps.npz"), **out)
+
+
 def main(which):
     if which in ("rng", "all"):
         gen_rng()
@@ -191,6 +253,8 @@ def main(which):
         gen_full()
     if which in ("dist", "all"):
         gen_dist()
+    if which in ("steps", "all"):
+        gen_steps()
     if which in ("nmpc3", "all"):
         # three-state controller model (config 2 read literally: CD-EKF and
         # OCP on the 3-state CSTR; ctrl_variant 0 = THREE_STATE) -> kernel K3g

@@ -30,3 +30,4 @@ def test_facade_client_runs_on_gpu(tmp_path):
     assert "multi-device records identical 1 (devices 2)" in out
     assert "qp status 0 u -1.000000000" in out  # active lower bound (u* = -1.6 unconstrained)
     assert "ocp converged 1" in out
+    assert "nmpc_step warm 1 status 0 u finite 1" in out
