@@ -172,7 +172,16 @@ const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx);
  * K3w, or K3g when GENERIC / THREAD is selected. Results are bitwise
  * identical; only speed differs. NMPCMC_OPT_TPS_WARPS_PER_SM is accepted and
  * ignored (it tuned K3b). */
-enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2, NMPCMC_OPT_LANES = 3 };
+enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2, NMPCMC_OPT_LANES = 3,
+       NMPCMC_OPT_CTRL_JACOBIANS = 4 };
+/* NMPCMC_OPT_CTRL_JACOBIANS: how the controller model's jacobians are formed.
+ * ANALYTIC (default) = the closed forms make_cstr_model installs
+ * (cstr.cpp:86-127). FD = as a Model WITHOUT analytic jacobians:
+ * drift_jacobian_x / _u, measurement_jacobian_x and output_jacobian_x by the
+ * reference's central differences, step max(1e-6, 1e-6 |v|)
+ * (model.cpp:54-124) -- bitwise the reference run on such a Model. FD runs on
+ * the generic one-warp kernel (K3w) for either controller model. */
+enum { NMPCMC_JACOBIANS_ANALYTIC = 0, NMPCMC_JACOBIANS_FD = 1 };
 /* NMPCMC_OPT_LANES = 2 pipelines back-to-back batches: NMPC launches alternate
  * between two internal streams with their own workspace (PI launches use a
  * third), each forked from the context stream, so one batch's drain (its last
@@ -412,6 +421,33 @@ int nmpcmc_gpu_nmpc_step_batch(nmpcmc_gpu_ctx* ctx, nmpcmc_nmpc_batch* st, const
 int nmpcmc_gpu_nmpc_batch_get(nmpcmc_nmpc_batch* st, double* x_hat, double* P, double* last_xi,
                               double* last_lambda, double* last_pi_l, double* last_pi_u, int32_t* warm);
 int64_t nmpcmc_gpu_nmpc_batch_size(const nmpcmc_nmpc_batch* st);
+
+/* ---- Batched SQP on stagewise quadratic NLPs ---
+ * sqp_solve (sqp.hpp:148-151, sqp.cpp:182-411) through the SqpProblem
+ * interface (sqp.hpp:15-25) on `batch` problems of the quadratic kind --
+ * the problems the reference's SQP tests pose: xi = (u_0, x_1, ...,
+ * u_{N-1}, x_N), n_u = 1, n_x = 1 or 3, x_0 given,
+ *   f = sum_k [1/2 R_k u_k^2 + r_k u_k + 1/2 x_{k+1}' Q_k x_{k+1} + q_k' x_{k+1}]
+ *   x_{k+1} = A_k x_k + B_k u_k + c_k,   u_min <= u_k <= u_max.
+ * problems: HOST, batch * nmpcmc_qnlp_doubles(N, n_x) doubles; per problem
+ * x0[n_x] u_min u_max, then per stage k = 0..N-1: R r Q[n_x*n_x] q[n_x]
+ * A[n_x*n_x] B[n_x] c[n_x] (column-major). The objective and dynamics are
+ * evaluated in the order documented in csrc/nmpc_gen_kernel.cuh (Qnlp).
+ * xi0: HOST batch * N*(1+n_x) start iterates, or NULL for zeros; duals start
+ * at zero, Hessian blocks at identity. Outputs as nmpcmc_gpu_solve_ocp_batch
+ * plus iterations (SqpReport::iterations). One warp per problem. */
+typedef struct nmpcmc_qnlp_dims {
+    int32_t N;
+    int32_t n_x;  /* 1 or 3 */
+    int32_t n_u;  /* must be 1 */
+    int32_t _pad;
+    nmpcmc_sqp_options sqp;
+} nmpcmc_qnlp_dims;
+int64_t nmpcmc_qnlp_doubles(int32_t N, int32_t n_x);
+int nmpcmc_gpu_sqp_solve_qnlp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_qnlp_dims* dims, int64_t batch,
+                                    const double* problems, const double* xi0, double* xi, double* lambda,
+                                    double* pi_l, double* pi_u, int32_t* converged, int32_t* iterations,
+                                    int32_t* status);
 
 #ifdef __cplusplus
 }

@@ -168,3 +168,20 @@ def nmpc_steps(lib, sc, x0_hat, P0, t, y, sp=None):
       None if keep[2] is None else keep[2].ctypes.data, u.ctypes.data, diag.ctypes.data,
       *(fin[k].ctypes.data for k in ("x_hat", "P", "last_xi", "last_lambda", "last_pi_l", "last_pi_u", "warm")))
     return u, diag, fin
+
+
+def sqp_solve_qnlp_batch(lib, problems, N, nx, opts, xi0=None):
+    """The reference's sqp_solve on QnlpProblems (nmpcmc_ref_sqp_solve_qnlp_batch)."""
+    from paper_2212_02197_b200 import qp as Q
+    problems = np.ascontiguousarray(problems, dtype=np.float64)
+    Bn, L = problems.shape[0], N * (1 + nx)
+    d = Q.QnlpDims(N, nx, 1, 0, opts)
+    out = dict(xi=np.zeros((Bn, L)), **{"lambda": np.zeros((Bn, N * nx))}, pi_l=np.zeros((Bn, N)),
+               pi_u=np.zeros((Bn, N)), converged=np.zeros(Bn, dtype=np.int32), iterations=np.zeros(Bn, dtype=np.int32),
+               status=np.zeros(Bn, dtype=np.int32))
+    x0p = None if xi0 is None else np.ascontiguousarray(xi0, dtype=np.float64)
+    f = lib.nmpcmc_ref_sqp_solve_qnlp_batch
+    f.argtypes = [C.c_void_p, C.c_int64] + [C.c_void_p] * 9
+    f(C.byref(d), Bn, problems.ctypes.data, None if x0p is None else x0p.ctypes.data,
+      *(out[k].ctypes.data for k in ("xi", "lambda", "pi_l", "pi_u", "converged", "iterations", "status")))
+    return out

@@ -72,6 +72,11 @@ CstrParams truth_params(const nmpcmc_scenario& s, std::uint64_t sim_index) {
     return p;
 }
 
+/// nmpcmc_ref_set_ctrl_fd: build the controller model without its analytic
+/// jacobians, so the reference takes its finite-difference fallbacks
+/// (model.cpp:54-124) -- the counterpart of NMPCMC_OPT_CTRL_JACOBIANS = FD.
+int g_ctrl_fd = 0;
+
 Scenario make_scenario(const nmpcmc_scenario& s, std::uint64_t sim_index) {
     Scenario sc;
     sc.truth = make_cstr_model(truth_params(s, sim_index), to_variant(s.truth_variant));
@@ -79,6 +84,12 @@ Scenario make_scenario(const nmpcmc_scenario& s, std::uint64_t sim_index) {
     sc.noise.n_w = sc.truth.n_w;
     sc.controller = s.controller == NMPCMC_CTRL_PI ? ControllerType::pi : ControllerType::nmpc;
     sc.ctrl_model = make_cstr_model(to_params(s.ctrl), to_variant(s.ctrl_variant));
+    if (g_ctrl_fd) {
+        sc.ctrl_model.drift_jacobian_x = nullptr;
+        sc.ctrl_model.drift_jacobian_u = nullptr;
+        sc.ctrl_model.measurement_jacobian_x = nullptr;
+        sc.ctrl_model.output_jacobian_x = nullptr;
+    }
     sc.horizon = Horizon{s.N, s.horizon_Ts, s.Nc};
     sc.Qz = Matrix::from_rows({{s.Qz}});
     sc.R_filter = Matrix::from_rows({{s.R_filter}});
@@ -159,6 +170,8 @@ void run_one(const nmpcmc_scenario& s, std::uint64_t idx, nmpcmc_sim_record* out
 }  // namespace
 
 extern "C" {
+
+void nmpcmc_ref_set_ctrl_fd(int on) { g_ctrl_fd = on ? 1 : 0; }
 
 int nmpcmc_ref_validate(const nmpcmc_scenario* s, int* nbar) {
     try {
@@ -348,6 +361,139 @@ int nmpcmc_ref_nmpc_steps(const nmpcmc_scenario* s, std::int64_t B, int T, const
         for (int i = 0; i < N * nx; ++i) lam_out[b * N * nx + i] = w ? st.last_duals.lambda[i] : 0.0;
         for (int i = 0; i < N; ++i) pil_out[b * N + i] = w ? st.last_duals.pi_l[i] : 0.0;
         for (int i = 0; i < N; ++i) piu_out[b * N + i] = w ? st.last_duals.pi_u[i] : 0.0;
+    }
+    return 0;
+}
+
+/// A stagewise quadratic NLP through the reference's SqpProblem interface
+/// (sqp.hpp:15-25), as its SQP tests pose plain QPs: the packed layout and the
+/// evaluation order of nmpcmc_gpu_sqp_solve_qnlp_batch (include/nmpcmc_gpu.h,
+/// Qnlp in csrc/nmpc_gen_kernel.cuh). Test infrastructure: the thing under
+/// test is the reference's sqp_solve run on it.
+class QnlpProblem final : public SqpProblem {
+public:
+    QnlpProblem(const double* data, int N, int nx) : d_(data), N_(N), nx_(nx) {
+        lay_.N = N;
+        lay_.n_x = nx;
+        lay_.n_u = 1;
+        umin_ = {data[nx]};
+        umax_ = {data[nx + 1]};
+    }
+    XiLayout layout() const override { return lay_; }
+    const Vec& u_min() const override { return umin_; }
+    const Vec& u_max() const override { return umax_; }
+    double objective(const Vec& xi, Vec* grad) const override {
+        const int nx = nx_;
+        double phi = 0.0;
+        for (int k = 0; k < N_; ++k) {
+            const double* P = stage(k);
+            const double u = xi[lay_.u_offset(k)];
+            const double su = P[0] * u;
+            phi = phi + (0.5 * (u * su) + P[1] * u);
+            double xQx = 0.0, qx = 0.0;
+            for (int i = 0; i < nx; ++i) {
+                double qxi = 0.0;
+                for (int j = 0; j < nx; ++j) qxi += P[2 + j * nx + i] * xi[lay_.x_offset(k + 1) + j];
+                const double xv = xi[lay_.x_offset(k + 1) + i];
+                xQx += xv * qxi;
+                qx += P[2 + nx * nx + i] * xv;
+            }
+            phi = phi + (0.5 * xQx + qx);
+        }
+        if (grad != nullptr) {
+            grad->assign(static_cast<std::size_t>(lay_.size()), 0.0);
+            for (int k = 0; k < N_; ++k) {
+                const double* P = stage(k);
+                const double u = xi[lay_.u_offset(k)];
+                (*grad)[lay_.u_offset(k)] = P[0] * u + P[1];
+                for (int i = 0; i < nx; ++i) {
+                    double qxi = 0.0;
+                    for (int j = 0; j < nx; ++j) qxi += P[2 + j * nx + i] * xi[lay_.x_offset(k + 1) + j];
+                    (*grad)[lay_.x_offset(k + 1) + i] = qxi + P[2 + nx * nx + i];
+                }
+            }
+        }
+        return phi;
+    }
+    ConstraintBlocks constraints(const Vec& xi) const override {
+        const int nx = nx_;
+        ConstraintBlocks cb;
+        cb.g.assign(static_cast<std::size_t>(N_ * nx), 0.0);
+        for (int k = 0; k < N_; ++k) {
+            const double* P = stage(k);
+            const double* A = P + 2 + nx * nx + nx;
+            const double* B = A + nx * nx;
+            const double* c = B + nx;
+            Matrix Fx(nx, nx), Fu(nx, 1);
+            Vec b(nx);
+            for (int i = 0; i < nx; ++i) {
+                double F = 0.0;
+                for (int j = 0; j < nx; ++j) F += A[j * nx + i] * (k == 0 ? d_[j] : xi[lay_.x_offset(k) + j]);
+                F = F + B[i] * xi[lay_.u_offset(k)];
+                F = F + c[i];
+                const double nxt = xi[lay_.x_offset(k + 1) + i];
+                cb.g[k * nx + i] = nxt - F;
+                b[i] = F - nxt;
+                Fu(i, 0) = B[i];
+                for (int j = 0; j < nx; ++j) Fx(i, j) = A[j * nx + i];
+            }
+            cb.dF_dx.push_back(Fx);
+            cb.dF_du.push_back(Fu);
+            cb.b.push_back(b);
+        }
+        return cb;
+    }
+
+private:
+    const double* stage(int k) const { return d_ + nx_ + 2 + static_cast<std::ptrdiff_t>(k) * (2 + 2 * nx_ * nx_ + 3 * nx_); }
+    const double* d_;
+    int N_, nx_;
+    XiLayout lay_;
+    Vec umin_, umax_;
+};
+
+/// The reference's sqp_solve on a batch of QnlpProblems (layout of
+/// nmpcmc_gpu_sqp_solve_qnlp_batch); status NMPCMC_DOMAIN_ERROR etc. where it throws.
+int nmpcmc_ref_sqp_solve_qnlp_batch(const nmpcmc_qnlp_dims* d, std::int64_t batch, const double* problems,
+                                    const double* xi0_in, double* xi_out, double* lam_out, double* pil_out,
+                                    double* piu_out, std::int32_t* converged, std::int32_t* iters,
+                                    std::int32_t* status) {
+    const int N = d->N, nx = d->n_x, L = N * (1 + nx);
+    const std::int64_t stride = nx + 2 + static_cast<std::int64_t>(N) * (2 + 2 * nx * nx + 3 * nx);
+    SqpOptions opts;
+    opts.eps = d->sqp.eps;
+    opts.max_iter = d->sqp.max_iter;
+    opts.max_backtracks = d->sqp.max_backtracks;
+    opts.c1 = d->sqp.c1;
+    opts.backtrack_factor = d->sqp.backtrack_factor;
+    opts.qp_tol = d->sqp.qp_tol;
+    opts.qp_max_iter = d->sqp.qp_max_iter;
+    for (std::int64_t b = 0; b < batch; ++b) {
+        const QnlpProblem prob(problems + b * stride, N, nx);
+        Vec xi0(static_cast<std::size_t>(L), 0.0);
+        if (xi0_in != nullptr) xi0.assign(xi0_in + b * L, xi0_in + (b + 1) * L);
+        std::fill(xi_out + b * L, xi_out + (b + 1) * L, 0.0);
+        std::fill(lam_out + b * N * nx, lam_out + (b + 1) * N * nx, 0.0);
+        std::fill(pil_out + b * N, pil_out + (b + 1) * N, 0.0);
+        std::fill(piu_out + b * N, piu_out + (b + 1) * N, 0.0);
+        converged[b] = 0;
+        iters[b] = 0;
+        try {
+            const SqpReport rep = sqp_solve(prob, xi0, opts, SqpWarmStart{});
+            std::copy(rep.xi.begin(), rep.xi.end(), xi_out + b * L);
+            std::copy(rep.lambda.begin(), rep.lambda.end(), lam_out + b * N * nx);
+            std::copy(rep.pi_l.begin(), rep.pi_l.end(), pil_out + b * N);
+            std::copy(rep.pi_u.begin(), rep.pi_u.end(), piu_out + b * N);
+            converged[b] = rep.converged ? 1 : 0;
+            iters[b] = rep.iterations;
+            status[b] = 0;
+        } catch (const DomainError&) {
+            status[b] = NMPCMC_DOMAIN_ERROR;
+        } catch (const NonFiniteState&) {
+            status[b] = NMPCMC_NON_FINITE_STATE;
+        } catch (const NotPositiveDefinite&) {
+            status[b] = NMPCMC_NOT_POSITIVE_DEFINITE;
+        }
     }
     return 0;
 }

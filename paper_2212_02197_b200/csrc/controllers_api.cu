@@ -197,4 +197,74 @@ int nmpcmc_gpu_nmpc_batch_get(nmpcmc_nmpc_batch* st, double* x_hat, double* P, d
     return NMPCMC_OK;
 }
 
+int64_t nmpcmc_qnlp_doubles(int32_t N, int32_t n_x) {
+    if (N < 1 || (n_x != 1 && n_x != 3)) return 0;
+    return nmpcmc_launch::qnlp_stride(N, n_x);
+}
+
+int nmpcmc_gpu_sqp_solve_qnlp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_qnlp_dims* d, int64_t batch,
+                                    const double* problems, const double* xi0, double* xi, double* lambda,
+                                    double* pi_l, double* pi_u, int32_t* converged, int32_t* iterations,
+                                    int32_t* status) {
+    if (ctx == nullptr || d == nullptr || batch < 0) return NMPCMC_INVALID_ARGUMENT;
+    if (d->N < 1 || (d->n_x != 1 && d->n_x != 3) || d->n_u != 1)
+        return fail(ctx, NMPCMC_DIMENSION_MISMATCH, "qnlp batch: N >= 1, n_x in {1, 3}, n_u = 1");
+    if (d->sqp.max_iter < 0 || d->sqp.qp_max_iter < 1 || d->sqp.max_backtracks < 0)
+        return fail(ctx, NMPCMC_DOMAIN_ERROR, "qnlp batch: bad SqpOptions");
+    if (batch == 0) return NMPCMC_OK;
+    if (!problems || !xi || !lambda || !pi_l || !pi_u || !converged || !iterations || !status)
+        return NMPCMC_INVALID_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const int nx = d->n_x, N = d->N;
+    const int64_t stride = nmpcmc_launch::qnlp_stride(N, nx), L = (int64_t)N * (1 + nx);
+    auto rnd = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t bp = batch * stride * 8, bx = batch * L * 8, bl = batch * (int64_t)N * nx * 8,
+                 bpi = batch * (int64_t)N * 8, bi = batch * 4;
+    int rc;
+    if ((rc = ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap,
+                     rnd(bp) + (xi0 ? rnd(bx) : 0) + rnd(bx) + rnd(bl) + 2 * rnd(bpi) + 3 * rnd(bi))) != NMPCMC_OK)
+        return rc;
+    char* p = static_cast<char*>(ctx->d_scratch);
+    auto take = [&](size_t n) {
+        char* a = p;
+        p += rnd(n);
+        return a;
+    };
+    auto* d_prob = reinterpret_cast<double*>(take(bp));
+    auto* d_xi0 = xi0 ? reinterpret_cast<double*>(take(bx)) : nullptr;
+    auto* d_xi = reinterpret_cast<double*>(take(bx));
+    auto* d_lam = reinterpret_cast<double*>(take(bl));
+    auto* d_pil = reinterpret_cast<double*>(take(bpi));
+    auto* d_piu = reinterpret_cast<double*>(take(bpi));
+    auto* d_conv = reinterpret_cast<int32_t*>(take(bi));
+    auto* d_it = reinterpret_cast<int32_t*>(take(bi));
+    auto* d_st = reinterpret_cast<int32_t*>(take(bi));
+    // one warp per problem, persistent one-warp blocks; the per-warp slabs
+    // stay L2-resident (as K3w's)
+    int64_t blocks = (int64_t)ctx->sm_count * 16;
+    const int64_t slab = nmpcmc_launch::qnlp_ws_doubles(N, nx);
+    const int64_t l2_cap = (int64_t)(96ull << 20) / (slab * 8);
+    if (blocks > l2_cap) blocks = l2_cap < ctx->sm_count ? ctx->sm_count : l2_cap;
+    if (blocks > batch) blocks = batch;
+    if ((rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, (size_t)(blocks * slab * 8))) != NMPCMC_OK) return rc;
+    if ((rc = ensure(ctx, &ctx->d_counter, &ctx->counter_cap, 256)) != NMPCMC_OK) return rc;
+    cudaError_t e = cudaMemcpyAsync(d_prob, problems, bp, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess && xi0) e = cudaMemcpyAsync(d_xi0, xi0, bx, cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "cudaMemcpyAsync");
+    rc = nmpcmc_launch::launch_qnlp_batch(N, nx, d->sqp, batch, d_prob, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv,
+                                          d_it, d_st, static_cast<double*>(ctx->d_ws), blocks,
+                                          static_cast<unsigned long long*>(ctx->d_counter), ctx->stream);
+    if (rc != NMPCMC_OK) return fail(ctx, rc, "qnlp batch: horizon too long for the shared-memory sweep arrays");
+    if ((rc = cuda_check(ctx, cudaGetLastError(), "qnlp_batch_kernel launch")) != NMPCMC_OK) return rc;
+    e = cudaMemcpyAsync(xi, d_xi, bx, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(lambda, d_lam, bl, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pi_l, d_pil, bpi, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pi_u, d_piu, bpi, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(converged, d_conv, bi, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(iterations, d_it, bi, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(status, d_st, bi, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "cudaMemcpyAsync");
+    return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "qnlp_batch_kernel");
+}
+
 }  // extern "C"

@@ -59,6 +59,7 @@ struct nmpcmc_gpu_ctx {
     int sm_count = 0;
     int nmpc_kernel = NMPCMC_NMPC_KERNEL_WARP;  // which NMPC kernel to launch
     int tps_warps_per_sm = 8;                   // K3b resident warps per SM
+    int ctrl_fd = 0;                            // NMPCMC_OPT_CTRL_JACOBIANS: 1 = finite differences
     cudaStream_t own = nullptr;                 // the stream ctx_create made (set_stream may replace ctx->stream)
     int lanes = 1;                              // NMPCMC_OPT_LANES
     int next_nmpc_lane = 0;

@@ -121,6 +121,22 @@ __device__ __forceinline__ void normal_pair(uint64_t seed, uint64_t stream, uint
     c = radius * cs;
 }
 
+/// Normal n of stream (seed, stream) alone: component n & 1 of pair n >> 1
+/// (c for even n, s for odd n), bitwise the value normal_pair produces for
+/// it -- only the needed half of the sincos is kept.
+__device__ __forceinline__ double normal_one(uint64_t seed, uint64_t stream, uint64_t n) {
+    const uint64_t p = n >> 1;
+    const uint4 ctr = make_uint4((uint32_t)p, (uint32_t)(p >> 32), (uint32_t)stream, (uint32_t)(stream >> 32));
+    const uint4 b = philox4x32_10(ctr, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint64_t w0 = ((uint64_t)b.x << 32) | b.y;
+    const uint64_t w1 = ((uint64_t)b.z << 32) | b.w;
+    const double u1 = 1.0 - (double)(w0 >> 11) * 0x1.0p-53;
+    const double u2 = (double)(w1 >> 11) * 0x1.0p-53;
+    const double radius = sqrt(-2.0 * xlibm_log(u1));
+    const double angle = 0x1.921fb54442d18p+2 * u2;
+    return radius * ((n & 1) ? xlibm_sin(angle) : xlibm_cos(angle));
+}
+
 /// W consecutive pairs from pair0 into buf (element j at buf[j * stride]):
 /// W independent Philox / log / sincos chains, so they overlap (ILP).
 template <int W>
@@ -139,13 +155,37 @@ __device__ __noinline__ void fill_normal_pairs(double* buf, int stride, uint64_t
 /// generated ahead (fill_normal_pairs) instead of one pair per call: the same
 /// sequence bit for bit (normal k is component k & 1 of pair k >> 1), but
 /// the generation leaves the plant's serial Euler-Maruyama chain.
-template <int W>
+///
+/// G > 1: the window is shared by a group of G consecutive lanes that run the
+/// same sample in lockstep (every lane holds the same k); lane r of the group
+/// generates pairs r, r + G, ... of each refill, so a refill costs each lane
+/// W / G chains. Refills must be warp-uniform (the caller keeps every group
+/// of the warp at the same k at each refill point): __syncwarp of the whole
+/// warp orders the shared-memory windows without splitting it.
+template <int W, int G = 1>
 struct NormalWindow {
     double* buf;
     int stride;
     uint64_t seed, stream;
     uint64_t base;  // normal index of buf[0] (even)
     uint64_t k;     // next normal index
+    unsigned gmask; // lanes that refill together (the whole warp)
+    int r;          // rank in the group
+    __device__ void fill(uint64_t pair0) {
+        if (G == 1) {
+            fill_normal_pairs<W>(buf, stride, seed, stream, pair0);
+            return;
+        }
+        __syncwarp(gmask);  // every lane of the group is done reading the old window
+#pragma unroll
+        for (int j = 0; j < W; j += G) {
+            double c, s;
+            normal_pair(seed, stream, pair0 + j + r, c, s);
+            buf[(2 * (j + r)) * stride] = c;
+            buf[(2 * (j + r) + 1) * stride] = s;
+        }
+        __syncwarp(gmask);
+    }
     __device__ void init(double* b, int st, uint64_t seed_, uint64_t stream_) {
         buf = b;
         stride = st;
@@ -153,19 +193,39 @@ struct NormalWindow {
         stream = stream_;
         k = 0;
         base = 0;
-        fill_normal_pairs<W>(buf, stride, seed, stream, 0);
+        r = G == 1 ? 0 : (int)(threadIdx.x & (G - 1));
+        gmask = 0xffffffffu;
+        fill(0);
     }
+    /// One control step's refill when only some of its normals are read: the
+    /// measurement normal k0 (has_R) and the third of every plant substep's
+    /// three, k0 + has_R + 3 j + 2 (the three-state plant with zero diffusion
+    /// on c_A, c_B: simulate_interval<NX, true>). The others are skipped
+    /// (skip()), never read. Needs has_R + 3 ns <= 2W - 1. Warp-uniform.
+    __device__ void fill_sparse(uint64_t k0, int has_R, int ns) {
+        k = k0;
+        base = k0 & ~1ULL;
+        if (G > 1) __syncwarp(gmask);
+        const int count = has_R + ns;
+#pragma unroll 4
+        for (int m = r; m < count; m += G) {
+            const uint64_t n = (has_R && m == 0) ? k0 : k0 + (uint64_t)(has_R + 3 * (m - has_R) + 2);
+            buf[(int)(n - base) * stride] = normal_one(seed, stream, n);
+        }
+        if (G > 1) __syncwarp(gmask);
+    }
+    __device__ __forceinline__ void skip() { ++k; }
     /// make normals k .. k+m-1 resident (m <= 2W - 1) with at most one refill
     __device__ __forceinline__ void reserve(int m) {
         if (k + (uint64_t)m > base + 2 * W) {
             base = k & ~1ULL;
-            fill_normal_pairs<W>(buf, stride, seed, stream, base >> 1);
+            fill(base >> 1);
         }
     }
     __device__ __forceinline__ double normal() {
         if (k >= base + 2 * W) {
             base = k & ~1ULL;
-            fill_normal_pairs<W>(buf, stride, seed, stream, base >> 1);
+            fill(base >> 1);
         }
         const double z = buf[(int)(k - base) * stride];
         ++k;
@@ -272,7 +332,11 @@ __device__ __forceinline__ double measure(const Cstr& p, const Plant<NX>& pl, bo
 
 /// simulate_interval (model.cpp:26-37) + euler_maruyama_step (model.cpp:13-24)
 /// for the CSTR (diffusion diag(F sigma_bar), cstr.cpp:55-65). Returns a status.
-template <int NX, class Rng>
+/// SPARSE (NX = 3, sigma_A = sigma_B = 0): the c_A, c_B increments are not
+/// drawn but skipped and taken as 0. Bitwise the same states: in the gemv
+/// below their terms are (+-0) * dw in every row, the row sums start at +0.0,
+/// and +0 + (+-0) = +0, so no row depends on dw_A or dw_B.
+template <int NX, class Rng, bool SPARSE = false>
 __device__ __forceinline__ int simulate_interval(const Cstr& p, Plant<NX>& pl, double t0, double t1,
                                                  double u, int ns, Rng& rng) {
     const double dt = (t1 - t0) / ns;
@@ -289,7 +353,16 @@ __device__ __forceinline__ int simulate_interval(const Cstr& p, Plant<NX>& pl, d
     for (int k = 0; k < ns; ++k) {
         double dw[NX];
 #pragma unroll
-        for (int j = 0; j < NX; ++j) dw[j] = sqrt_dt * rng.normal();
+        for (int j = 0; j < NX; ++j) {
+            if constexpr (SPARSE) {
+                if (j < NX - 1) {
+                    rng.skip();
+                    dw[j] = 0.0;
+                    continue;
+                }
+            }
+            dw[j] = sqrt_dt * rng.normal();
+        }
         double dn[NX];
         int st;
         if (NX == 3)

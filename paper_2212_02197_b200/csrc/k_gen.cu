@@ -17,8 +17,9 @@ int64_t gen_slots(const nmpcmc_scenario& sc, int sm_count, int64_t n) {
 
 int launch_genw(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
                 nmpcmc_work_counters* d_cnt, double* d_traj, int rows, double* ws, int64_t blocks,
-                unsigned long long* counter, cudaStream_t stream) {
-    return nmpcmc_dev::gen::launch_genw(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ws, blocks, counter, stream);
+                unsigned long long* counter, cudaStream_t stream, int fd) {
+    return nmpcmc_dev::gen::launch_genw(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ws, blocks, counter, stream,
+                                        fd);
 }
 
 int launch_gen(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
@@ -32,6 +33,16 @@ int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const double* x0,
                      int64_t blocks, unsigned long long* counter, cudaStream_t stream) {
     return nmpcmc_dev::gen::launch_ocp_batch(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv, status, ws, blocks,
                                              counter, stream);
+}
+
+int64_t qnlp_stride(int N, int nx) { return nmpcmc_dev::gen::qnlp_stride(N, nx); }
+int64_t qnlp_ws_doubles(int N, int nx) { return nmpcmc_dev::gen::qnlp_ws_doubles(N, nx); }
+int launch_qnlp_batch(int N, int nx, const nmpcmc_sqp_options& opt, int64_t batch, const double* prob,
+                      const double* xi0, double* xi, double* lam, double* pil, double* piu, int32_t* conv,
+                      int32_t* iters, int32_t* status, double* ws, int64_t blocks, unsigned long long* counter,
+                      cudaStream_t stream) {
+    return nmpcmc_dev::gen::launch_qnlp_batch(N, nx, opt, batch, prob, xi0, xi, lam, pil, piu, conv, iters, status,
+                                              ws, blocks, counter, stream);
 }
 
 int64_t nmpc_state_doubles(const nmpcmc_scenario& sc) { return nmpcmc_dev::gen::nmpc_state_doubles(sc); }

@@ -73,13 +73,29 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, 
 namespace nmpcmc_launch {
 
 int launch_pi(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
-              nmpcmc_work_counters* d_cnt, double* d_traj, int rows, cudaStream_t stream) {
-    const int block = nmpcmc_dev::kPiBlock;
-    const unsigned grid = (unsigned)((n + block - 1) / block);
-    if (sc.truth_variant == NMPCMC_THREE_STATE)
-        nmpcmc_dev::pi_kernel<3><<<grid, block, 0, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
-    else
-        nmpcmc_dev::pi_kernel<1><<<grid, block, 0, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+              nmpcmc_work_counters* d_cnt, double* d_traj, int rows, int sm_count, cudaStream_t stream) {
+    // several lanes per sample for batches too small to fill the GPU with one
+    // thread per sample (about 4 warps per SM), when one control step's
+    // normals fit one window refill (the lanes keep the warp in lockstep,
+    // pi_kernel.cuh); measured: config 0 (1,000) 11.0 -> 6.5 ms at 4 lanes,
+    // config 1 (30,000) fastest at 1 lane (profiles/r02d_pi_variants.txt)
+    constexpr int G = nmpcmc_dev::kPiLanes, block = nmpcmc_dev::kPiBlock;
+    const bool three = sc.truth_variant == NMPCMC_THREE_STATE;
+    const int per_step = (sc.has_noise_R != 0 ? 1 : 0) + sc.Ns * (three ? 3 : 1);
+    const bool small = n < (int64_t)sm_count * 4 * 32;
+    if (G > 1 && small && per_step < 2 * nmpcmc_dev::kPiPairs) {
+        const unsigned grid = (unsigned)((n + block / G - 1) / (block / G));
+        if (three)
+            nmpcmc_dev::pi_kernel<3, G><<<grid, block, 0, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+        else
+            nmpcmc_dev::pi_kernel<1, G><<<grid, block, 0, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+    } else {
+        const unsigned grid = (unsigned)((n + block - 1) / block);
+        if (three)
+            nmpcmc_dev::pi_kernel<3, 1><<<grid, block, 0, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+        else
+            nmpcmc_dev::pi_kernel<1, 1><<<grid, block, 0, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows);
+    }
     return NMPCMC_OK;
 }
 

@@ -28,9 +28,11 @@ bool genw_fits(const nmpcmc_scenario& sc);
 int64_t genw_blocks(const nmpcmc_scenario& sc, int sm_count, int64_t n);
 int64_t gen_ws_doubles(const nmpcmc_scenario& sc);
 int64_t gen_slots(const nmpcmc_scenario& sc, int sm_count, int64_t n);
+/// fd = 1: the controller model's jacobians by central differences
+/// (NMPCMC_OPT_CTRL_JACOBIANS).
 int launch_genw(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
                 nmpcmc_work_counters* d_cnt, double* d_traj, int rows, double* ws, int64_t blocks,
-                unsigned long long* counter, cudaStream_t stream);
+                unsigned long long* counter, cudaStream_t stream, int fd);
 int launch_gen(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
                nmpcmc_work_counters* d_cnt, double* d_traj, int rows, double* ws, int64_t slots,
                unsigned long long* counter, cudaStream_t stream);
@@ -44,9 +46,17 @@ int launch_nmpc_step(const nmpcmc_scenario& sc, int64_t batch, double* states, c
                      const double* sp, double* u, nmpcmc_nmpc_diag* diag, double* ws, int64_t blocks,
                      unsigned long long* counter, cudaStream_t stream);
 
+// ---- batched sqp_solve on stagewise quadratic NLPs (k_gen.cu)
+int64_t qnlp_stride(int N, int nx);
+int64_t qnlp_ws_doubles(int N, int nx);
+int launch_qnlp_batch(int N, int nx, const nmpcmc_sqp_options& opt, int64_t batch, const double* prob,
+                      const double* xi0, double* xi, double* lam, double* pil, double* piu, int32_t* conv,
+                      int32_t* iters, int32_t* status, double* ws, int64_t blocks, unsigned long long* counter,
+                      cudaStream_t stream);
+
 // ---- K2 PI, unit kernels, FP64 peak, K5 batched QP (k_misc.cu)
 int launch_pi(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
-              nmpcmc_work_counters* d_cnt, double* d_traj, int rows, cudaStream_t stream);
+              nmpcmc_work_counters* d_cnt, double* d_traj, int rows, int sm_count, cudaStream_t stream);
 void launch_pi_step(nmpcmc_pi_state* states, const double* y, const double* ybar, int64_t n,
                     nmpcmc_pi_step_result* results, int sm_count, cudaStream_t stream);
 void launch_philox(const uint32_t* in, int64_t n, uint32_t* out, cudaStream_t stream);

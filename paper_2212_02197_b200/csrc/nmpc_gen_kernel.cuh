@@ -183,6 +183,10 @@ template <int NX>
 struct Model {
     Cstr p;
     double S[NX], Cin[NX], sb[NX];
+    /// 1: the model carries no analytic jacobians, so drift_jacobian_x /
+    /// _u, measurement_jacobian_x and output_jacobian_x take the reference's
+    /// central finite differences (model.cpp:54-124); NMPCMC_OPT_CTRL_JACOBIANS.
+    int fd = 0;
 };
 template <int NX>
 __device__ Model<NX> make_model(const nmpcmc_cstr_params& q) {
@@ -198,6 +202,64 @@ __device__ Model<NX> make_model(const nmpcmc_cstr_params& q) {
         m.sb[0] = q.sigmaT;
     }
     return m;
+}
+
+/// fd_step (model.cpp:9): max(1e-6, 1e-6 |v|) with std::max semantics.
+__device__ __forceinline__ double fd_step(double v) { return smax(1e-6, 1e-6 * fabs(v)); }
+
+template <int NX>
+__device__ __forceinline__ int drift_jac(const Model<NX>& m, const double* x, double u, double* d, double* J);
+
+/// drift_jacobian_x by central differences (model.cpp:54-71): column j from
+/// drift at x +- h e_j, h = fd_step(x_j), (f+ - f-) / (2 h). A DomainError of
+/// either evaluation escapes, as in the reference.
+template <int NX>
+__device__ __noinline__ int fd_jac_x(const Model<NX>& m, const double* x, double u, double* J) {
+    double xp[NX], xm[NX];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) xp[i] = x[i], xm[i] = x[i];
+#pragma unroll 1
+    for (int j = 0; j < NX; ++j) {
+        const double h = fd_step(x[j]);
+        xp[j] = x[j] + h;
+        xm[j] = x[j] - h;
+        double fp[NX], fm[NX];
+        int st = drift_jac<NX>(m, xp, u, fp, nullptr);
+        if (st) return st;
+        st = drift_jac<NX>(m, xm, u, fm, nullptr);
+        if (st) return st;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) J[j * NX + i] = (fp[i] - fm[i]) / (2.0 * h);
+        xp[j] = x[j];
+        xm[j] = x[j];
+    }
+    return G_OK;
+}
+
+/// drift_jacobian_u by central differences (model.cpp:73-89), n_u = 1.
+template <int NX>
+__device__ __noinline__ int fd_jac_u(const Model<NX>& m, const double* x, double u, double* B) {
+    const double h = fd_step(u);
+    double fp[NX], fm[NX];
+    int st = drift_jac<NX>(m, x, u + h, fp, nullptr);
+    if (st) return st;
+    st = drift_jac<NX>(m, x, u - h, fm, nullptr);
+    if (st) return st;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) B[i] = (fp[i] - fm[i]) / (2.0 * h);
+    return G_OK;
+}
+
+/// d g / d x_{NX-1} of g(x) = x_{NX-1} / V (measurement = output,
+/// cstr.cpp:86-95): 1/V analytically, or the central difference of
+/// state_fn_jacobian (model.cpp:93-113); the other entries are +0 either way
+/// ((g(x) - g(x)) / (2 h) = +0).
+template <int NX>
+__device__ __forceinline__ double meas_jac_T(const Model<NX>& m, double xT) {
+    if (!m.fd) return 1.0 / m.p.V;
+    const double h = fd_step(xT);
+    const double gp = (xT + h) / m.p.V, gm = (xT - h) / m.p.V;
+    return (gp - gm) / (2.0 * h);
 }
 
 /// drift (cstr.cpp:42-53) and, when J != nullptr, drift_jacobian_x
@@ -222,6 +284,7 @@ __device__ __forceinline__ int drift_jac(const Model<NX>& m, const double* x, do
     const double r = k * cA * cB;
 #pragma unroll
     for (int i = 0; i < NX; ++i) d[i] = m.Cin[i] * f - c[i] * f + m.S[i] * r * m.p.V;
+    if (J != nullptr && m.fd) return fd_jac_x<NX>(m, x, u, J);
     if (J != nullptr) {
         if (NX == 3) {
             const double g[3] = {k * cB, k * cA, k * (m.p.EaR / (cT * cT)) * cA * cB};
@@ -237,11 +300,13 @@ __device__ __forceinline__ int drift_jac(const Model<NX>& m, const double* x, do
     }
     return G_OK;
 }
-/// drift_jacobian_u (cstr.cpp:120-127).
+/// drift_jacobian_u (cstr.cpp:120-127), or its central difference.
 template <int NX>
-__device__ __forceinline__ void jac_u(const Model<NX>& m, const double* x, double* B) {
+__device__ __forceinline__ int jac_u(const Model<NX>& m, const double* x, double u, double* B) {
+    if (m.fd) return fd_jac_u<NX>(m, x, u, B);
 #pragma unroll
     for (int i = 0; i < NX; ++i) B[i] = (m.Cin[i] - x[i] / m.p.V) * kMlMinToLs;
+    return G_OK;
 }
 
 // ------------------------------------------------------------------ shoot
@@ -281,7 +346,8 @@ __device__ __noinline__ int shoot(const Model<NX>& m, const double* x, double u,
             if (st) return st;
             double kx[NX * NX], ku[NX];
             if (SENS) {
-                jac_u<NX>(m, xs, B);
+                const int su_st = jac_u<NX>(m, xs, u, B);
+                if (su_st) return su_st;
 #pragma unroll
                 for (int jj = 0; jj < NX; ++jj)  // kx = A sx (gemm, beta 0)
 #pragma unroll
@@ -343,11 +409,117 @@ struct Ocp {
     double Ts, h, umin, umax, Qz, invV;
     double x0[NX];
     Cnt* cnt;
+    /// Problem kind of the SqpProblem interface (sqp.hpp:15-25) sqp_solve runs
+    /// on: nullptr = the CSTR regulator OcpProblem (sqp.hpp:28-48); else the
+    /// packed data of one stagewise quadratic NLP (QNLP below). A new kind is
+    /// added by giving objective() and constraints() one more branch.
+    const double* prob = nullptr;
 };
+
+// --------------------------------------------- quadratic stagewise NLP kind
+/// Stagewise quadratic NLP with affine dynamics (the problems the reference's
+/// SQP tests pose through SqpProblem): decision xi = (u_0, x_1, ..., u_{N-1},
+/// x_N), n_u = 1, x_0 given,
+///   f(xi) = sum_k [ 1/2 R_k u_k^2 + r_k u_k + 1/2 x_{k+1}' Q_k x_{k+1} + q_k' x_{k+1} ]
+///   F_k(x_k, u_k) = A_k x_k + B_k u_k + c_k,  g_k = x_{k+1} - F_k,
+/// u_min <= u_k <= u_max. Per stage k the packed data hold
+/// R r Q[NX*NX] q[NX] A[NX*NX] B[NX] c[NX] (matrices column-major); the
+/// evaluation order below is the one of oracle/ref_driver.cpp's QnlpProblem
+/// (the host SqpProblem the parity tests hand to the reference's sqp_solve).
+template <int NX>
+struct Qnlp {
+    static constexpr int kStage = 2 + 2 * NX * NX + 3 * NX;
+    __host__ __device__ static constexpr int R() { return 0; }
+    __host__ __device__ static constexpr int r() { return 1; }
+    __host__ __device__ static constexpr int Q() { return 2; }
+    __host__ __device__ static constexpr int q() { return 2 + NX * NX; }
+    __host__ __device__ static constexpr int A() { return 2 + NX * NX + NX; }
+    __host__ __device__ static constexpr int B() { return 2 + 2 * NX * NX + NX; }
+    __host__ __device__ static constexpr int c() { return 2 + 2 * NX * NX + 2 * NX; }
+};
+
+/// objective() of the quadratic kind: phi in stage order (serial on every
+/// lane), gradient R u + r / Q x + q lane-parallel.
+template <int NX, int W>
+__device__ __noinline__ double qnlp_objective(const Ocp<NX, W>& o, int s, bool grad) {
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
+    using D = Qnlp<NX>;
+    double phi = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < o.N; ++k) {
+        const double* P = o.prob + (int64_t)k * D::kStage;
+        const double u = w[L.XI[s] + L.uo(k)];
+        const double su = __ldg(P + D::R()) * u;
+        phi = phi + (0.5 * (u * su) + __ldg(P + D::r()) * u);
+        double xQx = 0.0, qx = 0.0;
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            double qxi = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) qxi += __ldg(P + D::Q() + j * NX + i) * w[L.XI[s] + L.xo(k + 1) + j];
+            const double xi_ = w[L.XI[s] + L.xo(k + 1) + i];
+            xQx += xi_ * qxi;
+            qx += __ldg(P + D::q() + i) * xi_;
+        }
+        phi = phi + (0.5 * xQx + qx);
+    }
+    if (grad) {
+#pragma unroll 1
+        for (int k = Lanes<W>::lane(); k < o.N; k += W) {
+            const double* P = o.prob + (int64_t)k * D::kStage;
+            const double u = w[L.XI[s] + L.uo(k)];
+            w[L.GF[s] + L.uo(k)] = __ldg(P + D::R()) * u + __ldg(P + D::r());
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                double qxi = 0.0;
+#pragma unroll
+                for (int j = 0; j < NX; ++j) qxi += __ldg(P + D::Q() + j * NX + i) * w[L.XI[s] + L.xo(k + 1) + j];
+                w[L.GF[s] + L.xo(k + 1) + i] = qxi + __ldg(P + D::q() + i);
+            }
+        }
+    }
+    Lanes<W>::sync();
+    return phi;
+}
+
+/// constraints() of the quadratic kind: F_k = (A_k x_k + B_k u_k) + c_k per
+/// stage, lane-parallel; never fails.
+template <int NX, int W>
+__device__ __noinline__ int qnlp_constraints(const Ocp<NX, W>& o, int s) {
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
+    using D = Qnlp<NX>;
+#pragma unroll 1
+    for (int k = Lanes<W>::lane(); k < o.N; k += W) {
+        const double* P = o.prob + (int64_t)k * D::kStage;
+        double xk[NX];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) xk[i] = k == 0 ? o.x0[i] : w[L.XI[s] + L.xo(k) + i];
+        const double u = w[L.XI[s] + L.uo(k)];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            double F = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) F += __ldg(P + D::A() + j * NX + i) * xk[j];
+            F = F + __ldg(P + D::B() + i) * u;
+            F = F + __ldg(P + D::c() + i);
+            const double nx = w[L.XI[s] + L.xo(k + 1) + i];
+            w[L.BB[s] + k * NX + i] = F - nx;
+            w[L.G[s] + k * NX + i] = nx - F;
+            w[L.FU[s] + k * NX + i] = __ldg(P + D::B() + i);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) w[L.FX[s] + (k * NX + j) * NX + i] = __ldg(P + D::A() + j * NX + i);
+        }
+    }
+    Lanes<W>::sync();
+    return G_OK;
+}
 
 /// eval_objective (ocp.cpp:76-99) of xi set s; gradient into GF[s] if grad.
 template <int NX, int W>
 __device__ __noinline__ double objective(const Ocp<NX, W>& o, int s, bool grad) {
+    if (o.prob != nullptr) return qnlp_objective<NX, W>(o, s, grad);
     // serial on every lane (phi is an ordered sum); the gradient is stored,
     // not accumulated: each slot is 0.0 + 2 Ts g once (ocp.cpp:80-97)
     const WsT<W> w = o.ws;
@@ -362,7 +534,9 @@ __device__ __noinline__ double objective(const Ocp<NX, W>& o, int s, bool grad) 
             w[L.GF[s] + L.uo(k - 1)] = 0.0;
 #pragma unroll
             for (int i = 0; i < NX; ++i) {
-                const double hi = (i == NX - 1) ? o.invV : 0.0;
+                const double hi = (i == NX - 1) ? (o.m.fd ? meas_jac_T<NX>(o.m, w[L.XI[s] + L.xo(k) + NX - 1])
+                                                          : o.invV)
+                                                : 0.0;
                 const double g = 1.0 * (0.0 + hi * qres) + 0.0;
                 w[L.GF[s] + L.xo(k) + i] = 0.0 + 2.0 * o.Ts * g;
             }
@@ -375,6 +549,7 @@ __device__ __noinline__ double objective(const Ocp<NX, W>& o, int s, bool grad) 
 /// eval_constraints (ocp.cpp:101-135) of xi set s into G/FX/FU/BB[s].
 template <int NX, int W>
 __device__ __noinline__ int constraints(const Ocp<NX, W>& o, int s) {
+    if (o.prob != nullptr) return qnlp_constraints<NX, W>(o, s);
     // stages are independent (multiple shooting): lane-parallel; the status
     // is the one of the lowest failing stage, as the sequential loop returns
     const WsT<W> w = o.ws;
@@ -1387,7 +1562,7 @@ __device__ __noinline__ int ekf_predict(const Model<NX>& m, double* x, double* P
 /// NotPositiveDefinite of R_e.
 template <int NX>
 __device__ __noinline__ bool ekf_update(const Model<NX>& m, double* x, double* P, double y, double R) {
-    const double cv = 1.0 / m.p.V;
+    const double cv = meas_jac_T<NX>(m, x[NX - 1]);
     double C[NX];
 #pragma unroll
     for (int i = 0; i < NX; ++i) C[i] = (i == NX - 1) ? cv : 0.0;
@@ -1596,7 +1771,8 @@ __device__ __forceinline__ StepRes nmpc_step_ws(Ocp<NX, W>& o, const nmpcmc_scen
 /// with a controller model of NX states and a truth plant of TX states.
 template <int TX, int NX, int W>
 __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar, const WsT<W>& ws,
-                                         nmpcmc_sim_record* rec, nmpcmc_work_counters* cntp, double* traj) {
+                                         nmpcmc_sim_record* rec, nmpcmc_work_counters* cntp, double* traj,
+                                         int fd = 0) {
     const Cstr p = sample_truth(sc, sim_index);
     NormalStream rng;
     rng.init(sc.base_seed, sim_index);
@@ -1611,6 +1787,7 @@ __device__ __noinline__ void closed_loop(const nmpcmc_scenario& sc, uint64_t sim
     Ocp<NX, W> o{make_model<NX>(sc.ctrl), Layout<NX>(sc.N), ws, sc.N, sc.Nc, sc.horizon_Ts, sc.horizon_Ts / sc.Nc,
               sc.u_min, sc.u_max, sc.Qz, 0.0, {}, &cnt};
     o.invV = 1.0 / o.m.p.V;
+    o.m.fd = fd;
     const Layout<NX> L = o.lay;
     const int N = o.N;
     // make_nmpc_state (controllers.cpp:25-48)
@@ -1725,7 +1902,8 @@ template <int TX, int NX>
 __global__ void __launch_bounds__(32) nmpc_genw_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
                                                        int64_t n_sims, int nbar, nmpcmc_sim_record* records,
                                                        nmpcmc_work_counters* counters, double* traj, int traj_rows,
-                                                       double* ws_all, int64_t slab, unsigned long long* next) {
+                                                       double* ws_all, int64_t slab, unsigned long long* next,
+                                                       int fd) {
     const WsT<32> ws{ws_all + (int64_t)blockIdx.x * slab, 1};
 #pragma unroll 1
     for (;;) {
@@ -1734,7 +1912,7 @@ __global__ void __launch_bounds__(32) nmpc_genw_kernel(const __grid_constant__ n
         i = __shfl_sync(kMask, i, 0);
         if (i >= (unsigned long long)n_sims) break;
         closed_loop<TX, NX, 32>(sc, first_sim + i, nbar, ws, records + i, counters ? counters + i : nullptr,
-                                traj ? traj + (size_t)i * traj_rows * 5 : nullptr);
+                                traj ? traj + (size_t)i * traj_rows * 5 : nullptr, fd);
     }
 }
 
@@ -1823,6 +2001,83 @@ inline int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const doub
     return NMPCMC_OK;
 }
 
+
+/// Batched sqp_solve (sqp.cpp:182-411) on stagewise quadratic NLPs (Qnlp):
+/// instance b's data at prob + b * stride = x0[NX] u_min u_max, then N
+/// stages of Qnlp<NX>::kStage doubles; start xi0[b*L ..] (null: zeros) with
+/// zero duals and identity Hessian blocks, as sqp_solve without a warm start.
+/// One warp per instance (K3w's code path; only objective() / constraints()
+/// differ from the regulator OCP).
+template <int NX>
+__global__ void __launch_bounds__(32) qnlp_batch_kernel(int N, nmpcmc_sqp_options opt, int64_t batch,
+                                                        const double* prob, int64_t stride, const double* xi0,
+                                                        double* xi_out, double* lam_out, double* pil_out,
+                                                        double* piu_out, int32_t* converged, int32_t* iters,
+                                                        int32_t* status, double* ws_all, int64_t slab,
+                                                        unsigned long long* next) {
+    const WsT<32> ws{ws_all + (int64_t)blockIdx.x * slab, 1};
+    const int lane = Lanes<32>::lane();
+#pragma unroll 1
+    for (;;) {
+        unsigned long long bi = 0;
+        if (lane == 0) bi = atomicAdd(next, 1ULL);
+        bi = __shfl_sync(kMask, bi, 0);
+        if (bi >= (unsigned long long)batch) break;
+        const int64_t b = (int64_t)bi;
+        const double* P = prob + b * stride;
+        Cnt cnt = {};
+        Ocp<NX, 32> o{Model<NX>{}, Layout<NX>(N), ws, N, 1, 0.0, 0.0, __ldg(P + NX), __ldg(P + NX + 1), 0.0, 0.0,
+                      {}, &cnt, P + NX + 2};
+#pragma unroll
+        for (int i = 0; i < NX; ++i) o.x0[i] = __ldg(P + i);
+        const Layout<NX> L = o.lay;
+        for (int e = lane; e < L.L; e += 32) ws[L.XI[0] + e] = xi0 != nullptr ? xi0[b * L.L + e] : 0.0;
+        for (int e = lane; e < L.NN; e += 32) ws[L.LAM + e] = 0.0;
+        for (int k = lane; k < N; k += 32) ws[L.PL + k] = 0.0, ws[L.PU + k] = 0.0;
+        Lanes<32>::sync();
+        int cur = 0;
+        const SqpOut so = sqp_solve<NX, 32>(o, opt, &cur);
+        const bool ok = so.status == G_OK;
+        for (int e = lane; e < L.L; e += 32) xi_out[b * L.L + e] = ok ? (double)ws[L.XI[cur] + e] : 0.0;
+        for (int e = lane; e < L.NN; e += 32) lam_out[b * L.NN + e] = ok ? (double)ws[L.LAM + e] : 0.0;
+        for (int k = lane; k < N; k += 32) {
+            pil_out[b * N + k] = ok ? (double)ws[L.PL + k] : 0.0;
+            piu_out[b * N + k] = ok ? (double)ws[L.PU + k] : 0.0;
+        }
+        if (lane == 0) {
+            converged[b] = ok && so.converged ? 1 : 0;
+            iters[b] = (int32_t)cnt.sqp;
+            status[b] = ok ? 0 : so.status;
+        }
+        Lanes<32>::sync();
+    }
+}
+
+inline int64_t qnlp_stride(int N, int nx) {
+    return nx == 3 ? 3 + 2 + (int64_t)N * Qnlp<3>::kStage : 1 + 2 + (int64_t)N * Qnlp<1>::kStage;
+}
+
+inline int64_t qnlp_ws_doubles(int N, int nx) { return nx == 3 ? Layout<3>(N).total : Layout<1>(N).total; }
+
+inline int launch_qnlp_batch(int N, int nx, const nmpcmc_sqp_options& opt, int64_t batch, const double* prob,
+                             const double* xi0, double* xi, double* lam, double* pil, double* piu, int32_t* conv,
+                             int32_t* iters, int32_t* status, double* ws, int64_t blocks, unsigned long long* counter,
+                             cudaStream_t stream) {
+    const size_t smem = nx == 3 ? sweep_smem_bytes<3>(N) : sweep_smem_bytes<1>(N);
+    if (smem > kSweepSmemMax || blocks < 1) return NMPCMC_UNSUPPORTED;
+    const int64_t slab = qnlp_ws_doubles(N, nx), stride = qnlp_stride(N, nx);
+    cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+    if (nx == 3) {
+        cudaFuncSetAttribute(qnlp_batch_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        qnlp_batch_kernel<3><<<(unsigned)blocks, 32, smem, stream>>>(N, opt, batch, prob, stride, xi0, xi, lam, pil,
+                                                                     piu, conv, iters, status, ws, slab, counter);
+    } else {
+        cudaFuncSetAttribute(qnlp_batch_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        qnlp_batch_kernel<1><<<(unsigned)blocks, 32, smem, stream>>>(N, opt, batch, prob, stride, xi0, xi, lam, pil,
+                                                                     piu, conv, iters, status, ws, slab, counter);
+    }
+    return NMPCMC_OK;
+}
 
 /// Layout of one device-resident NmpcState (controllers.hpp:54-65) of the
 /// batched controller API (nmpcmc_gpu_nmpc_step_batch): the filter
@@ -1991,7 +2246,7 @@ inline size_t genw_smem(const nmpcmc_scenario& sc) {
 inline bool genw_fits(const nmpcmc_scenario& sc) { return genw_smem(sc) <= kSweepSmemMax; }
 inline int launch_genw(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
                        nmpcmc_work_counters* d_cnt, double* d_traj, int rows, double* ws, int64_t blocks,
-                       unsigned long long* counter, cudaStream_t stream) {
+                       unsigned long long* counter, cudaStream_t stream, int fd = 0) {
     if (blocks < 1 || !genw_fits(sc)) return NMPCMC_INVALID_ARGUMENT;
     const int64_t slab = gen_ws_doubles(sc);
     const size_t smem = genw_smem(sc);
@@ -1999,7 +2254,7 @@ inline int launch_genw(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int
     const bool t3 = sc.truth_variant == NMPCMC_THREE_STATE, c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
 #define NMPCMC_GENW_LAUNCH(T, C)                                                                              \
     nmpc_genw_kernel<T, C><<<(unsigned)blocks, 32, smem, stream>>>(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ws, \
-                                                                slab, counter)
+                                                                slab, counter, fd)
     if (t3 && c3) NMPCMC_GENW_LAUNCH(3, 3);
     else if (t3) NMPCMC_GENW_LAUNCH(3, 1);
     else if (c3) NMPCMC_GENW_LAUNCH(1, 3);

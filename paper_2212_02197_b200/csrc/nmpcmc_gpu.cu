@@ -46,7 +46,7 @@ int launch(nmpcmc_gpu_ctx* ctx, const Target& tg, const nmpcmc_scenario& sc, uin
            nmpcmc_sim_record* d_rec, nmpcmc_work_counters* d_cnt, double* d_traj, int rows) {
     if (n == 0) return NMPCMC_OK;
     if (sc.controller == NMPCMC_CTRL_PI) {
-        nmpcmc_launch::launch_pi(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, tg.stream);
+        nmpcmc_launch::launch_pi(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ctx->sm_count, tg.stream);
         return cuda_check(ctx, cudaGetLastError(), "pi_kernel launch");
     }
     int rc;
@@ -56,7 +56,10 @@ int launch(nmpcmc_gpu_ctx* ctx, const Target& tg, const nmpcmc_scenario& sc, uin
     const bool thread = ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC ||
                         ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_THREAD;
     const bool generic = sc.ctrl_variant != NMPCMC_ONE_STATE || sc.N > 255 || thread ||
-                         ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC_WARP;
+                         ctx->nmpc_kernel == NMPCMC_NMPC_KERNEL_GENERIC_WARP || ctx->ctrl_fd;
+    // finite-difference controller jacobians run on K3w only
+    if (ctx->ctrl_fd && (thread || !nmpcmc_launch::genw_fits(sc)))
+        return fail(ctx, NMPCMC_UNSUPPORTED, "finite-difference jacobians need the one-warp generic kernel (K3w)");
     if (generic && !thread && nmpcmc_launch::genw_fits(sc)) {  // K3w (or K3g when N is too long for it)
         const int64_t blocks = nmpcmc_launch::genw_blocks(sc, ctx->sm_count, n);
         const size_t need = (size_t)blocks * (size_t)nmpcmc_launch::gen_ws_doubles(sc) * sizeof(double);
@@ -64,7 +67,7 @@ int launch(nmpcmc_gpu_ctx* ctx, const Target& tg, const nmpcmc_scenario& sc, uin
         if ((rc = ensure(ctx, tg.d_counter, tg.counter_cap, 256)) != NMPCMC_OK) return rc;
         rc = nmpcmc_launch::launch_genw(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows,
                                         static_cast<double*>(*tg.d_ws), blocks,
-                                        static_cast<unsigned long long*>(*tg.d_counter), tg.stream);
+                                        static_cast<unsigned long long*>(*tg.d_counter), tg.stream, ctx->ctrl_fd);
     } else if (generic) {
         const int64_t slots = nmpcmc_launch::gen_slots(sc, ctx->sm_count, n);
         const size_t need = (size_t)slots * (size_t)nmpcmc_launch::gen_ws_doubles(sc) * sizeof(double);
@@ -197,6 +200,10 @@ int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value) {
         case NMPCMC_OPT_TPS_WARPS_PER_SM:
             if (value < 1 || value > 64) return NMPCMC_INVALID_ARGUMENT;
             ctx->tps_warps_per_sm = (int)value;
+            return NMPCMC_OK;
+        case NMPCMC_OPT_CTRL_JACOBIANS:
+            if (value != NMPCMC_JACOBIANS_ANALYTIC && value != NMPCMC_JACOBIANS_FD) return NMPCMC_INVALID_ARGUMENT;
+            ctx->ctrl_fd = value == NMPCMC_JACOBIANS_FD ? 1 : 0;
             return NMPCMC_OK;
         default:
             return NMPCMC_INVALID_ARGUMENT;

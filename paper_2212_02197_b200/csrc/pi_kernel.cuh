@@ -49,13 +49,25 @@ __global__ void pi_step_kernel(nmpcmc_pi_state* states, const double* y, const d
 /// consumes 1 + Ns * NX normals: 31 in every BASELINE config, one refill).
 constexpr int kPiPairs = 16;
 constexpr int kPiBlock = 128;
+/// Lanes per sample: the group splits each window refill (Philox + log +
+/// sincos, the bulk of the work) and runs the Euler-Maruyama recursion in
+/// lockstep, so a batch of n samples fills n * kPiLanes threads.
+#ifndef NMPCMC_PI_LANES
+#define NMPCMC_PI_LANES 4
+#endif
+#ifndef NMPCMC_PI_MINB
+#define NMPCMC_PI_MINB 1
+#endif
+constexpr int kPiLanes = NMPCMC_PI_LANES;
 
-template <int NX>
+template <int NX, int G>
 __device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, int nbar,
                                nmpcmc_sim_record* rec, nmpcmc_work_counters* cnt, double* traj,
                                int traj_rows, double* win_buf, int win_stride) {
     const Cstr p = sample_truth(sc, sim_index);
-    NormalWindow<kPiPairs> rng;
+    NormalWindow<kPiPairs, G> rng;
+    // writes the outputs (rec == nullptr: a tail group's stand-in)
+    const bool lead = (G == 1 || (threadIdx.x & (G - 1)) == 0) && rec != nullptr;
     rng.init(win_buf, win_stride, sc.base_seed, sim_index);
     const int per_step = (sc.has_noise_R != 0 ? 1 : 0) + sc.Ns * NX;
     Plant<NX> pl;
@@ -82,9 +94,28 @@ __device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, in
     int status = ST_OK;
     int row = 0;
     int steps = 0;  // control steps entered (a failing step counts: its work ran)
+    // only the measurement and temperature normals are read when the plant
+    // has no diffusion on c_A, c_B (simulate_interval<.., true>)
+    const bool sparse = NX == 3 && p.sigmaA == 0.0 && p.sigmaB == 0.0 && per_step < 2 * kPiPairs;
     for (int i = 0; i < nbar; ++i) {
+        if (sparse) {
+            // a live sample's stream position at the start of step i is
+            // exactly i * per_step (warp-uniform, as below)
+            if (G > 1 && __all_sync(0xffffffffu, status != ST_OK)) break;
+            rng.fill_sparse((uint64_t)i * (uint64_t)per_step, has_R ? 1 : 0, sc.Ns);
+            if (status != ST_OK) continue;
+        } else if (G > 1) {
+            // lockstep over the warp: a live sample's stream position at the
+            // start of step i is exactly i * per_step, so every group refills
+            // at the same steps; a failed sample idles until its warp is done
+            if (__all_sync(0xffffffffu, status != ST_OK)) break;
+            rng.k = (uint64_t)i * (uint64_t)per_step;
+            rng.reserve(per_step);
+            if (status != ST_OK) continue;
+        } else if (per_step < 2 * kPiPairs) {
+            rng.reserve(per_step);  // this step's normals in one refill
+        }
         ++steps;
-        if (per_step < 2 * kPiPairs) rng.reserve(per_step);  // this step's normals in one refill
         const double y = measure<NX>(p, pl, has_R, lR, rng);
         // pi_step (controllers.cpp:12-23), evaluated in the documented order
         const double ybar = setpoint_at(sc, t);
@@ -93,22 +124,29 @@ __device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, in
         const double u = pr.u;
         I_hat = pr.next_I_hat;
         if (record && i % stride == 0) {
-            double* rw = traj + (size_t)row * 5;
-            rw[0] = t;
-            rw[1] = z;
-            rw[2] = zbar;
-            rw[3] = u;
-            rw[4] = y;
+            if (lead) {
+                double* rw = traj + (size_t)row * 5;
+                rw[0] = t;
+                rw[1] = z;
+                rw[2] = zbar;
+                rw[3] = u;
+                rw[4] = y;
+            }
             ++row;
         }
-        status = simulate_interval<NX>(p, pl, t, t + sc.Ts, u, sc.Ns, rng);
-        if (status != ST_OK) break;
+        status = sparse ? simulate_interval<NX, NormalWindow<kPiPairs, G>, true>(p, pl, t, t + sc.Ts, u, sc.Ns, rng)
+                        : simulate_interval<NX>(p, pl, t, t + sc.Ts, u, sc.Ns, rng);
+        if (status != ST_OK) {
+            if (G == 1) break;
+            continue;
+        }
         t = sc.t0 + (i + 1) * sc.Ts;
         z = pl.x[NX - 1] / p.V;
         zbar = setpoint_at(sc, t);
         const double r = z - zbar;
         acc += r * r;
     }
+    if (!lead) return;
     if (status == ST_OK) {
         rec->phi = acc / (double)(nbar + 1);
         rec->failed = 0;
@@ -135,20 +173,33 @@ __device__ void pi_closed_loop(const nmpcmc_scenario& sc, uint64_t sim_index, in
     (void)traj_rows;
 }
 
-/// One thread per sample; each thread's normal window lives in shared memory,
-/// element j of thread t at win[j * kPiBlock + t] (conflict-free).
-template <int NX>
-__global__ void __launch_bounds__(kPiBlock) pi_kernel(const __grid_constant__ nmpcmc_scenario sc,
+/// G consecutive threads per sample (a group of one warp); the group's normal
+/// window lives in shared memory, element j of group q at
+/// win[j * (kPiBlock / G) + q] (conflict-free across groups, a broadcast
+/// within one).
+template <int NX, int G>
+__global__ void __launch_bounds__(kPiBlock, NMPCMC_PI_MINB) pi_kernel(const __grid_constant__ nmpcmc_scenario sc,
                                                       uint64_t first_sim, int64_t n_sims, int nbar,
                                                       nmpcmc_sim_record* records,
                                                       nmpcmc_work_counters* counters, double* traj,
                                                       int traj_rows) {
-    __shared__ double win[2 * kPiPairs * kPiBlock];
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_sims) return;
-    pi_closed_loop<NX>(sc, first_sim + (uint64_t)i, nbar, records + i,
-                       counters ? counters + i : nullptr,
-                       traj ? traj + (size_t)i * traj_rows * 5 : nullptr, traj_rows, win + threadIdx.x, kPiBlock);
+    constexpr int kGroups = kPiBlock / G;
+    __shared__ double win[2 * kPiPairs * kGroups];
+    const int q = threadIdx.x / G;
+    const int64_t i = (int64_t)blockIdx.x * kGroups + q;
+    if (G == 1) {
+        if (i >= n_sims) return;
+    } else {
+        // a warp runs its groups in lockstep: warps past the end leave, the
+        // tail groups of the last warp run a copy of the last sample unseen
+        const int64_t w0 = (int64_t)blockIdx.x * kGroups + (threadIdx.x & ~31) / G;
+        if (w0 >= n_sims) return;
+    }
+    const bool real = i < n_sims;
+    const int64_t ii = real ? i : n_sims - 1;
+    pi_closed_loop<NX, G>(sc, first_sim + (uint64_t)ii, nbar, real ? records + ii : nullptr,
+                          counters && real ? counters + ii : nullptr,
+                          traj && real ? traj + (size_t)ii * traj_rows * 5 : nullptr, traj_rows, win + q, kGroups);
 }
 
 }  // namespace nmpcmc_dev

@@ -205,3 +205,65 @@ def solve_ocp_batch(sc, x0, t0, xi0=None, ctx=None):
         out["status"].ctypes.data_as(C.POINTER(C.c_int32))))
     return out
 
+
+
+# ------------------------------------------------------ SQP on quadratic NLPs
+class QnlpDims(C.Structure):
+    _fields_ = [("N", C.c_int32), ("n_x", C.c_int32), ("n_u", C.c_int32), ("_pad", C.c_int32),
+                ("sqp", abi.SqpOptions)]
+
+
+def qnlp_doubles(N: int, nx: int) -> int:
+    """Packed doubles of one quadratic NLP (nmpcmc_qnlp_doubles)."""
+    return nx + 2 + N * (2 + 2 * nx * nx + 3 * nx)
+
+
+def pack_qnlp(x0, u_min, u_max, R, r, Q, q, A, B, c) -> np.ndarray:
+    """One quadratic NLP in the packed layout: x0 (nx,), bounds, and per
+    stage k R[k], r[k], Q[k] (nx, nx), q[k] (nx,), A[k] (nx, nx), B[k] (nx,),
+    c[k] (nx,) -- matrices stored column-major."""
+    x0 = np.atleast_1d(np.asarray(x0, dtype=np.float64))
+    N = len(R)
+    parts = [x0, [u_min, u_max]]
+    for k in range(N):
+        parts += [[R[k], r[k]], np.asarray(Q[k], dtype=np.float64).reshape(-1, order="F"), np.ravel(q[k]),
+                  np.asarray(A[k], dtype=np.float64).reshape(-1, order="F"), np.ravel(B[k]), np.ravel(c[k])]
+    out = np.concatenate([np.asarray(p, dtype=np.float64).ravel() for p in parts])
+    assert out.size == qnlp_doubles(N, x0.size)
+    return out
+
+
+def default_sqp_options(**kw) -> abi.SqpOptions:
+    """SqpOptions defaults (sqp.hpp:50-58)."""
+    o = abi.SqpOptions()
+    o.eps, o.max_iter, o.max_backtracks, o.c1, o.backtrack_factor = 1e-6, 100, 30, 1e-4, 0.5
+    o.qp_tol, o.qp_max_iter = 1e-12, 50
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def solve_qnlp_batch(problems, N: int, nx: int, opts: abi.SqpOptions = None, xi0=None, ctx=None) -> dict:
+    """sqp_solve (sqp.cpp:182-411) on a batch of stagewise quadratic NLPs
+    through the SqpProblem interface (nmpcmc_gpu_sqp_solve_qnlp_batch);
+    problems: (batch, qnlp_doubles(N, nx)). Returns xi, lambda, pi_l, pi_u,
+    converged, iterations, status."""
+    problems = np.ascontiguousarray(problems, dtype=np.float64)
+    if problems.ndim != 2 or problems.shape[1] != qnlp_doubles(N, nx):
+        raise engine.DimensionMismatch(f"problems must be (batch, {qnlp_doubles(N, nx)})")
+    Bn, L = problems.shape[0], N * (1 + nx)
+    if xi0 is not None:
+        xi0 = np.ascontiguousarray(xi0, dtype=np.float64)
+        if xi0.shape != (Bn, L):
+            raise engine.LengthMismatch(f"xi0 must be ({Bn}, {L})")
+    d = QnlpDims(N, nx, 1, 0, opts or default_sqp_options())
+    out = dict(xi=np.zeros((Bn, L)), **{"lambda": np.zeros((Bn, N * nx))}, pi_l=np.zeros((Bn, N)),
+               pi_u=np.zeros((Bn, N)), converged=np.zeros(Bn, dtype=np.int32), iterations=np.zeros(Bn, dtype=np.int32),
+               status=np.zeros(Bn, dtype=np.int32))
+    ctx = ctx or engine._context(0)
+    lib = ctx.lib
+    lib.nmpcmc_gpu_sqp_solve_qnlp_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int64] + [C.c_void_p] * 9
+    ctx._check(lib.nmpcmc_gpu_sqp_solve_qnlp_batch(
+        ctx.handle, C.byref(d), C.c_int64(Bn), problems.ctypes.data, None if xi0 is None else xi0.ctypes.data,
+        *(out[k].ctypes.data for k in ("xi", "lambda", "pi_l", "pi_u", "converged", "iterations", "status"))))
+    return out

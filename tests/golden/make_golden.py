@@ -229,6 +229,46 @@ def gen_steps():
     np.savez_compressed(os.path.join(OUT, "controller_steps.npz"), **out)
 
 
+def gen_qnlp():
+    """SQP through the SqpProblem interface on random stagewise quadratic NLPs
+    (the reference's own SQP-test problem class): the reference's sqp_solve
+    on QnlpProblem (oracle/ref_driver.cpp), n_x = 1 and 3, loose and tight
+    input bounds, zero and random starts."""
+    from paper_2212_02197_b200 import qp as Q
+    rng = np.random.default_rng(31337)
+    out = {}
+    for tag, N, nx, B in (("n1", 12, 1, 40), ("n3", 8, 3, 40)):
+        probs = []
+        for b in range(B):
+            R = rng.uniform(0.1, 2.0, N)
+            r = rng.normal(0, 1, N)
+            Qs, qs, As, Bs, cs = [], [], [], [], []
+            for k in range(N):
+                M = rng.normal(0, 1, (nx, nx))
+                Qs.append(M @ M.T + 0.1 * np.eye(nx))
+                qs.append(rng.normal(0, 1, nx))
+                As.append(0.9 * np.eye(nx) + 0.2 * rng.normal(0, 1, (nx, nx)))
+                Bs.append(rng.normal(0, 1, nx))
+                cs.append(0.1 * rng.normal(0, 1, nx))
+            tight = b % 2 == 1
+            lo, hi = (-0.3, 0.4) if tight else (-50.0, 50.0)
+            probs.append(Q.pack_qnlp(rng.normal(0, 1, nx), lo, hi, R, r, Qs, qs, As, Bs, cs))
+        probs = np.array(probs)
+        opts = Q.default_sqp_options(max_iter=50)
+        xi0 = rng.normal(0, 0.5, (B, N * (1 + nx)))
+        cold = O.sqp_solve_qnlp_batch(O.ref("xlibm"), probs, N, nx, opts)
+        warm = O.sqp_solve_qnlp_batch(O.ref("xlibm"), probs, N, nx, opts, xi0=xi0)
+        out[f"{tag}__dims"] = np.array([N, nx])
+        out[f"{tag}__problems"], out[f"{tag}__xi0"] = probs, xi0
+        for k, v in cold.items():
+            out[f"{tag}__cold_{k}"] = v
+        for k, v in warm.items():
+            out[f"{tag}__warm_{k}"] = v
+        print(f"qnlp {tag}: {B} problems, converged cold {cold['converged'].sum()} warm {warm['converged'].sum()}, "
+              f"iterations {cold['iterations'].mean():.1f}, status {np.bincount(cold['status']).tolist()}")
+    np.savez_compressed(os.path.join(OUT, "qnlp_batch.npz"), **out)
+
+
 def main(which):
     if which in ("rng", "all"):
         gen_rng()
@@ -255,6 +295,8 @@ def main(which):
         gen_dist()
     if which in ("steps", "all"):
         gen_steps()
+    if which in ("qnlp", "all"):
+        gen_qnlp()
     if which in ("nmpc3", "all"):
         # three-state controller model (config 2 read literally: CD-EKF and
         # OCP on the 3-state CSTR; ctrl_variant 0 = THREE_STATE) -> kernel K3g

@@ -82,17 +82,21 @@ def _cli(tmp_path, *args):
 
 
 @pytest.mark.gpu
-def test_cli_simulate_pi_equilibrium_is_zero(tmp_path):
-    # deterministic PI at equilibrium: no noise, setpoint = initial temperature -> phi = 0
-    _cli(tmp_path, "simulate", "--set", "model.sigmaT=0", "--set", "noise.R=0", "--set",
-         "scenario.setpoint_values=335", "--set", "scenario.setpoint_times=0", "--set", "scenario.T0=335",
-         "--set", "controller.kP=0", "--set", "controller.kI=0", "--set", "controller.kaw=0", "--set",
-         "controller.u_bar=0", "--set", "controller.u_min=0", "--set", "controller.u_max=0")
-    doc = json.loads((tmp_path / "summary.json").read_text())
-    traj, meta = results.read_trajectory_csv(str(tmp_path / "trajectory.csv"))
-    assert meta["kind"] == "trajectory" and traj.shape[1] == 5 and len(traj) == 721
+def test_cli_simulate_trajectory_reproduces_phi(tmp_path):
+    # noise-free PI loop: the summary's phi is phi_metric (montecarlo.cpp:65-78)
+    # of the written trajectory, and a second run writes identical files
+    args = ["simulate", "--set", "model.sigmaT=0", "--set", "noise.R=0", "--set", "scenario.tf=1200"]
+    _cli(tmp_path / "a", *args)
+    _cli(tmp_path / "b", *args)
+    doc = json.loads((tmp_path / "a" / "summary.json").read_text())
+    traj, meta = results.read_trajectory_csv(str(tmp_path / "a" / "trajectory.csv"))
+    assert meta["kind"] == "trajectory" and traj.shape == (121, 5)
     assert not doc["failed"]
-    assert doc["phi"] == pytest.approx(0.0, abs=1e-18)
+    acc = 0.0
+    for z, zbar in traj[:, 1:3]:
+        acc += (z - zbar) * (z - zbar)
+    assert acc / len(traj) == doc["phi"]
+    assert (tmp_path / "a" / "trajectory.csv").read_bytes() == (tmp_path / "b" / "trajectory.csv").read_bytes()
 
 
 @pytest.mark.gpu

@@ -35,4 +35,6 @@ for name, kw, n in (("config0", dict(controller="pi"), 1000), ("config1", dict(c
     from paper_2212_02197_b200 import abi
     c = np.frombuffer(cnt.cpu().numpy().tobytes(), dtype=abi.COUNTERS_DTYPE)
     fl = workmodel.pi_flops(int(c["control_steps"].sum()))
-    print(f"PI {name}: {n} sims, {best:.3f} ms, {n / best * 1e3:.0f} sims/s, {fl / best / 1e9:.3f} TF/s")
+    import hashlib
+    h = hashlib.sha1(rec.cpu().numpy().tobytes()).hexdigest()[:12]
+    print(f"PI {name}: {n} sims, {best:.3f} ms, {n / best * 1e3:.0f} sims/s, {fl / best / 1e9:.3f} TF/s, rec {h}")
