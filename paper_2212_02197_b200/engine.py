@@ -215,6 +215,13 @@ class Context:
         K3w, or K3g when 'generic' is selected."""
         self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 1, self.KERNELS[kind]))
 
+    def set_ctrl_jacobians(self, kind: str):
+        """'analytic' (default, make_cstr_model's closed forms) or 'fd': the
+        controller model's jacobians by the reference's central differences
+        (model.cpp:54-124), as for a Model without analytic jacobians; runs
+        on K3w."""
+        self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 4, {"analytic": 0, "fd": 1}[kind]))
+
     def set_stream(self, stream_ptr: int):
         self._check(self.lib.nmpcmc_gpu_set_stream(self.handle, C.c_void_p(stream_ptr)))
 

@@ -269,6 +269,20 @@ def gen_qnlp():
     np.savez_compressed(os.path.join(OUT, "qnlp_batch.npz"), **out)
 
 
+def gen_fd():
+    """Finite-difference controller jacobians (model.cpp:54-124): the
+    reference with the controller model's analytic jacobians removed
+    (nmpcmc_ref_set_ctrl_fd), one- and three-state controller models."""
+    for libm in ("xlibm", "glibc"):
+        O.ref(libm).nmpcmc_ref_set_ctrl_fd(1)
+    try:
+        gen_case("nmpc_fd_n30", dict(controller="nmpc", N=30, n_steps=60, perturb=True), 16, 1)
+        gen_case("nmpc3_fd_n20", dict(controller="nmpc", N=20, n_steps=30, ctrl_variant=0), 8, 0)
+    finally:
+        for libm in ("xlibm", "glibc"):
+            O.ref(libm).nmpcmc_ref_set_ctrl_fd(0)
+
+
 def main(which):
     if which in ("rng", "all"):
         gen_rng()
@@ -297,6 +311,8 @@ def main(which):
         gen_steps()
     if which in ("qnlp", "all"):
         gen_qnlp()
+    if which in ("fd", "all"):
+        gen_fd()
     if which in ("nmpc3", "all"):
         # three-state controller model (config 2 read literally: CD-EKF and
         # OCP on the 3-state CSTR; ctrl_variant 0 = THREE_STATE) -> kernel K3g

@@ -95,3 +95,25 @@ def test_k3w_matches_k3g_three_state_at_scale(gpu_ctx):
     assert_records_equal(a, b)
     for f in ("control_steps", "ipm_stage_iters", "sqp_iterations", "qp_solves", "ls_evals"):
         np.testing.assert_array_equal(ca[f], cb[f])
+
+
+# ---------------------------------------------------------------- FD jacobians
+@pytest.mark.parametrize("name", ["nmpc_fd_n30", "nmpc3_fd_n20"])
+def test_fd_jacobians_bitwise_vs_reference_without_analytic_jacobians(name):
+    """NMPCMC_OPT_CTRL_JACOBIANS = FD against the reference run on a
+    controller Model without analytic jacobians (model.cpp:54-124 fallbacks)."""
+    from paper_2212_02197_b200 import engine
+    d, kw, sc = load_golden(name)
+    ctx = engine.Context(0)
+    ctx.set_ctrl_jacobians("fd")
+    want = d["rec_xlibm"]
+    got, _ = ctx.run(sc, int(d["first"]), len(want))
+    assert_records_equal(got, want)
+    if "traj_xlibm" in d.files:
+        sct = configs.make_scenario(**kw, record=True)
+        _, traj = ctx.run_traj(sct, int(d["first"]), d["traj_xlibm"].shape[0])
+        np.testing.assert_array_equal(traj, d["traj_xlibm"])
+    # and the analytic default differs (the FD path really ran)
+    ctx.set_ctrl_jacobians("analytic")
+    ana, _ = ctx.run(sc, int(d["first"]), len(want))
+    assert not np.array_equal(ana["phi"], want["phi"])
