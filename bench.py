@@ -7,8 +7,9 @@ eps=1e-6, 720 control steps of Ts=10 s, 10 Euler-Maruyama substeps) with
 per-sample Gaussian parameter uncertainty, run side by side with the PI batch
 on identical noise streams and parameters. One step = one batch of S NMPC
 samples + the same S PI samples, consecutive global sample indices of the
-30,000-sample config (S = 7,500 divides 30,000, so every batch lies inside
-the config's index set and 4 steps cover it exactly; each rank takes its own
+30,000-sample config (S = 10,000 divides 30,000, so every batch lies inside
+the config's index set and the default 3 steps cover it exactly; 4.2 waves of
+2,368 resident samples per batch, profiles/r02/r02g_bench_S*.json; each rank takes its own
 batches: weak scaling, no data-path collective). value = NMPC samples per
 second of the whole job (the PI batch is inside the timed step). At the end
 the last step's records are all-gathered by the library over NCCL and the
@@ -46,8 +47,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sims-per-step", type=int, default=7500,
-                    help="NMPC (and PI) samples per rank per step (7,500 = 30,000 / 4: batches tile config 3)")
+    ap.add_argument("--sims-per-step", type=int, default=10000,
+                    help="NMPC (and PI) samples per rank per step (10,000 = 30,000 / 3: batches tile config 3)")
     ap.add_argument("--horizon", type=int, default=60)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-legs", action="store_true", help="skip the config 0/1/2 and three-state side legs")
@@ -388,7 +389,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cores = os.cpu_count() or 1
-            n = args.cpu_sample or 2 * cores
+            n = args.cpu_sample or 4 * cores
             _, wn, cores = cpu_pool(sc_n, 0, n)
             _, wp, _ = cpu_pool(sc_p, 0, n)
             cpu = {"value": n / (wn + wp), "unit": "sims/s", "cores": cores, "kind": "reference",

@@ -53,9 +53,24 @@
 #define NMPCMC_LOCAL_OCP(name, src) const Ocp& name = src
 #endif
 
+// Unroll factors of the serial Riccati / rollout loops (experiments; 1 =
+// the measured default, the kernel is instruction-cache sensitive).
+#ifndef NMPCMC_UNROLL_FACTOR
+#define NMPCMC_UNROLL_FACTOR 1
+#endif
+#ifndef NMPCMC_UNROLL_VECTOR
+#define NMPCMC_UNROLL_VECTOR 1
+#endif
+#ifndef NMPCMC_UNROLL_ROLLOUT
+#define NMPCMC_UNROLL_ROLLOUT 1
+#endif
+
 namespace nmpcmc_dev {
 
 constexpr unsigned FULLMASK = 0xffffffffu;
+constexpr int kUnrollFactor = NMPCMC_UNROLL_FACTOR;
+constexpr int kUnrollVector = NMPCMC_UNROLL_VECTOR;
+constexpr int kUnrollRollout = NMPCMC_UNROLL_ROLLOUT;
 #define kNaN __longlong_as_double(0x7ff8000000000000LL)
 constexpr double kEpsMach = 0x1.0p-52;  // numeric_limits<double>::epsilon (sqp.cpp:71)
 
@@ -422,7 +437,7 @@ __device__ __noinline__ bool factor_sweep(const Ocp& o) {
     pvec[N] = pv;
     // the head of the P chain (ju, Wr, bar) is loaded one stage ahead
     double ju = Ju[N - 1], wr = Wr[N - 1], br = bar[N - 1];
-#pragma unroll 1
+#pragma unroll kUnrollFactor
     for (int k = N - 1; k >= 0; --k) {
         const int kn = k > 0 ? k - 1 : 0;
         const double jun = Ju[kn], wrn = Wr[kn], brn = bar[kn];
@@ -533,7 +548,7 @@ __device__ __noinline__ void vector_sweep(const Ocp& o) {
     pvec[N] = pv;
     // operands at the head of the pv chain are loaded one stage ahead
     double vl = val[N], rd = rdyn[N - 1], ju = Ju[N - 1], rh = rhat[N - 1];
-#pragma unroll 1
+#pragma unroll kUnrollVector
     for (int k = N - 1; k >= 0; --k) {
         const int kn = k > 0 ? k - 1 : 0;
         const double vln = val[kn + 1], rdn = rdyn[kn], jun = Ju[kn], rhn = rhat[kn];
@@ -583,7 +598,7 @@ __device__ __noinline__ void rollout(int N) {
     // the loop is latency-bound on the dx chain: stage k+1's operands are
     // loaded while stage k computes, so no shared-memory latency sits on it
     double g = gain[1], f = dff[1], jx = Jx[1], rd = rdyn[1], ju = Ju[1];
-#pragma unroll 1
+#pragma unroll kUnrollRollout
     for (int k = 1; k < N; ++k) {
         const int kn = k + 1 < N ? k + 1 : k;
         const double gn = gain[kn], fn = dff[kn], jxn = Jx[kn], rdn = rdyn[kn], jun = Ju[kn];
