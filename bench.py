@@ -194,6 +194,16 @@ def _traffic(kernel_control_steps_per_launch):
         f"scaled to this launch's control steps ({t['source']})")
 
 
+def _k3_name(sc):
+    """The NMPC kernel the library dispatches for sc (nmpcmc_gpu.cu launch():
+    K3 for a one-state controller with N <= 255, stride ws_stride_for(N))."""
+    from paper_2212_02197_b200 import abi
+    if sc.ctrl_variant != abi.ONE_STATE or sc.N > 255:
+        return f"nmpc_genw_kernel<{3 if sc.truth_variant == abi.THREE_STATE else 1},3> (K3w, one warp per sample)"
+    st = 32 if sc.N < 32 else 64 if sc.N < 64 else 128 if sc.N < 128 else 256
+    return f"nmpc_kernel<{3 if sc.truth_variant == abi.THREE_STATE else 1},{st}> (K3, one warp per sample)"
+
+
 def run_ours(args):
     import ctypes as C
 
@@ -426,7 +436,7 @@ def run_ours(args):
             "gpu_launches": 2 * K,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_fma, "unit": "TFLOP/s",
                          "frac": achieved / peak_fma, "traffic": traffic, "traffic_note": traffic_note,
-                         "kernel": "nmpc_kernel (K3, one warp per sample)",
+                         "kernel": _k3_name(sc_n),
                          "kernel_ms_per_step": 1e3 * nmpc_kernel_s / K,
                          "kernel_time": "pipeline period elapsed/K (launches overlap on two lanes)" if lanes
                                         else "CUDA events around each launch on its stream",
