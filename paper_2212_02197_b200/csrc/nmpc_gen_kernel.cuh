@@ -59,9 +59,13 @@ using Ws = WsT<1>;
 /// per block): 32-bit LDS/STS addressing and LDS latency on the serial
 /// recursions. K3g keeps them in its global slab.
 extern __shared__ __align__(16) double gen_smem[];
+/// JX / JU: K3w's shared-memory copies of the current QP's constraint
+/// jacobians (FX[s], FU[s], constant during one solve_qp), staged once per QP
+/// so the serial sweeps read them with LDS latency instead of L1/L2 misses
+/// on the dependency chain (r02j profile: 14 % of K3w's stall samples).
 template <int NX>
 struct SweepLay {
-    int FP, FLL, FLY, FK, FG, PV, DFF, total;
+    int FP, FLL, FLY, FK, FG, PV, DFF, JX, JU, total;
     __host__ __device__ explicit SweepLay(int N) {
         FP = 0;
         FLL = FP + (N + 1) * NX * NX;
@@ -70,7 +74,9 @@ struct SweepLay {
         FG = FK + N * NX;
         PV = FG + N * NX;
         DFF = PV + (N + 1) * NX;
-        total = DFF + N;
+        JX = DFF + N;
+        JU = JX + N * NX * NX;
+        total = JU + N * NX;
     }
 };
 /// Bytes of shared memory K3w needs per block; K3w runs only if it fits.
@@ -662,8 +668,11 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
     const ArrT<W> aFK = sweep_arr<W>(w, oFK, SL.FK);
     const ArrT<W> aFG = sweep_arr<W>(w, oFG, SL.FG);
     const int oFXs = L.FX[v.s], oFUs = L.FU[v.s], oWB = L.WB, oXIs = L.XI[v.s], oGFs = L.GF[v.s];
-    auto Jx_ = [&](int k, int i, int j) -> double { return w[oFXs + (k * NX + j) * NX + i]; };
-    auto Ju_ = [&](int k, int i) -> double { return w[oFUs + k * NX + i]; };
+    // K3w: the shared-memory copies staged by solve_qp; K3g: the set in place
+    const ArrT<W> aJX = sweep_arr<W>(w, oFXs, SL.JX);
+    const ArrT<W> aJU = sweep_arr<W>(w, oFUs, SL.JU);
+    auto Jx_ = [&](int k, int i, int j) -> double { return aJX[(k * NX + j) * NX + i]; };
+    auto Ju_ = [&](int k, int i) -> double { return aJU[k * NX + i]; };
     const int nN = o.N;
     auto Wb_ = [&](int k, int i, int j) -> double {
         const int ld = k == 0 ? 1 : (k < nN ? NX + 1 : NX);
@@ -820,8 +829,11 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
     const ArrT<W> aPV = sweep_arr<W>(w, oPV, SL.PV);
     const ArrT<W> aDFF = sweep_arr<W>(w, oDFF, SL.DFF);
     const int oFXs = L.FX[v.s], oFUs = L.FU[v.s], oWB = L.WB, oXIs = L.XI[v.s], oGFs = L.GF[v.s];
-    auto Jx_ = [&](int k, int i, int j) -> double { return w[oFXs + (k * NX + j) * NX + i]; };
-    auto Ju_ = [&](int k, int i) -> double { return w[oFUs + k * NX + i]; };
+    // K3w: the shared-memory copies staged by solve_qp; K3g: the set in place
+    const ArrT<W> aJX = sweep_arr<W>(w, oFXs, SL.JX);
+    const ArrT<W> aJU = sweep_arr<W>(w, oFUs, SL.JU);
+    auto Jx_ = [&](int k, int i, int j) -> double { return aJX[(k * NX + j) * NX + i]; };
+    auto Ju_ = [&](int k, int i) -> double { return aJU[k * NX + i]; };
     const int nN = o.N;
     auto Wb_ = [&](int k, int i, int j) -> double {
         const int ld = k == 0 ? 1 : (k < nN ? NX + 1 : NX);
@@ -1074,6 +1086,12 @@ __device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_
     const WsT<W> w = o.ws;
     const Layout<NX> L = o.lay;
     const int N = o.N, lane = Lanes<W>::lane();
+    if (W > 1) {  // stage the sweeps' jacobian operands (SweepLay JX / JU)
+        const SweepLay<NX> SL(N);
+        for (int e = lane; e < N * NX * NX; e += W) gen_smem[SL.JX + e] = w[L.FX[v.s] + e];
+        for (int e = lane; e < N * NX; e += W) gen_smem[SL.JU + e] = w[L.FU[v.s] + e];
+        Lanes<W>::sync();
+    }
     int m = 0;
     double scale = 1.0;  // data_scale: an order-independent max (NaN ignored)
     bool domain = false;
