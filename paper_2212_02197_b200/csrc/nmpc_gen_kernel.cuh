@@ -63,9 +63,12 @@ extern __shared__ __align__(16) double gen_smem[];
 /// jacobians (FX[s], FU[s], constant during one solve_qp), staged once per QP
 /// so the serial sweeps read them with LDS latency instead of L1/L2 misses
 /// on the dependency chain (r02j profile: 14 % of K3w's stall samples).
+/// RS / RD / RH: the IPM residuals the vector sweep reads (K3w keeps them in
+/// shared memory; K3g in its slab at Layout's offsets). TG: the products of
+/// the complementarity gap's ordered sums, formed lane-parallel.
 template <int NX>
 struct SweepLay {
-    int FP, FLL, FLY, FK, FG, PV, DFF, JX, JU, total;
+    int FP, FLL, FLY, FK, FG, PV, DFF, JX, JU, RS, RD, RH, TG, total;
     __host__ __device__ explicit SweepLay(int N) {
         FP = 0;
         FLL = FP + (N + 1) * NX * NX;
@@ -76,7 +79,11 @@ struct SweepLay {
         DFF = PV + (N + 1) * NX;
         JX = DFF + N;
         JU = JX + N * NX * NX;
-        total = JU + N * NX;
+        RS = JU + N * NX;
+        RD = RS + N * (1 + NX);
+        RH = RD + N * NX;
+        TG = RH + N;
+        total = TG + 2 * N;
     }
 };
 /// Bytes of shared memory K3w needs per block; K3w runs only if it fits.
@@ -846,11 +853,14 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
 
     const int N = o.N;
     auto P = [&](int k, int i, int j) -> double { return aFP[(k * NX + j) * NX + i]; };
-    auto bh = [&](int k, int i) -> double { return -w[oRD + k * NX + i]; };
+    const ArrT<W> aRS = sweep_arr<W>(w, oRS, SL.RS);
+    const ArrT<W> aRD = sweep_arr<W>(w, oRD, SL.RD);
+    const ArrT<W> aRH = sweep_arr<W>(w, oRH, SL.RH);
+    auto bh = [&](int k, int i) -> double { return -aRD[k * NX + i]; };
     double pvn[NX];  // p_{k+1}, carried in registers (see rfactor)
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
-        pvn[i] = w[oRS + L.xo(N) + i];
+        pvn[i] = aRS[L.xo(N) + i];
         aPV[N * NX + i] = pvn[i];
     }
 #pragma unroll 1
@@ -868,7 +878,7 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
             double s = 0.0;
 #pragma unroll
             for (int j = 0; j < NX; ++j) s += Ju_(k, j) * t[j];
-            hv = 1.0 * s + 1.0 * w[oRH + k];
+            hv = 1.0 * s + 1.0 * aRH[k];
         }
         const double l = aFLL[k];
         if (FAST) {
@@ -887,7 +897,7 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
                 double s = 0.0;
 #pragma unroll
                 for (int j = 0; j < NX; ++j) s += Jx_(k, j, i) * t[j];
-                double p = 1.0 * s + 1.0 * w[oRS + L.xo(k) + i];
+                double p = 1.0 * s + 1.0 * aRS[L.xo(k) + i];
                 p = 1.0 * (0.0 + aFG[k * NX + i] * dff) + 1.0 * p;
                 aPV[k * NX + i] = p;
                 pvn[i] = p;
@@ -953,6 +963,9 @@ __device__ __noinline__ void qp_resid(const QpView<NX, W> v) {
     const WsT<W> w = o.ws;
     const Layout<NX> L = o.lay;
     const int N = o.N;
+    const SweepLay<NX> SL(N);
+    const ArrT<W> aRS = sweep_arr<W>(w, L.RS, SL.RS);
+    const ArrT<W> aRD = sweep_arr<W>(w, L.RD, SL.RD);
     auto dxi = [&](int e) -> double { return w[L.QDXI + e]; };
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k < N; k += W) {
@@ -971,7 +984,7 @@ __device__ __noinline__ void qp_resid(const QpView<NX, W> v) {
             r = -1.0 * s + 1.0 * r;
         }
         r += w[L.QNU + k] - w[L.QNL + k];
-        w[L.RS + L.uo(k)] = r;
+        aRS[L.uo(k)] = r;
         double d[NX];
 #pragma unroll
         for (int i = 0; i < NX; ++i) d[i] = dxi(L.xo(k + 1) + i) + -1.0 * v.b(k, i);
@@ -985,7 +998,7 @@ __device__ __noinline__ void qp_resid(const QpView<NX, W> v) {
             }
         }
 #pragma unroll
-        for (int i = 0; i < NX; ++i) w[L.RD + k * NX + i] = -1.0 * (0.0 + v.Ju(k, i) * vk) + 1.0 * d[i];
+        for (int i = 0; i < NX; ++i) aRD[k * NX + i] = -1.0 * (0.0 + v.Ju(k, i) * vk) + 1.0 * d[i];
     }
 #pragma unroll 1
     for (int k = 1 + Lanes<W>::lane(); k <= N; k += W) {
@@ -1010,7 +1023,7 @@ __device__ __noinline__ void qp_resid(const QpView<NX, W> v) {
             }
         }
 #pragma unroll
-        for (int i = 0; i < NX; ++i) w[L.RS + L.xo(k) + i] = x[i] + w[L.QMU + (k - 1) * NX + i];
+        for (int i = 0; i < NX; ++i) aRS[L.xo(k) + i] = x[i] + w[L.QMU + (k - 1) * NX + i];
     }
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k < N; k += W) {
@@ -1028,12 +1041,15 @@ __device__ __forceinline__ void qp_csolve(const QpView<NX, W> v) {
     const Ocp<NX, W>& o = *v.o;
     const WsT<W> w = o.ws;
     const Layout<NX> L = o.lay;
+    const SweepLay<NX> SL(o.N);
+    const ArrT<W> aRS = sweep_arr<W>(w, L.RS, SL.RS);
+    const ArrT<W> aRH = sweep_arr<W>(w, L.RH, SL.RH);
 #pragma unroll 1
     for (int k = Lanes<W>::lane(); k < o.N; k += W) {
-        double x = w[L.RS + L.uo(k)];
+        double x = aRS[L.uo(k)];
         if (dfinite(v.lb(k))) x -= (w[L.CL + k] - w[L.QNL + k] * w[L.RL + k]) / w[L.SL + k];
         if (dfinite(v.ub(k))) x += (w[L.CU + k] - w[L.QNU + k] * w[L.RU + k]) / w[L.SU + k];
-        w[L.RH + k] = x;
+        aRH[k] = x;
     }
     Lanes<W>::sync();
     rsolve<NX, W>(v);
@@ -1086,10 +1102,12 @@ __device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_
     const WsT<W> w = o.ws;
     const Layout<NX> L = o.lay;
     const int N = o.N, lane = Lanes<W>::lane();
+    const SweepLay<NX> SLq(N);
+    const ArrT<W> aRSq = sweep_arr<W>(w, L.RS, SLq.RS);
+    const ArrT<W> aRDq = sweep_arr<W>(w, L.RD, SLq.RD);
     if (W > 1) {  // stage the sweeps' jacobian operands (SweepLay JX / JU)
-        const SweepLay<NX> SL(N);
-        for (int e = lane; e < N * NX * NX; e += W) gen_smem[SL.JX + e] = w[L.FX[v.s] + e];
-        for (int e = lane; e < N * NX; e += W) gen_smem[SL.JU + e] = w[L.FU[v.s] + e];
+        for (int e = lane; e < N * NX * NX; e += W) gen_smem[SLq.JX + e] = w[L.FX[v.s] + e];
+        for (int e = lane; e < N * NX; e += W) gen_smem[SLq.JU + e] = w[L.FU[v.s] + e];
         Lanes<W>::sync();
     }
     int m = 0;
@@ -1137,17 +1155,32 @@ __device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_
     for (int it = 0;; ++it) {
         qp_resid<NX, W>(v);
         double gap = 0.0;
-        if (m > 0) {  // ordered sums: serial on every lane
+        if (m > 0) {  // ordered sums: products lane-parallel, sums serial on every lane
+            const ArrT<W> aTG = sweep_arr<W>(w, L.FLL, SLq.TG);
             double dl = 0.0, du = 0.0;
+            if (W > 1) {
 #pragma unroll 1
-            for (int k = 0; k < N; ++k) dl += w[L.SL + k] * w[L.QNL + k];
+                for (int k = lane; k < N; k += W) {
+                    aTG[k] = w[L.SL + k] * w[L.QNL + k];
+                    aTG[N + k] = w[L.SU + k] * w[L.QNU + k];
+                }
+                Lanes<W>::sync();
 #pragma unroll 1
-            for (int k = 0; k < N; ++k) du += w[L.SU + k] * w[L.QNU + k];
+                for (int k = 0; k < N; ++k) dl += aTG[k];
+#pragma unroll 1
+                for (int k = 0; k < N; ++k) du += aTG[N + k];
+                Lanes<W>::sync();
+            } else {
+#pragma unroll 1
+                for (int k = 0; k < N; ++k) dl += w[L.SL + k] * w[L.QNL + k];
+#pragma unroll 1
+                for (int k = 0; k < N; ++k) du += w[L.SU + k] * w[L.QNU + k];
+            }
             gap = (dl + du) / m;
         }
         double ns = 0.0, nd = 0.0, nl = 0.0, nu = 0.0;
-        for (int e = lane; e < L.L; e += W) ns = inf_fold(ns, w[L.RS + e]);
-        for (int e = lane; e < L.NN; e += W) nd = inf_fold(nd, w[L.RD + e]);
+        for (int e = lane; e < L.L; e += W) ns = inf_fold(ns, aRSq[e]);
+        for (int e = lane; e < L.NN; e += W) nd = inf_fold(nd, aRDq[e]);
 #pragma unroll 1
         for (int k = lane; k < N; k += W) {
             nl = inf_fold(nl, w[L.RL + k]);
