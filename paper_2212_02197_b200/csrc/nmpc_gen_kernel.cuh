@@ -65,10 +65,14 @@ extern __shared__ __align__(16) double gen_smem[];
 /// on the dependency chain (r02j profile: 14 % of K3w's stall samples).
 /// RS / RD / RH: the IPM residuals the vector sweep reads (K3w keeps them in
 /// shared memory; K3g in its slab at Layout's offsets). TG: the products of
-/// the complementarity gap's ordered sums, formed lane-parallel.
+/// the complementarity gap's ordered sums, formed lane-parallel. LB / UB /
+/// RR / QQ: the QP's input bounds and the R and Q parts of the Hessian
+/// blocks, staged once per QP (constant during solve_qp) for the lane loops
+/// and the factor sweep. At N = 60, NX = 3 the layout is 26.4 KB, so 8
+/// one-warp blocks (the register limit) still fit an SM.
 template <int NX>
 struct SweepLay {
-    int FP, FLL, FLY, FK, FG, PV, DFF, JX, JU, RS, RD, RH, TG, total;
+    int FP, FLL, FLY, FK, FG, PV, DFF, JX, JU, RS, RD, RH, TG, LB, UB, RR, QQ, total;
     __host__ __device__ explicit SweepLay(int N) {
         FP = 0;
         FLL = FP + (N + 1) * NX * NX;
@@ -83,7 +87,11 @@ struct SweepLay {
         RD = RS + N * (1 + NX);
         RH = RD + N * NX;
         TG = RH + N;
-        total = TG + 2 * N;
+        LB = TG + 2 * N;
+        UB = LB + N;
+        RR = UB + N;
+        QQ = RR + N + 1;
+        total = QQ + (N + 1) * NX * NX;
     }
 };
 /// Bytes of shared memory K3w needs per block; K3w runs only if it fits.
@@ -638,11 +646,12 @@ struct QpView {
     int s;  // evaluation set of the current iterate
     // cached by value, so the accessors need no reload through *o after stores
     WsT<W> w;
-    int N, WB, GFs, FXs, FUs, BBs, XIs;
+    int N, WB, GFs, FXs, FUs, BBs, XIs, sLB, sUB;
     double umin, umax;
     __device__ QpView(const Ocp<NX, W>* op, int set)
         : o(op), s(set), w(op->ws), N(op->N), WB(op->lay.WB), GFs(op->lay.GF[set]), FXs(op->lay.FX[set]),
-          FUs(op->lay.FU[set]), BBs(op->lay.BB[set]), XIs(op->lay.XI[set]), umin(op->umin), umax(op->umax) {}
+          FUs(op->lay.FU[set]), BBs(op->lay.BB[set]), XIs(op->lay.XI[set]), sLB(SweepLay<NX>(op->N).LB),
+          sUB(SweepLay<NX>(op->N).UB), umin(op->umin), umax(op->umax) {}
     __device__ double Wb(int k, int i, int j) const {
         const int ld = k == 0 ? 1 : (k < N ? NX + 1 : NX);
         return w[WB + k * Layout<NX>::B + j * ld + i];
@@ -656,8 +665,11 @@ struct QpView {
     __device__ double Ju(int k, int i) const { return w[FUs + k * NX + i]; }
     __device__ double b(int k, int i) const { return w[BBs + k * NX + i]; }
     __device__ double u(int k) const { return w[XIs + Layout<NX>::W * k]; }
-    __device__ double lb(int k) const { return umin - u(k); }
-    __device__ double ub(int k) const { return umax - u(k); }
+    // K3w reads the copies solve_qp staged (SweepLay LB / UB)
+    __device__ double lb(int k) const { return W > 1 ? gen_smem[sLB + k] : umin - u(k); }
+    __device__ double ub(int k) const { return W > 1 ? gen_smem[sUB + k] : umax - u(k); }
+    __device__ double lb_src(int k) const { return umin - u(k); }
+    __device__ double ub_src(int k) const { return umax - u(k); }
 };
 
 /// riccati_factor (qp.cpp:73-110) with barrier diagonal BAR. Returns true on
@@ -685,8 +697,15 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
         const int ld = k == 0 ? 1 : (k < nN ? NX + 1 : NX);
         return w[oWB + k * Layout<NX>::B + j * ld + i];
     };
-    auto R_ = [&](int k) -> double { return k == 0 ? Wb_(0, 0, 0) : Wb_(k, NX, NX); };
-    auto Q_ = [&](int k, int i, int j) -> double { return Wb_(k, i, j); };
+    // K3w: R and Q from the copies solve_qp staged (SweepLay RR / QQ)
+    auto R_ = [&](int k) -> double {
+        if (W > 1) return gen_smem[SL.RR + k];
+        return k == 0 ? Wb_(0, 0, 0) : Wb_(k, NX, NX);
+    };
+    auto Q_ = [&](int k, int i, int j) -> double {
+        if (W > 1) return gen_smem[SL.QQ + (k * NX + j) * NX + i];
+        return Wb_(k, i, j);
+    };
     auto M_ = [&](int k, int i) -> double { return Wb_(k, i, NX); };
     (void)oXIs, (void)oGFs;
 
@@ -1105,9 +1124,21 @@ __device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_
     const SweepLay<NX> SLq(N);
     const ArrT<W> aRSq = sweep_arr<W>(w, L.RS, SLq.RS);
     const ArrT<W> aRDq = sweep_arr<W>(w, L.RD, SLq.RD);
-    if (W > 1) {  // stage the sweeps' jacobian operands (SweepLay JX / JU)
+    if (W > 1) {  // stage the QP's constant operands (SweepLay JX JU LB UB RR QQ)
         for (int e = lane; e < N * NX * NX; e += W) gen_smem[SLq.JX + e] = w[L.FX[v.s] + e];
         for (int e = lane; e < N * NX; e += W) gen_smem[SLq.JU + e] = w[L.FU[v.s] + e];
+#pragma unroll 1
+        for (int k = lane; k <= N; k += W) {
+            if (k < N) {
+                gen_smem[SLq.LB + k] = v.lb_src(k);
+                gen_smem[SLq.UB + k] = v.ub_src(k);
+                gen_smem[SLq.RR + k] = v.R(k);
+            }
+#pragma unroll
+            for (int j = 0; j < NX; ++j)
+#pragma unroll
+                for (int i = 0; i < NX; ++i) gen_smem[SLq.QQ + (k * NX + j) * NX + i] = k == 0 ? 0.0 : v.Q(k, i, j);
+        }
         Lanes<W>::sync();
     }
     int m = 0;
@@ -1223,12 +1254,31 @@ __device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_
         if (m > 0 && gap > 0.0) {
             const double aa = qp_step<NX, W>(v, 1.0);
             double ga = 0.0;
+            if (W > 1) {
+                // products lane-parallel, the ordered sum serial on every lane;
+                // an absent bound contributes +0.0, which leaves ga unchanged
+                // (ga starts at +0 and a sum from +0 is never -0)
 #pragma unroll 1
-            for (int k = 0; k < N; ++k) {
-                if (dfinite(v.lb(k)))
-                    ga += (w[L.SL + k] + aa * w[L.DSL + k]) * (w[L.QNL + k] + aa * w[L.DNL + k]);
-                if (dfinite(v.ub(k)))
-                    ga += (w[L.SU + k] + aa * w[L.DSU + k]) * (w[L.QNU + k] + aa * w[L.DNU + k]);
+                for (int k = lane; k < N; k += W) {
+                    gen_smem[SLq.TG + 2 * k] =
+                        dfinite(v.lb(k)) ? (w[L.SL + k] + aa * w[L.DSL + k]) * (w[L.QNL + k] + aa * w[L.DNL + k])
+                                         : 0.0;
+                    gen_smem[SLq.TG + 2 * k + 1] =
+                        dfinite(v.ub(k)) ? (w[L.SU + k] + aa * w[L.DSU + k]) * (w[L.QNU + k] + aa * w[L.DNU + k])
+                                         : 0.0;
+                }
+                Lanes<W>::sync();
+#pragma unroll 1
+                for (int e = 0; e < 2 * N; ++e) ga += gen_smem[SLq.TG + e];
+                Lanes<W>::sync();
+            } else {
+#pragma unroll 1
+                for (int k = 0; k < N; ++k) {
+                    if (dfinite(v.lb(k)))
+                        ga += (w[L.SL + k] + aa * w[L.DSL + k]) * (w[L.QNL + k] + aa * w[L.DNL + k]);
+                    if (dfinite(v.ub(k)))
+                        ga += (w[L.SU + k] + aa * w[L.DSU + k]) * (w[L.QNU + k] + aa * w[L.DNU + k]);
+                }
             }
             ga /= m;
             const double ratio = smax(0.0, ga / gap);

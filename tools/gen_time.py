@@ -9,10 +9,15 @@ sc = configs.make_scenario("nmpc", n_steps=steps, N=N, perturb=True, ctrl_varian
 ctx = engine.Context(0)
 ctx.set_nmpc_kernel(kind)
 ctx.run(sc, 0, min(n, 256))
-t = time.perf_counter()
-rec, cnt = ctx.run(sc, 0, n, counters=True)
-dt = time.perf_counter() - t
+reps = int(os.environ.get("GEN_TIME_REPS", "3"))
+times = []
+for _ in range(reps):
+    t = time.perf_counter()
+    rec, cnt = ctx.run(sc, 0, n, counters=True)
+    times.append(time.perf_counter() - t)
+dt = min(times)
 ipm = int(cnt["ipm_stage_iters"].sum())
 print(f"{kind} ctrl_variant={cv} n={n} steps={steps} N={N}: {dt*1e3:.1f} ms, {n*steps/720/dt:.2f} sims/s (720-step equiv), "
       f"{ipm/dt/1e6:.1f} M ipm-stage-iters/s, {workmodel.nmpc_flops(cnt, 3 if cv == 0 else 1)/dt/1e12:.3f} TF/s, "
-      f"failed {int(rec['failed'].sum())}, rec {hashlib.sha1(rec.tobytes()).hexdigest()[:12]}", flush=True)
+      f"failed {int(rec['failed'].sum())}, rec {hashlib.sha1(rec.tobytes()).hexdigest()[:12]}, "
+      f"runs ms {[round(x * 1e3, 1) for x in times]}", flush=True)
