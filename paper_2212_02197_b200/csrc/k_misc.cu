@@ -82,7 +82,10 @@ int launch_pi(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nm
     constexpr int G = nmpcmc_dev::kPiLanes, block = nmpcmc_dev::kPiBlock;
     const bool three = sc.truth_variant == NMPCMC_THREE_STATE;
     const int per_step = (sc.has_noise_R != 0 ? 1 : 0) + sc.Ns * (three ? 3 : 1);
-    const bool small = n < (int64_t)sm_count * 4 * 32;
+#ifndef NMPCMC_PI_SMALL_WARPS
+#define NMPCMC_PI_SMALL_WARPS 4
+#endif
+    const bool small = n < (int64_t)sm_count * NMPCMC_PI_SMALL_WARPS * 32;
     if (G > 1 && small && per_step < 2 * nmpcmc_dev::kPiPairs) {
         const unsigned grid = (unsigned)((n + block / G - 1) / (block / G));
         if (three)

@@ -254,10 +254,19 @@ extern __shared__ __align__(16) double smem_nmpc[];
 #ifndef NMPCMC_IPM_SMEM
 #define NMPCMC_IPM_SMEM 0
 #endif
+// NMPCMC_CERT_SMEM = 1 keeps the certificate inputs of the fast Riccati
+// sweeps (written by the serial sweeps, read by the lane-parallel certify
+// loops) in shared memory instead of the L2 slab.
+#ifndef NMPCMC_CERT_SMEM
+#define NMPCMC_CERT_SMEM 1  // measured +1 % (profiles/r02/r02o_k3_cert_ab.txt)
+#endif
 enum SmemId {
     S_JX, S_JU, S_WQ, S_WM, S_WR, S_BAR, S_RDYN, S_RHAT, S_RSX,
     S_CHOLH, S_RINV, S_VAL, S_GAIN, S_GMAT, S_PVEC, S_DFF,
     S_DDU, S_DDX,
+#if NMPCMC_CERT_SMEM
+    S_CHH, S_CA1, S_CQ1, S_CG1,
+#endif
     S_TMP,  // three strides
     S_IPM0 = S_TMP + 3,
 #if NMPCMC_IPM_SMEM
@@ -270,7 +279,9 @@ enum GlobId {
     G_U, G_X, G_TU, G_TX, G_LAM, G_PIL, G_PIU,
     G_GX, G_G, G_TGX, G_TG, G_TJX, G_TJU,
     G_SIG, G_SP,
+#if !NMPCMC_CERT_SMEM
     G_CHH, G_CA1, G_CQ1, G_CG1,  // certificate inputs of the fast Riccati sweeps
+#endif
     G_IPM0,
 #if NMPCMC_IPM_SMEM
     kGlobArrays = G_IPM0
@@ -293,6 +304,11 @@ static __device__ __noinline__ double qdiv(double a, double b) { return a / b; }
 
 #define SA(id) (smem_nmpc + (id) * ST)
 #define GA(id) (o.gws + (id) * ST)
+#if NMPCMC_CERT_SMEM
+#define CA(name) SA(S_##name)
+#else
+#define CA(name) GA(G_##name)
+#endif
 
 __host__ __device__ inline size_t ws_bytes_for(int ST) { return (size_t)kSmemArrays * ST * sizeof(double); }
 __host__ __device__ inline size_t gws_bytes_for(int ST) { return (size_t)kGlobArrays * ST * sizeof(double); }
@@ -427,10 +443,10 @@ __device__ __noinline__ bool factor_sweep(const Ocp& o) {
     double* gmat = SA(S_GMAT);
     double* pvec = SA(S_PVEC);
     double* dff = SA(S_DFF);
-    double* chh = GA(G_CHH);
-    double* ca1 = GA(G_CA1);
-    double* cq1 = GA(G_CQ1);
-    double* cg1 = GA(G_CG1);
+    double* chh = CA(CHH);
+    double* ca1 = CA(CA1);
+    double* cq1 = CA(CQ1);
+    double* cg1 = CA(CG1);
     double P = Wq[N];
     double pv = rsx[N - 1];  // pvec[N] = qhat[N]
     val[N] = P;
@@ -510,10 +526,10 @@ __device__ __noinline__ bool factor_sweep(const Ocp& o) {
 template <int ST>
 __device__ __forceinline__ bool certify_factor_k(const Ocp& o, int k) {
     const double l = SA(S_CHOLH)[k];
-    const double q1 = GA(G_CQ1)[k];
-    bool ok = cert_sqrt(GA(G_CHH)[k], l) && cert_div(GA(G_CA1)[k], l, q1) && cert_div(q1, l, -SA(S_DFF)[k]);
+    const double q1 = CA(CQ1)[k];
+    bool ok = cert_sqrt(CA(CHH)[k], l) && cert_div(CA(CA1)[k], l, q1) && cert_div(q1, l, -SA(S_DFF)[k]);
     if (k >= 1) {
-        const double g1 = GA(G_CG1)[k];
+        const double g1 = CA(CG1)[k];
         ok = ok && cert_div(SA(S_GMAT)[k], l, g1) && cert_div(g1, l, -SA(S_GAIN)[k]);
     }
     return ok;
@@ -522,8 +538,8 @@ __device__ __forceinline__ bool certify_factor_k(const Ocp& o, int k) {
 template <int ST>
 __device__ __forceinline__ bool certify_vector_k(const Ocp& o, int k) {
     const double l = SA(S_CHOLH)[k];
-    const double q1 = GA(G_CQ1)[k];
-    return cert_div(GA(G_CA1)[k], l, q1) && cert_div(q1, l, -SA(S_DFF)[k]);
+    const double q1 = CA(CQ1)[k];
+    return cert_div(CA(CA1)[k], l, q1) && cert_div(q1, l, -SA(S_DFF)[k]);
 }
 
 /// Corrector backward vector sweep with the cached factor (qp.cpp:122-141);
@@ -542,8 +558,8 @@ __device__ __noinline__ void vector_sweep(const Ocp& o) {
     const double* gmat = SA(S_GMAT);
     double* pvec = SA(S_PVEC);
     double* dff = SA(S_DFF);
-    double* ca1 = GA(G_CA1);
-    double* cq1 = GA(G_CQ1);
+    double* ca1 = CA(CA1);
+    double* cq1 = CA(CQ1);
     double pv = rsx[N - 1];
     pvec[N] = pv;
     // operands at the head of the pv chain are loaded one stage ahead
@@ -1783,6 +1799,7 @@ inline int launch_ocp1(const nmpcmc_scenario& sc, int64_t batch, const double* x
 
 #undef SA
 #undef GA
+#undef CA
 #undef IA
 
 }  // namespace nmpcmc_dev
