@@ -116,6 +116,27 @@ __device__ __forceinline__ ArrT<W> sweep_arr(const WsT<W>& w, int goff, int soff
     return ArrT<W>{gen_smem + soff, 1};
 }
 
+/// Ordered sum s = init + t(0) + t(1) + ... + t(n-1), left to right, the
+/// reference's serial reduction order. K3w forms the terms lane-parallel into
+/// the shared-memory scratch (n <= cap doubles) and then adds them serially on
+/// every lane, so the serial chain reads LDS instead of slab loads; K3g (or a
+/// missing scratch) adds them directly. Bitwise the same either way: every
+/// term is the same IEEE expression and the additions happen in index order.
+template <int W, class T>
+__device__ __forceinline__ double ordered_sum(double init, int n, double* scratch, int cap, const T& term) {
+    double acc = init;
+    if (W > 1 && scratch != nullptr && n <= cap) {
+        for (int e = (int)(threadIdx.x & 31); e < n; e += W) scratch[e] = term(e);
+        __syncwarp();
+#pragma unroll 4
+        for (int e = 0; e < n; ++e) acc += scratch[e];
+        __syncwarp();
+    } else {
+        for (int e = 0; e < n; ++e) acc += term(e);
+    }
+    return acc;
+}
+
 /// Lane helpers: W = 1 (thread per sample) or 32 (warp per sample).
 constexpr unsigned kMask = 0xffffffffu;
 template <int W>
@@ -331,11 +352,22 @@ __device__ __forceinline__ int jac_u(const Model<NX>& m, const double* x, double
 }
 
 // ------------------------------------------------------------------ shoot
+#ifndef NMPCMC_SHOOT_MODEL_COPY
+#define NMPCMC_SHOOT_MODEL_COPY 1  // measured +3.5 % three-state (profiles/r02/r02s_k3w_model_ab.txt)
+#endif
 /// shoot (ocp.cpp:9-74): Nc RK4 steps of (F, Fx, Fu). Column-major Fx.
 /// The RK4 weighted sum a + 2b + 2c + d accumulates left to right.
 template <int NX, bool SENS>
-__device__ __noinline__ int shoot(const Model<NX>& m, const double* x, double u, double h, int nc, double* F,
+__device__ __noinline__ int shoot(const Model<NX>& m_in, const double* x, double u, double h, int nc, double* F,
                                   double* Fx, double* Fu) {
+#if NMPCMC_SHOOT_MODEL_COPY
+    // a private copy: the stores to F / Fx / Fu may alias the caller's model
+    // (both live in local memory), which would force a reload of every model
+    // field after each store inside the RK4 loop
+    const Model<NX> m = m_in;
+#else
+    const Model<NX>& m = m_in;
+#endif
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
         F[i] = x[i];
@@ -545,21 +577,24 @@ __device__ __noinline__ double objective(const Ocp<NX, W>& o, int s, bool grad) 
     // not accumulated: each slot is 0.0 + 2 Ts g once (ocp.cpp:80-97)
     const WsT<W> w = o.ws;
     const Layout<NX> L = o.lay;
+    // scalars hoisted: the stores below may alias the Ocp (local memory)
+    const double V = o.m.p.V, Qz = o.Qz, Ts = o.Ts, invV = o.invV;
+    const int N = o.N;
     double phi = 0.0;
 #pragma unroll 1
-    for (int k = 1; k <= o.N; ++k) {
-        const double res = w[L.XI[s] + L.xo(k) + NX - 1] / o.m.p.V - w[L.SP + k - 1];
-        const double qres = 1.0 * (0.0 + o.Qz * res) + 0.0;
-        phi += o.Ts * (0.0 + res * qres);
+    for (int k = 1; k <= N; ++k) {
+        const double res = w[L.XI[s] + L.xo(k) + NX - 1] / V - w[L.SP + k - 1];
+        const double qres = 1.0 * (0.0 + Qz * res) + 0.0;
+        phi += Ts * (0.0 + res * qres);
         if (grad) {
             w[L.GF[s] + L.uo(k - 1)] = 0.0;
 #pragma unroll
             for (int i = 0; i < NX; ++i) {
                 const double hi = (i == NX - 1) ? (o.m.fd ? meas_jac_T<NX>(o.m, w[L.XI[s] + L.xo(k) + NX - 1])
-                                                          : o.invV)
+                                                          : invV)
                                                 : 0.0;
                 const double g = 1.0 * (0.0 + hi * qres) + 0.0;
-                w[L.GF[s] + L.xo(k) + i] = 0.0 + 2.0 * o.Ts * g;
+                w[L.GF[s] + L.xo(k) + i] = 0.0 + 2.0 * Ts * g;
             }
         }
     }
@@ -1363,13 +1398,13 @@ __device__ __noinline__ bool kkt_ok(const Ocp<NX, W>& o, int s, int LAMo, int PL
     for (int k = lane; k < o.N; k += W) w[L.HO + L.uo(k)] += w[PUo + k] - w[PLo + k];
     Lanes<W>::sync();
     double sd = 1.0;
-    if (m > 0) {  // ordered one-norm sums: serial on every lane
-        double a = 0.0, b = 0.0, c = 0.0;
-        for (int e = 0; e < L.NN; ++e) a += fabs(w[LAMo + e]);
-#pragma unroll 1
-        for (int k = 0; k < o.N; ++k) b += fabs(w[PLo + k]);
-#pragma unroll 1
-        for (int k = 0; k < o.N; ++k) c += fabs(w[PUo + k]);
+    if (m > 0) {  // ordered one-norm sums (ordered_sum: terms lane-parallel on K3w)
+        const SweepLay<NX> SL(o.N);
+        double* scr = W > 1 ? gen_smem + SL.JX : nullptr;  // JX / JU are free outside solve_qp
+        const int cap = o.N * NX * (NX + 1);
+        const double a = ordered_sum<W>(0.0, L.NN, scr, cap, [&](int e) { return fabs(w[LAMo + e]); });
+        const double b = ordered_sum<W>(0.0, o.N, scr, cap, [&](int k) { return fabs(w[PLo + k]); });
+        const double c = ordered_sum<W>(0.0, o.N, scr, cap, [&](int k) { return fabs(w[PUo + k]); });
         sd = smax(100.0, (a + b + c) / m) / 100.0;
     }
     double gl = 0.0, gg = 0.0;
@@ -1503,11 +1538,14 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_o
         first = false;
         // line_search (sqp.cpp:22-59); the trial of the accepted step is the
         // new iterate (identical by construction, sqp.cpp:331-352)
-        double pen = 0.0;
-        for (int e = 0; e < L.NN; ++e) pen += w[L.SIG + e] * fabs(w[L.G[s] + e]);
+        const SweepLay<NX> SLs(N);
+        double* scr = W > 1 ? gen_smem + SLs.JX : nullptr;  // JX / JU are free outside solve_qp
+        const int cap = N * NX * (NX + 1);
+        const double pen =
+            ordered_sum<W>(0.0, L.NN, scr, cap, [&](int e) { return w[L.SIG + e] * fabs(w[L.G[s] + e]); });
         const double m0 = f + pen;
-        double gd = 0.0;
-        for (int e = 0; e < L.L; ++e) gd += w[L.GF[s] + e] * w[L.QDXI + e];
+        const double gd =
+            ordered_sum<W>(0.0, L.L, scr, cap, [&](int e) { return w[L.GF[s] + e] * w[L.QDXI + e]; });
         const double dd = gd - pen;
         const int t = 1 - s;
         double a = 1.0, merit = 0.0, ft = 0.0;
@@ -1522,10 +1560,8 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_o
             if (st == G_DOMAIN) return SqpOut{false, G_DOMAIN};
             o.cnt->ls += 1;  // counted like K3: a trial that raises DomainError ends the solve uncounted
             tfin = st == G_OK;
-            if (tfin) {
-                merit = ft;
-                for (int e = 0; e < L.NN; ++e) merit += w[L.SIG + e] * fabs(w[L.G[t] + e]);
-            }
+            if (tfin)
+                merit = ordered_sum<W>(ft, L.NN, scr, cap, [&](int e) { return w[L.SIG + e] * fabs(w[L.G[t] + e]); });
             ok = dfinite(merit) && merit <= m0 + op.c1 * a * dd;
             if (ok || bt >= op.max_backtracks) break;
             a *= op.backtrack_factor;

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 300 python tools/prof_launch.py nmpc3 1184 3 60 generic_warp > gpurun_out/r02j_prof_plain.txt 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:nmpc_genw_kernel -s 1 -c 1 -o gpurun_out/r02j_k3w python tools/prof_launch.py nmpc3 1184 3 60 generic_warp > gpurun_out/r02j_ncu.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:pi_kernel -s 1 -c 1 -o gpurun_out/r02j_pi python tools/prof_launch.py pi 30000 720 > gpurun_out/r02j_ncu_pi.log 2>&1
