@@ -357,8 +357,18 @@ def run_ours(args):
         r = np.frombuffer(rec.cpu().numpy().tobytes(), dtype=abi.RECORD_DTYPE)
         return s, c, r
 
+    # final statistics: the library all-gathers the last timed step's records
+    # over NCCL (one rank: a device copy) and K4 reduces them on the device
+    last = W + K - 1
+    all_n = torch.empty(world * S * rec_sz, dtype=torch.uint8, device="cuda")
+    all_p = torch.empty(world * S * rec_sz, dtype=torch.uint8, device="cuda")
+    ctx.allgather_records(rec_n[last].data_ptr(), S, all_n.data_ptr())
+    ctx.allgather_records(rec_p[last].data_ptr(), S, all_p.data_ptr())
+    an, hn = ctx.aggregate_device(all_n.data_ptr(), world * S, bins=0)
+    ap_, _ = ctx.aggregate_device(all_p.data_ptr(), world * S)
+
     legs = {}
-    if not args.no_legs and rank == 0:
+    if not args.no_legs and rank == 0 and world == 1:  # single-GPU side measurements
         # PI at BASELINE configs 0 and 1 (one launch each); flops from the
         # counters (failed samples count the steps they ran)
         for name, kw, n in (("pi_config0", dict(controller="pi"), 1000),
@@ -380,16 +390,6 @@ def run_ours(args):
                           "achieved_tflops": workmodel.nmpc_flops(c, nx=nx) / s / 1e12,
                           "failed": int(r["failed"].sum()),
                           "note": "one launch of n samples (includes the final wave's drain)"}
-
-    # final statistics: the library all-gathers the last timed step's records
-    # over NCCL (one rank: a device copy) and K4 reduces them on the device
-    last = W + K - 1
-    all_n = torch.empty(world * S * rec_sz, dtype=torch.uint8, device="cuda")
-    all_p = torch.empty(world * S * rec_sz, dtype=torch.uint8, device="cuda")
-    ctx.allgather_records(rec_n[last].data_ptr(), S, all_n.data_ptr())
-    ctx.allgather_records(rec_p[last].data_ptr(), S, all_p.data_ptr())
-    an, hn = ctx.aggregate_device(all_n.data_ptr(), world * S, bins=0)
-    ap_, _ = ctx.aggregate_device(all_p.data_ptr(), world * S)
     stats = {"samples": world * S, "computed_by": "K4 on the device after the library's NCCL all-gather",
              "nmpc": {k: an[k] for k in ("n_failed", "mean", "variance", "ocp_solves", "ocp_failures",
                                          "ocp_success_pct")} | {"hist_bins": int(len(hn.counts))},
