@@ -332,6 +332,36 @@ int nmpcmc_gpu_solve_ocp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, i
                                double* lambda, double* pi_l, double* pi_u, int32_t* converged,
                                int32_t* status);
 
+/* SqpIterationLog (sqp.hpp:64-77): one record per SQP iteration, pushed
+ * where sqp_solve pushes it (sqp.cpp:274, :327, :350, :406). qp_status is
+ * NMPCMC_QP_OPTIMAL / _MAXITER / _FAILED. */
+typedef struct nmpcmc_sqp_iter_log {
+    double alpha;
+    double merit_before;
+    double merit_after;
+    double directional_derivative;
+    double grad_l_inf;   /* at iteration start */
+    double g_inf;        /* at iteration start */
+    double step_inf;     /* |alpha * delta_xi|_inf */
+    int32_t ls_evals;
+    int32_t qp_iterations;
+    int32_t qp_status;
+    int32_t armijo_exhausted;
+    int32_t bfgs_reset;
+    int32_t _pad;
+} nmpcmc_sqp_iter_log;
+/* The OCP service with SqpReport's per-iteration trace (SqpReport::trace,
+ * sqp.hpp:90) and iteration count: trace[b * max_trace ..] holds up to
+ * max_trace records of instance b, trace_len[b] the number sqp_solve pushed
+ * (may exceed max_trace; the excess is dropped), iterations[b] =
+ * SqpReport::iterations. HOST buffers; runs on K3w's code path for either
+ * controller model. Bitwise the reference's trace. */
+int nmpcmc_gpu_solve_ocp_batch_traced(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, int64_t batch,
+                                      const double* x0, const double* t0, const double* xi0, double* xi,
+                                      double* lambda, double* pi_l, double* pi_u, int32_t* converged,
+                                      int32_t* status, int32_t* iterations, int32_t max_trace,
+                                      nmpcmc_sqp_iter_log* trace, int32_t* trace_len);
+
 /* ---- Batched standalone stagewise QP ----------
  * solve_qp (qp.hpp:47-56, qp.cpp:173-423; mode 0) or riccati_factor_solve
  * (qp.hpp:42-45, qp.cpp:157-171; mode 1) for `batch` independent QPs of the

@@ -185,3 +185,24 @@ def sqp_solve_qnlp_batch(lib, problems, N, nx, opts, xi0=None):
     f(C.byref(d), Bn, problems.ctypes.data, None if x0p is None else x0p.ctypes.data,
       *(out[k].ctypes.data for k in ("xi", "lambda", "pi_l", "pi_u", "converged", "iterations", "status")))
     return out
+
+
+def solve_ocp_batch_traced(lib, sc, x0, t0, xi0=None, max_trace=32):
+    """The reference's sqp_solve on the regulator OcpProblem with
+    SqpReport::iterations and ::trace (nmpcmc_ref_solve_ocp_batch_traced)."""
+    from paper_2212_02197_b200 import qp as Q
+    x0 = np.ascontiguousarray(np.atleast_2d(x0), dtype=np.float64)
+    t0 = np.ascontiguousarray(t0, dtype=np.float64).reshape(-1)
+    B, nx, N = x0.shape[0], x0.shape[1], sc.N
+    L = N * (1 + nx)
+    out = dict(xi=np.zeros((B, L)), **{"lambda": np.zeros((B, N * nx))}, pi_l=np.zeros((B, N)),
+               pi_u=np.zeros((B, N)), converged=np.zeros(B, dtype=np.int32), status=np.zeros(B, dtype=np.int32),
+               iterations=np.zeros(B, dtype=np.int32), trace=np.zeros((B, max_trace), dtype=Q.SQP_LOG_DTYPE),
+               trace_len=np.zeros(B, dtype=np.int32))
+    x0p = None if xi0 is None else np.ascontiguousarray(xi0, dtype=np.float64)
+    f = lib.nmpcmc_ref_solve_ocp_batch_traced
+    f.argtypes = [C.POINTER(abi.Scenario), C.c_int64] + [C.c_void_p] * 10 + [C.c_int32, C.c_void_p, C.c_void_p]
+    f(C.byref(sc), B, x0.ctypes.data, t0.ctypes.data, None if x0p is None else x0p.ctypes.data,
+      *(out[k].ctypes.data for k in ("xi", "lambda", "pi_l", "pi_u", "converged", "status", "iterations")),
+      max_trace, out["trace"].ctypes.data, out["trace_len"].ctypes.data)
+    return out

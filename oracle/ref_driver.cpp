@@ -582,9 +582,27 @@ int nmpcmc_ref_solve_qp_batch(const nmpcmc_qp_dims* d, std::int64_t batch, const
 /// (controllers.cpp:134-145) and its cold start (controllers.cpp:166-185) when
 /// xi0 is NULL, else the given iterate with zero duals. status[b]: 0, or
 /// NMPCMC_DOMAIN_ERROR if a DomainError escaped.
+int nmpcmc_ref_solve_ocp_batch_traced(const nmpcmc_scenario* s, std::int64_t batch, const double* x0,
+                                      const double* t0, const double* xi0_in, double* xi_out, double* lam_out,
+                                      double* pil_out, double* piu_out, std::int32_t* converged,
+                                      std::int32_t* status, std::int32_t* iterations, std::int32_t max_trace,
+                                      nmpcmc_sqp_iter_log* trace, std::int32_t* trace_len);
+
 int nmpcmc_ref_solve_ocp_batch(const nmpcmc_scenario* s, std::int64_t batch, const double* x0, const double* t0,
                                const double* xi0_in, double* xi_out, double* lam_out, double* pil_out,
                                double* piu_out, std::int32_t* converged, std::int32_t* status) {
+    return nmpcmc_ref_solve_ocp_batch_traced(s, batch, x0, t0, xi0_in, xi_out, lam_out, pil_out, piu_out, converged,
+                                             status, nullptr, 0, nullptr, nullptr);
+}
+
+/// As nmpcmc_ref_solve_ocp_batch, plus SqpReport::iterations and the
+/// SqpReport::trace records (sqp.hpp:64-90) in the layout of
+/// nmpcmc_sqp_iter_log (any of the three may be NULL).
+int nmpcmc_ref_solve_ocp_batch_traced(const nmpcmc_scenario* s, std::int64_t batch, const double* x0,
+                                      const double* t0, const double* xi0_in, double* xi_out, double* lam_out,
+                                      double* pil_out, double* piu_out, std::int32_t* converged,
+                                      std::int32_t* status, std::int32_t* iterations, std::int32_t max_trace,
+                                      nmpcmc_sqp_iter_log* trace, std::int32_t* trace_len) {
     const int nx = nx_of(s->ctrl_variant), N = s->N, L = N * (1 + nx);
     SqpOptions opts;
     opts.eps = s->sqp.eps;
@@ -615,6 +633,8 @@ int nmpcmc_ref_solve_ocp_batch(const nmpcmc_scenario* s, std::int64_t batch, con
         std::fill(pil_out + b * N, pil_out + (b + 1) * N, 0.0);
         std::fill(piu_out + b * N, piu_out + (b + 1) * N, 0.0);
         converged[b] = 0;
+        if (iterations) iterations[b] = 0;
+        if (trace_len) trace_len[b] = 0;
         try {
             const OcpProblem problem(std::move(nlp));
             Vec xi0;
@@ -634,6 +654,25 @@ int nmpcmc_ref_solve_ocp_batch(const nmpcmc_scenario* s, std::int64_t batch, con
                 }
             }
             const SqpReport rep = sqp_solve(problem, xi0, opts, SqpWarmStart{});
+            if (iterations) iterations[b] = rep.iterations;
+            if (trace_len) trace_len[b] = static_cast<std::int32_t>(rep.trace.size());
+            for (std::size_t q = 0; trace && q < rep.trace.size() && q < static_cast<std::size_t>(max_trace); ++q) {
+                const SqpIterationLog& lg = rep.trace[q];
+                nmpcmc_sqp_iter_log& d = trace[b * max_trace + static_cast<std::int64_t>(q)];
+                d = nmpcmc_sqp_iter_log{};
+                d.alpha = lg.alpha;
+                d.merit_before = lg.merit_before;
+                d.merit_after = lg.merit_after;
+                d.directional_derivative = lg.directional_derivative;
+                d.grad_l_inf = lg.grad_l_inf;
+                d.g_inf = lg.g_inf;
+                d.step_inf = lg.step_inf;
+                d.ls_evals = lg.ls_evals;
+                d.qp_iterations = lg.qp_iterations;
+                d.qp_status = static_cast<std::int32_t>(lg.qp_status);
+                d.armijo_exhausted = lg.armijo_exhausted ? 1 : 0;
+                d.bfgs_reset = lg.bfgs_reset ? 1 : 0;
+            }
             std::copy(rep.xi.begin(), rep.xi.end(), xo);
             std::copy(rep.lambda.begin(), rep.lambda.end(), lam_out + b * N * nx);
             std::copy(rep.pi_l.begin(), rep.pi_l.end(), pil_out + b * N);

@@ -267,4 +267,77 @@ int nmpcmc_gpu_sqp_solve_qnlp_batch(nmpcmc_gpu_ctx* ctx, const nmpcmc_qnlp_dims*
     return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "qnlp_batch_kernel");
 }
 
+int nmpcmc_gpu_solve_ocp_batch_traced(nmpcmc_gpu_ctx* ctx, const nmpcmc_scenario* sc, int64_t batch,
+                                      const double* x0, const double* t0, const double* xi0, double* xi,
+                                      double* lambda, double* pi_l, double* pi_u, int32_t* converged,
+                                      int32_t* status, int32_t* iterations, int32_t max_trace,
+                                      nmpcmc_sqp_iter_log* trace, int32_t* trace_len) {
+    if (ctx == nullptr || sc == nullptr || batch < 0 || max_trace < 0) return NMPCMC_INVALID_ARGUMENT;
+    if (batch > 0 && (!x0 || !t0 || !xi || !lambda || !pi_l || !pi_u || !converged || !status || !iterations ||
+                      !trace_len || (max_trace > 0 && !trace)))
+        return NMPCMC_INVALID_ARGUMENT;
+    if (sc->controller != NMPCMC_CTRL_NMPC) return fail(ctx, NMPCMC_INVALID_ARGUMENT, "OCP batch: NMPC scenario");
+    int32_t nbar = 0;
+    int rc = nmpcmc_gpu_validate(sc, &nbar);
+    if (rc != NMPCMC_OK) return fail(ctx, rc, "scenario validation failed");
+    if (batch == 0) return NMPCMC_OK;
+    if (!nmpcmc_launch::genw_fits(*sc))
+        return fail(ctx, NMPCMC_UNSUPPORTED, "OCP batch: horizon too long for the shared-memory sweep arrays");
+    cudaSetDevice(ctx->device);
+    const int nx = nx_of(*sc);
+    const int64_t L = (int64_t)sc->N * (1 + nx), NN = (int64_t)sc->N * nx;
+    const size_t b_x0 = batch * nx * 8, b_t0 = batch * 8, b_xi = batch * L * 8, b_lam = batch * NN * 8,
+                 b_pi = batch * sc->N * 8, b_i = batch * 4, b_tr = (size_t)batch * max_trace * sizeof(nmpcmc_sqp_iter_log);
+    auto rnd = [](size_t n) { return (n + 255) / 256 * 256; };
+    const size_t total = rnd(b_x0) + rnd(b_t0) + (xi0 ? rnd(b_xi) : 0) + rnd(b_xi) + rnd(b_lam) + 2 * rnd(b_pi) +
+                         4 * rnd(b_i) + rnd(b_tr);
+    if ((rc = ensure(ctx, &ctx->d_scratch, &ctx->scratch_cap, total)) != NMPCMC_OK) return rc;
+    char* p = static_cast<char*>(ctx->d_scratch);
+    auto take = [&](size_t n) {
+        char* a = p;
+        p += rnd(n);
+        return a;
+    };
+    auto* d_x0 = reinterpret_cast<double*>(take(b_x0));
+    auto* d_t0 = reinterpret_cast<double*>(take(b_t0));
+    auto* d_xi0 = xi0 ? reinterpret_cast<double*>(take(b_xi)) : nullptr;
+    auto* d_xi = reinterpret_cast<double*>(take(b_xi));
+    auto* d_lam = reinterpret_cast<double*>(take(b_lam));
+    auto* d_pil = reinterpret_cast<double*>(take(b_pi));
+    auto* d_piu = reinterpret_cast<double*>(take(b_pi));
+    auto* d_conv = reinterpret_cast<int32_t*>(take(b_i));
+    auto* d_st = reinterpret_cast<int32_t*>(take(b_i));
+    auto* d_it = reinterpret_cast<int32_t*>(take(b_i));
+    auto* d_tl = reinterpret_cast<int32_t*>(take(b_i));
+    auto* d_tr = max_trace > 0 ? reinterpret_cast<nmpcmc_sqp_iter_log*>(take(b_tr)) : nullptr;
+    const int64_t blocks = nmpcmc_launch::genw_blocks(*sc, ctx->sm_count, batch);
+    const size_t ws_b = (size_t)blocks * (size_t)nmpcmc_launch::gen_ws_doubles(*sc) * sizeof(double);
+    if ((rc = ensure(ctx, &ctx->d_ws, &ctx->ws_cap, ws_b)) != NMPCMC_OK) return rc;
+    if ((rc = ensure(ctx, &ctx->d_counter, &ctx->counter_cap, 256)) != NMPCMC_OK) return rc;
+    cudaError_t e = cudaMemcpyAsync(d_x0, x0, b_x0, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_t0, t0, b_t0, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess && xi0) e = cudaMemcpyAsync(d_xi0, xi0, b_xi, cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "cudaMemcpyAsync");
+    // the trace buffer pointer is non-null even when max_trace == 0, so the
+    // kernel still counts the records into trace_len
+    nmpcmc_sqp_iter_log* tr_arg = d_tr != nullptr ? d_tr : reinterpret_cast<nmpcmc_sqp_iter_log*>(d_tl);
+    rc = nmpcmc_launch::launch_ocp_batch(*sc, batch, d_x0, d_t0, d_xi0, d_xi, d_lam, d_pil, d_piu, d_conv, d_st,
+                                         static_cast<double*>(ctx->d_ws), blocks,
+                                         static_cast<unsigned long long*>(ctx->d_counter), ctx->stream, d_it,
+                                         max_trace, tr_arg, d_tl);
+    if (rc != NMPCMC_OK) return fail(ctx, rc, "OCP batch: unsupported configuration");
+    if ((rc = cuda_check(ctx, cudaGetLastError(), "ocp_batch_kernel launch")) != NMPCMC_OK) return rc;
+    e = cudaMemcpyAsync(xi, d_xi, b_xi, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(lambda, d_lam, b_lam, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pi_l, d_pil, b_pi, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(pi_u, d_piu, b_pi, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(converged, d_conv, b_i, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(status, d_st, b_i, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(iterations, d_it, b_i, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(trace_len, d_tl, b_i, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess && d_tr) e = cudaMemcpyAsync(trace, d_tr, b_tr, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "cudaMemcpyAsync");
+    return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "ocp_batch_kernel");
+}
+
 }  // extern "C"

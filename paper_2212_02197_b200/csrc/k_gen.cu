@@ -30,9 +30,10 @@ int launch_gen(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, n
 
 int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const double* x0, const double* t0, const double* xi0,
                      double* xi, double* lam, double* pil, double* piu, int32_t* conv, int32_t* status, double* ws,
-                     int64_t blocks, unsigned long long* counter, cudaStream_t stream) {
+                     int64_t blocks, unsigned long long* counter, cudaStream_t stream, int32_t* iters, int max_trace,
+                     nmpcmc_sqp_iter_log* trace, int32_t* trace_len) {
     return nmpcmc_dev::gen::launch_ocp_batch(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv, status, ws, blocks,
-                                             counter, stream);
+                                             counter, stream, iters, max_trace, trace, trace_len);
 }
 
 int64_t qnlp_stride(int N, int nx) { return nmpcmc_dev::gen::qnlp_stride(N, nx); }

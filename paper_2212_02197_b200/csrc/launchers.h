@@ -38,7 +38,8 @@ int launch_gen(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, n
                unsigned long long* counter, cudaStream_t stream);
 int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const double* x0, const double* t0, const double* xi0,
                      double* xi, double* lam, double* pil, double* piu, int32_t* conv, int32_t* status, double* ws,
-                     int64_t blocks, unsigned long long* counter, cudaStream_t stream);
+                     int64_t blocks, unsigned long long* counter, cudaStream_t stream, int32_t* iters = nullptr,
+                     int max_trace = 0, nmpcmc_sqp_iter_log* trace = nullptr, int32_t* trace_len = nullptr);
 
 // ---- controller-level API: batched nmpc_step on K3w's path (k_gen.cu)
 int64_t nmpc_state_doubles(const nmpcmc_scenario& sc);

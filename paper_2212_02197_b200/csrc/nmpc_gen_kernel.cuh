@@ -467,6 +467,11 @@ struct Ocp {
     /// packed data of one stagewise quadratic NLP (QNLP below). A new kind is
     /// added by giving objective() and constraints() one more branch.
     const double* prob = nullptr;
+    /// SqpReport::trace (sqp.hpp:64-90) of the next sqp_solve: up to
+    /// trace_cap SqpIterationLog records (null: no trace), count in *trace_len.
+    nmpcmc_sqp_iter_log* trace = nullptr;
+    int trace_cap = 0;
+    int32_t* trace_len = nullptr;
 };
 
 // --------------------------------------------- quadratic stagewise NLP kind
@@ -1151,7 +1156,7 @@ __device__ __forceinline__ double inf_fold(double m, double x) { return smax(m, 
 /// solve_qp (qp.cpp:173-423): Mehrotra predictor-corrector interior point.
 /// Result in QDXI, QMU, QNL, QNU.
 template <int NX, int W>
-__device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_iter) {
+__device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_iter, int* iters_out = nullptr) {
     const Ocp<NX, W>& o = *v.o;
     const WsT<W> w = o.ws;
     const Layout<NX> L = o.lay;
@@ -1217,8 +1222,9 @@ __device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_
     }
     Lanes<W>::sync();
     int status = QP_FAILED;
+    int it = 0;  // completed iterations (QpSolution::iterations, qp.cpp:410)
 #pragma unroll 1
-    for (int it = 0;; ++it) {
+    for (;; ++it) {
         qp_resid<NX, W>(v);
         double gap = 0.0;
         if (m > 0) {  // ordered sums: products lane-parallel, sums serial on every lane
@@ -1351,6 +1357,7 @@ __device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_
         x = smin(smax(x, v.lb(k)), v.ub(k));
     }
     Lanes<W>::sync();
+    if (iters_out) *iters_out = it;
     return status;
 }
 
@@ -1387,7 +1394,7 @@ __device__ void add_jt(const Ocp<NX, W>& o, int s, int LAMo, int H) {
 /// then check_convergence (sqp.cpp:86-96).
 template <int NX, int W>
 __device__ __noinline__ bool kkt_ok(const Ocp<NX, W>& o, int s, int LAMo, int PLo, int PUo, int m,
-                                    double eps) {
+                                    double eps, double* gl_out = nullptr, double* gg_out = nullptr) {
     const WsT<W> w = o.ws;
     const Layout<NX> L = o.lay;
     const int lane = Lanes<W>::lane();
@@ -1412,6 +1419,8 @@ __device__ __noinline__ bool kkt_ok(const Ocp<NX, W>& o, int s, int LAMo, int PL
     for (int e = lane; e < L.NN; e += W) gg = inf_fold(gg, w[L.G[s] + e]);
     gl = Lanes<W>::max_fold(gl);
     gg = Lanes<W>::max_fold(gg);
+    if (gl_out) *gl_out = gl;  // rep.grad_l_inf / rep.g_inf (sqp.cpp:249-250)
+    if (gg_out) *gg_out = gg;
     return gl / sd <= eps && gg <= eps;
 }
 
@@ -1503,22 +1512,48 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_o
         if (st != G_OK) return SqpOut{false, G_OK};
     }
     bool first = true;
+    // SqpIterationLog records (sqp.hpp:64-77) when a trace buffer is given;
+    // pushed where sqp.cpp pushes them (:274, :327, :350, :406)
+    int n_log = 0;
+    nmpcmc_sqp_iter_log lg{};
+    auto push_log = [&]() {
+        if (o.trace != nullptr && n_log < o.trace_cap && lane == 0) o.trace[n_log] = lg;
+        ++n_log;
+    };
+    auto finish_log = [&]() {
+        if (o.trace_len != nullptr && lane == 0) *o.trace_len = n_log;
+    };
 #pragma unroll 1
     for (int it = 0;; ++it) {
-        if (kkt_ok<NX, W>(o, s, L.LAM, L.PL, L.PU, m, op.eps)) return SqpOut{true, G_OK};
+        double gl0 = 0.0, gg0 = 0.0;
+        if (kkt_ok<NX, W>(o, s, L.LAM, L.PL, L.PU, m, op.eps, &gl0, &gg0)) {
+            finish_log();
+            return SqpOut{true, G_OK};
+        }
         if (it >= op.max_iter) break;
+        lg = nmpcmc_sqp_iter_log{};
+        lg.qp_status = QP_FAILED;
+        lg.grad_l_inf = gl0;
+        lg.g_inf = gg0;
         o.cnt->sqp_stage += N;
         const QpView<NX, W> v(&o, s);
-        int qs = solve_qp<NX, W>(v, op.qp_tol, op.qp_max_iter);
+        int qit = 0;
+        int qs = solve_qp<NX, W>(v, op.qp_tol, op.qp_max_iter, &qit);
         o.cnt->qp += 1;
         if (qs == QP_DOMAIN) return SqpOut{false, G_DOMAIN};
         if (qs == QP_FAILED) {
             identity_blocks<NX, W>(o);
-            qs = solve_qp<NX, W>(v, op.qp_tol, op.qp_max_iter);
+            lg.bfgs_reset = 1;
+            qs = solve_qp<NX, W>(v, op.qp_tol, op.qp_max_iter, &qit);
             o.cnt->qp += 1;
             if (qs == QP_DOMAIN) return SqpOut{false, G_DOMAIN};
-            if (qs == QP_FAILED) break;
+            if (qs == QP_FAILED) {
+                push_log();
+                break;
+            }
         }
+        lg.qp_iterations = qit;
+        lg.qp_status = qs;
         if (kkt_ok<NX, W>(o, s, L.QMU, L.QNL, L.QNU, m, op.eps)) {
             for (int e = lane; e < L.NN; e += W) w[L.LAM + e] = w[L.QMU + e];
 #pragma unroll 1
@@ -1527,6 +1562,7 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_o
                 w[L.PU + k] = w[L.QNU + k];
             }
             Lanes<W>::sync();
+            finish_log();
             return SqpOut{true, G_OK};
         }
         // merit_weights_update (sqp.cpp:12-20)
@@ -1550,6 +1586,7 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_o
         const int t = 1 - s;
         double a = 1.0, merit = 0.0, ft = 0.0;
         bool ok = false, tfin = false;
+        int evals = 0;
 #pragma unroll 1
         for (int bt = 0;; ++bt) {
             for (int e = lane; e < L.L; e += W) w[L.XI[t] + e] = w[L.XI[s] + e] + a * w[L.QDXI + e];
@@ -1559,6 +1596,7 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_o
             const int st = constraints<NX, W>(o, t);
             if (st == G_DOMAIN) return SqpOut{false, G_DOMAIN};
             o.cnt->ls += 1;  // counted like K3: a trial that raises DomainError ends the solve uncounted
+            ++evals;
             tfin = st == G_OK;
             if (tfin)
                 merit = ordered_sum<W>(ft, L.NN, scr, cap, [&](int e) { return w[L.SIG + e] * fabs(w[L.G[t] + e]); });
@@ -1566,8 +1604,25 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_o
             if (ok || bt >= op.max_backtracks) break;
             a *= op.backtrack_factor;
         }
-        if (!ok && !dfinite(merit)) break;
-        if (!tfin) break;  // the re-evaluation at xn would throw NonFiniteState
+        lg.alpha = a;
+        lg.merit_before = m0;
+        lg.merit_after = merit;
+        lg.directional_derivative = dd;
+        lg.ls_evals = evals;
+        lg.armijo_exhausted = ok ? 0 : 1;
+        if (!ok && !dfinite(merit)) {
+            push_log();
+            break;
+        }
+        if (o.trace != nullptr) {  // step_inf = max |alpha dxi| (std::max: NaN ignored)
+            double si = 0.0;
+            for (int e = lane; e < L.L; e += W) si = inf_fold(si, a * w[L.QDXI + e]);
+            lg.step_inf = Lanes<W>::max_fold(si);
+        }
+        if (!tfin) {  // the re-evaluation at xn would throw NonFiniteState
+            push_log();
+            break;
+        }
         // duals (sqp.cpp:355-364)
         for (int e = lane; e < L.NN; e += W) w[L.LAM + e] += a * (w[L.QMU + e] - w[L.LAM + e]);
 #pragma unroll 1
@@ -1599,12 +1654,17 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_o
         }
         lost = Lanes<W>::any(lost);
         Lanes<W>::sync();
-        if (lost) identity_blocks<NX, W>(o);
+        if (lost) {
+            identity_blocks<NX, W>(o);
+            lg.bfgs_reset = 1;
+        }
         f = ft;
         s = t;
         *cur = s;
         o.cnt->sqp += 1;  // completed SQP steps, as K3 counts them
+        push_log();
     }
+    finish_log();
     return SqpOut{false, G_OK};
 }
 
@@ -2062,7 +2122,9 @@ __global__ void __launch_bounds__(32) ocp_batch_kernel(const __grid_constant__ n
                                                        const double* x0, const double* t0, const double* xi0,
                                                        double* xi_out, double* lam_out, double* pil_out,
                                                        double* piu_out, int32_t* converged, int32_t* status,
-                                                       double* ws_all, int64_t slab, unsigned long long* next) {
+                                                       double* ws_all, int64_t slab, unsigned long long* next,
+                                                       int32_t* iters_out, int max_trace,
+                                                       nmpcmc_sqp_iter_log* trace, int32_t* trace_len) {
     const WsT<32> ws{ws_all + (int64_t)blockIdx.x * slab, 1};
     const int lane = Lanes<32>::lane();
 #pragma unroll 1
@@ -2080,6 +2142,12 @@ __global__ void __launch_bounds__(32) ocp_batch_kernel(const __grid_constant__ n
         const int N = o.N;
 #pragma unroll
         for (int i = 0; i < NX; ++i) o.x0[i] = x0[b * NX + i];
+        if (trace != nullptr) {
+            o.trace = trace + b * max_trace;
+            o.trace_cap = max_trace;
+            o.trace_len = trace_len + b;
+            if (lane == 0) trace_len[b] = 0;
+        }
         for (int k = lane; k < N; k += 32) ws[L.SP + k] = setpoint_at(sc, t0[b] + (k + 1) * sc.Ts);
         int st = G_OK;
         if (xi0 != nullptr) {
@@ -2115,6 +2183,7 @@ __global__ void __launch_bounds__(32) ocp_batch_kernel(const __grid_constant__ n
         if (lane == 0) {
             converged[b] = ok && so.converged ? 1 : 0;
             status[b] = ok ? 0 : so.status;
+            if (iters_out != nullptr) iters_out[b] = (int32_t)cnt.sqp;
         }
         Lanes<32>::sync();
     }
@@ -2123,7 +2192,8 @@ __global__ void __launch_bounds__(32) ocp_batch_kernel(const __grid_constant__ n
 inline int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const double* x0, const double* t0,
                             const double* xi0, double* xi, double* lam, double* pil, double* piu, int32_t* conv,
                             int32_t* status, double* ws, int64_t blocks, unsigned long long* counter,
-                            cudaStream_t stream) {
+                            cudaStream_t stream, int32_t* iters = nullptr, int max_trace = 0,
+                            nmpcmc_sqp_iter_log* trace = nullptr, int32_t* trace_len = nullptr) {
     const bool c3 = sc.ctrl_variant == NMPCMC_THREE_STATE;
     const int64_t slab = c3 ? Layout<3>(sc.N).total : Layout<1>(sc.N).total;
     const size_t smem = c3 ? sweep_smem_bytes<3>(sc.N) : sweep_smem_bytes<1>(sc.N);
@@ -2131,10 +2201,12 @@ inline int launch_ocp_batch(const nmpcmc_scenario& sc, int64_t batch, const doub
     cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
     if (c3)
         ocp_batch_kernel<3><<<(unsigned)blocks, 32, smem, stream>>>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv,
-                                                                    status, ws, slab, counter);
+                                                                    status, ws, slab, counter, iters, max_trace,
+                                                                    trace, trace_len);
     else
         ocp_batch_kernel<1><<<(unsigned)blocks, 32, smem, stream>>>(sc, batch, x0, t0, xi0, xi, lam, pil, piu, conv,
-                                                                    status, ws, slab, counter);
+                                                                    status, ws, slab, counter, iters, max_trace,
+                                                                    trace, trace_len);
     return NMPCMC_OK;
 }
 

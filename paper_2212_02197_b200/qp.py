@@ -267,3 +267,48 @@ def solve_qnlp_batch(problems, N: int, nx: int, opts: abi.SqpOptions = None, xi0
         ctx.handle, C.byref(d), C.c_int64(Bn), problems.ctypes.data, None if xi0 is None else xi0.ctypes.data,
         *(out[k].ctypes.data for k in ("xi", "lambda", "pi_l", "pi_u", "converged", "iterations", "status"))))
     return out
+
+
+
+# ------------------------------------------------ SQP trace (SqpIterationLog)
+SQP_LOG_DTYPE = np.dtype([("alpha", "<f8"), ("merit_before", "<f8"), ("merit_after", "<f8"),
+                          ("directional_derivative", "<f8"), ("grad_l_inf", "<f8"), ("g_inf", "<f8"),
+                          ("step_inf", "<f8"), ("ls_evals", "<i4"), ("qp_iterations", "<i4"), ("qp_status", "<i4"),
+                          ("armijo_exhausted", "<i4"), ("bfgs_reset", "<i4"), ("_pad", "<i4")])
+assert SQP_LOG_DTYPE.itemsize == 80
+
+
+def solve_ocp_batch_traced(sc, x0, t0, xi0=None, max_trace=32, ctx=None) -> dict:
+    """solve_ocp_batch plus SqpReport::iterations and the per-iteration
+    SqpIterationLog trace (sqp.hpp:64-90): trace (B, max_trace) records of
+    SQP_LOG_DTYPE, trace_len (B,) (nmpcmc_gpu_solve_ocp_batch_traced)."""
+    nx, N = (3 if sc.ctrl_variant == abi.THREE_STATE else 1), sc.N
+    L = N * (1 + nx)
+    x0 = np.asarray(x0, dtype=np.float64)
+    if x0.ndim == 1 and nx == 1:
+        x0 = x0.reshape(-1, 1)
+    if x0.ndim != 2 or x0.shape[1] != nx:
+        raise engine.LengthMismatch(f"solve_ocp_batch_traced: x0 must have shape (B, {nx}), got {x0.shape}")
+    x0 = np.ascontiguousarray(x0)
+    B = x0.shape[0]
+    t0 = np.ascontiguousarray(t0, dtype=np.float64).reshape(-1)
+    if t0.size != B:
+        raise engine.LengthMismatch(f"solve_ocp_batch_traced: t0 needs {B} entries, got {t0.size}")
+    if xi0 is not None:
+        xi0 = np.ascontiguousarray(xi0, dtype=np.float64)
+        if xi0.shape != (B, L):
+            raise engine.LengthMismatch(f"solve_ocp_batch_traced: xi0 must have shape ({B}, {L})")
+    out = dict(xi=np.zeros((B, L)), **{"lambda": np.zeros((B, N * nx))}, pi_l=np.zeros((B, N)),
+               pi_u=np.zeros((B, N)), converged=np.zeros(B, dtype=np.int32), status=np.zeros(B, dtype=np.int32),
+               iterations=np.zeros(B, dtype=np.int32), trace=np.zeros((B, max_trace), dtype=SQP_LOG_DTYPE),
+               trace_len=np.zeros(B, dtype=np.int32))
+    ctx = ctx or engine._context(0)
+    lib = ctx.lib
+    lib.nmpcmc_gpu_solve_ocp_batch_traced.argtypes = ([C.c_void_p, C.POINTER(abi.Scenario), C.c_int64] +
+                                                       [C.c_void_p] * 10 + [C.c_int32, C.c_void_p, C.c_void_p])
+    ctx._check(lib.nmpcmc_gpu_solve_ocp_batch_traced(
+        ctx.handle, C.byref(sc), C.c_int64(B), x0.ctypes.data, t0.ctypes.data,
+        None if xi0 is None else xi0.ctypes.data,
+        *(out[k].ctypes.data for k in ("xi", "lambda", "pi_l", "pi_u", "converged", "status", "iterations")),
+        int(max_trace), out["trace"].ctypes.data, out["trace_len"].ctypes.data))
+    return out

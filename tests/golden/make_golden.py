@@ -283,6 +283,27 @@ def gen_fd():
             O.ref(libm).nmpcmc_ref_set_ctrl_fd(0)
 
 
+def gen_trace():
+    """SqpReport::iterations and ::trace (SqpIterationLog, sqp.hpp:64-90) of
+    the reference's sqp_solve on the OCP fixtures' instances (ocp_batch.npz),
+    cold and warm."""
+    d = np.load(os.path.join(OUT, "ocp_batch.npz"))
+    out = {}
+    for tag in ("one", "three"):
+        kw = json.loads(str(d[f"{tag}__kwargs"]))
+        sc = configs.make_scenario(**kw)
+        x0, t0, xi0 = d[f"{tag}__x0"], d[f"{tag}__t0"], d[f"{tag}__xi0"]
+        for start in ("cold", "warm"):
+            r = O.solve_ocp_batch_traced(O.ref("xlibm"), sc, x0, t0, xi0=xi0 if start == "warm" else None,
+                                         max_trace=24)
+            for k, v in r.items():
+                out[f"{tag}__{start}_{k}"] = v
+            print(f"trace {tag} {start}: iterations mean {r['iterations'].mean():.1f}, records {r['trace_len'].sum()}, "
+                  f"bfgs resets {int(r['trace']['bfgs_reset'].sum())}, exhausted {int(r['trace']['armijo_exhausted'].sum())}")
+        out[f"{tag}__kwargs"] = np.array(json.dumps(kw))
+    np.savez_compressed(os.path.join(OUT, "ocp_trace.npz"), **out)
+
+
 def main(which):
     if which in ("rng", "all"):
         gen_rng()
@@ -313,6 +334,8 @@ def main(which):
         gen_qnlp()
     if which in ("fd", "all"):
         gen_fd()
+    if which in ("trace", "all"):
+        gen_trace()
     if which in ("nmpc3", "all"):
         # three-state controller model (config 2 read literally: CD-EKF and
         # OCP on the 3-state CSTR; ctrl_variant 0 = THREE_STATE) -> kernel K3g
