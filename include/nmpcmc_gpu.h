@@ -173,7 +173,15 @@ const char* nmpcmc_gpu_last_error(const nmpcmc_gpu_ctx* ctx);
  * identical; only speed differs. NMPCMC_OPT_TPS_WARPS_PER_SM is accepted and
  * ignored (it tuned K3b). */
 enum { NMPCMC_OPT_NMPC_KERNEL = 1, NMPCMC_OPT_TPS_WARPS_PER_SM = 2, NMPCMC_OPT_LANES = 3,
-       NMPCMC_OPT_CTRL_JACOBIANS = 4 };
+       NMPCMC_OPT_CTRL_JACOBIANS = 4, NMPCMC_OPT_PI_KERNEL = 5 };
+/* NMPCMC_OPT_PI_KERNEL selects the PI closed-loop kernel. AUTO (default) =
+ * the warp-specialised kernel (one consumer warp of 32 samples, producer warps
+ * generating the normals ahead; 7 producers when the batch leaves SMs idle,
+ * else 3) whenever a control step reads at most 40 normals, else the
+ * lanes kernel; LANES = one thread (or 4 lanes, small batches) per sample
+ * with the normals in a per-sample window; WS3 / WS7 = the warp-specialised
+ * kernel with 3 / 7 producer warps. Results are bitwise identical. */
+enum { NMPCMC_PI_KERNEL_AUTO = 0, NMPCMC_PI_KERNEL_LANES = 1, NMPCMC_PI_KERNEL_WS3 = 3, NMPCMC_PI_KERNEL_WS7 = 7 };
 /* NMPCMC_OPT_CTRL_JACOBIANS: how the controller model's jacobians are formed.
  * ANALYTIC (default) = the closed forms make_cstr_model installs
  * (cstr.cpp:86-127). FD = as a Model WITHOUT analytic jacobians:

@@ -62,6 +62,7 @@ struct nmpcmc_gpu_ctx {
     int ctrl_fd = 0;                            // NMPCMC_OPT_CTRL_JACOBIANS: 1 = finite differences
     cudaStream_t own = nullptr;                 // the stream ctx_create made (set_stream may replace ctx->stream)
     int lanes = 1;                              // NMPCMC_OPT_LANES
+    int pi_kernel = NMPCMC_PI_KERNEL_AUTO;      // NMPCMC_OPT_PI_KERNEL
     int next_nmpc_lane = 0;
     Lane lane[3];
     cudaEvent_t fork = nullptr;

@@ -336,9 +336,11 @@ __device__ __forceinline__ double measure(const Cstr& p, const Plant<NX>& pl, bo
 /// drawn but skipped and taken as 0. Bitwise the same states: in the gemv
 /// below their terms are (+-0) * dw in every row, the row sums start at +0.0,
 /// and +0 + (+-0) = +0, so no row depends on dw_A or dw_B.
-template <int NX, class Rng, bool SPARSE = false>
-__device__ __forceinline__ int simulate_interval(const Cstr& p, Plant<NX>& pl, double t0, double t1,
-                                                 double u, int ns, Rng& rng) {
+/// simulate_interval_d: the same with the drift supplied by the caller,
+/// drift(x, u, dn) -> status (simulate_interval passes drift3 / drift1).
+template <int NX, class Rng, bool SPARSE, class Drift>
+__device__ __forceinline__ int simulate_interval_d(const Cstr& p, Plant<NX>& pl, double t0, double t1,
+                                                   double u, int ns, Rng& rng, const Drift& drift) {
     const double dt = (t1 - t0) / ns;
     const double sqrt_dt = sqrt(dt);
     const double f = u * kMlMinToLs;
@@ -364,11 +366,7 @@ __device__ __forceinline__ int simulate_interval(const Cstr& p, Plant<NX>& pl, d
             dw[j] = sqrt_dt * rng.normal();
         }
         double dn[NX];
-        int st;
-        if (NX == 3)
-            st = drift3(p, pl.x, u, dn);
-        else
-            st = drift1(p, pl.x[0], u, dn);
+        const int st = drift(pl.x, u, dn);
         if (st != ST_OK) return st;
         double next[NX];
 #pragma unroll
@@ -387,6 +385,16 @@ __device__ __forceinline__ int simulate_interval(const Cstr& p, Plant<NX>& pl, d
         for (int i = 0; i < NX; ++i) pl.x[i] = next[i];
     }
     return ST_OK;
+}
+
+template <int NX, class Rng, bool SPARSE = false>
+__device__ __forceinline__ int simulate_interval(const Cstr& p, Plant<NX>& pl, double t0, double t1,
+                                                 double u, int ns, Rng& rng) {
+    return simulate_interval_d<NX, Rng, SPARSE>(p, pl, t0, t1, u, ns, rng,
+                                                [&](const double* x, double uu, double* dn) -> int {
+                                                    if (NX == 3) return drift3(p, x, uu, dn);
+                                                    return drift1(p, x[0], uu, dn);
+                                                });
 }
 
 }  // namespace nmpcmc_dev

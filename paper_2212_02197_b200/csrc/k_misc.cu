@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, 
 namespace nmpcmc_launch {
 
 int launch_pi(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
-              nmpcmc_work_counters* d_cnt, double* d_traj, int rows, int sm_count, cudaStream_t stream) {
+              nmpcmc_work_counters* d_cnt, double* d_traj, int rows, int sm_count, int pi_kernel,
+              cudaStream_t stream) {
     // several lanes per sample for batches too small to fill the GPU with one
     // thread per sample (about 4 warps per SM), when one control step's
     // normals fit one window refill (the lanes keep the warp in lockstep,
@@ -82,6 +83,50 @@ int launch_pi(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nm
     constexpr int G = nmpcmc_dev::kPiLanes, block = nmpcmc_dev::kPiBlock;
     const bool three = sc.truth_variant == NMPCMC_THREE_STATE;
     const int per_step = (sc.has_noise_R != 0 ? 1 : 0) + sc.Ns * (three ? 3 : 1);
+    // warp-specialised kernel (K2ws): one consumer warp of 32 samples per
+    // block, P producer warps generating the normals ahead; more producers
+    // when the batch leaves SMs idle
+#ifndef NMPCMC_PI_WS
+#define NMPCMC_PI_WS 1
+#endif
+    const bool sparse = three && sc.truth.sigmaA == 0.0 && sc.truth.sigmaB == 0.0;
+    const int reads = nmpcmc_dev::pi_ws_reads(sc, sparse);
+    if (NMPCMC_PI_WS != 0 && pi_kernel != NMPCMC_PI_KERNEL_LANES && reads <= nmpcmc_dev::kPiWsMaxPerStep &&
+        nbar > 0) {
+        const int64_t blocks = (n + 31) / 32;
+        const int P = pi_kernel == NMPCMC_PI_KERNEL_WS3 || pi_kernel == NMPCMC_PI_KERNEL_WS7
+                          ? pi_kernel
+                          : (NMPCMC_PI_WS > 1 ? NMPCMC_PI_WS : (blocks >= 2 * (int64_t)sm_count ? 3 : 7));
+        const size_t smem = (size_t)nmpcmc_dev::kPiWsSlots * reads * 32 * sizeof(double);
+        const unsigned grid = (unsigned)blocks;
+        // the whole grid is one wave only if the shared-memory carveout
+        // admits the register-limited block count (the default carveout
+        // capped it at 5 blocks per SM: 1.58 waves at config 1)
+#define NMPCMC_PI_WS_LAUNCH(NX, PP, SP)                                                                    \
+    do {                                                                                                    \
+        cudaFuncSetAttribute(nmpcmc_dev::pi_ws_kernel<NX, PP, SP>, cudaFuncAttributePreferredSharedMemoryCarveout, \
+                             cudaSharedmemCarveoutMaxShared);                                               \
+        nmpcmc_dev::pi_ws_kernel<NX, PP, SP><<<grid, 32 * (1 + PP), smem, stream>>>(sc, first, n, nbar, d_rec, \
+                                                                                    d_cnt, d_traj, rows);   \
+    } while (0)
+        if (P == 3) {
+            if (!three)
+                NMPCMC_PI_WS_LAUNCH(1, 3, false);
+            else if (sparse)
+                NMPCMC_PI_WS_LAUNCH(3, 3, true);
+            else
+                NMPCMC_PI_WS_LAUNCH(3, 3, false);
+        } else {
+            if (!three)
+                NMPCMC_PI_WS_LAUNCH(1, 7, false);
+            else if (sparse)
+                NMPCMC_PI_WS_LAUNCH(3, 7, true);
+            else
+                NMPCMC_PI_WS_LAUNCH(3, 7, false);
+        }
+#undef NMPCMC_PI_WS_LAUNCH
+        return NMPCMC_OK;
+    }
 #ifndef NMPCMC_PI_SMALL_WARPS
 #define NMPCMC_PI_SMALL_WARPS 4
 #endif

@@ -57,7 +57,8 @@ int launch_qnlp_batch(int N, int nx, const nmpcmc_sqp_options& opt, int64_t batc
 
 // ---- K2 PI, unit kernels, FP64 peak, K5 batched QP (k_misc.cu)
 int launch_pi(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int nbar, nmpcmc_sim_record* d_rec,
-              nmpcmc_work_counters* d_cnt, double* d_traj, int rows, int sm_count, cudaStream_t stream);
+              nmpcmc_work_counters* d_cnt, double* d_traj, int rows, int sm_count, int pi_kernel,
+              cudaStream_t stream);
 void launch_pi_step(nmpcmc_pi_state* states, const double* y, const double* ybar, int64_t n,
                     nmpcmc_pi_step_result* results, int sm_count, cudaStream_t stream);
 void launch_philox(const uint32_t* in, int64_t n, uint32_t* out, cudaStream_t stream);

@@ -46,7 +46,7 @@ int launch(nmpcmc_gpu_ctx* ctx, const Target& tg, const nmpcmc_scenario& sc, uin
            nmpcmc_sim_record* d_rec, nmpcmc_work_counters* d_cnt, double* d_traj, int rows) {
     if (n == 0) return NMPCMC_OK;
     if (sc.controller == NMPCMC_CTRL_PI) {
-        nmpcmc_launch::launch_pi(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ctx->sm_count, tg.stream);
+        nmpcmc_launch::launch_pi(sc, first, n, nbar, d_rec, d_cnt, d_traj, rows, ctx->sm_count, ctx->pi_kernel, tg.stream);
         return cuda_check(ctx, cudaGetLastError(), "pi_kernel launch");
     }
     int rc;
@@ -200,6 +200,12 @@ int nmpcmc_gpu_set_option(nmpcmc_gpu_ctx* ctx, int32_t option, int64_t value) {
         case NMPCMC_OPT_TPS_WARPS_PER_SM:
             if (value < 1 || value > 64) return NMPCMC_INVALID_ARGUMENT;
             ctx->tps_warps_per_sm = (int)value;
+            return NMPCMC_OK;
+        case NMPCMC_OPT_PI_KERNEL:
+            if (value != NMPCMC_PI_KERNEL_AUTO && value != NMPCMC_PI_KERNEL_LANES && value != NMPCMC_PI_KERNEL_WS3 &&
+                value != NMPCMC_PI_KERNEL_WS7)
+                return NMPCMC_INVALID_ARGUMENT;
+            ctx->pi_kernel = (int)value;
             return NMPCMC_OK;
         case NMPCMC_OPT_CTRL_JACOBIANS:
             if (value != NMPCMC_JACOBIANS_ANALYTIC && value != NMPCMC_JACOBIANS_FD) return NMPCMC_INVALID_ARGUMENT;

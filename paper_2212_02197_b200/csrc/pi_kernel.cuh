@@ -12,6 +12,7 @@
 // recursion itself stays serial.
 #pragma once
 
+#include "certified_math.cuh"
 #include "device_common.cuh"
 
 namespace nmpcmc_dev {
@@ -200,6 +201,249 @@ __global__ void __launch_bounds__(kPiBlock, NMPCMC_PI_MINB) pi_kernel(const __gr
     pi_closed_loop<NX, G>(sc, first_sim + (uint64_t)ii, nbar, real ? records + ii : nullptr,
                           counters && real ? counters + ii : nullptr,
                           traj && real ? traj + (size_t)ii * traj_rows * 5 : nullptr, traj_rows, win + q, kGroups);
+}
+
+// ---------------------------------------------- warp-specialised PI (K2ws)
+// One consumer warp runs 32 samples' closed loops (one thread per sample,
+// the serial Euler-Maruyama chain); P producer warps of the same block
+// generate the normals those 32 samples read, one control step at a time,
+// into a ring of kPiWsSlots shared-memory slots. The normals do not depend
+// on the state (a live sample's stream position at step i is i * per_step),
+// so producers run ahead of the consumer by up to kPiWsSlots steps and the
+// Philox + log + sincos work, the bulk of the arithmetic, overlaps the
+// latency-bound recursion instead of sitting on it. Slot s of step i holds
+// normal m of sample l at [m * 32 + l]: the consumer's reads are
+// conflict-free, and a producer warp writes one m for 32 samples.
+// Handshake: named barriers FULL(s) = 1 + s (producers arrive, consumer
+// syncs) and EMPTY(s) = 1 + kPiWsSlots + s (consumer arrives, producers sync).
+constexpr int kPiWsSlots = 3;
+constexpr int kPiWsMaxPerStep = 40;  // normals read per control step (40 KB ring)
+
+/// Normal source of one consumer lane: the current slot's column.
+struct SlotRng {
+    const double* p;
+    __device__ __forceinline__ double normal() {
+        const double z = *p;
+        p += 32;
+        return z;
+    }
+    __device__ __forceinline__ void skip() {}
+};
+
+// Barrier ids are immediates (a switch over the slot), so ptxas reserves only
+// the 2 kPiWsSlots + 1 barriers in use: a register id makes it reserve all
+// 16, and the SM's barrier budget then caps residency at 4 blocks per SM
+// (measured: 1.58 waves at config 1 instead of one).
+template <int ID>
+__device__ __forceinline__ void bar_sync_id(int n) {
+    asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(n) : "memory");
+}
+template <int ID>
+__device__ __forceinline__ void bar_arrive_id(int n) {
+    asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+    static_assert(kPiWsSlots == 3, "one case per barrier id");
+    switch (id) {
+        case 1: bar_sync_id<1>(n); break;
+        case 2: bar_sync_id<2>(n); break;
+        case 3: bar_sync_id<3>(n); break;
+        case 4: bar_sync_id<4>(n); break;
+        case 5: bar_sync_id<5>(n); break;
+        default: bar_sync_id<6>(n); break;
+    }
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    switch (id) {
+        case 1: bar_arrive_id<1>(n); break;
+        case 2: bar_arrive_id<2>(n); break;
+        case 3: bar_arrive_id<3>(n); break;
+        case 4: bar_arrive_id<4>(n); break;
+        case 5: bar_arrive_id<5>(n); break;
+        default: bar_arrive_id<6>(n); break;
+    }
+}
+
+/// Normals a control step reads (SPARSE: the measurement one and the c_T
+/// increment of every substep; else all per_step of them).
+__host__ __device__ inline int pi_ws_reads(const nmpcmc_scenario& sc, bool sparse) {
+    const int nx = sc.truth_variant == NMPCMC_THREE_STATE ? 3 : 1;
+    const int has_R = sc.has_noise_R != 0 ? 1 : 0;
+    return sparse ? has_R + sc.Ns : has_R + sc.Ns * nx;
+}
+
+/// The plant drift (cstr.cpp:36-53) with the divisions by the constant
+/// volume V as Markstein corrections on the per-sample reciprocal
+/// yV = RN(1/V) (3 dependent operations instead of an IEEE division on the
+/// Euler-Maruyama chain). Each quotient's certificate (cert_div: the exact
+/// fma residual proves it is RN(n / V)) is folded into ok; the caller
+/// replays the control step with IEEE divisions unless every one held, so
+/// the states are bitwise those of drift3 / drift1.
+template <int NX>
+__device__ __forceinline__ int drift_fv(const Cstr& p, const double* n, double u, double* dn, double yV, bool& ok) {
+    const double f = u * kMlMinToLs;
+    if (NX == 3) {
+        const double c0 = fast_div(n[0], p.V, yV), c1 = fast_div(n[1], p.V, yV), c2 = fast_div(n[2], p.V, yV);
+        ok &= cert_div_bf(n[0], p.V, c0) & cert_div_bf(n[1], p.V, c1) & cert_div_bf(n[2], p.V, c2);
+        if (c2 <= 0.0) return ST_DOMAIN;
+        const double r = p.k0 * xlibm_exp(-p.EaR / c2) * c0 * c1;
+        dn[0] = p.cA_in * f - c0 * f + -1.0 * r * p.V;
+        dn[1] = p.cB_in * f - c1 * f + -2.0 * r * p.V;
+        dn[2] = p.cT_in * f - c2 * f + p.beta * r * p.V;
+        return ST_OK;
+    }
+    const double c = fast_div(n[0], p.V, yV);
+    ok &= cert_div_bf(n[0], p.V, c);
+    const Conc1 cc = conc1(p, c);
+    if (cc.cT <= 0.0) return ST_DOMAIN;
+    const double r = p.k0 * xlibm_exp(-p.EaR / cc.cT) * cc.cA * cc.cB;
+    dn[0] = p.cT_in * f - c * f + p.beta * r * p.V;
+    return ST_OK;
+}
+
+template <int NX, int P, bool SPARSE>
+__global__ void __launch_bounds__(32 * (1 + P), P == 3 ? 7 : 3) pi_ws_kernel(const __grid_constant__ nmpcmc_scenario sc,
+                                                             uint64_t first_sim, int64_t n_sims, int nbar,
+                                                             nmpcmc_sim_record* records,
+                                                             nmpcmc_work_counters* counters, double* traj,
+                                                             int traj_rows) {
+    extern __shared__ double ring[];
+    __shared__ int stop;
+    constexpr int kThreads = 32 * (1 + P);
+    const int lane = threadIdx.x & 31;
+    const int64_t base = (int64_t)blockIdx.x * 32;
+    const int has_R = sc.has_noise_R != 0 ? 1 : 0;
+    const int per_step = has_R + sc.Ns * NX;
+    const int reads = SPARSE ? has_R + sc.Ns : per_step;
+    const int items = reads * 32;
+    if (threadIdx.x == 0) stop = 0;
+    __syncthreads();
+
+    if (threadIdx.x >= 32) {
+        // ---- producers: item j of a slot is normal j >> 5 of sample j & 31
+        const int t = threadIdx.x - 32;
+        for (int i = 0; i < nbar; ++i) {
+            const int s = i % kPiWsSlots;
+            if (i >= kPiWsSlots) named_sync(1 + kPiWsSlots + s, kThreads);
+            if (*(volatile int*)&stop == 0) {
+                double* slot = ring + s * items;
+                const uint64_t k0 = (uint64_t)i * (uint64_t)per_step;
+                for (int j = t; j < items; j += 32 * P) {
+                    const int m = j >> 5;
+                    int64_t idx = base + (j & 31);
+                    if (idx >= n_sims) idx = n_sims - 1;  // tail lanes run a copy, unseen
+                    const uint64_t nn =
+                        SPARSE ? (has_R && m == 0 ? k0 : k0 + (uint64_t)(has_R + 3 * (m - has_R) + 2)) : k0 + m;
+                    slot[j] = normal_one(sc.base_seed, first_sim + (uint64_t)idx, nn);
+                }
+            }
+            named_arrive(1 + s, kThreads);
+        }
+        return;
+    }
+
+    // ---- consumer: run_closed_loop's PI branch, as pi_closed_loop<NX, 1>
+    const int64_t ig = base + lane;
+    const bool real = ig < n_sims;
+    const int64_t ii = real ? ig : n_sims - 1;
+    const uint64_t sim_index = first_sim + (uint64_t)ii;
+    const Cstr p = sample_truth(sc, sim_index);
+    Plant<NX> pl;
+#pragma unroll
+    for (int q = 0; q < NX; ++q) pl.x[q] = sc.x0[q];
+    const bool hasR = has_R != 0;
+    const double lR = hasR ? chol_semidef_1x1(sc.noise_R) : 0.0;
+    const double yV = 1.0 / p.V;
+    const double kP = sc.pi.kP, kI = sc.pi.kI, kaw = sc.pi.kaw, u_bar = sc.pi.u_bar;
+    const double Ts = sc.Ts, u_min = sc.u_min, u_max = sc.u_max;
+    double I_hat = sc.pi.I_hat;
+    const int stride = sc.record_stride < 1 ? 1 : sc.record_stride;
+    double* tr = (traj != nullptr && real) ? traj + (size_t)ii * traj_rows * 5 : nullptr;
+
+    double t = sc.t0;
+    double z = pl.x[NX - 1] / p.V;
+    double zbar = setpoint_at(sc, t);
+    double acc = 0.0;
+    {
+        const double r = z - zbar;
+        acc += r * r;
+    }
+    int status = ST_OK;
+    int row = 0;
+    int steps = 0;
+    for (int i = 0; i < nbar; ++i) {
+        const int s = i % kPiWsSlots;
+        named_sync(1 + s, kThreads);
+        if (status == ST_OK) {
+            SlotRng rng{ring + s * items + lane};
+            ++steps;
+            const double y = measure<NX>(p, pl, hasR, lR, rng);
+            const double ybar = setpoint_at(sc, t);
+            const nmpcmc_pi_state ps{kP, kI, kaw, Ts, u_bar, u_min, u_max, I_hat};
+            const nmpcmc_pi_step_result pr = pi_law(ps, y, ybar);
+            const double u = pr.u;
+            I_hat = pr.next_I_hat;
+            if (tr != nullptr && i % stride == 0) {
+                double* rw = tr + (size_t)row * 5;
+                rw[0] = t;
+                rw[1] = z;
+                rw[2] = zbar;
+                rw[3] = u;
+                rw[4] = y;
+                ++row;
+            }
+            // fast divisions by V; the step is replayed with IEEE ones from
+            // the saved state unless every quotient was certified
+            const Plant<NX> pl0 = pl;
+            const SlotRng rng0 = rng;
+            bool ok = true;
+            status = simulate_interval_d<NX, SlotRng, SPARSE>(
+                p, pl, t, t + sc.Ts, u, sc.Ns, rng,
+                [&](const double* x, double uu, double* dn) -> int { return drift_fv<NX>(p, x, uu, dn, yV, ok); });
+            if (!ok) {
+                pl = pl0;
+                rng = rng0;
+                status = simulate_interval<NX, SlotRng, SPARSE>(p, pl, t, t + sc.Ts, u, sc.Ns, rng);
+            }
+            if (status == ST_OK) {
+                t = sc.t0 + (i + 1) * sc.Ts;
+                z = pl.x[NX - 1] / p.V;
+                zbar = setpoint_at(sc, t);
+                const double r = z - zbar;
+                acc += r * r;
+            }
+        }
+        // producers stop generating once every sample of the warp has failed
+        // (they still keep the handshake going to the end)
+        const bool done = __all_sync(0xffffffffu, status != ST_OK);
+        if (done && lane == 0) *(volatile int*)&stop = 1;
+        if (i + kPiWsSlots < nbar) named_arrive(1 + kPiWsSlots + s, kThreads);
+    }
+    if (!real) return;
+    nmpcmc_sim_record* rec = records + ii;
+    if (status == ST_OK) {
+        rec->phi = acc / (double)(nbar + 1);
+        rec->failed = 0;
+        if (tr != nullptr) {
+            double* rw = tr + (size_t)row * 5;
+            rw[0] = t;
+            rw[1] = z;
+            rw[2] = zbar;
+            rw[3] = __longlong_as_double(0x7ff8000000000000LL);
+            rw[4] = __longlong_as_double(0x7ff8000000000000LL);
+        }
+    } else {
+        rec->phi = __longlong_as_double(0x7ff8000000000000LL);
+        rec->failed = 1;
+    }
+    rec->ocp_solves = 0;
+    rec->ocp_failures = 0;
+    rec->status = status;
+    if (counters != nullptr) {
+        nmpcmc_work_counters c = {};
+        c.control_steps = steps;
+        counters[ii] = c;
+    }
 }
 
 }  // namespace nmpcmc_dev

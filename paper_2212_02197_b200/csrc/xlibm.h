@@ -100,9 +100,12 @@ XLIBM_FN double xlibm_exp(double x) {
     if (x > 0x1.62e42fefa39efp+9) return XLIBM_INF;  // > ln(DBL_MAX)
     if (x < -0x1.74910d52d3052p+9) return 0.0;       // < ln(2^-1075)
     double z = x * XLIBM_EXP_INV_LN2N;
-    double kd = z + XLIBM_SHIFT;
-    kd = kd - XLIBM_SHIFT;
-    int64_t k = (int64_t)kd;
+    double kds = z + XLIBM_SHIFT;
+    // kds = SHIFT + round(z) exactly (|z| < 2^18 here): the integer is the
+    // difference of the bit patterns, so no float-to-int conversion sits on
+    // the dependency chain; kd = round(z) as before
+    int64_t k = (int64_t)(xlibm_asu64(kds) - xlibm_asu64(XLIBM_SHIFT));
+    double kd = kds - XLIBM_SHIFT;
     double r = xlibm_fma(-kd, XLIBM_EXP_LN2N_HI, x);
     r = xlibm_fma(-kd, XLIBM_EXP_LN2N_LO, r);
     int j = (int)(k & 127);
@@ -169,9 +172,9 @@ XLIBM_FN void xlibm_sincos(double x, double* s_out, double* c_out) {
         *c_out = x - x;
         return;
     }
-    double nd = x * XLIBM_INV_PIO64 + XLIBM_SHIFT;
-    nd = nd - XLIBM_SHIFT;
-    int64_t n = (int64_t)nd;
+    double nds = x * XLIBM_INV_PIO64 + XLIBM_SHIFT;
+    int64_t n = (int64_t)(xlibm_asu64(nds) - xlibm_asu64(XLIBM_SHIFT));  // as in xlibm_exp
+    double nd = nds - XLIBM_SHIFT;
     // r + r_lo = x - n pi/64: the P1 product and difference are exact, the
     // P2 step is a TwoSum, P3 only feeds the low word.
     double t = xlibm_fma(-nd, XLIBM_PIO64_1, x);

@@ -215,6 +215,16 @@ class Context:
         K3w, or K3g when 'generic' is selected."""
         self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 1, self.KERNELS[kind]))
 
+    PI_KERNELS = {"auto": 0, "lanes": 1, "ws3": 3, "ws7": 7}
+
+    def set_pi_kernel(self, kind: str):
+        """NMPCMC_OPT_PI_KERNEL: 'auto' (default: the warp-specialised kernel,
+        one consumer warp of 32 samples with producer warps generating the
+        normals ahead), 'lanes' (one thread or 4 lanes per sample), 'ws3' /
+        'ws7' (warp-specialised with 3 / 7 producer warps); bitwise-identical
+        results."""
+        self._check(self.lib.nmpcmc_gpu_set_option(self.handle, 5, self.PI_KERNELS[kind]))
+
     def set_ctrl_jacobians(self, kind: str):
         """'analytic' (default, make_cstr_model's closed forms) or 'fd': the
         controller model's jacobians by the reference's central differences

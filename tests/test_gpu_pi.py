@@ -78,3 +78,50 @@ def test_pi_validation_errors_raise(gpu_ctx):
     bad.Ns = 0
     with pytest.raises(engine.DomainError):
         gpu_ctx.run(bad, 0, 4)
+
+
+@pytest.fixture(scope="module")
+def pi_kernel_ctxs():
+    out = {}
+    for kind in ("lanes", "ws3", "ws7"):
+        c = engine.Context(0)
+        c.set_pi_kernel(kind)
+        out[kind] = c
+    yield out
+    for c in out.values():
+        c.close()
+
+
+@pytest.mark.parametrize("kind", ["lanes", "ws3", "ws7"])
+@pytest.mark.parametrize("name", PI_CASES)
+def test_pi_kernel_variants_bitwise(pi_kernel_ctxs, kind, name):
+    """Every PI kernel (NMPCMC_OPT_PI_KERNEL) reproduces the exact-libm
+    reference fixtures bitwise, records and trajectories."""
+    c = pi_kernel_ctxs[kind]
+    d, kw, sc = load_golden(name)
+    want = d["rec_xlibm"]
+    got, _ = c.run(sc, int(d["first"]), len(want))
+    assert_records_equal(got, want)
+    if "traj_xlibm" in d:
+        sct = configs.make_scenario(**kw, record=True)
+        _, traj = c.run_traj(sct, int(d["first"]), d["traj_xlibm"].shape[0])
+        np.testing.assert_array_equal(traj, d["traj_xlibm"])
+
+
+@pytest.mark.parametrize("kw", [dict(perturb=True), dict(perturb=True, sigma_abc=True), dict(one_state=True)])
+def test_pi_kernel_variants_agree_at_scale(pi_kernel_ctxs, kw):
+    """10,000 samples (a full wave of the 3-producer kernel) with a ragged
+    tail: all PI kernels give identical records and work counters; dense
+    normal reads (diffusion on every state) and the one-state plant too."""
+    from paper_2212_02197_b200 import abi
+    tv = abi.ONE_STATE if kw.get("one_state") else abi.THREE_STATE
+    sc = configs.make_scenario("pi", perturb=kw.get("perturb", False), truth_variant=tv)
+    if kw.get("sigma_abc"):
+        sc.truth.sigmaA = 0.01
+        sc.truth.sigmaB = 0.02
+    n = 10007
+    res = {k: c.run(sc, 5, n, counters=True) for k, c in pi_kernel_ctxs.items()}
+    base_rec, base_cnt = res["lanes"]
+    for k in ("ws3", "ws7"):
+        assert_records_equal(res[k][0], base_rec)
+        np.testing.assert_array_equal(res[k][1], base_cnt)

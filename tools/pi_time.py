@@ -1,7 +1,8 @@
 """Device time of the PI closed-loop kernel (K2) on BASELINE configs 0 and 1:
 best of R launches, CUDA events on the context stream.
 
-  python tools/pi_time.py [reps]
+  python tools/pi_time.py [reps] [kernels]   (kernels: comma list of
+  auto,lanes,ws3,ws7; default auto)
 """
 import os
 import sys
@@ -13,11 +14,13 @@ import torch
 from paper_2212_02197_b200 import configs, engine, workmodel
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+kernels = sys.argv[2].split(",") if len(sys.argv) > 2 else ["auto"]
 ctx = engine.Context(0)
 stream = torch.cuda.Stream()
 ctx.set_stream(stream.cuda_stream)
-for name, kw, n in (("config0", dict(controller="pi"), 1000), ("config1", dict(controller="pi", perturb=True), 30000),
-                    ("config1_x4", dict(controller="pi", perturb=True), 120000)):
+for kern, (name, kw, n) in [(k, c) for k in kernels for c in (("config0", dict(controller="pi"), 1000), ("config1", dict(controller="pi", perturb=True), 30000),
+                    ("config1_x4", dict(controller="pi", perturb=True), 120000))]:
+    ctx.set_pi_kernel(kern)
     sc = configs.make_scenario(**kw)
     rec = torch.empty(n * 24, dtype=torch.uint8, device="cuda")
     cnt = torch.empty(n * 64, dtype=torch.uint8, device="cuda")
@@ -37,4 +40,4 @@ for name, kw, n in (("config0", dict(controller="pi"), 1000), ("config1", dict(c
     fl = workmodel.pi_flops(int(c["control_steps"].sum()))
     import hashlib
     h = hashlib.sha1(rec.cpu().numpy().tobytes()).hexdigest()[:12]
-    print(f"PI {name}: {n} sims, {best:.3f} ms, {n / best * 1e3:.0f} sims/s, {fl / best / 1e9:.3f} TF/s, rec {h}")
+    print(f"PI[{kern}] {name}: {n} sims, {best:.3f} ms, {n / best * 1e3:.0f} sims/s, {fl / best / 1e9:.3f} TF/s, rec {h}")

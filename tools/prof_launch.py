@@ -25,6 +25,8 @@ def main():
     ctx = engine.Context(0)
     if ctrl == "nmpc":
         ctx.set_nmpc_kernel(kernel)
+    elif os.environ.get("NMPCMC_PI_KERNEL"):
+        ctx.set_pi_kernel(os.environ["NMPCMC_PI_KERNEL"])
     ctx.run(sc, 0, n)
     t = time.perf_counter()
     rec, cnt = ctx.run(sc, 0, n, counters=True)
