@@ -44,7 +44,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not extra and out == LIB and not _stale(out):
         return LIB
     os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
-    objdir = os.path.join(os.path.dirname(os.path.abspath(out)), "obj" + ("_x" if (extra or out != LIB) else ""))
+    # experiment builds get their own object directory, so several can run at once
+    objdir = os.path.join(os.path.dirname(os.path.abspath(out)),
+                          "obj" + ("_" + os.path.splitext(os.path.basename(out))[0] if (extra or out != LIB) else ""))
     os.makedirs(objdir, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
 

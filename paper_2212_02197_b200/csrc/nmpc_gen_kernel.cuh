@@ -867,12 +867,141 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
     }
     return false;
 }
+
+// ------------------------------------------------ lane-split sweeps (K3w)
+// In the serial sweeps above a warp does the same NX x NX block arithmetic on
+// all 32 lanes. The elements of each block product are independent dot
+// products, so K3w gives lane (lane % NX^2) ONE element (row i, column j) of
+// every NX x NX product and lane (lane % NX) one component of every NX-vector,
+// and passes operands between lanes with shuffles. Each element is still the
+// same left-to-right sum over the same operands (s = 0.0; s += a*b ...; the
+// gemm epilogue), so results are bitwise those of rfactor_t / rsolve_t; the
+// warp issues ~3x fewer FP64 instructions per stage.
+#ifndef NMPCMC_SPLIT_SWEEPS
+#define NMPCMC_SPLIT_SWEEPS 1
+#endif
+
+/// riccati_factor (qp.cpp:73-110), fast forms, one block element per lane.
+/// Returns true on NotPositiveDefinite; *cert is false if any fast
+/// sqrt/division was not certified (the caller replays rfactor_t<FAST=false>).
+template <int NX>
+__device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_out) {
+    constexpr int W = 32;
+    constexpr unsigned kFull = 0xffffffffu;
+    const Ocp<NX, W>& o = *v.o;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
+    const int oBAR = L.BAR, oWB = L.WB;
+    const SweepLay<NX> SL(o.N);
+    double* const aFP = gen_smem + SL.FP;
+    double* const aFLL = gen_smem + SL.FLL;
+    double* const aFLY = gen_smem + SL.FLY;
+    double* const aFK = gen_smem + SL.FK;
+    double* const aFG = gen_smem + SL.FG;
+    const double* const aJX = gen_smem + SL.JX;
+    const double* const aJU = gen_smem + SL.JU;
+    const double* const aRR = gen_smem + SL.RR;
+    const double* const aQQ = gen_smem + SL.QQ;
+    const int N = o.N;
+    const int e = (int)(threadIdx.x & 31) % (NX * NX);
+    const int i = e % NX, j = e / NX;  // this lane's element: row i, column j
+    bool cert = true;
+    double Pn = aQQ[(N * NX + j) * NX + i];  // P_{k+1}(i, j)
+    aFP[(N * NX + j) * NX + i] = Pn;
+#pragma unroll 1
+    for (int k = N - 1; k >= 0; --k) {
+        double ju[NX], row[NX];
+#pragma unroll
+        for (int l = 0; l < NX; ++l) {
+            ju[l] = aJU[k * NX + l];
+            row[l] = __shfl_sync(kFull, Pn, i + NX * l);  // P_{k+1}(i, l)
+        }
+        double pju;  // (P Ju)(i)
+        {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < NX; ++l) s += row[l] * ju[l];
+            pju = 1.0 * s + 0.0;
+        }
+        double H;
+        {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < NX; ++l) s += ju[l] * __shfl_sync(kFull, pju, l);  // lane l holds row l
+            H = 1.0 * s + 0.0;
+        }
+        H += aRR[k];
+        H += w[oBAR + k];
+        if (H <= 0.0 || !dfinite(H)) {  // cholesky_factor (linalg.cpp:69-103); H is lane-uniform
+            __syncwarp();
+            return true;
+        }
+        double l, y;
+        fast_sqrt(H, l, y);
+        cert &= cert_sqrt_bf(H, l);
+        aFLL[k] = l;
+        aFLY[k] = y;
+        if (k >= 1) {
+            double pjx;  // (P Jx)(i, j)
+            {
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m < NX; ++m) s += row[m] * aJX[(k * NX + j) * NX + m];
+                pjx = 1.0 * s + 0.0;
+            }
+            double col[NX];  // (P Jx)(m, j)
+#pragma unroll
+            for (int m = 0; m < NX; ++m) col[m] = __shfl_sync(kFull, pjx, m + NX * j);
+            double G;  // G(j)
+            {
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m < NX; ++m) s += ju[m] * col[m];
+                G = 1.0 * s + 0.0;
+            }
+            {
+                const int ld = k < N ? NX + 1 : NX;
+                G += w[oWB + k * Layout<NX>::B + NX * ld + j];  // M(k, j)
+            }
+            double t = cdiv_seed(G, l, y, cert);  // cholesky_solve of the 1x1 factor, then negate
+            t = cdiv_seed(t, l, y, cert);
+            const double K = -t;
+            double pk;  // (Jx' P Jx)(i, j)
+            {
+                double s = 0.0;
+#pragma unroll
+                for (int m = 0; m < NX; ++m) s += aJX[(k * NX + i) * NX + m] * col[m];
+                pk = 1.0 * s + 0.0;
+            }
+            pk += aQQ[(k * NX + j) * NX + i];
+            const double Gi = __shfl_sync(kFull, G, NX * i);  // lane (0, i) holds G(i)
+            pk = 1.0 * (0.0 + Gi * K) + 1.0 * pk;
+            // symmetrize (linalg.cpp:227-235): 0.5 * (lower + upper)
+            const double pt = __shfl_sync(kFull, pk, j + NX * i);  // element (j, i)
+            if (i > j) pk = 0.5 * (pk + pt);
+            if (i < j) pk = 0.5 * (pt + pk);
+            aFK[k * NX + j] = K;
+            aFG[k * NX + j] = G;
+            aFP[(k * NX + j) * NX + i] = pk;
+            Pn = pk;
+        }
+    }
+    *cert_out = __all_sync(kFull, cert);
+    __syncwarp();
+    return false;
+}
+
 /// riccati_factor with the certified fast sqrt/division; any uncertified
 /// stage (or a fast NotPositiveDefinite) replays the sweep with IEEE ops.
 template <int NX, int W>
 __device__ __forceinline__ bool rfactor(const QpView<NX, W> v) {
     bool cert = true;
-    bool npd = rfactor_t<NX, W, true>(v, &cert);
+    bool npd;
+    if constexpr (W == 32 && NX > 1 && NMPCMC_SPLIT_SWEEPS) {
+        npd = rfactor_split<NX>(v, &cert);
+    } else {
+        npd = rfactor_t<NX, W, true>(v, &cert);
+    }
     if (npd || !cert) npd = rfactor_t<NX, W, false>(v, nullptr);
     return npd;
 }
@@ -1006,11 +1135,116 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
     }
     return cert;
 }
+
+/// riccati_solve_vectors (qp.cpp:116-155), fast forms, one vector component
+/// per lane (see rfactor_split). Returns false if a fast division was not
+/// certified (the caller replays rsolve_t<FAST=false>).
+template <int NX>
+__device__ __noinline__ bool rsolve_split(const QpView<NX, 32> v) {
+    constexpr int W = 32;
+    constexpr unsigned kFull = 0xffffffffu;
+    const Ocp<NX, W>& o = *v.o;
+    const WsT<W> w = o.ws;
+    const Layout<NX> L = o.lay;
+    const int oDMU = L.DMU, oDXI = L.DXI;
+    const SweepLay<NX> SL(o.N);
+    const double* const aFP = gen_smem + SL.FP;
+    const double* const aFLL = gen_smem + SL.FLL;
+    const double* const aFLY = gen_smem + SL.FLY;
+    const double* const aFK = gen_smem + SL.FK;
+    const double* const aFG = gen_smem + SL.FG;
+    double* const aPV = gen_smem + SL.PV;
+    double* const aDFF = gen_smem + SL.DFF;
+    const double* const aJX = gen_smem + SL.JX;
+    const double* const aJU = gen_smem + SL.JU;
+    const double* const aRS = gen_smem + SL.RS;
+    const double* const aRD = gen_smem + SL.RD;
+    const double* const aRH = gen_smem + SL.RH;
+    const int N = o.N;
+    const int i = (int)(threadIdx.x & 31) % NX;  // this lane's vector component
+    bool cert = true;
+    double pvn = aRS[L.xo(N) + i];  // p_{k+1}(i)
+    aPV[N * NX + i] = pvn;
+#pragma unroll 1
+    for (int k = N - 1; k >= 0; --k) {
+        double t;
+        {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += aFP[((k + 1) * NX + j) * NX + i] * -aRD[k * NX + j];
+            t = 1.0 * s + 1.0 * pvn;
+        }
+        double tj[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) tj[j] = __shfl_sync(kFull, t, j);
+        double hv;
+        {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += aJU[k * NX + j] * tj[j];
+            hv = 1.0 * s + 1.0 * aRH[k];
+        }
+        const double l = aFLL[k], y = aFLY[k];
+        hv = cdiv_seed(hv, l, y, cert);
+        hv = cdiv_seed(hv, l, y, cert);
+        const double dff = -hv;
+        aDFF[k] = dff;
+        if (k >= 1) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += aJX[(k * NX + i) * NX + j] * tj[j];
+            double p = 1.0 * s + 1.0 * aRS[L.xo(k) + i];
+            p = 1.0 * (0.0 + aFG[k * NX + i] * dff) + 1.0 * p;
+            aPV[k * NX + i] = p;
+            pvn = p;
+        }
+    }
+    double dx[NX];  // the whole state step, on every lane
+#pragma unroll
+    for (int j = 0; j < NX; ++j) dx[j] = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) {
+        double du = aDFF[k];
+        if (k >= 1) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += aFK[k * NX + j] * dx[j];
+            du = 1.0 * s + 1.0 * du;
+        }
+        w[oDXI + L.uo(k)] = du;
+        double dn = -aRD[k * NX + i];
+        if (k >= 1) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) s += aJX[(k * NX + j) * NX + i] * dx[j];
+            dn = 1.0 * s + 1.0 * dn;
+        }
+        dn = 1.0 * (0.0 + aJU[k * NX + i] * du) + 1.0 * dn;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) dx[j] = __shfl_sync(kFull, dn, j);
+        w[oDXI + L.uo(k) + 1 + i] = dn;
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) s += aFP[((k + 1) * NX + j) * NX + i] * dx[j];
+        const double mv = 1.0 * s + 1.0 * aPV[(k + 1) * NX + i];
+        w[oDMU + k * NX + i] = -mv;
+    }
+    cert = __all_sync(kFull, cert);
+    __syncwarp();
+    return cert;
+}
+
 /// riccati_solve_vectors with the certified fast division (replayed with
 /// IEEE ops if any quotient is not certified).
 template <int NX, int W>
 __device__ __forceinline__ void rsolve(const QpView<NX, W> v) {
-    if (!rsolve_t<NX, W, true>(v)) rsolve_t<NX, W, false>(v);
+    bool ok;
+    if constexpr (W == 32 && NX > 1 && NMPCMC_SPLIT_SWEEPS) {
+        ok = rsolve_split<NX>(v);
+    } else {
+        ok = rsolve_t<NX, W, true>(v);
+    }
+    if (!ok) rsolve_t<NX, W, false>(v);
 }
 
 enum : int { QP_OPTIMAL = 0, QP_MAXITER = 1, QP_FAILED = 2, QP_DOMAIN = 3 };
