@@ -884,6 +884,8 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
 /// riccati_factor (qp.cpp:73-110), fast forms, one block element per lane.
 /// Returns true on NotPositiveDefinite; *cert is false if any fast
 /// sqrt/division was not certified (the caller replays rfactor_t<FAST=false>).
+/// The operands of stage k-1 are loaded while stage k computes, so neither
+/// shared-memory nor slab (BAR, M) latency sits on the recursion.
 template <int NX>
 __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_out) {
     constexpr int W = 32;
@@ -908,30 +910,47 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
     bool cert = true;
     double Pn = aQQ[(N * NX + j) * NX + i];  // P_{k+1}(i, j)
     aFP[(N * NX + j) * NX + i] = Pn;
-#pragma unroll 1
-    for (int k = N - 1; k >= 0; --k) {
-        double ju[NX], row[NX];
+    // stage operands: Ju, columns j and i of Jx, Q(i, j), R, BAR, M(j)
+    struct Ops {
+        double ju[NX], jxj[NX], jxi[NX], qq, rr, bar, mj;
+    };
+    auto load_ops = [&](int k) {
+        Ops n;
 #pragma unroll
         for (int l = 0; l < NX; ++l) {
-            ju[l] = aJU[k * NX + l];
-            row[l] = __shfl_sync(kFull, Pn, i + NX * l);  // P_{k+1}(i, l)
+            n.ju[l] = aJU[k * NX + l];
+            n.jxj[l] = aJX[(k * NX + j) * NX + l];
+            n.jxi[l] = aJX[(k * NX + i) * NX + l];
         }
+        n.qq = aQQ[(k * NX + j) * NX + i];
+        n.rr = aRR[k];
+        n.bar = w[oBAR + k];
+        n.mj = w[oWB + k * Layout<NX>::B + NX * (NX + 1) + j];  // M(k, j), 1 <= k < N (unused at k = 0)
+        return n;
+    };
+    Ops c = load_ops(N - 1);
+#pragma unroll 1
+    for (int k = N - 1; k >= 0; --k) {
+        const Ops nx = load_ops(k > 0 ? k - 1 : 0);
+        double row[NX];
+#pragma unroll
+        for (int l = 0; l < NX; ++l) row[l] = __shfl_sync(kFull, Pn, i + NX * l);  // P_{k+1}(i, l)
         double pju;  // (P Ju)(i)
         {
             double s = 0.0;
 #pragma unroll
-            for (int l = 0; l < NX; ++l) s += row[l] * ju[l];
+            for (int l = 0; l < NX; ++l) s += row[l] * c.ju[l];
             pju = 1.0 * s + 0.0;
         }
         double H;
         {
             double s = 0.0;
 #pragma unroll
-            for (int l = 0; l < NX; ++l) s += ju[l] * __shfl_sync(kFull, pju, l);  // lane l holds row l
+            for (int l = 0; l < NX; ++l) s += c.ju[l] * __shfl_sync(kFull, pju, l);  // lane l holds row l
             H = 1.0 * s + 0.0;
         }
-        H += aRR[k];
-        H += w[oBAR + k];
+        H += c.rr;
+        H += c.bar;
         if (H <= 0.0 || !dfinite(H)) {  // cholesky_factor (linalg.cpp:69-103); H is lane-uniform
             __syncwarp();
             return true;
@@ -946,7 +965,7 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
             {
                 double s = 0.0;
 #pragma unroll
-                for (int m = 0; m < NX; ++m) s += row[m] * aJX[(k * NX + j) * NX + m];
+                for (int m = 0; m < NX; ++m) s += row[m] * c.jxj[m];
                 pjx = 1.0 * s + 0.0;
             }
             double col[NX];  // (P Jx)(m, j)
@@ -956,13 +975,10 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
             {
                 double s = 0.0;
 #pragma unroll
-                for (int m = 0; m < NX; ++m) s += ju[m] * col[m];
+                for (int m = 0; m < NX; ++m) s += c.ju[m] * col[m];
                 G = 1.0 * s + 0.0;
             }
-            {
-                const int ld = k < N ? NX + 1 : NX;
-                G += w[oWB + k * Layout<NX>::B + NX * ld + j];  // M(k, j)
-            }
+            G += c.mj;
             double t = cdiv_seed(G, l, y, cert);  // cholesky_solve of the 1x1 factor, then negate
             t = cdiv_seed(t, l, y, cert);
             const double K = -t;
@@ -970,10 +986,10 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
             {
                 double s = 0.0;
 #pragma unroll
-                for (int m = 0; m < NX; ++m) s += aJX[(k * NX + i) * NX + m] * col[m];
+                for (int m = 0; m < NX; ++m) s += c.jxi[m] * col[m];
                 pk = 1.0 * s + 0.0;
             }
-            pk += aQQ[(k * NX + j) * NX + i];
+            pk += c.qq;
             const double Gi = __shfl_sync(kFull, G, NX * i);  // lane (0, i) holds G(i)
             pk = 1.0 * (0.0 + Gi * K) + 1.0 * pk;
             // symmetrize (linalg.cpp:227-235): 0.5 * (lower + upper)
@@ -985,6 +1001,7 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
             aFP[(k * NX + j) * NX + i] = pk;
             Pn = pk;
         }
+        c = nx;
     }
     *cert_out = __all_sync(kFull, cert);
     __syncwarp();
@@ -1138,7 +1155,8 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
 
 /// riccati_solve_vectors (qp.cpp:116-155), fast forms, one vector component
 /// per lane (see rfactor_split). Returns false if a fast division was not
-/// certified (the caller replays rsolve_t<FAST=false>).
+/// certified (the caller replays rsolve_t<FAST=false>). Stage operands, and
+/// the recursion-free product P_{k+1} bhat_k, are formed one stage ahead.
 template <int NX>
 __device__ __noinline__ bool rsolve_split(const QpView<NX, 32> v) {
     constexpr int W = 32;
@@ -1165,15 +1183,34 @@ __device__ __noinline__ bool rsolve_split(const QpView<NX, 32> v) {
     bool cert = true;
     double pvn = aRS[L.xo(N) + i];  // p_{k+1}(i)
     aPV[N * NX + i] = pvn;
+    // backward: s = (P_{k+1} bhat_k)(i), Ju, rh, the pivot and its seed,
+    // column i of Jx, qhat_k(i), G(i)
+    struct Back {
+        double s, ju[NX], rh, l, y, jx[NX], rs, fg;
+    };
+    auto load_back = [&](int k) {
+        Back n;
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) s += aFP[((k + 1) * NX + j) * NX + i] * -aRD[k * NX + j];
+        n.s = s;
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+            n.ju[j] = aJU[k * NX + j];
+            n.jx[j] = aJX[(k * NX + i) * NX + j];
+        }
+        n.rh = aRH[k];
+        n.l = aFLL[k];
+        n.y = aFLY[k];
+        n.rs = aRS[L.xo(k > 0 ? k : 1) + i];  // unused at k = 0
+        n.fg = aFG[k * NX + i];
+        return n;
+    };
+    Back c = load_back(N - 1);
 #pragma unroll 1
     for (int k = N - 1; k >= 0; --k) {
-        double t;
-        {
-            double s = 0.0;
-#pragma unroll
-            for (int j = 0; j < NX; ++j) s += aFP[((k + 1) * NX + j) * NX + i] * -aRD[k * NX + j];
-            t = 1.0 * s + 1.0 * pvn;
-        }
+        const Back nx = load_back(k > 0 ? k - 1 : 0);
+        const double t = 1.0 * c.s + 1.0 * pvn;
         double tj[NX];
 #pragma unroll
         for (int j = 0; j < NX; ++j) tj[j] = __shfl_sync(kFull, t, j);
@@ -1181,53 +1218,74 @@ __device__ __noinline__ bool rsolve_split(const QpView<NX, 32> v) {
         {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < NX; ++j) s += aJU[k * NX + j] * tj[j];
-            hv = 1.0 * s + 1.0 * aRH[k];
+            for (int j = 0; j < NX; ++j) s += c.ju[j] * tj[j];
+            hv = 1.0 * s + 1.0 * c.rh;
         }
-        const double l = aFLL[k], y = aFLY[k];
-        hv = cdiv_seed(hv, l, y, cert);
-        hv = cdiv_seed(hv, l, y, cert);
+        hv = cdiv_seed(hv, c.l, c.y, cert);
+        hv = cdiv_seed(hv, c.l, c.y, cert);
         const double dff = -hv;
         aDFF[k] = dff;
         if (k >= 1) {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < NX; ++j) s += aJX[(k * NX + i) * NX + j] * tj[j];
-            double p = 1.0 * s + 1.0 * aRS[L.xo(k) + i];
-            p = 1.0 * (0.0 + aFG[k * NX + i] * dff) + 1.0 * p;
+            for (int j = 0; j < NX; ++j) s += c.jx[j] * tj[j];
+            double p = 1.0 * s + 1.0 * c.rs;
+            p = 1.0 * (0.0 + c.fg * dff) + 1.0 * p;
             aPV[k * NX + i] = p;
             pvn = p;
         }
+        c = nx;
     }
+    // forward: dff, K, bhat(i), row i of Jx, Ju(i), row i of P_{k+1}, p_{k+1}(i)
+    struct Fwd {
+        double dff, fk[NX], bh, jx[NX], ju, fp[NX], pv;
+    };
+    auto load_fwd = [&](int k) {
+        Fwd n;
+        n.dff = aDFF[k];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+            n.fk[j] = aFK[k * NX + j];  // unused at k = 0
+            n.jx[j] = aJX[(k * NX + j) * NX + i];
+            n.fp[j] = aFP[((k + 1) * NX + j) * NX + i];
+        }
+        n.bh = -aRD[k * NX + i];
+        n.ju = aJU[k * NX + i];
+        n.pv = aPV[(k + 1) * NX + i];
+        return n;
+    };
     double dx[NX];  // the whole state step, on every lane
 #pragma unroll
     for (int j = 0; j < NX; ++j) dx[j] = 0.0;
+    Fwd f = load_fwd(0);
 #pragma unroll 1
     for (int k = 0; k < N; ++k) {
-        double du = aDFF[k];
+        const Fwd nf = load_fwd(k + 1 < N ? k + 1 : k);
+        double du = f.dff;
         if (k >= 1) {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < NX; ++j) s += aFK[k * NX + j] * dx[j];
+            for (int j = 0; j < NX; ++j) s += f.fk[j] * dx[j];
             du = 1.0 * s + 1.0 * du;
         }
-        w[oDXI + L.uo(k)] = du;
-        double dn = -aRD[k * NX + i];
+        double dn = f.bh;
         if (k >= 1) {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < NX; ++j) s += aJX[(k * NX + j) * NX + i] * dx[j];
+            for (int j = 0; j < NX; ++j) s += f.jx[j] * dx[j];
             dn = 1.0 * s + 1.0 * dn;
         }
-        dn = 1.0 * (0.0 + aJU[k * NX + i] * du) + 1.0 * dn;
+        dn = 1.0 * (0.0 + f.ju * du) + 1.0 * dn;
 #pragma unroll
         for (int j = 0; j < NX; ++j) dx[j] = __shfl_sync(kFull, dn, j);
-        w[oDXI + L.uo(k) + 1 + i] = dn;
         double s = 0.0;
 #pragma unroll
-        for (int j = 0; j < NX; ++j) s += aFP[((k + 1) * NX + j) * NX + i] * dx[j];
-        const double mv = 1.0 * s + 1.0 * aPV[(k + 1) * NX + i];
+        for (int j = 0; j < NX; ++j) s += f.fp[j] * dx[j];
+        const double mv = 1.0 * s + 1.0 * f.pv;
+        w[oDXI + L.uo(k)] = du;
+        w[oDXI + L.uo(k) + 1 + i] = dn;
         w[oDMU + k * NX + i] = -mv;
+        f = nf;
     }
     cert = __all_sync(kFull, cert);
     __syncwarp();
