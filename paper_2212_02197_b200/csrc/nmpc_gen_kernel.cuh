@@ -881,6 +881,18 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
 #define NMPCMC_SPLIT_SWEEPS 1
 #endif
 
+/// a / b from y ~ 1/b as cdiv_seed computes it, without the certificate (the
+/// split sweeps stash the operands and certify them lane-parallel afterwards).
+__device__ __forceinline__ double div_seed(double a, double b, double y) {
+    const double q0 = a * y;
+    const double q = __fma_rn(__fma_rn(-b, q0, a), y, q0);
+    return a == 0.0 ? q0 : q;
+}
+/// cdiv_seed's certificate of q = a / b.
+__device__ __forceinline__ bool div_seed_ok(double a, double b, double q) {
+    return (a == 0.0) | cert_div_bf(a, b, q);
+}
+
 /// riccati_factor (qp.cpp:73-110), fast forms, one block element per lane.
 /// Returns true on NotPositiveDefinite; *cert is false if any fast
 /// sqrt/division was not certified (the caller replays rfactor_t<FAST=false>).
@@ -904,10 +916,15 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
     const double* const aJU = gen_smem + SL.JU;
     const double* const aRR = gen_smem + SL.RR;
     const double* const aQQ = gen_smem + SL.QQ;
+    // certificate inputs, checked lane-parallel after the sweep: the pivots'
+    // radicands in DFF and the first quotients G / l in RH..TG (3 N doubles,
+    // contiguous); all three are dead between qp_resid's sums and qp_csolve
+    double* const cH = gen_smem + SL.DFF;
+    double* const cQ1 = gen_smem + SL.RH;
+    static_assert(NX <= 3, "the RH..TG scratch holds NX <= 3 quotients per stage");
     const int N = o.N;
     const int e = (int)(threadIdx.x & 31) % (NX * NX);
     const int i = e % NX, j = e / NX;  // this lane's element: row i, column j
-    bool cert = true;
     double Pn = aQQ[(N * NX + j) * NX + i];  // P_{k+1}(i, j)
     aFP[(N * NX + j) * NX + i] = Pn;
     // stage operands: Ju, columns j and i of Jx, Q(i, j), R, BAR, M(j)
@@ -957,7 +974,7 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
         }
         double l, y;
         fast_sqrt(H, l, y);
-        cert &= cert_sqrt_bf(H, l);
+        cH[k] = H;
         aFLL[k] = l;
         aFLY[k] = y;
         if (k >= 1) {
@@ -979,8 +996,9 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
                 G = 1.0 * s + 0.0;
             }
             G += c.mj;
-            double t = cdiv_seed(G, l, y, cert);  // cholesky_solve of the 1x1 factor, then negate
-            t = cdiv_seed(t, l, y, cert);
+            double t = div_seed(G, l, y);  // cholesky_solve of the 1x1 factor, then negate
+            cQ1[k * NX + j] = t;
+            t = div_seed(t, l, y);
             const double K = -t;
             double pk;  // (Jx' P Jx)(i, j)
             {
@@ -1002,6 +1020,16 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
             Pn = pk;
         }
         c = nx;
+    }
+    __syncwarp();
+    // certificates (cert_sqrt_bf / cdiv_seed's), one stage entry per lane
+    bool cert = true;
+#pragma unroll 1
+    for (int k = (int)(threadIdx.x & 31); k < N; k += W) cert &= cert_sqrt_bf(cH[k], aFLL[k]);
+#pragma unroll 1
+    for (int q = NX + (int)(threadIdx.x & 31); q < N * NX; q += W) {
+        const double pl = aFLL[q / NX], q1 = cQ1[q];
+        cert &= div_seed_ok(aFG[q], pl, q1) & div_seed_ok(q1, pl, -aFK[q]);
     }
     *cert_out = __all_sync(kFull, cert);
     __syncwarp();
@@ -1178,9 +1206,12 @@ __device__ __noinline__ bool rsolve_split(const QpView<NX, 32> v) {
     const double* const aRS = gen_smem + SL.RS;
     const double* const aRD = gen_smem + SL.RD;
     const double* const aRH = gen_smem + SL.RH;
+    // certificate inputs of the two divisions per stage, checked lane-parallel
+    // after the backward sweep (TG is free between the gap sums)
+    double* const cA = gen_smem + SL.TG;
     const int N = o.N;
+    double* const cQ1 = cA + N;
     const int i = (int)(threadIdx.x & 31) % NX;  // this lane's vector component
-    bool cert = true;
     double pvn = aRS[L.xo(N) + i];  // p_{k+1}(i)
     aPV[N * NX + i] = pvn;
     // backward: s = (P_{k+1} bhat_k)(i), Ju, rh, the pivot and its seed,
@@ -1221,8 +1252,10 @@ __device__ __noinline__ bool rsolve_split(const QpView<NX, 32> v) {
             for (int j = 0; j < NX; ++j) s += c.ju[j] * tj[j];
             hv = 1.0 * s + 1.0 * c.rh;
         }
-        hv = cdiv_seed(hv, c.l, c.y, cert);
-        hv = cdiv_seed(hv, c.l, c.y, cert);
+        cA[k] = hv;
+        hv = div_seed(hv, c.l, c.y);
+        cQ1[k] = hv;
+        hv = div_seed(hv, c.l, c.y);
         const double dff = -hv;
         aDFF[k] = dff;
         if (k >= 1) {
@@ -1235,6 +1268,16 @@ __device__ __noinline__ bool rsolve_split(const QpView<NX, 32> v) {
             pvn = p;
         }
         c = nx;
+    }
+    bool cert = true;  // every lane stored the same (lane-uniform) certificate inputs
+#pragma unroll 1
+    for (int k = (int)(threadIdx.x & 31); k < N; k += W) {
+        const double pl = aFLL[k], q1 = cQ1[k];
+        cert &= div_seed_ok(cA[k], pl, q1) & div_seed_ok(q1, pl, -aDFF[k]);
+    }
+    if (!__all_sync(kFull, cert)) {
+        __syncwarp();
+        return false;
     }
     // forward: dff, K, bhat(i), row i of Jx, Ju(i), row i of P_{k+1}, p_{k+1}(i)
     struct Fwd {
@@ -1287,9 +1330,8 @@ __device__ __noinline__ bool rsolve_split(const QpView<NX, 32> v) {
         w[oDMU + k * NX + i] = -mv;
         f = nf;
     }
-    cert = __all_sync(kFull, cert);
     __syncwarp();
-    return cert;
+    return true;
 }
 
 /// riccati_solve_vectors with the certified fast division (replayed with
