@@ -70,6 +70,15 @@ extern __shared__ __align__(16) double gen_smem[];
 /// blocks, staged once per QP (constant during solve_qp) for the lane loops
 /// and the factor sweep. At N = 60, NX = 3 the layout is 26.4 KB, so 8
 /// one-warp blocks (the register limit) still fit an SM.
+// NMPCMC_K3W_NOQQ = 1: the Hessian blocks Q, R are not staged in shared memory;
+// the lane-split factor sweep reads them from the slab one stage ahead. Frees
+// 4.8 KB per warp at N = 60, NX = 3 (experiment: more resident warps).
+#ifndef NMPCMC_K3W_NOQQ
+#define NMPCMC_K3W_NOQQ 0
+#endif
+#ifndef NMPCMC_K3W_MIN_BLOCKS
+#define NMPCMC_K3W_MIN_BLOCKS 1
+#endif
 template <int NX>
 struct SweepLay {
     int FP, FLL, FLY, FK, FG, PV, DFF, JX, JU, RS, RD, RH, TG, LB, UB, RR, QQ, total;
@@ -90,8 +99,8 @@ struct SweepLay {
         LB = TG + 2 * N;
         UB = LB + N;
         RR = UB + N;
-        QQ = RR + N + 1;
-        total = QQ + (N + 1) * NX * NX;
+        QQ = RR + (NMPCMC_K3W_NOQQ ? 0 : N + 1);
+        total = QQ + (NMPCMC_K3W_NOQQ ? 0 : (N + 1) * NX * NX);
     }
 };
 /// Bytes of shared memory K3w needs per block; K3w runs only if it fits.
@@ -739,11 +748,11 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
     };
     // K3w: R and Q from the copies solve_qp staged (SweepLay RR / QQ)
     auto R_ = [&](int k) -> double {
-        if (W > 1) return gen_smem[SL.RR + k];
+        if (W > 1 && !NMPCMC_K3W_NOQQ) return gen_smem[SL.RR + k];
         return k == 0 ? Wb_(0, 0, 0) : Wb_(k, NX, NX);
     };
     auto Q_ = [&](int k, int i, int j) -> double {
-        if (W > 1) return gen_smem[SL.QQ + (k * NX + j) * NX + i];
+        if (W > 1 && !NMPCMC_K3W_NOQQ) return gen_smem[SL.QQ + (k * NX + j) * NX + i];
         return Wb_(k, i, j);
     };
     auto M_ = [&](int k, int i) -> double { return Wb_(k, i, NX); };
@@ -914,8 +923,19 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
     double* const aFG = gen_smem + SL.FG;
     const double* const aJX = gen_smem + SL.JX;
     const double* const aJU = gen_smem + SL.JU;
-    const double* const aRR = gen_smem + SL.RR;
-    const double* const aQQ = gen_smem + SL.QQ;
+    // this lane's element: row i, column j
+    auto i_of = [] { return ((int)(threadIdx.x & 31) % (NX * NX)) % NX; };
+    auto j_of = [] { return ((int)(threadIdx.x & 31) % (NX * NX)) / NX; };
+    // Q(k, i, j) and R(k): the staged copies, or the W blocks in the slab
+    auto Qk = [&](int k) -> double {
+        if (!NMPCMC_K3W_NOQQ) return gen_smem[SL.QQ + (k * NX + j_of()) * NX + i_of()];
+        const int ld = k < o.N ? NX + 1 : NX;  // k >= 1
+        return w[oWB + k * Layout<NX>::B + j_of() * ld + i_of()];
+    };
+    auto Rk = [&](int k) -> double {
+        if (!NMPCMC_K3W_NOQQ) return gen_smem[SL.RR + k];
+        return k == 0 ? w[oWB] : w[oWB + k * Layout<NX>::B + NX * (NX + 1) + NX];
+    };
     // certificate inputs, checked lane-parallel after the sweep: the pivots'
     // radicands in DFF and the first quotients G / l in RH..TG (3 N doubles,
     // contiguous); all three are dead between qp_resid's sums and qp_csolve
@@ -923,9 +943,8 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
     double* const cQ1 = gen_smem + SL.RH;
     static_assert(NX <= 3, "the RH..TG scratch holds NX <= 3 quotients per stage");
     const int N = o.N;
-    const int e = (int)(threadIdx.x & 31) % (NX * NX);
-    const int i = e % NX, j = e / NX;  // this lane's element: row i, column j
-    double Pn = aQQ[(N * NX + j) * NX + i];  // P_{k+1}(i, j)
+    const int i = i_of(), j = j_of();
+    double Pn = Qk(N);  // P_{k+1}(i, j)
     aFP[(N * NX + j) * NX + i] = Pn;
     // stage operands: Ju, columns j and i of Jx, Q(i, j), R, BAR, M(j)
     struct Ops {
@@ -939,8 +958,8 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
             n.jxj[l] = aJX[(k * NX + j) * NX + l];
             n.jxi[l] = aJX[(k * NX + i) * NX + l];
         }
-        n.qq = aQQ[(k * NX + j) * NX + i];
-        n.rr = aRR[k];
+        n.qq = Qk(k > 0 ? k : 1);  // unused at k = 0
+        n.rr = Rk(k);
         n.bar = w[oBAR + k];
         n.mj = w[oWB + k * Layout<NX>::B + NX * (NX + 1) + j];  // M(k, j), 1 <= k < N (unused at k = 0)
         return n;
@@ -1506,12 +1525,15 @@ __device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_
             if (k < N) {
                 gen_smem[SLq.LB + k] = v.lb_src(k);
                 gen_smem[SLq.UB + k] = v.ub_src(k);
-                gen_smem[SLq.RR + k] = v.R(k);
+                if (!NMPCMC_K3W_NOQQ) gen_smem[SLq.RR + k] = v.R(k);
             }
+            if (!NMPCMC_K3W_NOQQ) {
 #pragma unroll
-            for (int j = 0; j < NX; ++j)
+                for (int j = 0; j < NX; ++j)
 #pragma unroll
-                for (int i = 0; i < NX; ++i) gen_smem[SLq.QQ + (k * NX + j) * NX + i] = k == 0 ? 0.0 : v.Q(k, i, j);
+                    for (int i = 0; i < NX; ++i)
+                        gen_smem[SLq.QQ + (k * NX + j) * NX + i] = k == 0 ? 0.0 : v.Q(k, i, j);
+            }
         }
         Lanes<W>::sync();
     }
@@ -2430,7 +2452,7 @@ __global__ void __launch_bounds__(kGenBlock) nmpc_gen_kernel(const __grid_consta
 /// K3w: one warp per sample, persistent one-warp blocks pulling samples from
 /// an atomic counter; workspace = one contiguous slab per block.
 template <int TX, int NX>
-__global__ void __launch_bounds__(32) nmpc_genw_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
+__global__ void __launch_bounds__(32, NMPCMC_K3W_MIN_BLOCKS) nmpc_genw_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
                                                        int64_t n_sims, int nbar, nmpcmc_sim_record* records,
                                                        nmpcmc_work_counters* counters, double* traj, int traj_rows,
                                                        double* ws_all, int64_t slab, unsigned long long* next,
@@ -2772,7 +2794,10 @@ inline int64_t genw_blocks_t(int sm_count, int64_t n, int64_t slab_doubles, int 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, nmpc_genw_kernel<TX, NX>, 32, smem);
     if (b < 1) b = 1;
     int64_t blocks = (int64_t)sm_count * b;
-    const int64_t l2_cap = (int64_t)(96ull << 20) / (slab_doubles * 8);
+#ifndef NMPCMC_K3W_L2_CAP_MB
+#define NMPCMC_K3W_L2_CAP_MB 96
+#endif
+    const int64_t l2_cap = (int64_t)((unsigned long long)NMPCMC_K3W_L2_CAP_MB << 20) / (slab_doubles * 8);
     if (blocks > l2_cap) blocks = l2_cap < sm_count ? sm_count : l2_cap;
     return blocks < n ? blocks : n;
 }
