@@ -70,11 +70,17 @@ extern __shared__ __align__(16) double gen_smem[];
 /// blocks, staged once per QP (constant during solve_qp) for the lane loops
 /// and the factor sweep. At N = 60, NX = 3 the layout is 26.4 KB, so 8
 /// one-warp blocks (the register limit) still fit an SM.
-// NMPCMC_K3W_NOQQ = 1: the Hessian blocks Q, R are not staged in shared memory;
-// the lane-split factor sweep reads them from the slab one stage ahead. Frees
-// 4.8 KB per warp at N = 60, NX = 3 (experiment: more resident warps).
+// NMPCMC_K3W_NOQQ = 1 (default): the Hessian blocks Q, R are not staged in
+// shared memory; the lane-split factor sweep reads them from the slab one
+// stage ahead. Frees 4.8 KB per warp at N = 60, NX = 3, which the SM gives to
+// L1 (measured +5 %, profiles/r02/r02J_k3w_noqq_ab.txt).
 #ifndef NMPCMC_K3W_NOQQ
-#define NMPCMC_K3W_NOQQ 0
+#define NMPCMC_K3W_NOQQ 1
+#endif
+// NMPCMC_K3W_NOJX = 1: likewise for the constraint jacobians Jx, Ju (6.7 KB);
+// measured 5 % slower (r02K_k3w_nojx_ab.txt), so they stay staged.
+#ifndef NMPCMC_K3W_NOJX
+#define NMPCMC_K3W_NOJX 0
 #endif
 #ifndef NMPCMC_K3W_MIN_BLOCKS
 #define NMPCMC_K3W_MIN_BLOCKS 1
@@ -91,8 +97,8 @@ struct SweepLay {
         PV = FG + N * NX;
         DFF = PV + (N + 1) * NX;
         JX = DFF + N;
-        JU = JX + N * NX * NX;
-        RS = JU + N * NX;
+        JU = JX + (NMPCMC_K3W_NOJX ? 0 : N * NX * NX);
+        RS = JU + (NMPCMC_K3W_NOJX ? 0 : N * NX);
         RD = RS + N * (1 + NX);
         RH = RD + N * NX;
         TG = RH + N;
@@ -123,6 +129,13 @@ template <int W>
 __device__ __forceinline__ ArrT<W> sweep_arr(const WsT<W>& w, int goff, int soff) {
     if (W == 1) return ArrT<W>{w.p + (int64_t)goff * w.T, w.T};
     return ArrT<W>{gen_smem + soff, 1};
+}
+
+/// The constraint jacobians for the sweeps: the staged copy, or the slab.
+template <int W>
+__device__ __forceinline__ ArrT<W> jac_arr(const WsT<W>& w, int goff, int soff) {
+    if (W > 1 && NMPCMC_K3W_NOJX) return ArrT<W>{w.p + goff, 1};
+    return sweep_arr<W>(w, goff, soff);
 }
 
 /// Ordered sum s = init + t(0) + t(1) + ... + t(n-1), left to right, the
@@ -737,8 +750,8 @@ __device__ __noinline__ bool rfactor_t(const QpView<NX, W> v, bool* cert) {
     const ArrT<W> aFG = sweep_arr<W>(w, oFG, SL.FG);
     const int oFXs = L.FX[v.s], oFUs = L.FU[v.s], oWB = L.WB, oXIs = L.XI[v.s], oGFs = L.GF[v.s];
     // K3w: the shared-memory copies staged by solve_qp; K3g: the set in place
-    const ArrT<W> aJX = sweep_arr<W>(w, oFXs, SL.JX);
-    const ArrT<W> aJU = sweep_arr<W>(w, oFUs, SL.JU);
+    const ArrT<W> aJX = jac_arr<W>(w, oFXs, SL.JX);
+    const ArrT<W> aJU = jac_arr<W>(w, oFUs, SL.JU);
     auto Jx_ = [&](int k, int i, int j) -> double { return aJX[(k * NX + j) * NX + i]; };
     auto Ju_ = [&](int k, int i) -> double { return aJU[k * NX + i]; };
     const int nN = o.N;
@@ -921,8 +934,8 @@ __device__ __noinline__ bool rfactor_split(const QpView<NX, 32> v, bool* cert_ou
     double* const aFLY = gen_smem + SL.FLY;
     double* const aFK = gen_smem + SL.FK;
     double* const aFG = gen_smem + SL.FG;
-    const double* const aJX = gen_smem + SL.JX;
-    const double* const aJU = gen_smem + SL.JU;
+    const double* const aJX = NMPCMC_K3W_NOJX ? w.p + L.FX[v.s] : gen_smem + SL.JX;
+    const double* const aJU = NMPCMC_K3W_NOJX ? w.p + L.FU[v.s] : gen_smem + SL.JU;
     // this lane's element: row i, column j
     auto i_of = [] { return ((int)(threadIdx.x & 31) % (NX * NX)) % NX; };
     auto j_of = [] { return ((int)(threadIdx.x & 31) % (NX * NX)) / NX; };
@@ -1089,8 +1102,8 @@ __device__ __noinline__ bool rsolve_t(const QpView<NX, W> v) {
     const ArrT<W> aDFF = sweep_arr<W>(w, oDFF, SL.DFF);
     const int oFXs = L.FX[v.s], oFUs = L.FU[v.s], oWB = L.WB, oXIs = L.XI[v.s], oGFs = L.GF[v.s];
     // K3w: the shared-memory copies staged by solve_qp; K3g: the set in place
-    const ArrT<W> aJX = sweep_arr<W>(w, oFXs, SL.JX);
-    const ArrT<W> aJU = sweep_arr<W>(w, oFUs, SL.JU);
+    const ArrT<W> aJX = jac_arr<W>(w, oFXs, SL.JX);
+    const ArrT<W> aJU = jac_arr<W>(w, oFUs, SL.JU);
     auto Jx_ = [&](int k, int i, int j) -> double { return aJX[(k * NX + j) * NX + i]; };
     auto Ju_ = [&](int k, int i) -> double { return aJU[k * NX + i]; };
     const int nN = o.N;
@@ -1220,8 +1233,8 @@ __device__ __noinline__ bool rsolve_split(const QpView<NX, 32> v) {
     const double* const aFG = gen_smem + SL.FG;
     double* const aPV = gen_smem + SL.PV;
     double* const aDFF = gen_smem + SL.DFF;
-    const double* const aJX = gen_smem + SL.JX;
-    const double* const aJU = gen_smem + SL.JU;
+    const double* const aJX = NMPCMC_K3W_NOJX ? w.p + L.FX[v.s] : gen_smem + SL.JX;
+    const double* const aJU = NMPCMC_K3W_NOJX ? w.p + L.FU[v.s] : gen_smem + SL.JU;
     const double* const aRS = gen_smem + SL.RS;
     const double* const aRD = gen_smem + SL.RD;
     const double* const aRH = gen_smem + SL.RH;
@@ -1518,8 +1531,10 @@ __device__ __noinline__ int solve_qp(const QpView<NX, W> v, double tol, int max_
     const ArrT<W> aRSq = sweep_arr<W>(w, L.RS, SLq.RS);
     const ArrT<W> aRDq = sweep_arr<W>(w, L.RD, SLq.RD);
     if (W > 1) {  // stage the QP's constant operands (SweepLay JX JU LB UB RR QQ)
-        for (int e = lane; e < N * NX * NX; e += W) gen_smem[SLq.JX + e] = w[L.FX[v.s] + e];
-        for (int e = lane; e < N * NX; e += W) gen_smem[SLq.JU + e] = w[L.FU[v.s] + e];
+        if (!NMPCMC_K3W_NOJX) {
+            for (int e = lane; e < N * NX * NX; e += W) gen_smem[SLq.JX + e] = w[L.FX[v.s] + e];
+            for (int e = lane; e < N * NX; e += W) gen_smem[SLq.JU + e] = w[L.FU[v.s] + e];
+        }
 #pragma unroll 1
         for (int k = lane; k <= N; k += W) {
             if (k < N) {
@@ -1763,8 +1778,9 @@ __device__ __noinline__ bool kkt_ok(const Ocp<NX, W>& o, int s, int LAMo, int PL
     double sd = 1.0;
     if (m > 0) {  // ordered one-norm sums (ordered_sum: terms lane-parallel on K3w)
         const SweepLay<NX> SL(o.N);
-        double* scr = W > 1 ? gen_smem + SL.JX : nullptr;  // JX / JU are free outside solve_qp
-        const int cap = o.N * NX * (NX + 1);
+        // scratch outside solve_qp: its staged jacobians, or its residual arrays RS RD
+        double* scr = W > 1 ? gen_smem + (NMPCMC_K3W_NOJX ? SL.RS : SL.JX) : nullptr;
+        const int cap = NMPCMC_K3W_NOJX ? o.N * (2 * NX + 1) : o.N * NX * (NX + 1);
         const double a = ordered_sum<W>(0.0, L.NN, scr, cap, [&](int e) { return fabs(w[LAMo + e]); });
         const double b = ordered_sum<W>(0.0, o.N, scr, cap, [&](int k) { return fabs(w[PLo + k]); });
         const double c = ordered_sum<W>(0.0, o.N, scr, cap, [&](int k) { return fabs(w[PUo + k]); });
@@ -1931,8 +1947,9 @@ __device__ __noinline__ SqpOut sqp_solve(const Ocp<NX, W>& o, const nmpcmc_sqp_o
         // line_search (sqp.cpp:22-59); the trial of the accepted step is the
         // new iterate (identical by construction, sqp.cpp:331-352)
         const SweepLay<NX> SLs(N);
-        double* scr = W > 1 ? gen_smem + SLs.JX : nullptr;  // JX / JU are free outside solve_qp
-        const int cap = N * NX * (NX + 1);
+        // scratch outside solve_qp: its staged jacobians, or its residual arrays RS RD
+        double* scr = W > 1 ? gen_smem + (NMPCMC_K3W_NOJX ? SLs.RS : SLs.JX) : nullptr;
+        const int cap = NMPCMC_K3W_NOJX ? N * (2 * NX + 1) : N * NX * (NX + 1);
         const double pen =
             ordered_sum<W>(0.0, L.NN, scr, cap, [&](int e) { return w[L.SIG + e] * fabs(w[L.G[s] + e]); });
         const double m0 = f + pen;
@@ -2452,7 +2469,12 @@ __global__ void __launch_bounds__(kGenBlock) nmpc_gen_kernel(const __grid_consta
 /// K3w: one warp per sample, persistent one-warp blocks pulling samples from
 /// an atomic counter; workspace = one contiguous slab per block.
 template <int TX, int NX>
-__global__ void __launch_bounds__(32, NMPCMC_K3W_MIN_BLOCKS) nmpc_genw_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
+#ifdef NMPCMC_K3W_MAXNREG
+__global__ void __maxnreg__(NMPCMC_K3W_MAXNREG) nmpc_genw_kernel(
+#else
+__global__ void __launch_bounds__(32, NMPCMC_K3W_MIN_BLOCKS) nmpc_genw_kernel(
+#endif
+const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
                                                        int64_t n_sims, int nbar, nmpcmc_sim_record* records,
                                                        nmpcmc_work_counters* counters, double* traj, int traj_rows,
                                                        double* ws_all, int64_t slab, unsigned long long* next,
