@@ -380,8 +380,8 @@ __device__ __forceinline__ int jac_u(const Model<NX>& m, const double* x, double
 /// shoot (ocp.cpp:9-74): Nc RK4 steps of (F, Fx, Fu). Column-major Fx.
 /// The RK4 weighted sum a + 2b + 2c + d accumulates left to right.
 template <int NX, bool SENS>
-__device__ __noinline__ int shoot(const Model<NX>& m_in, const double* x, double u, double h, int nc, double* F,
-                                  double* Fx, double* Fu) {
+__device__ __noinline__ int shoot(const Model<NX>& m_in, const double* x, double u, double h, int nc,
+                                  double* F_out, double* Fx_out, double* Fu_out) {
 #if NMPCMC_SHOOT_MODEL_COPY
     // a private copy: the stores to F / Fx / Fu may alias the caller's model
     // (both live in local memory), which would force a reload of every model
@@ -390,6 +390,22 @@ __device__ __noinline__ int shoot(const Model<NX>& m_in, const double* x, double
 #else
     const Model<NX>& m = m_in;
 #endif
+    // the running (F, Fx, Fu) live in registers; the caller's arrays (local
+    // memory) are written once on the way out, with the values the reference's
+    // in-place update would hold at that point
+    double F[NX], Fx[NX * NX], Fu[NX];
+    auto put = [&](int st) {
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            F_out[i] = F[i];
+            if (SENS) {
+                Fu_out[i] = Fu[i];
+#pragma unroll
+                for (int l = 0; l < NX; ++l) Fx_out[l * NX + i] = Fx[l * NX + i];
+            }
+        }
+        return st;
+    };
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
         F[i] = x[i];
@@ -418,11 +434,11 @@ __device__ __noinline__ int shoot(const Model<NX>& m_in, const double* x, double
             }
             double k[NX], A[NX * NX], B[NX];
             const int st = drift_jac<NX>(m, xs, u, k, SENS ? A : nullptr);
-            if (st) return st;
+            if (st) return put(st);
             double kx[NX * NX], ku[NX];
             if (SENS) {
                 const int su_st = jac_u<NX>(m, xs, u, B);
-                if (su_st) return su_st;
+                if (su_st) return put(su_st);
 #pragma unroll
                 for (int jj = 0; jj < NX; ++jj)  // kx = A sx (gemm, beta 0)
 #pragma unroll
@@ -470,8 +486,8 @@ __device__ __noinline__ int shoot(const Model<NX>& m_in, const double* x, double
     }
 #pragma unroll
     for (int i = 0; i < NX; ++i)
-        if (!dfinite(F[i])) return G_NONFINITE;
-    return G_OK;
+        if (!dfinite(F[i])) return put(G_NONFINITE);
+    return put(G_OK);
 }
 
 // -------------------------------------------------------------------- OCP
