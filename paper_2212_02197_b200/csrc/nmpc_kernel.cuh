@@ -65,8 +65,19 @@
 #define NMPCMC_UNROLL_ROLLOUT 1
 #endif
 
+// Unroll factors of the lane-parallel stage loops (k = lane, lane + 32, ...)
+// of solve_qp and of the shooting loop (experiments; 1 = the default).
+#ifndef NMPCMC_UNROLL_QP_LANES
+#define NMPCMC_UNROLL_QP_LANES 1
+#endif
+#ifndef NMPCMC_UNROLL_SHOOT_LANES
+#define NMPCMC_UNROLL_SHOOT_LANES 1
+#endif
+
 namespace nmpcmc_dev {
 
+constexpr int kUnrollQpLanes = NMPCMC_UNROLL_QP_LANES;
+constexpr int kUnrollShootLanes = NMPCMC_UNROLL_SHOOT_LANES;
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr int kUnrollFactor = NMPCMC_UNROLL_FACTOR;
 constexpr int kUnrollVector = NMPCMC_UNROLL_VECTOR;
@@ -364,7 +375,7 @@ __device__ __noinline__ int eval_constraints(const Ocp& o, const double* U, cons
                                              double* Ju, Cnt* cnt) {
     const int lane = threadIdx.x & 31;
     int first_bad = 0x7fffffff;
-#pragma unroll 1
+#pragma unroll kUnrollShootLanes
     for (int k = lane; k < o.N; k += 32) {
         const double xk = (k == 0) ? o.x0 : X[k - 1];
         double F, Sx, Su;
@@ -715,7 +726,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o_in, double tol, int max_iter, 
     double ds = 1.0;
     int nfin = 0;
     bool bad = false;
-#pragma unroll 1
+#pragma unroll kUnrollQpLanes
     for (int k = lane; k < N; k += 32) {
         const double lb = umin - U[k];
         const double ub = umax - U[k];
@@ -760,7 +771,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o_in, double tol, int max_iter, 
         // residuals() (qp.cpp:237-284); the gap terms go to TMP for the
         // ordered sums
         double ninf = 0.0, dinf = 0.0, linf = 0.0, uinf = 0.0;
-#pragma unroll 1
+#pragma unroll kUnrollQpLanes
         for (int k = lane; k < N; k += 32) {
             const double ju = Ju[k];
             const double vk = dU[k], muk = mu[k];
@@ -850,7 +861,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o_in, double tol, int max_iter, 
             for (int pass = 0;; ++pass) {
                 bool cert = true;
                 alpha_aff = 1.0;
-#pragma unroll 1
+#pragma unroll kUnrollQpLanes
                 for (int k = lane; k < N; k += 32) {
                     if (fast_ok) cert = cert && certify_factor_k<ST>(o, k);
                     const double u = U[k];
@@ -877,7 +888,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o_in, double tol, int max_iter, 
             }
             alpha_aff = warp_min_pos(alpha_aff);  // step lengths lie in (0, 1]
             if (m > 0 && gap > 0.0) {
-#pragma unroll 1
+#pragma unroll kUnrollQpLanes
                 for (int k = lane; k < N; k += 32) {
                     const double u = U[k];
                     const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
@@ -902,7 +913,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o_in, double tol, int max_iter, 
         __syncwarp();
         // corrector rc + condensed rhs (qp.cpp:390-395, :288-305) from the
         // stored affine directions
-#pragma unroll 1
+#pragma unroll kUnrollQpLanes
         for (int k = lane; k < N; k += 32) {
             const double u = U[k];
             const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
@@ -929,7 +940,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o_in, double tol, int max_iter, 
         for (bool vfast = true;; vfast = false) {
             bool cert = true;
             alpha = 1.0;
-#pragma unroll 1
+#pragma unroll kUnrollQpLanes
             for (int k = lane; k < N; k += 32) {
                 if (vfast) cert = cert && certify_vector_k<ST>(o, k);
                 const double u = U[k];
@@ -946,7 +957,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o_in, double tol, int max_iter, 
         }
         alpha = warp_min_pos(alpha);
         // update (qp.cpp:398-410)
-#pragma unroll 1
+#pragma unroll kUnrollQpLanes
         for (int k = lane; k < N; k += 32) {
             const double u = U[k];
             const bool fl = dfinite(umin - u), fu = dfinite(umax - u);
@@ -968,7 +979,7 @@ __device__ __noinline__ int solve_qp(const Ocp& o_in, double tol, int max_iter, 
         __syncwarp();
     }
     // final clamp (qp.cpp:414-419)
-#pragma unroll 1
+#pragma unroll kUnrollQpLanes
     for (int k = lane; k < N; k += 32) {
         const double lb = umin - U[k], ub = umax - U[k];
         dU[k] = smin(smax(dU[k], lb), ub);
