@@ -1623,10 +1623,20 @@ __device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_
 /// from a global atomic counter -- the device form of run_monte_carlo's worker
 /// pool (montecarlo.cpp:218-238) -- so long and short samples balance.
 template <int NX, int ST>
+// Resident one-warp blocks per SM the kernel is compiled for. 12 (168
+// registers, 3 warps per SM sub-partition) beats 16 (128 registers) by 4 %,
+// and 13 / 14 (152 / 144 registers), 11 (184) and 8 (236) are no better
+// (profiles/r02/r02T_k3_minblocks_ab.txt): fewer spills per warp; the larger
+// L1 that fewer blocks leave is not what pays (same file, TMP-alias run).
 #ifndef NMPCMC_MIN_BLOCKS
-#define NMPCMC_MIN_BLOCKS 16
+#define NMPCMC_MIN_BLOCKS 12
 #endif
-__global__ void __launch_bounds__(32, NMPCMC_MIN_BLOCKS) nmpc_kernel(const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
+#ifdef NMPCMC_K3_MAXNREG
+__global__ void __maxnreg__(NMPCMC_K3_MAXNREG) nmpc_kernel(
+#else
+__global__ void __launch_bounds__(32, NMPCMC_MIN_BLOCKS) nmpc_kernel(
+#endif
+const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
                                                   int64_t n_sims, int nbar, nmpcmc_sim_record* records,
                                                   nmpcmc_work_counters* counters, double* traj, int traj_rows,
                                                   double* gws_all, unsigned long long* next) {
