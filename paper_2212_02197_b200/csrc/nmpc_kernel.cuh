@@ -1719,8 +1719,14 @@ inline int launch_nmpc(const nmpcmc_scenario& sc, uint64_t first, int64_t n, int
 /// for instance b, sqp_solve on the regulator OCP from x0[b] at t0[b], cold
 /// start as nmpc_step (start_iterate) or the given xi0 with zero duals. The
 /// iterate is scattered back to the interleaved xi layout (u_k, x_{k+1}).
+// The OCP service keeps the round-1 residency (16 warps per SM, 128 registers):
+// at 20,000 instances 12 and 16 measure the same within the run-to-run spread
+// of the service benchmark (257k-284k OCPs/s, profiles/r02/r02N, r02Y, r02a2).
+#ifndef NMPCMC_OCP1_MIN_BLOCKS
+#define NMPCMC_OCP1_MIN_BLOCKS 16
+#endif
 template <int ST>
-__global__ void __launch_bounds__(32, NMPCMC_MIN_BLOCKS)
+__global__ void __launch_bounds__(32, NMPCMC_OCP1_MIN_BLOCKS)
     ocp1_kernel(const __grid_constant__ nmpcmc_scenario sc, int64_t batch, const double* x0, const double* t0,
                 const double* xi0, double* xi_out, double* lam_out, double* pil_out, double* piu_out,
                 int32_t* conv_out, int32_t* status_out, double* gws_all, unsigned long long* next) {
