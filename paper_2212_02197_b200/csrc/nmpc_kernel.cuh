@@ -1622,19 +1622,27 @@ __device__ __noinline__ void nmpc_closed_loop(const nmpcmc_scenario& sc, uint64_
 /// Persistent blocks (one warp, one sample at a time) pull sample indices
 /// from a global atomic counter -- the device form of run_monte_carlo's worker
 /// pool (montecarlo.cpp:218-238) -- so long and short samples balance.
-template <int NX, int ST>
 // Resident one-warp blocks per SM the kernel is compiled for. 12 (168
 // registers, 3 warps per SM sub-partition) beats 16 (128 registers) by 4 %,
 // and 13 / 14 (152 / 144 registers), 11 (184) and 8 (236) are no better
 // (profiles/r02/r02T_k3_minblocks_ab.txt): fewer spills per warp; the larger
 // L1 that fewer blocks leave is not what pays (same file, TMP-alias run).
+// At the short stride (N < 32: one round of every stage loop) 16 still wins
+// by 8 % (r02b2_k3_minblocks_other_N.txt); N = 120 gains 6 % at 12.
 #ifndef NMPCMC_MIN_BLOCKS
 #define NMPCMC_MIN_BLOCKS 12
 #endif
+#ifndef NMPCMC_MIN_BLOCKS_SHORT
+#define NMPCMC_MIN_BLOCKS_SHORT 16
+#endif
+__host__ __device__ constexpr int k3_min_blocks(int stride) {
+    return stride <= 32 ? NMPCMC_MIN_BLOCKS_SHORT : NMPCMC_MIN_BLOCKS;
+}
+template <int NX, int ST>
 #ifdef NMPCMC_K3_MAXNREG
 __global__ void __maxnreg__(NMPCMC_K3_MAXNREG) nmpc_kernel(
 #else
-__global__ void __launch_bounds__(32, NMPCMC_MIN_BLOCKS) nmpc_kernel(
+__global__ void __launch_bounds__(32, k3_min_blocks(ST)) nmpc_kernel(
 #endif
 const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
                                                   int64_t n_sims, int nbar, nmpcmc_sim_record* records,
