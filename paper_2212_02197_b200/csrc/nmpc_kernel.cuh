@@ -267,39 +267,41 @@ extern __shared__ __align__(16) double smem_nmpc[];
 #endif
 // NMPCMC_CERT_SMEM = 1 keeps the certificate inputs of the fast Riccati
 // sweeps (written by the serial sweeps, read by the lane-parallel certify
-// loops) in shared memory instead of the L2 slab.
+// loops) in shared memory instead of the L2 slab -- at strides up to 64, where
+// it measured +1 % (profiles/r02/r02o_k3_cert_ab.txt). At stride 128 the four
+// extra arrays cost two resident samples per SM (8 instead of 10) and 8 %
+// (r02f2_k3_n120_cert_ab.txt), so there they stay in the slab. The layout is
+// therefore a function of the stride: S_TMP, S_IPM0, G_IPM0 and the array
+// counts below are expressions in the template parameter ST.
 #ifndef NMPCMC_CERT_SMEM
-#define NMPCMC_CERT_SMEM 1  // measured +1 % (profiles/r02/r02o_k3_cert_ab.txt)
+#define NMPCMC_CERT_SMEM 1
 #endif
+__host__ __device__ constexpr bool cert_in_smem(int stride) { return NMPCMC_CERT_SMEM && stride <= 64; }
 enum SmemId {
     S_JX, S_JU, S_WQ, S_WM, S_WR, S_BAR, S_RDYN, S_RHAT, S_RSX,
     S_CHOLH, S_RINV, S_VAL, S_GAIN, S_GMAT, S_PVEC, S_DFF,
     S_DDU, S_DDX,
-#if NMPCMC_CERT_SMEM
-    S_CHH, S_CA1, S_CQ1, S_CG1,
-#endif
-    S_TMP,  // three strides
-    S_IPM0 = S_TMP + 3,
-#if NMPCMC_IPM_SMEM
-    kSmemArrays = S_IPM0 + 14
-#else
-    kSmemArrays = S_IPM0
-#endif
+    S_CHH, S_CA1, S_CQ1, S_CG1,  // only if cert_in_smem(ST)
+    kSmemFixed = S_CHH
 };
 enum GlobId {
     G_U, G_X, G_TU, G_TX, G_LAM, G_PIL, G_PIU,
     G_GX, G_G, G_TGX, G_TG, G_TJX, G_TJU,
     G_SIG, G_SP,
-#if !NMPCMC_CERT_SMEM
-    G_CHH, G_CA1, G_CQ1, G_CG1,  // certificate inputs of the fast Riccati sweeps
-#endif
-    G_IPM0,
-#if NMPCMC_IPM_SMEM
-    kGlobArrays = G_IPM0
-#else
-    kGlobArrays = G_IPM0 + 14
-#endif
+    G_CHH, G_CA1, G_CQ1, G_CG1,  // certificate inputs of the fast Riccati sweeps, unless cert_in_smem(ST)
+    kGlobFixed = G_CHH
 };
+__host__ __device__ constexpr int smem_tmp(int stride) { return kSmemFixed + (cert_in_smem(stride) ? 4 : 0); }
+__host__ __device__ constexpr int smem_arrays(int stride) {
+    return smem_tmp(stride) + 3 + (NMPCMC_IPM_SMEM ? 14 : 0);
+}
+__host__ __device__ constexpr int glob_ipm0(int stride) { return kGlobFixed + (cert_in_smem(stride) ? 0 : 4); }
+__host__ __device__ constexpr int glob_arrays(int stride) {
+    return glob_ipm0(stride) + (NMPCMC_IPM_SMEM ? 0 : 14);
+}
+#define S_TMP smem_tmp(ST)  // three strides
+#define S_IPM0 (smem_tmp(ST) + 3)
+#define G_IPM0 glob_ipm0(ST)
 /// interior-point arrays: DU DX MU NL NU SL SU RSU RCL RCU DSL DSU DNL DNU
 enum IpmId { I_DU, I_DX, I_MU, I_NL, I_NU, I_SL, I_SU, I_RSU, I_RCL, I_RCU, I_DSL, I_DSU, I_DNL, I_DNU };
 #if NMPCMC_IPM_SMEM
@@ -315,14 +317,10 @@ static __device__ __noinline__ double qdiv(double a, double b) { return a / b; }
 
 #define SA(id) (smem_nmpc + (id) * ST)
 #define GA(id) (o.gws + (id) * ST)
-#if NMPCMC_CERT_SMEM
-#define CA(name) SA(S_##name)
-#else
-#define CA(name) GA(G_##name)
-#endif
+#define CA(name) (cert_in_smem(ST) ? SA(S_##name) : GA(G_##name))
 
-__host__ __device__ inline size_t ws_bytes_for(int ST) { return (size_t)kSmemArrays * ST * sizeof(double); }
-__host__ __device__ inline size_t gws_bytes_for(int ST) { return (size_t)kGlobArrays * ST * sizeof(double); }
+__host__ __device__ inline size_t ws_bytes_for(int ST) { return (size_t)smem_arrays(ST) * ST * sizeof(double); }
+__host__ __device__ inline size_t gws_bytes_for(int ST) { return (size_t)glob_arrays(ST) * ST * sizeof(double); }
 
 /// Scalars of one NMPC problem instance (NlpInstance, ocp.hpp:25-34).
 struct Ocp {
@@ -1648,7 +1646,7 @@ const __grid_constant__ nmpcmc_scenario sc, uint64_t first_sim,
                                                   int64_t n_sims, int nbar, nmpcmc_sim_record* records,
                                                   nmpcmc_work_counters* counters, double* traj, int traj_rows,
                                                   double* gws_all, unsigned long long* next) {
-    double* gws = gws_all + (size_t)blockIdx.x * kGlobArrays * ST;
+    double* gws = gws_all + (size_t)blockIdx.x * glob_arrays(ST) * ST;
 #pragma unroll 1
     for (;;) {
         unsigned long long i = 0;
@@ -1738,7 +1736,7 @@ __global__ void __launch_bounds__(32, NMPCMC_OCP1_MIN_BLOCKS)
     ocp1_kernel(const __grid_constant__ nmpcmc_scenario sc, int64_t batch, const double* x0, const double* t0,
                 const double* xi0, double* xi_out, double* lam_out, double* pil_out, double* piu_out,
                 int32_t* conv_out, int32_t* status_out, double* gws_all, unsigned long long* next) {
-    double* gws = gws_all + (size_t)blockIdx.x * kGlobArrays * ST;
+    double* gws = gws_all + (size_t)blockIdx.x * glob_arrays(ST) * ST;
     const int lane = threadIdx.x & 31;
 #pragma unroll 1
     for (;;) {
